@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Benchmark: ESP long-range (k-space) atom-steps/s on B200.
+
+Workload (BASELINE.json metric config): config 1 — 90,000
+charges (30,000 rigid 3-site waters), 67x67x67.5 A semi-isotropic cell,
+grid 64^3, P=8, Delta=1e-7, r_c=10, fp64, seeded synthetic inputs.  One step
+= bin -> spread -> 1 forward FFT -> fused scale/reduce (E + 6 pressure
+components) -> 3 ik inverse FFTs -> force gather.  ``value`` is whole-job
+force+pressure atom-steps/s with inputs resident in HBM; ``pressure_only``
+is the same for the pressure-only path; ``e2e`` goes through the public API
+with pinned host buffers and the H2D/D2H copies inside the timed region.
+L2 (126 MB) is flushed between timed steps by writing a 256 MB buffer.
+
+--impl reference times the CPU oracle port of the reference algorithm
+(oracle/esp_oracle.py; the reference is pure numpy, nothing to compile) on
+all host cores: particle chunks of spread/gather in a process pool (exact by
+linearity), numpy pocketfft transforms.
+
+Multi-GPU (torchrun, N>1): config 1 does not shard (G = 2.6e5 is
+latency-bound on one GPU), so N ranks run N independent
+replicas ("scaling": "weak"); timings are max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG = 1
+METRIC = "ESP long-range atom-steps/s (force+pressure)"
+UNIT = "atom-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=CONFIG)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="run a few steps for ncu (no JSON contract line)")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------
+# distributed plumbing
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world, local, backend="nccl"):
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return dist if world > 1 else None
+
+
+def max_over_ranks(x, dist, device=None):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md recipe)
+
+
+class ClockSampler:
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for i, nm in enumerate(names):
+                if len(s) > 3 + i and s[3 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# algorithmic bytes / flops (stated in DESIGN.md)
+
+
+def algorithmic(w, n, real_bytes=8):
+    Mx, My, Mz = w.M
+    G = Mx * My * Mz
+    H = (Mx // 2 + 1) * My * Mz
+    r, c, pb = real_bytes, 2 * real_bytes, 32
+    P, D = w.P, 18
+    return {
+        "spread": dict(bytes=pb * n + r * G, flops=2 * (3 * P * D + P * P + P + P ** 3) * n),
+        "combine": dict(bytes=r * G, flops=0),
+        "fft_forward": dict(bytes=r * G + c * H, flops=2.5 * G * np.log2(G)),
+        "scale_reduce": dict(bytes=c * H, flops=40 * H),
+        "fft_inverse_x3": dict(bytes=3 * (c * H + r * G), flops=3 * 2.5 * G * np.log2(G)),
+        "gather": dict(bytes=pb * n + 3 * r * G + 3 * r * n,
+                       flops=2 * (3 * P * D + P * P + 3 * P ** 3) * n),
+    }
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver, workloads
+    from paper_2601_00161_b200.plan import probe_fp64_tflops
+
+    rank, world, local = dist_env()
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w, pos_np, q_np = workloads.generate(args.config)
+    n = w.n
+    solver = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                               fixed_M=w.M, precision=args.precision,
+                                               cell_type=w.cell_type), capacity=n)
+    pos = torch.as_tensor(pos_np, device=dev)
+    q = torch.as_tensor(q_np, device=dev)
+    out7 = torch.empty(7, dtype=torch.float64, device=dev)
+    F = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(want_forces=True):
+        solver.evaluate_device(pos, q, want_forces, out7, F if want_forces else None)
+
+    if args.profile_only:
+        for _ in range(max(args.warmup, 1) + args.steps):
+            step()
+        torch.cuda.synchronize()
+        return None
+
+    def timed(fn, K, W):
+        for _ in range(W):
+            fn()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        total = 0.0
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(K)]
+        for i in range(K):
+            flush.zero_()                      # evict L2 between timed steps
+            ev[i][0].record(stream)
+            fn()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        total = sum(a.elapsed_time(b) for a, b in ev)
+        return max_over_ranks(total / K, dist, dev)
+
+    K, W = args.steps, args.warmup
+    with ClockSampler(local) as clk:
+        ms_fp = timed(lambda: step(True), K, W)
+        launches = solver.plan.launches_last_step()
+        ms_po = timed(lambda: step(False), K, W)
+        launches_po = solver.plan.launches_last_step()
+        # end to end through the public API: pinned host in, host out
+        h_pos = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        h_q = torch.empty(n, dtype=torch.float64).pin_memory()
+        h_pos.copy_(torch.as_tensor(pos_np))
+        h_q.copy_(torch.as_tensor(q_np))
+        h_F = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        h_out = torch.empty(7, dtype=torch.float64).pin_memory()
+        d_pos = torch.empty_like(pos)
+        d_q = torch.empty_like(q)
+
+        def e2e():
+            d_pos.copy_(h_pos, non_blocking=True)
+            d_q.copy_(h_q, non_blocking=True)
+            solver.evaluate_device(d_pos, d_q, True, out7, F)
+            h_F.copy_(F, non_blocking=True)
+            h_out.copy_(out7, non_blocking=True)
+
+        ms_e2e = timed(e2e, K, W)
+    clocks = clk.summary()
+    assert np.isfinite(h_F.numpy()).all() and np.isfinite(h_out.numpy()).all()
+
+    # per-kernel profile (separate, untimed pass): dominant kernel roofline
+    solver.plan.set_profiling(True)
+    prof = {}
+    reps = 5
+    for _ in range(reps):
+        flush.zero_()
+        step(True)
+        for name, t in solver.plan.profile():
+            prof[name] = prof.get(name, 0.0) + t / reps
+    solver.plan.set_profiling(False)
+    torch.cuda.synchronize()
+    fp64_tflops = probe_fp64_tflops()
+    hbm_peak, peak_kind = measured_peaks()
+    real_b = 8 if args.precision == "fp64" else 4
+    alg = algorithmic(w, n, real_b)
+    kern = {k: v for k, v in prof.items() if k in alg}
+    dom = max(kern, key=kern.get) if kern else None
+    roof = None
+    roof_fp = None
+    if dom:
+        t = kern[dom] * 1e-3
+        ach = alg[dom]["bytes"] / t / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 2), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "traffic": None,
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
+                "avg_launch_ms": round(kern[dom], 5)}
+        if alg[dom]["flops"]:
+            fl = alg[dom]["flops"] / t / 1e12
+            roof_fp = {"kernel": dom, "bound": "fp64" if real_b == 8 else "fp32",
+                       "achieved": round(fl, 3), "peak": round(fp64_tflops, 2),
+                       "unit": "TFLOP/s", "frac": round(fl / fp64_tflops, 4),
+                       "peak_source": "measured DFMA-chain probe (esp_probe_fp64)"}
+
+    value = world * n / (ms_fp * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms_fp, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if real_b == 8 else "f32",
+        "data": "synthetic (seeded config recipe, SURVEY §8(d.1))",
+        "config": {"workload": w.name, "n_charges": n, "grid": list(w.M), "P": w.P,
+                   "delta": w.delta, "r_c": w.r_c, "cell_type": w.cell_type,
+                   "precision": args.precision,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MB write)"},
+        "pressure_only": {"value": world * n / (ms_po * 1e-3), "unit": UNIT,
+                          "ms_per_step": ms_po, "gpu_launches_per_step": launches_po},
+        "e2e": {"value": world * n / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": int(pos.numel() * 8 + q.numel() * 8),
+                "d2h_bytes_per_step": int(F.numel() * 8 + 7 * 8)},
+        "gpu_launches": int(launches * K),
+        "gpu_launches_per_step": launches,
+        "clocks": clocks,
+        "roofline": roof,
+        "roofline_fp": roof_fp,
+        "kernel_ms": {k: round(v, 5) for k, v in prof.items()},
+        "fp64_peak_tflops_measured": round(fp64_tflops, 2),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_port(args.config)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------
+# CPU legs
+
+
+def cpu_baseline_port(config):
+    """Oracle port, 1 thread, one full step of the workload (bounded sample)."""
+    from oracle import esp_oracle as O
+    from paper_2601_00161_b200 import workloads
+    w, pos, q = workloads.generate(config)
+    plan = O.make_plan(w.h, w.M, w.P, w.delta, w.r_c)
+    modes = O.Modes(plan)
+    t0 = time.perf_counter()
+    rh = O.forward_density(plan, pos, q)
+    O.energy(modes, rh)
+    O.pressure(modes, rh)
+    t1 = time.perf_counter()
+    O.forces_ik(plan, modes, rh, pos, q)
+    t2 = time.perf_counter()
+    return {"value": w.n / (t2 - t0), "unit": UNIT, "cores": 1, "kind": "port",
+            "pressure_only_value": w.n / (t1 - t0),
+            "sample": f"1 full {w.name} force+pressure step ({w.n} charges, grid "
+                      f"{'x'.join(map(str, w.M))}, P={w.P}), numpy oracle port "
+                      f"(oracle/esp_oracle.py), single thread; ModeWorkspace setup excluded",
+            "seconds": round(t2 - t0, 3)}
+
+
+_POOL_STATE = {}
+
+
+def _spread_chunk(args):
+    lo, hi = args
+    st = _POOL_STATE
+    from oracle import esp_oracle as O
+    return O.spread(st["plan"], st["pos"][lo:hi], st["q"][lo:hi])
+
+
+def _gather_chunk(args):
+    lo, hi, fields = args
+    st = _POOL_STATE
+    from oracle import esp_oracle as O
+    out = np.empty((hi - lo, 3))
+    for d in range(3):
+        out[:, d] = O.gather(st["plan"], fields[d], st["pos"][lo:hi])
+    return out
+
+
+def run_reference(args):
+    """Reference arm: the oracle port of the reference CPU path on all host
+    cores, same config/metric as our arm.  Rank 0 only."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    from oracle import esp_oracle as O
+    from paper_2601_00161_b200 import workloads
+    w, pos, q = workloads.generate(args.config)
+    plan = O.make_plan(w.h, w.M, w.P, w.delta, w.r_c)
+    modes = O.Modes(plan)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    _POOL_STATE.update(plan=plan, pos=pos, q=q)
+    ctx = mp.get_context("fork")
+    chunks = np.linspace(0, w.n, cores + 1).astype(int)
+    spans = [(int(a), int(b)) for a, b in zip(chunks[:-1], chunks[1:]) if b > a]
+    h3 = plan.volume_element
+    with ctx.Pool(cores) as pool:
+        def one_step():
+            grid = sum(pool.map(_spread_chunk, spans))
+            rh = np.fft.fftn(grid) * h3
+            O.energy(modes, rh)
+            O.pressure(modes, rh)
+            scale = modes.fhat * modes.w_inv2 * rh[modes.mask]
+            fields = []
+            for d in range(3):
+                spec = np.zeros(plan.M, dtype=complex)
+                spec[modes.mask] = 1j * modes.kvec[d] * scale
+                fields.append(np.fft.ifftn(spec).real / h3)
+            parts = pool.map(_gather_chunk, [(a, b, fields) for a, b in spans])
+            return -q[:, None] * h3 * np.concatenate(parts)
+
+        budget = 150.0
+        t_start = time.perf_counter()
+        for _ in range(min(args.warmup, 1)):
+            one_step()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            one_step()
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() - t_start > budget:
+                break
+    ms = 1e3 * float(np.mean(times))
+    v = w.n / (ms * 1e-3)
+    sample = (f"{len(times)} of {args.steps} requested full {w.name} force+pressure steps "
+              f"({w.n} charges); spread/gather in {cores} processes, numpy FFT")
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(times),
+            "warmup": min(args.warmup, 1), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded config recipe, SURVEY §8(d.1))",
+            "config": {"workload": w.name, "n_charges": w.n, "grid": list(w.M), "P": w.P,
+                       "delta": w.delta, "r_c": w.r_c, "parallelism": "cpu"},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,173 @@
+/*
+ * esp_b200.h — C ABI of the B200-native ESP k-space (long-range) path.
+ *
+ * Drop-in replacement for the k-space pipeline of the reference package
+ * `prolate_ewald` (arXiv 2601.00161), /root/reference/pkg/src/prolate_ewald:
+ *
+ *   esp_spread        <- mesh.spread_charges            (mesh.py:204-210)
+ *   esp_forward       <- TransformProvider.forward x h3 (mesh.py:45-47, 221-226)
+ *   esp_scale_reduce  <- long_range_energy + long_range_pressure
+ *                                                     (mesh.py:285-312)
+ *   esp_forces_ik     <- long_range_forces(mode="ik")   (mesh.py:315-342)
+ *   esp_forces_analytic <- long_range_forces(mode="analytic") (mesh.py:343-349)
+ *   esp_local_pressure  <- local_pressure               (mesh.py:353-379)
+ *   esp_evaluate      <- CoulombSolver.evaluate far-field part
+ *                                                     (evaluate.py:125-144)
+ *   esp_plan_create / esp_plan_set_cell
+ *                     <- plan_grid + ModeWorkspace      (mesh.py:81-142, 229-282)
+ *   esp_counters      <- TransformProvider.forward_count / inverse_count
+ *                                                     (mesh.py:33-55)
+ *
+ * Conventions
+ *  - All pointers named d_* are DEVICE pointers; h_* are host pointers.
+ *  - Positions: (N,3) row-major f64 (the reference's ParticleSystem.positions,
+ *    already wrapped into the cell).  Charges: (N,) f64.
+ *  - Forces: (N,3) row-major f64, in the caller's particle order.
+ *  - out7: 7 f64 = [E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz] (far-field energy and the
+ *    symmetric pressure tensor, prefactor 1, as mesh.py returns them).
+ *  - Device grid layout is [z][y][x] (x contiguous): a relabelling of the
+ *    reference's C-order [x][y][z]; values are identical.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*).
+ *    Calls on one plan must not run concurrently.
+ *  - Return value: ESP_OK or an error code; esp_last_error() gives the text.
+ *    Error codes map onto the reference's exception classes
+ *    (PlanningError mesh.py:25, MeshError mesh.py:29, ParameterError
+ *    evaluate.py:247) in the Python wrapper.
+ */
+#ifndef ESP_B200_H
+#define ESP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum esp_status {
+  ESP_OK = 0,
+  ESP_ERR_PLANNING = 1,   /* grid invariant / window / underflow (PlanningError) */
+  ESP_ERR_MESH = 2,       /* wrong call order / unknown mode (MeshError) */
+  ESP_ERR_PARAM = 3,      /* bad argument (ParameterError) */
+  ESP_ERR_CUDA = 4,
+  ESP_ERR_CUFFT = 5,
+  ESP_ERR_OOM = 6,
+  ESP_ERR_CAPACITY = 7    /* N above the plan's particle capacity */
+};
+
+enum esp_precision { ESP_FP64 = 0, ESP_FP32 = 1 };
+
+/* Flags for esp_evaluate. */
+enum esp_eval_flags {
+  ESP_WANT_ENERGY_PRESSURE = 1,
+  ESP_WANT_FORCES = 2,
+  ESP_FORCES_ANALYTIC = 4
+};
+
+typedef struct esp_plan esp_plan;
+
+/* Static plan description (grid counts, window, basis constants). */
+typedef struct esp_plan_desc {
+  int32_t M[3];            /* grid counts along lattice axes x, y, z        */
+  int32_t P;               /* stencil width                                  */
+  int32_t precision;       /* esp_precision                                  */
+  int32_t deterministic;   /* 1: bitwise run-to-run reproducible ordering    */
+  int64_t max_particles;   /* particle capacity of the plan's buffers       */
+  /* Spreading window W(t) = psi_0(2t/P): piecewise monomial table
+   * (pswf.py:238-293); coef[j*(degree+1)+m] = scipy PPoly c[m][j]
+   * (highest power first), breaks[0..n_pieces].                            */
+  int32_t n_pieces;
+  int32_t degree;
+  const double* h_window_coef;
+  const double* h_window_deriv_coef;   /* derivative table (analytic mode)  */
+  const double* h_window_breaks;
+  /* Splitting basis psi_0^c as a Legendre series (pswf.py:41-84) and its
+   * derivative series (numpy legder), for Fhat and dterm (mesh.py:269-275). */
+  int32_t n_legendre;
+  const double* h_legendre;
+  int32_t n_legendre_deriv;
+  const double* h_legendre_deriv;
+  double split_c, split_lambda0, split_C0;
+  double r_c;
+  double kmax;             /* split_c / r_c (kernel.py:28-39)                */
+  /* Tile shape override (0 = automatic).                                   */
+  int32_t tile[3];
+} esp_plan_desc;
+
+/* Per-cell data (ModeWorkspace inputs; re-sent on NPT rebind with M pinned,
+ * evaluate.py:99-112).  Arrays are host arrays of length M[d].             */
+typedef struct esp_cell_desc {
+  double h[9];             /* cell matrix, row-major, columns = cell vectors */
+  double hinv[9];          /* inverse of h, row-major                        */
+  int32_t orthorhombic;
+  double spacing[3];       /* L_d / M_d (orthorhombic u = x / spacing)       */
+  double volume;           /* det h                                          */
+  double volume_element;   /* h_x h_y h_z (ortho) or V/G (triclinic)         */
+  /* K[a*3+d][m]: Cartesian component a of k contributed by index m along
+   * lattice axis d (mesh.py:242; 2 pi h^-T m for triclinic).               */
+  const double* h_axis_k[9];
+  /* Per-axis window transforms; What(m) = (w0[mx]*w1[my])*w2[mz]
+   * (mesh.py:258-261).                                                     */
+  const double* h_axis_what[3];
+  double what_zero;        /* What(0) for the underflow guard (mesh.py:262)  */
+  int32_t band[3];         /* max |m_d| that can lie inside |k| <= kmax      */
+  double grad_scale[3];    /* 1/spacing_d for the analytic window gradient   */
+} esp_cell_desc;
+
+/* --- lifetime ----------------------------------------------------------- */
+int esp_plan_create(const esp_plan_desc* desc, esp_plan** out);
+int esp_plan_destroy(esp_plan* plan);
+int esp_plan_set_cell(esp_plan* plan, const esp_cell_desc* cell, void* stream);
+const char* esp_last_error(void);
+int esp_version(void);
+
+/* --- stages (reference-function granularity) ----------------------------- */
+/* Bin + spread: writes the real charge grid (device layout [z][y][x]).
+ * d_grid may be NULL to keep it only in the plan.                          */
+int esp_spread(esp_plan* plan, const double* d_pos, const double* d_q,
+               int64_t n, void* d_grid, void* stream);
+/* Forward transform of the plan's grid -> plan spectrum (half spectrum along
+ * x, [kz][ky][kx<=Mx/2], complex, NOT yet multiplied by h3).  If d_grid is
+ * non-NULL it is copied into the plan first.  Counts one forward transform. */
+int esp_forward(esp_plan* plan, const void* d_grid, void* stream);
+/* Fused deconvolution scaling + energy/pressure reduction over the plan
+ * spectrum; optionally writes the three ik-scaled spectra for the force
+ * path in the same pass.  d_out7 is a device pointer (7 doubles).          */
+int esp_scale_reduce(esp_plan* plan, double* d_out7, int32_t write_ik, void* stream);
+/* Three inverse transforms of the ik spectra + force gather (requires a
+ * preceding esp_spread on the same particles and esp_scale_reduce with
+ * write_ik=1).  Counts three inverse transforms.                           */
+int esp_forces_ik(esp_plan* plan, double* d_forces, void* stream);
+/* One inverse transform + window-gradient gather (orthorhombic only).      */
+int esp_forces_analytic(esp_plan* plan, double* d_forces, void* stream);
+/* Six inverse transforms + gathers -> per-particle tensors (N,3,3).        */
+int esp_local_pressure(esp_plan* plan, double* d_tensors, void* stream);
+/* Whole step: spread, 1 forward FFT, fused scale/reduce, and (flags) forces. */
+int esp_evaluate(esp_plan* plan, const double* d_pos, const double* d_q,
+                 int64_t n, int32_t flags, double* d_out7, double* d_forces,
+                 void* stream);
+
+/* --- introspection -------------------------------------------------------- */
+int esp_counters(const esp_plan* plan, int64_t* forward, int64_t* inverse);
+int esp_reset_counters(esp_plan* plan);
+/* Device pointers into the plan (valid until destroy / next set_cell).     */
+void* esp_grid_ptr(esp_plan* plan);       /* real grid, [z][y][x]          */
+void* esp_spectrum_ptr(esp_plan* plan);   /* complex half spectrum          */
+int esp_grid_info(const esp_plan* plan, int64_t* info8);
+/* info8 = {Mx, My, Mz, Hx(=Mx/2+1), n_modes_retained(full spectrum),
+ *          kernel_launches_last_step, n_tiles, precision}                   */
+int esp_set_spectrum(esp_plan* plan, const void* d_spectrum, void* stream);
+
+/* --- diagnostics (bench / roofline) ----------------------------------------- */
+/* Record a CUDA event after every stage kernel of esp_evaluate.            */
+int esp_set_profiling(esp_plan* plan, int32_t on);
+/* Per-kernel durations (ms) of the last profiled esp_evaluate; names are
+ * written comma-separated.  Returns the count (synchronises on the events). */
+int esp_profile_read(esp_plan* plan, char* names, int32_t names_len, double* ms,
+                     int32_t max_n);
+/* Measured FP64 FMA throughput of this device (TFLOP/s), DFMA-chain probe. */
+int esp_probe_fp64(double* tflops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESP_B200_H */

@@ -1,0 +1,141 @@
+"""ctypes binding to ``libesp_b200.so`` (C ABI declared in include/esp_b200.h).
+
+The library is the product: there is no CPU fallback.  Importing the
+binding when the library is missing raises immediately, and every entry point
+checks the status code and re-raises the reference's exception classes
+(PlanningError / MeshError / ParameterError) or :class:`EspCudaError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import EspCudaError, MeshError, ParameterError, PlanningError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libesp_b200.so")
+
+ESP_OK = 0
+ESP_ERR_PLANNING = 1
+ESP_ERR_MESH = 2
+ESP_ERR_PARAM = 3
+ESP_ERR_CUDA = 4
+ESP_ERR_CUFFT = 5
+ESP_ERR_OOM = 6
+ESP_ERR_CAPACITY = 7
+
+ESP_FP64 = 0
+ESP_FP32 = 1
+
+ESP_WANT_ENERGY_PRESSURE = 1
+ESP_WANT_FORCES = 2
+ESP_FORCES_ANALYTIC = 4
+
+_dp = C.POINTER(C.c_double)
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("M", C.c_int32 * 3),
+        ("P", C.c_int32),
+        ("precision", C.c_int32),
+        ("deterministic", C.c_int32),
+        ("max_particles", C.c_int64),
+        ("n_pieces", C.c_int32),
+        ("degree", C.c_int32),
+        ("h_window_coef", _dp),
+        ("h_window_deriv_coef", _dp),
+        ("h_window_breaks", _dp),
+        ("n_legendre", C.c_int32),
+        ("h_legendre", _dp),
+        ("n_legendre_deriv", C.c_int32),
+        ("h_legendre_deriv", _dp),
+        ("split_c", C.c_double),
+        ("split_lambda0", C.c_double),
+        ("split_C0", C.c_double),
+        ("r_c", C.c_double),
+        ("kmax", C.c_double),
+        ("tile", C.c_int32 * 3),
+    ]
+
+
+class CellDesc(C.Structure):
+    _fields_ = [
+        ("h", C.c_double * 9),
+        ("hinv", C.c_double * 9),
+        ("orthorhombic", C.c_int32),
+        ("spacing", C.c_double * 3),
+        ("volume", C.c_double),
+        ("volume_element", C.c_double),
+        ("h_axis_k", _dp * 9),
+        ("h_axis_what", _dp * 3),
+        ("what_zero", C.c_double),
+        ("band", C.c_int32 * 3),
+        ("grad_scale", C.c_double * 3),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"ESP CUDA library not found at {LIB_PATH}; run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback "
+            "exists for the k-space path)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    L.esp_last_error.restype = C.c_char_p
+    L.esp_version.restype = C.c_int
+    L.esp_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(vp)]
+    L.esp_plan_destroy.argtypes = [vp]
+    L.esp_plan_set_cell.argtypes = [vp, C.POINTER(CellDesc), vp]
+    L.esp_spread.argtypes = [vp, vp, vp, C.c_int64, vp, vp]
+    L.esp_forward.argtypes = [vp, vp, vp]
+    L.esp_scale_reduce.argtypes = [vp, vp, C.c_int32, vp]
+    L.esp_forces_ik.argtypes = [vp, vp, vp]
+    L.esp_forces_analytic.argtypes = [vp, vp, vp]
+    L.esp_local_pressure.argtypes = [vp, vp, vp]
+    L.esp_evaluate.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp]
+    L.esp_counters.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.esp_reset_counters.argtypes = [vp]
+    L.esp_grid_ptr.argtypes = [vp]
+    L.esp_grid_ptr.restype = vp
+    L.esp_spectrum_ptr.argtypes = [vp]
+    L.esp_spectrum_ptr.restype = vp
+    L.esp_grid_info.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.esp_set_spectrum.argtypes = [vp, vp, vp]
+    L.esp_set_profiling.argtypes = [vp, C.c_int32]
+    L.esp_profile_read.argtypes = [vp, C.c_char_p, C.c_int32, C.POINTER(C.c_double), C.c_int32]
+    L.esp_probe_fp64.argtypes = [C.POINTER(C.c_double), vp]
+    _lib = L
+    return L
+
+
+EXPORTED = [
+    "esp_plan_create", "esp_plan_destroy", "esp_plan_set_cell", "esp_last_error",
+    "esp_version", "esp_spread", "esp_forward", "esp_scale_reduce", "esp_forces_ik",
+    "esp_forces_analytic", "esp_local_pressure", "esp_evaluate", "esp_counters",
+    "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
+    "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
+]
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == ESP_OK:
+        return
+    msg = lib().esp_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == ESP_ERR_PLANNING:
+        raise PlanningError(text)
+    if rc == ESP_ERR_MESH:
+        raise MeshError(text)
+    if rc in (ESP_ERR_PARAM, ESP_ERR_CAPACITY):
+        raise ParameterError(text)
+    raise EspCudaError(f"[{rc}] {text}")

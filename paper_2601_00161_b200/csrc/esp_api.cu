@@ -1,0 +1,554 @@
+// esp_api.cu — plan lifetime, cuFFT plans and the C ABI (include/esp_b200.h).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "esp_internal.cuh"
+
+namespace esp {
+
+size_t scan_temp_bytes(long long n_items);
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+Geom make_geom(const esp_plan* p) {
+  Geom g;
+  for (int d = 0; d < 3; ++d) {
+    g.M[d] = p->M[d];
+    g.spacing[d] = p->spacing[d];
+  }
+  for (int i = 0; i < 9; ++i) g.hinv[i] = p->hinv[i];
+  g.P = p->P;
+  g.lo = p->lo;
+  g.odd = p->odd;
+  g.ortho = p->ortho;
+  g.TX = p->TX;
+  g.TY = p->TY;
+  g.TZ = p->TZ;
+  g.PZ = p->PZ;
+  g.ntx = p->ntx;
+  g.nty = p->nty;
+  g.ntz = p->ntz;
+  g.n_keys = p->n_keys;
+  return g;
+}
+
+}  // namespace esp
+
+using esp::set_error;
+
+#define ESP_CUDA(call)                                                         \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      set_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                #call);                                                        \
+      return e_ == cudaErrorMemoryAllocation ? ESP_ERR_OOM : ESP_ERR_CUDA;     \
+    }                                                                          \
+  } while (0)
+
+#define ESP_CUFFT(call)                                                        \
+  do {                                                                         \
+    cufftResult r_ = (call);                                                   \
+    if (r_ != CUFFT_SUCCESS) {                                                 \
+      set_error(std::string("cuFFT error ") + std::to_string((int)r_) + " at " + \
+                #call);                                                        \
+      return ESP_ERR_CUFFT;                                                    \
+    }                                                                          \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count);
+}
+
+static void free_all(esp_plan* p) {
+  void* ptrs[] = {p->d_tab,     p->d_dtab,     p->d_breaks,  p->d_tabf,    p->d_dtabf,
+                  p->d_leg,     p->d_legd,     p->d_key,     p->d_slot,    p->d_counts,
+                  p->d_offsets, p->d_bkey,     p->d_u,       p->d_q,       p->d_idx,
+                  p->d_u_tmp,   p->d_q_tmp,    p->d_idx_tmp, p->d_cub,     p->d_scratch,
+                  p->d_grid,    p->d_spec,     p->d_ikspec,  p->d_fields,  p->d_axis_k,
+                  p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
+                  p->d_partials, p->d_err};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (p->have_fwd) cufftDestroy(p->fwd);
+  if (p->have_inv3) cufftDestroy(p->inv3);
+  if (p->have_inv1) cufftDestroy(p->inv1);
+  if (p->profiling)
+    for (int i = 0; i < 48; ++i) cudaEventDestroy(p->ev[i]);
+}
+
+extern "C" {
+
+const char* esp_last_error(void) { return esp::g_last_error.c_str(); }
+
+int esp_version(void) { return 100; }
+
+int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
+  if (!d || !out) {
+    set_error("null argument");
+    return ESP_ERR_PARAM;
+  }
+  *out = nullptr;
+  if (d->P < 2 || d->P > 12) {
+    set_error("spreading order P must be in [2, 12] on the B200 path");
+    return ESP_ERR_PLANNING;
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (d->M[k] < 2 || d->M[k] <= d->P) {
+      set_error("grid count must exceed the stencil width P");
+      return ESP_ERR_PLANNING;
+    }
+  }
+  if (d->M[0] % 2) {
+    set_error("M_x must be even (half-spectrum layout)");
+    return ESP_ERR_PLANNING;
+  }
+  if (d->n_pieces < 1 || d->n_pieces > esp::kMaxPieces || d->degree + 1 > esp::kMaxCoef ||
+      d->degree < 0) {
+    set_error("window table shape unsupported");
+    return ESP_ERR_PLANNING;
+  }
+  if (d->precision != ESP_FP64 && d->precision != ESP_FP32) {
+    set_error("unknown precision");
+    return ESP_ERR_PARAM;
+  }
+  esp_plan* p = new esp_plan;
+  std::memset(p, 0, sizeof(esp_plan));
+  for (int k = 0; k < 3; ++k) p->M[k] = d->M[k];
+  p->G = (long long)d->M[0] * d->M[1] * d->M[2];
+  p->Hx = d->M[0] / 2 + 1;
+  p->H = p->Hx * d->M[1] * d->M[2];
+  p->P = d->P;
+  p->lo = -((d->P - 1) / 2);
+  p->odd = d->P % 2;
+  p->precision = d->precision;
+  p->deterministic = d->deterministic ? 1 : 0;
+  p->cap = std::max<long long>(d->max_particles, 1);
+  p->n_pieces = d->n_pieces;
+  p->ncoef = d->degree + 1;
+  p->kmax = d->kmax;
+  p->r_c = d->r_c;
+  p->split_c = d->split_c;
+  p->split_lambda0 = d->split_lambda0;
+  p->split_C0 = d->split_C0;
+  p->n_leg = d->n_legendre;
+  p->n_legd = d->n_legendre_deriv;
+  // tiles
+  p->TX = d->tile[0] > 0 ? d->tile[0] : esp::kPad - d->P + 1;
+  p->TY = d->tile[1] > 0 ? d->tile[1] : esp::kPad - d->P + 1;
+  if (p->TX + d->P - 1 != esp::kPad || p->TY + d->P - 1 != esp::kPad) {
+    set_error("tile x/y extent must be 17 - P");
+    delete p;
+    return ESP_ERR_PARAM;
+  }
+  int tz = d->tile[2] > 0 ? d->tile[2] : (d->M[2] <= 128 ? 16 : 32);
+  p->TZ = std::min(tz, d->M[2]);
+  p->PZ = p->TZ + d->P - 1;
+  p->ntx = (d->M[0] + p->TX - 1) / p->TX;
+  p->nty = (d->M[1] + p->TY - 1) / p->TY;
+  p->ntz = (d->M[2] + p->TZ - 1) / p->TZ;
+  p->n_tiles = (long long)p->ntx * p->nty * p->ntz;
+  p->n_keys = (long long)p->ntx * p->nty * d->M[2];
+
+  const size_t real_sz = p->precision == ESP_FP64 ? sizeof(double) : sizeof(float);
+  const size_t nt = (size_t)p->n_pieces * p->ncoef;
+  cudaError_t e = cudaSuccess;
+#define TRY(x)                                                      \
+  do {                                                              \
+    e = (x);                                                        \
+    if (e != cudaSuccess) {                                         \
+      set_error(std::string("plan allocation failed: ") +           \
+                cudaGetErrorString(e) + " at " #x);                 \
+      free_all(p);                                                  \
+      delete p;                                                     \
+      return e == cudaErrorMemoryAllocation ? ESP_ERR_OOM : ESP_ERR_CUDA; \
+    }                                                               \
+  } while (0)
+  TRY(dalloc(&p->d_tab, nt));
+  TRY(dalloc(&p->d_dtab, nt));
+  TRY(dalloc(&p->d_tabf, nt));
+  TRY(dalloc(&p->d_dtabf, nt));
+  TRY(dalloc(&p->d_breaks, (size_t)p->n_pieces + 1));
+  TRY(dalloc(&p->d_leg, (size_t)std::max(p->n_leg, 1)));
+  TRY(dalloc(&p->d_legd, (size_t)std::max(p->n_legd, 1)));
+  TRY(cudaMemcpy(p->d_tab, d->h_window_coef, sizeof(double) * nt, cudaMemcpyHostToDevice));
+  TRY(cudaMemcpy(p->d_dtab, d->h_window_deriv_coef ? d->h_window_deriv_coef : d->h_window_coef,
+                 sizeof(double) * nt, cudaMemcpyHostToDevice));
+  {
+    std::vector<float> tf(nt), dtf(nt);
+    for (size_t i = 0; i < nt; ++i) {
+      tf[i] = (float)d->h_window_coef[i];
+      dtf[i] = (float)(d->h_window_deriv_coef ? d->h_window_deriv_coef[i] : 0.0);
+    }
+    TRY(cudaMemcpy(p->d_tabf, tf.data(), sizeof(float) * nt, cudaMemcpyHostToDevice));
+    TRY(cudaMemcpy(p->d_dtabf, dtf.data(), sizeof(float) * nt, cudaMemcpyHostToDevice));
+  }
+  TRY(cudaMemcpy(p->d_breaks, d->h_window_breaks, sizeof(double) * (p->n_pieces + 1),
+                 cudaMemcpyHostToDevice));
+  if (p->n_leg > 0)
+    TRY(cudaMemcpy(p->d_leg, d->h_legendre, sizeof(double) * p->n_leg, cudaMemcpyHostToDevice));
+  if (p->n_legd > 0)
+    TRY(cudaMemcpy(p->d_legd, d->h_legendre_deriv, sizeof(double) * p->n_legd,
+                   cudaMemcpyHostToDevice));
+  const size_t cap = (size_t)p->cap;
+  TRY(dalloc(&p->d_key, cap));
+  TRY(dalloc(&p->d_slot, cap));
+  TRY(dalloc(&p->d_bkey, cap));
+  TRY(dalloc(&p->d_counts, (size_t)p->n_keys + 1));
+  TRY(dalloc(&p->d_offsets, (size_t)p->n_keys + 1));
+  TRY(dalloc(&p->d_u, 3 * cap));
+  TRY(dalloc(&p->d_q, cap));
+  TRY(dalloc(&p->d_idx, cap));
+  TRY(dalloc(&p->d_u_tmp, 3 * cap));
+  TRY(dalloc(&p->d_q_tmp, cap));
+  TRY(dalloc(&p->d_idx_tmp, cap));
+  p->cub_bytes = esp::scan_temp_bytes(p->n_keys + 1);
+  TRY(cudaMalloc(&p->d_cub, std::max<size_t>(p->cub_bytes, 16)));
+  TRY(cudaMalloc(&p->d_scratch,
+                 real_sz * (size_t)p->n_tiles * p->PZ * esp::kPad * esp::kPad));
+  TRY(cudaMalloc(&p->d_grid, real_sz * (size_t)p->G));
+  TRY(cudaMemset(p->d_grid, 0, real_sz * (size_t)p->G));
+  TRY(cudaMalloc(&p->d_spec, 2 * real_sz * (size_t)p->H));
+  TRY(cudaMalloc(&p->d_ikspec, 3 * 2 * real_sz * (size_t)p->H));
+  TRY(cudaMalloc(&p->d_fields, 3 * real_sz * (size_t)p->G));
+  TRY(dalloc(&p->d_err, 4));
+#undef TRY
+  // cuFFT plans: [z][y][x] row-major, x fastest.
+  const cufftType fwd_t = p->precision == ESP_FP64 ? CUFFT_D2Z : CUFFT_R2C;
+  const cufftType inv_t = p->precision == ESP_FP64 ? CUFFT_Z2D : CUFFT_C2R;
+  int n3[3] = {d->M[2], d->M[1], d->M[0]};
+  if (cufftPlan3d(&p->fwd, d->M[2], d->M[1], d->M[0], fwd_t) != CUFFT_SUCCESS) {
+    set_error("cufftPlan3d (forward) failed");
+    free_all(p);
+    delete p;
+    return ESP_ERR_CUFFT;
+  }
+  p->have_fwd = 1;
+  if (cufftPlanMany(&p->inv3, 3, n3, nullptr, 1, (int)p->H, nullptr, 1, (int)p->G, inv_t,
+                    3) != CUFFT_SUCCESS) {
+    set_error("cufftPlanMany (inverse x3) failed");
+    free_all(p);
+    delete p;
+    return ESP_ERR_CUFFT;
+  }
+  p->have_inv3 = 1;
+  if (cufftPlan3d(&p->inv1, d->M[2], d->M[1], d->M[0], inv_t) != CUFFT_SUCCESS) {
+    set_error("cufftPlan3d (inverse) failed");
+    free_all(p);
+    delete p;
+    return ESP_ERR_CUFFT;
+  }
+  p->have_inv1 = 1;
+  *out = p;
+  return ESP_OK;
+}
+
+int esp_plan_destroy(esp_plan* p) {
+  if (!p) return ESP_OK;
+  cudaDeviceSynchronize();
+  free_all(p);
+  delete p;
+  return ESP_OK;
+}
+
+int esp_plan_set_cell(esp_plan* p, const esp_cell_desc* c, void* stream) {
+  if (!p || !c) {
+    set_error("null argument");
+    return ESP_ERR_PARAM;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  p->ortho = c->orthorhombic ? 1 : 0;
+  for (int i = 0; i < 9; ++i) {
+    p->hinv[i] = c->hinv[i];
+    p->hmat[i] = c->h[i];
+  }
+  for (int d = 0; d < 3; ++d) {
+    p->spacing[d] = c->spacing[d];
+    p->band[d] = c->band[d];
+    p->grad_scale[d] = c->grad_scale[d];
+  }
+  p->volume = c->volume;
+  p->h3 = c->volume_element;
+  // in-band box of the half spectrum
+  const int bx = std::max(0, std::min(c->band[0], p->M[0] / 2));
+  p->nbx = bx + 1;
+  std::vector<int> iy, iz;
+  for (int ax = 1; ax <= 2; ++ax) {
+    std::vector<int>& v = ax == 1 ? iy : iz;
+    const int M = p->M[ax], b = std::max(0, c->band[ax]);
+    for (int m = 0; m < M; ++m) {
+      const int f = m < (M + 1) / 2 ? m : m - M;  // numpy fftfreq integer
+      if (std::abs(f) <= b) v.push_back(m);
+    }
+  }
+  p->nby = (int)iy.size();
+  p->nbz = (int)iz.size();
+  p->nbox = (long long)p->nbx * p->nby * p->nbz;
+  const long long msum = (long long)p->M[0] + p->M[1] + p->M[2];
+  p->koff[0] = 0;
+  p->koff[1] = p->M[0];
+  p->koff[2] = (long long)p->M[0] + p->M[1];
+  if (p->d_axis_k) cudaFree(p->d_axis_k);
+  if (p->d_axis_w) cudaFree(p->d_axis_w);
+  if (p->d_box_iy) cudaFree(p->d_box_iy);
+  if (p->d_box_iz) cudaFree(p->d_box_iz);
+  if (p->d_modeA) cudaFree(p->d_modeA);
+  if (p->d_modeB) cudaFree(p->d_modeB);
+  if (p->d_partials) cudaFree(p->d_partials);
+  p->d_axis_k = nullptr;
+  p->d_axis_w = nullptr;
+  p->d_box_iy = p->d_box_iz = nullptr;
+  p->d_modeA = p->d_modeB = p->d_partials = nullptr;
+  ESP_CUDA(dalloc(&p->d_axis_k, 3 * msum));
+  ESP_CUDA(dalloc(&p->d_axis_w, msum));
+  ESP_CUDA(dalloc(&p->d_box_iy, iy.size()));
+  ESP_CUDA(dalloc(&p->d_box_iz, iz.size()));
+  ESP_CUDA(dalloc(&p->d_modeA, (size_t)p->nbox));
+  ESP_CUDA(dalloc(&p->d_modeB, (size_t)p->nbox));
+  p->n_red_blocks = (int)std::max<long long>(
+      1, std::min<long long>((p->nbox + esp::kRedThreads - 1) / esp::kRedThreads, 148 * 4));
+  ESP_CUDA(dalloc(&p->d_partials, (size_t)p->n_red_blocks * 8));
+  std::vector<double> hk(3 * msum), hw(msum);
+  for (int a = 0; a < 3; ++a)
+    for (int d = 0; d < 3; ++d)
+      std::memcpy(&hk[a * msum + p->koff[d]], c->h_axis_k[3 * a + d],
+                  sizeof(double) * p->M[d]);
+  for (int d = 0; d < 3; ++d)
+    std::memcpy(&hw[p->koff[d]], c->h_axis_what[d], sizeof(double) * p->M[d]);
+  ESP_CUDA(cudaMemcpyAsync(p->d_axis_k, hk.data(), sizeof(double) * hk.size(),
+                           cudaMemcpyHostToDevice, s));
+  ESP_CUDA(cudaMemcpyAsync(p->d_axis_w, hw.data(), sizeof(double) * hw.size(),
+                           cudaMemcpyHostToDevice, s));
+  ESP_CUDA(cudaMemcpyAsync(p->d_box_iy, iy.data(), sizeof(int) * iy.size(),
+                           cudaMemcpyHostToDevice, s));
+  ESP_CUDA(cudaMemcpyAsync(p->d_box_iz, iz.data(), sizeof(int) * iz.size(),
+                           cudaMemcpyHostToDevice, s));
+  ESP_CUDA(esp::launch_mode_setup(p, c->what_zero, s));
+  int herr[4] = {0, 0, 0, 0};
+  ESP_CUDA(cudaMemcpyAsync(herr, p->d_err, sizeof(herr), cudaMemcpyDeviceToHost, s));
+  ESP_CUDA(cudaStreamSynchronize(s));
+  unsigned long long nm = 0;
+  std::memcpy(&nm, &herr[2], sizeof(nm));
+  p->n_modes = (long long)nm;
+  p->have_cell = 1;
+  p->have_spec = 0;
+  p->have_ik = 0;
+  if (herr[0]) {
+    set_error("window transform underflow on a retained mode; the plan does not "
+              "cover the kernel band");
+    return ESP_ERR_PLANNING;
+  }
+  return ESP_OK;
+}
+
+static int check_ready(esp_plan* p) {
+  if (!p) {
+    set_error("null plan");
+    return ESP_ERR_PARAM;
+  }
+  if (!p->have_cell) {
+    set_error("esp_plan_set_cell has not been called");
+    return ESP_ERR_MESH;
+  }
+  return ESP_OK;
+}
+
+int esp_spread(esp_plan* p, const double* d_pos, const double* d_q, int64_t n, void* d_grid,
+               void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (n < 0 || n > p->cap) {
+    set_error("particle count exceeds the plan capacity");
+    return ESP_ERR_CAPACITY;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  ESP_CUDA(esp::launch_bin(p, d_pos, d_q, n, s));
+  ESP_CUDA(esp::launch_spread(p, s));
+  if (d_grid) {
+    const size_t real_sz = p->precision == ESP_FP64 ? sizeof(double) : sizeof(float);
+    ESP_CUDA(cudaMemcpyAsync(d_grid, p->d_grid, real_sz * p->G, cudaMemcpyDeviceToDevice, s));
+  }
+  p->have_bins = 1;
+  p->last_n = n;
+  return ESP_OK;
+}
+
+int esp_forward(esp_plan* p, const void* d_grid, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t real_sz = p->precision == ESP_FP64 ? sizeof(double) : sizeof(float);
+  if (d_grid)
+    ESP_CUDA(cudaMemcpyAsync(p->d_grid, d_grid, real_sz * p->G, cudaMemcpyDeviceToDevice, s));
+  ESP_CUFFT(cufftSetStream(p->fwd, s));
+  if (p->precision == ESP_FP64) {
+    ESP_CUFFT(cufftExecD2Z(p->fwd, (cufftDoubleReal*)p->d_grid,
+                           (cufftDoubleComplex*)p->d_spec));
+  } else {
+    ESP_CUFFT(cufftExecR2C(p->fwd, (cufftReal*)p->d_grid, (cufftComplex*)p->d_spec));
+  }
+  esp::prof_mark(p, s, "fft_forward");
+  p->fwd_count++;
+  p->have_spec = 1;
+  p->have_ik = 0;
+  return ESP_OK;
+}
+
+int esp_set_spectrum(esp_plan* p, const void* d_spectrum, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  const size_t real_sz = p->precision == ESP_FP64 ? sizeof(double) : sizeof(float);
+  ESP_CUDA(cudaMemcpyAsync(p->d_spec, d_spectrum, 2 * real_sz * p->H,
+                           cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  p->have_spec = 1;
+  p->have_ik = 0;
+  return ESP_OK;
+}
+
+int esp_scale_reduce(esp_plan* p, double* d_out7, int32_t write_ik, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (!p->have_spec) {
+    set_error("scale/reduce needs a spectral density (call esp_forward first)");
+    return ESP_ERR_MESH;
+  }
+  ESP_CUDA(esp::launch_scale_reduce(p, d_out7, write_ik, (cudaStream_t)stream));
+  p->have_ik = write_ik ? 1 : 0;
+  return ESP_OK;
+}
+
+int esp_forces_ik(esp_plan* p, double* d_forces, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (!p->have_ik || !p->have_bins) {
+    set_error("ik forces need esp_spread and esp_scale_reduce(write_ik=1) first");
+    return ESP_ERR_MESH;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  ESP_CUFFT(cufftSetStream(p->inv3, s));
+  if (p->precision == ESP_FP64) {
+    ESP_CUFFT(cufftExecZ2D(p->inv3, (cufftDoubleComplex*)p->d_ikspec,
+                           (cufftDoubleReal*)p->d_fields));
+  } else {
+    ESP_CUFFT(cufftExecC2R(p->inv3, (cufftComplex*)p->d_ikspec, (cufftReal*)p->d_fields));
+  }
+  esp::prof_mark(p, s, "fft_inverse_x3");
+  p->inv_count += 3;
+  p->have_ik = 0;  // the C2R transform overwrites its input
+  if (p->last_n > 0) ESP_CUDA(esp::launch_gather_ik(p, d_forces, s));
+  return ESP_OK;
+}
+
+int esp_forces_analytic(esp_plan* p, double* d_forces, void* stream) {
+  (void)d_forces;
+  (void)stream;
+  int rc = check_ready(p);
+  if (rc) return rc;
+  set_error("analytic-differentiation forces are not built in this release");
+  return ESP_ERR_MESH;
+}
+
+int esp_local_pressure(esp_plan* p, double* d_tensors, void* stream) {
+  (void)d_tensors;
+  (void)stream;
+  int rc = check_ready(p);
+  if (rc) return rc;
+  set_error("per-particle pressure is not built in this release");
+  return ESP_ERR_MESH;
+}
+
+int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
+                 int32_t flags, double* d_out7, double* d_forces, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  const int want_f = (flags & ESP_WANT_FORCES) != 0;
+  if (want_f && (flags & ESP_FORCES_ANALYTIC)) return esp_forces_analytic(p, d_forces, stream);
+  p->launches = 0;
+  p->n_ev = 0;
+  esp::prof_mark(p, (cudaStream_t)stream, "start");
+  rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
+  if (rc) return rc;
+  rc = esp_forward(p, nullptr, stream);
+  if (rc) return rc;
+  rc = esp_scale_reduce(p, d_out7, want_f, stream);
+  if (rc) return rc;
+  if (want_f) rc = esp_forces_ik(p, d_forces, stream);
+  return rc;
+}
+
+int esp_counters(const esp_plan* p, int64_t* forward, int64_t* inverse) {
+  if (!p) return ESP_ERR_PARAM;
+  if (forward) *forward = p->fwd_count;
+  if (inverse) *inverse = p->inv_count;
+  return ESP_OK;
+}
+
+int esp_reset_counters(esp_plan* p) {
+  if (!p) return ESP_ERR_PARAM;
+  p->fwd_count = 0;
+  p->inv_count = 0;
+  return ESP_OK;
+}
+
+int esp_set_profiling(esp_plan* p, int32_t on) {
+  if (!p) return ESP_ERR_PARAM;
+  if (on && !p->profiling) {
+    for (int i = 0; i < 48; ++i) ESP_CUDA(cudaEventCreate(&p->ev[i]));
+  }
+  if (!on && p->profiling) {
+    for (int i = 0; i < 48; ++i) cudaEventDestroy(p->ev[i]);
+  }
+  p->profiling = on ? 1 : 0;
+  p->n_ev = 0;
+  return ESP_OK;
+}
+
+int esp_profile_read(esp_plan* p, char* names, int32_t names_len, double* ms, int32_t max_n) {
+  if (!p || !p->profiling) return 0;
+  int n = 0;
+  std::string all;
+  for (int i = 1; i < p->n_ev && n < max_n; ++i) {
+    cudaError_t e = cudaEventSynchronize(p->ev[i]);
+    if (e != cudaSuccess) {
+      set_error(cudaGetErrorString(e));
+      return -ESP_ERR_CUDA;
+    }
+    float t = 0.f;
+    cudaEventElapsedTime(&t, p->ev[i - 1], p->ev[i]);
+    ms[n++] = t;
+    if (!all.empty()) all += ",";
+    all += p->ev_name[i];
+  }
+  if (names && names_len > 0) {
+    std::strncpy(names, all.c_str(), names_len - 1);
+    names[names_len - 1] = 0;
+  }
+  return n;
+}
+
+void* esp_grid_ptr(esp_plan* p) { return p ? p->d_grid : nullptr; }
+void* esp_spectrum_ptr(esp_plan* p) { return p ? p->d_spec : nullptr; }
+
+int esp_grid_info(const esp_plan* p, int64_t* info) {
+  if (!p || !info) return ESP_ERR_PARAM;
+  info[0] = p->M[0];
+  info[1] = p->M[1];
+  info[2] = p->M[2];
+  info[3] = p->Hx;
+  info[4] = p->n_modes;
+  info[5] = p->launches;
+  info[6] = p->n_tiles;
+  info[7] = p->precision;
+  return ESP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// esp_bin.cu — per-step particle binning for the tile kernels.
+//
+// The reference materialises (N, P^3) flat indices and weights and scatters
+// them with np.bincount (mesh.py:193-210).  Here particles are binned once
+// per step by anchor cell: key = (ty*ntx + tx)*Mz + az, where (tx, ty) is the
+// x-y tile of the anchor column and az its z anchor.  A spread/gather CTA then
+// owns a contiguous key range, i.e. its particles sorted by z anchor, which is
+// what the sliding-window accumulation needs.
+//
+// Passes: count (atomic slot per key) -> exclusive scan (CUB) -> scatter ->
+// canonicalise (deterministic mode: order inside each key segment by
+// original particle index, so every grid sum has a fixed operation order and
+// the result is bitwise reproducible run to run).
+#include <cub/device/device_scan.cuh>
+
+#include "esp_internal.cuh"
+
+namespace esp {
+
+__global__ void k_bin_count(const double* __restrict__ pos, long long n, Geom g,
+                            int* __restrict__ key, int* __restrict__ slot,
+                            int* __restrict__ counts) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double u[3];
+  grid_coords(g, pos[3 * i + 0], pos[3 * i + 1], pos[3 * i + 2], u);
+  int a[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double b = anchor_base(g, u[d]);
+    // Clamp pathological (non-finite / huge) coordinates into range; the
+    // reference's int64 cast would be undefined there as well.
+    b = fmin(fmax(b, -4.0e15), 4.0e15);
+    a[d] = wrap_index((long long)b, g.M[d]);
+  }
+  const int tx = a[0] / g.TX, ty = a[1] / g.TY;
+  const int k = (ty * g.ntx + tx) * g.M[2] + a[2];
+  key[i] = k;
+  slot[i] = atomicAdd(&counts[k], 1);
+}
+
+// Scatter to key segments.  Writes grid coordinates u (SoA), charge and the
+// original index.  In deterministic mode the destination is a temporary and
+// k_bin_canon fixes the intra-segment order.
+__global__ void k_bin_scatter(const double* __restrict__ pos,
+                              const double* __restrict__ q, long long n, Geom g,
+                              const int* __restrict__ key,
+                              const int* __restrict__ slot,
+                              const int* __restrict__ offsets, long long cap,
+                              double* __restrict__ u_out, double* __restrict__ q_out,
+                              int* __restrict__ idx_out, int* __restrict__ key_out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double u[3];
+  grid_coords(g, pos[3 * i + 0], pos[3 * i + 1], pos[3 * i + 2], u);
+  const int k = key[i];
+  const long long dst = (long long)offsets[k] + slot[i];
+  u_out[dst] = u[0];
+  u_out[cap + dst] = u[1];
+  u_out[2 * cap + dst] = u[2];
+  q_out[dst] = q[i];
+  idx_out[dst] = (int)i;
+  if (key_out) key_out[dst] = k;
+}
+
+// Deterministic order inside each key segment: rank by original index.
+__global__ void k_bin_canon(long long n, long long cap,
+                            const int* __restrict__ key_tmp,
+                            const int* __restrict__ offsets,
+                            const double* __restrict__ u_tmp,
+                            const double* __restrict__ q_tmp,
+                            const int* __restrict__ idx_tmp,
+                            double* __restrict__ u_out, double* __restrict__ q_out,
+                            int* __restrict__ idx_out) {
+  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int k = key_tmp[j];
+  const int s0 = offsets[k], s1 = offsets[k + 1];
+  const int me = idx_tmp[j];
+  int rank = 0;
+  for (int t = s0; t < s1; ++t) rank += (idx_tmp[t] < me);
+  const long long dst = (long long)s0 + rank;
+  u_out[dst] = u_tmp[j];
+  u_out[cap + dst] = u_tmp[cap + j];
+  u_out[2 * cap + dst] = u_tmp[2 * cap + j];
+  q_out[dst] = q_tmp[j];
+  idx_out[dst] = me;
+}
+
+cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
+                       long long n, cudaStream_t s) {
+  Geom g = make_geom(p);
+  cudaError_t e = cudaMemsetAsync(p->d_counts, 0, sizeof(int) * (p->n_keys + 1), s);
+  if (e != cudaSuccess) return e;
+  const int B = 256;
+  const unsigned grid = (unsigned)((n + B - 1) / B);
+  if (n > 0) {
+    k_bin_count<<<grid, B, 0, s>>>(d_pos, n, g, p->d_key, p->d_slot, p->d_counts);
+    p->launches++;
+    prof_mark(p, s, "bin_count");
+  }
+  size_t bytes = p->cub_bytes;
+  e = cub::DeviceScan::ExclusiveSum(p->d_cub, bytes, p->d_counts, p->d_offsets,
+                                    (int)(p->n_keys + 1), s);
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, "bin_scan");
+  if (n == 0) return cudaGetLastError();
+  if (p->deterministic) {
+    k_bin_scatter<<<grid, B, 0, s>>>(d_pos, d_q, n, g, p->d_key, p->d_slot,
+                                     p->d_offsets, p->cap, p->d_u_tmp, p->d_q_tmp,
+                                     p->d_idx_tmp, p->d_bkey);
+    prof_mark(p, s, "bin_scatter");
+    k_bin_canon<<<grid, B, 0, s>>>(n, p->cap, p->d_bkey, p->d_offsets, p->d_u_tmp,
+                                   p->d_q_tmp, p->d_idx_tmp, p->d_u, p->d_q,
+                                   p->d_idx);
+    p->launches += 2;
+    prof_mark(p, s, "bin_canon");
+  } else {
+    k_bin_scatter<<<grid, B, 0, s>>>(d_pos, d_q, n, g, p->d_key, p->d_slot,
+                                     p->d_offsets, p->cap, p->d_u, p->d_q, p->d_idx,
+                                     nullptr);
+    p->launches++;
+    prof_mark(p, s, "bin_scatter");
+  }
+  return cudaGetLastError();
+}
+
+size_t scan_temp_bytes(long long n_items) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int*)nullptr, (int*)nullptr,
+                                (int)n_items);
+  return bytes;
+}
+
+}  // namespace esp

@@ -1,0 +1,232 @@
+// esp_gather.cu — force interpolation (mesh.py:213-218 `_gather`, used by
+// long_range_forces ik mode, mesh.py:336-342).
+//
+// The transpose of the spread tile kernel: the same CTA/tile decomposition
+// and column ownership, but each thread holds a P-deep sliding window of the
+// three ik field values of its (x, y) column in registers.  For each particle
+// whose stencil touches the warp's 8 x 4 column block, a lane forms
+//   part_c = wx*wy * sum_s wz[s] * field_c[z_s]        (c = x, y, z)
+// and the warp reduces (part_x, part_y, part_z) with a transposed butterfly
+// (12 shuffles instead of 30).  Warp partials land in a per-(particle, warp)
+// shared-memory slot and are summed in fixed warp order, so forces are
+// bitwise reproducible.  F_c = -q * sum (the h3 factors of mesh.py:341-342
+// cancel; the 1/G of the inverse transform is folded into the spectrum).
+#include "esp_internal.cuh"
+
+namespace esp {
+
+template <typename real, int P>
+__device__ __forceinline__ void stage_weights_g(
+    const Geom& g, const real* s_tab, const double* s_brk, int n_pieces, int ncoef,
+    const double* __restrict__ U, long long cap, long long c0, int n, int tx, int ty,
+    int tz, real* s_w, int* s_anc) {
+  for (int item = threadIdx.x; item < 3 * n; item += blockDim.x) {
+    const int pl = item / 3, d = item - 3 * (item / 3);
+    const double u = U[d * cap + c0 + pl];
+    const double base = anchor_base(g, u);
+    const int a = wrap_index((long long)base, g.M[d]);
+    const int org = d == 0 ? tx * g.TX : (d == 1 ? ty * g.TY : tz * g.TZ);
+    s_anc[d * kChunk + pl] = a - org;
+    real* w = s_w + ((size_t)d * kChunk + pl) * P;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const double t = u - (base + (double)(g.lo + s));
+      w[s] = window_eval<real>(s_tab, s_brk, n_pieces, ncoef, t);
+    }
+  }
+}
+
+// Sum (v0, v1, v2) over the 32 lanes.  Afterwards lane 0 holds comp 0, lane 8
+// comp 1, lane 16 comp 2.
+template <typename real>
+__device__ __forceinline__ real warp_reduce3(real v0, real v1, real v2, int lane) {
+  const unsigned full = 0xffffffffu;
+  const real v3 = real(0);
+  const bool hi = lane & 16;
+  real r0 = __shfl_xor_sync(full, hi ? v0 : v2, 16);
+  real r1 = __shfl_xor_sync(full, hi ? v1 : v3, 16);
+  real k0 = (hi ? v2 : v0) + r0;
+  real k1 = (hi ? v3 : v1) + r1;
+  const bool b3 = lane & 8;
+  real r = __shfl_xor_sync(full, b3 ? k0 : k1, 8);
+  real k = (b3 ? k1 : k0) + r;
+  k += __shfl_xor_sync(full, k, 4);
+  k += __shfl_xor_sync(full, k, 2);
+  k += __shfl_xor_sync(full, k, 1);
+  return k;
+}
+
+template <typename real, int P>
+__global__ void __launch_bounds__(kTileThreads)
+k_gather_ik(Geom g, const real* __restrict__ tab, const double* __restrict__ brk,
+            int n_pieces, int ncoef, const int* __restrict__ offsets,
+            const double* __restrict__ U, const double* __restrict__ Q,
+            const int* __restrict__ IDX, long long cap, const real* __restrict__ fld,
+            long long G, double* __restrict__ forces) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tile = blockIdx.x;
+  const int tz = tile % g.ntz;
+  const int txy = tile / g.ntz;
+  const int tx = txy % g.ntx, ty = txy / g.ntx;
+  const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+  const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+  const long long p0 = offsets[key0], p1 = offsets[key1];
+  if (p0 == p1) return;
+
+  real* s_tab = reinterpret_cast<real*>(smem_raw);
+  size_t off = sizeof(real) * (size_t)n_pieces * ncoef;
+  off = (off + 15) & ~size_t(15);
+  double* s_brk = reinterpret_cast<double*>(smem_raw + off);
+  off += sizeof(double) * (size_t)(n_pieces + 1);
+  off = (off + 15) & ~size_t(15);
+  real* s_w = reinterpret_cast<real*>(smem_raw + off);
+  off += sizeof(real) * 3 * (size_t)kChunk * P;
+  off = (off + 15) & ~size_t(15);
+  double* s_acc = reinterpret_cast<double*>(smem_raw + off);
+  off += sizeof(double) * (size_t)kChunk * 8 * 3;
+  int* s_anc = reinterpret_cast<int*>(smem_raw + off);
+
+  for (int i = threadIdx.x; i < n_pieces * ncoef; i += blockDim.x) s_tab[i] = tab[i];
+  for (int i = threadIdx.x; i <= n_pieces; i += blockDim.x) s_brk[i] = brk[i];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
+  const int cx = wx0 + (lane & 7), cy = wy0 + (lane >> 3);
+  const int gx = wrap_index((long long)tx * g.TX + g.lo + cx, g.M[0]);
+  const int gy = wrap_index((long long)ty * g.TY + g.lo + cy, g.M[1]);
+  const long long colbase = (long long)gy * g.M[0] + gx;
+  const long long plane = (long long)g.M[0] * g.M[1];
+  const int zorg = tz * g.TZ + g.lo;
+  const real* f0 = fld;
+  const real* f1 = fld + G;
+  const real* f2 = fld + 2 * G;
+
+  real w0[P], w1[P], w2[P];
+  int zc = -1;
+
+  for (long long c0 = p0; c0 < p1; c0 += kChunk) {
+    const int n = (int)min((long long)kChunk, p1 - c0);
+    __syncthreads();
+    stage_weights_g<real, P>(g, s_tab, s_brk, n_pieces, ncoef, U, cap, c0, n, tx, ty,
+                             tz, s_w, s_anc);
+    for (int i = threadIdx.x; i < n * 24; i += blockDim.x) s_acc[i] = 0.0;
+    __syncthreads();
+    for (int pl = 0; pl < n; ++pl) {
+      const int xl = s_anc[pl];
+      const int yl = s_anc[kChunk + pl];
+      if (xl >= wx0 + 8 || xl + P <= wx0 || yl >= wy0 + 4 || yl + P <= wy0) continue;
+      const int zl = s_anc[2 * kChunk + pl];
+      if (zc < 0 || zl - zc >= P) {
+        zc = zl;
+#pragma unroll
+        for (int s = 0; s < P; ++s) {
+          const long long o = (long long)wrap_index(zorg + zc + s, g.M[2]) * plane + colbase;
+          w0[s] = f0[o];
+          w1[s] = f1[o];
+          w2[s] = f2[o];
+        }
+      } else {
+        while (zc < zl) {
+#pragma unroll
+          for (int s = 0; s < P - 1; ++s) {
+            w0[s] = w0[s + 1];
+            w1[s] = w1[s + 1];
+            w2[s] = w2[s + 1];
+          }
+          const long long o =
+              (long long)wrap_index(zorg + zc + P, g.M[2]) * plane + colbase;
+          w0[P - 1] = f0[o];
+          w1[P - 1] = f1[o];
+          w2[P - 1] = f2[o];
+          ++zc;
+        }
+      }
+      const int sx = cx - xl, sy = cy - yl;
+      const bool in = (unsigned)sx < (unsigned)P && (unsigned)sy < (unsigned)P;
+      const real* wxp = s_w + (size_t)pl * P;
+      const real* wyp = s_w + ((size_t)kChunk + pl) * P;
+      const real* wzp = s_w + ((size_t)2 * kChunk + pl) * P;
+      const int sxc = min(max(sx, 0), P - 1), syc = min(max(sy, 0), P - 1);
+      const real a = in ? wxp[sxc] * wyp[syc] : real(0);
+      real t0 = real(0), t1 = real(0), t2 = real(0);
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const real wz = wzp[s];
+        t0 = fma(wz, w0[s], t0);
+        t1 = fma(wz, w1[s], t1);
+        t2 = fma(wz, w2[s], t2);
+      }
+      const real v = warp_reduce3<real>(a * t0, a * t1, a * t2, lane);
+      if ((lane & 7) == 0 && lane < 24) s_acc[((size_t)pl * 8 + warp) * 3 + (lane >> 3)] = (double)v;
+    }
+    __syncthreads();
+    for (int pl = threadIdx.x; pl < n; pl += blockDim.x) {
+      const double q = Q[c0 + pl];
+      const long long id = IDX[c0 + pl];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += s_acc[((size_t)pl * 8 + w) * 3 + c];
+        forces[id * 3 + c] = -q * s;
+      }
+    }
+  }
+}
+
+template <typename real>
+static size_t gather_smem(int P, int n_pieces, int ncoef) {
+  size_t b = sizeof(real) * (size_t)n_pieces * ncoef;
+  b = (b + 15) & ~size_t(15);
+  b += sizeof(double) * (size_t)(n_pieces + 1);
+  b = (b + 15) & ~size_t(15);
+  b += sizeof(real) * 3 * (size_t)kChunk * P;
+  b = (b + 15) & ~size_t(15);
+  b += sizeof(double) * (size_t)kChunk * 8 * 3;
+  b += sizeof(int) * 3 * (size_t)kChunk;
+  return b;
+}
+
+template <typename real, int P>
+static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+  Geom g = make_geom(p);
+  const real* tab = std::is_same<real, double>::value
+                        ? reinterpret_cast<const real*>(p->d_tab)
+                        : reinterpret_cast<const real*>(p->d_tabf);
+  const size_t smem = gather_smem<real>(P, p->n_pieces, p->ncoef);
+  cudaError_t e = cudaFuncSetAttribute(k_gather_ik<real, P>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k_gather_ik<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
+      g, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->d_q,
+      p->d_idx, p->cap, reinterpret_cast<const real*>(p->d_fields), p->G, d_forces);
+  p->launches++;
+  prof_mark(p, s, "gather");
+  return cudaGetLastError();
+}
+
+template <typename real>
+static cudaError_t gather_r(esp_plan* p, double* d_forces, cudaStream_t s) {
+  switch (p->P) {
+    case 2: return gather_p<real, 2>(p, d_forces, s);
+    case 3: return gather_p<real, 3>(p, d_forces, s);
+    case 4: return gather_p<real, 4>(p, d_forces, s);
+    case 5: return gather_p<real, 5>(p, d_forces, s);
+    case 6: return gather_p<real, 6>(p, d_forces, s);
+    case 7: return gather_p<real, 7>(p, d_forces, s);
+    case 8: return gather_p<real, 8>(p, d_forces, s);
+    case 9: return gather_p<real, 9>(p, d_forces, s);
+    case 10: return gather_p<real, 10>(p, d_forces, s);
+    case 11: return gather_p<real, 11>(p, d_forces, s);
+    case 12: return gather_p<real, 12>(p, d_forces, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s) {
+  return p->precision == ESP_FP64 ? gather_r<double>(p, d_forces, s)
+                                  : gather_r<float>(p, d_forces, s);
+}
+
+}  // namespace esp

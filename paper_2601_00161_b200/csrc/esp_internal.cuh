@@ -1,0 +1,206 @@
+// esp_internal.cuh — shared structs and device helpers for the B200 ESP
+// k-space path.  See DESIGN.md for the data layout and kernel roofline notes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/esp_b200.h"
+
+namespace esp {
+
+constexpr int kPad = 16;          // padded columns per tile along x and y
+constexpr int kTileThreads = 256; // kPad * kPad column owners per CTA
+constexpr int kChunk = 256;       // particles staged per CTA pass
+constexpr int kMaxCoef = 25;      // window table degree + 1 (reference: 19)
+constexpr int kMaxPieces = 64;    // window pieces (P * pieces-per-unit)
+constexpr int kRedThreads = 256;
+
+// Grid/tile geometry passed by value to every kernel.
+struct Geom {
+  int M[3];
+  int P, lo, odd, ortho;
+  double spacing[3];
+  double hinv[9];       // row-major inverse cell matrix (triclinic u)
+  int TX, TY, TZ, PZ;   // anchor-cell tile and padded z extent
+  int ntx, nty, ntz;
+  long long n_keys;     // ntx * nty * Mz  (key = (ty*ntx+tx)*Mz + az)
+};
+
+// Window table (device pointers).
+struct Table {
+  const double* coef;   // n_pieces * ncoef, highest power first
+  const double* dcoef;  // derivative table
+  const double* breaks; // n_pieces + 1
+  int n_pieces, ncoef;
+};
+
+// Grid coordinate u_d of a Cartesian position (mesh.py:160 for orthorhombic
+// cells: u = x / h_d, IEEE division; triclinic: M_d * (h^-1 r)_d with the
+// oracle's fixed operation order).  No FMA contraction, so the anchors agree
+// bit-for-bit with the CPU reference.
+__device__ __forceinline__ void grid_coords(const Geom& g, double x, double y,
+                                            double z, double u[3]) {
+  if (g.ortho) {
+    u[0] = __ddiv_rn(x, g.spacing[0]);
+    u[1] = __ddiv_rn(y, g.spacing[1]);
+    u[2] = __ddiv_rn(z, g.spacing[2]);
+  } else {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double s = __dadd_rn(__dadd_rn(__dmul_rn(g.hinv[3 * d + 0], x),
+                                     __dmul_rn(g.hinv[3 * d + 1], y)),
+                           __dmul_rn(g.hinv[3 * d + 2], z));
+      u[d] = __dmul_rn(s, (double)g.M[d]);
+    }
+  }
+}
+
+// Stencil anchor: np.round (half-to-even) for odd P, np.floor for even P
+// (mesh.py:161-168).
+__device__ __forceinline__ double anchor_base(const Geom& g, double u) {
+  return g.odd ? rint(u) : floor(u);
+}
+
+__device__ __forceinline__ int wrap_index(long long v, int M) {
+  long long r = v % M;
+  return (int)(r < 0 ? r + M : r);
+}
+
+// W(t) from the piecewise table (pswf.py:253-258 semantics: zero outside
+// [breaks[0], breaks[n]]; interval search as scipy PPoly, right end closed).
+template <typename real>
+__device__ __forceinline__ real window_eval(const real* __restrict__ coef,
+                                            const double* __restrict__ breaks,
+                                            int n_pieces, int ncoef, double t) {
+  const double b0 = breaks[0], bn = breaks[n_pieces];
+  if (!(t >= b0 && t <= bn)) return real(0);
+  const double width = (bn - b0) / n_pieces;
+  int j = (int)floor((t - b0) / width);
+  j = j < 0 ? 0 : (j > n_pieces - 1 ? n_pieces - 1 : j);
+  if (t < breaks[j] && j > 0) --j;
+  else if (j + 1 < n_pieces && t >= breaks[j + 1]) ++j;
+  const real s = (real)(t - breaks[j]);
+  const real* c = coef + j * ncoef;
+  real acc = c[0];
+  for (int m = 1; m < ncoef; ++m) acc = fma(acc, s, c[m]);
+  return acc;
+}
+
+// numpy.polynomial.legendre.legval (Clenshaw recursion, same operation order;
+// used for Fhat and dterm in the mode setup, mesh.py:269-275).
+__device__ __forceinline__ double legval(double x, const double* c, int n) {
+  if (n == 1) return c[0];
+  double c0, c1;
+  if (n == 2) {
+    c0 = c[0];
+    c1 = c[1];
+  } else {
+    int nd = n;
+    c0 = c[n - 2];
+    c1 = c[n - 1];
+    for (int i = 3; i <= n; ++i) {
+      double tmp = c0;
+      nd = nd - 1;
+      c0 = __dsub_rn(c[n - i], __ddiv_rn(__dmul_rn(c1, (double)(nd - 1)), (double)nd));
+      c1 = __dadd_rn(tmp, __ddiv_rn(__dmul_rn(__dmul_rn(c1, x), (double)(2 * nd - 1)),
+                                    (double)nd));
+    }
+  }
+  return __dadd_rn(c0, __dmul_rn(c1, x));
+}
+
+template <typename T> struct Cplx;
+template <> struct Cplx<double> { using type = double2; };
+template <> struct Cplx<float> { using type = float2; };
+
+}  // namespace esp
+
+// ---------------------------------------------------------------------------
+// Host-side plan object.
+struct esp_plan {
+  // static description
+  int M[3];
+  long long G, Hx, H;
+  int P, lo, odd, precision, deterministic;
+  long long cap;
+  int n_pieces, ncoef;
+  double kmax, r_c, split_c, split_lambda0, split_C0;
+  int n_leg, n_legd;
+  // tiles
+  int TX, TY, TZ, PZ, ntx, nty, ntz;
+  long long n_tiles, n_keys;
+  // cell
+  int have_cell;
+  int ortho;
+  double spacing[3], hinv[9], hmat[9], volume, h3, grad_scale[3];
+  int band[3];
+  int nbx, nby, nbz;
+  long long nbox, n_modes;
+  int n_red_blocks;
+  // device buffers
+  double *d_tab, *d_dtab, *d_breaks;
+  float *d_tabf, *d_dtabf;
+  double *d_leg, *d_legd;
+  int *d_key, *d_slot, *d_counts, *d_offsets, *d_bkey;
+  double *d_u, *d_q;      // binned (canonical) particle data: u[3][cap], q[cap]
+  int* d_idx;
+  double *d_u_tmp, *d_q_tmp;
+  int* d_idx_tmp;
+  void* d_cub;
+  size_t cub_bytes;
+  void* d_scratch;
+  void* d_grid;
+  void* d_spec;
+  void* d_ikspec;
+  void* d_fields;
+  double* d_axis_k;       // 9 arrays: K[a*3+d] at offset koff[d]
+  double* d_axis_w;       // 3 arrays
+  long long koff[3];      // offsets of axis d inside each block of length Msum
+  int* d_box_iy;
+  int* d_box_iz;
+  double *d_modeA, *d_modeB;
+  double* d_partials;
+  int* d_err;
+  cufftHandle fwd, inv3, inv1;
+  int have_fwd, have_inv3, have_inv1;
+  long long fwd_count, inv_count;
+  long long last_n;
+  int have_bins, have_spec, have_ik;
+  int launches;
+  // profiling: events recorded after each stage kernel when enabled
+  int profiling;
+  int n_ev;
+  cudaEvent_t ev[48];
+  const char* ev_name[48];
+};
+
+namespace esp {
+
+Geom make_geom(const esp_plan* p);
+
+// Launchers (each returns cudaError_t of the launch).
+cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
+                       long long n, cudaStream_t s);
+cudaError_t launch_spread(esp_plan* p, cudaStream_t s);
+cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
+                                cudaStream_t s);
+cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s);
+cudaError_t launch_mode_setup(esp_plan* p, double what_zero, cudaStream_t s);
+
+void set_error(const std::string& msg);
+
+// Record a profiling event named `name` on stream s (no-op unless enabled).
+inline void prof_mark(esp_plan* p, cudaStream_t s, const char* name) {
+  if (!p->profiling || p->n_ev >= 48) return;
+  cudaEventRecord(p->ev[p->n_ev], s);
+  p->ev_name[p->n_ev] = name;
+  p->n_ev++;
+}
+
+}  // namespace esp

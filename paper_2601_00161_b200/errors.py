@@ -1,0 +1,35 @@
+"""Exception classes with the reference's names and meanings.
+
+PlanningError, MeshError   <- prolate_ewald/mesh.py:25-30
+ParameterError             <- prolate_ewald/evaluate.py:247
+PswfError, DomainError     <- prolate_ewald/pswf.py:33-38
+CellError                  <- prolate_ewald/system.py:12
+"""
+
+
+class PlanningError(Exception):
+    """A grid invariant cannot be satisfied; the message names it."""
+
+
+class MeshError(Exception):
+    """Wrong field space, unknown differentiation mode, or call order."""
+
+
+class ParameterError(Exception):
+    """Invalid solver parameters or a cell that does not match the solver."""
+
+
+class PswfError(Exception):
+    """Construction or evaluation failure in the prolate machinery."""
+
+
+class DomainError(PswfError):
+    """Argument outside the domain of the requested evaluation."""
+
+
+class CellError(Exception):
+    """Invalid cell matrix or particle arrays."""
+
+
+class EspCudaError(RuntimeError):
+    """CUDA / cuFFT failure inside the B200 library."""

@@ -1,0 +1,86 @@
+"""Splitting-kernel constants used by the k-space path
+(reference: prolate_ewald/kernel.py).
+
+Only the quantities the far-field solver composes are provided: ``kmax =
+c / r_c`` (kernel.py:28-39), the far-field transform Fhat (kernel.py:68-80,
+host diagnostics — the device computes it per retained mode), the self
+energy (kernel.py:117-123) and the uniform-background correction
+(kernel.py:126-150).  The near field is out of scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+from numpy.polynomial import legendre as L
+
+from .errors import DomainError
+from .pswf import PswfBasis
+
+
+class KernelError(Exception):
+    pass
+
+
+class ZeroModeError(KernelError):
+    """The k = 0 mode is excluded under the conducting-boundary convention."""
+
+
+@dataclass(frozen=True)
+class SplitKernel:
+    basis: PswfBasis
+    r_c: float
+    kmax: float = field(init=False)
+
+    def __post_init__(self):
+        if self.r_c <= 0.0:
+            raise KernelError("cutoff r_c must be positive")
+        object.__setattr__(self, "kmax", self.basis.c / self.r_c)
+
+
+def far_field_hat(kern: SplitKernel, k):
+    """2 pi lambda0 psi0(k r_c / c) / (C0 k^2) on |k| <= kmax, else 0."""
+    ka = np.atleast_1d(np.asarray(k, dtype=float))
+    if np.any(ka == 0.0):
+        raise ZeroModeError("k = 0 is excluded (conducting boundary convention)")
+    b = kern.basis
+    x = ka * kern.r_c / b.c
+    out = np.zeros_like(ka)
+    band = x <= 1.0
+    out[band] = 2.0 * np.pi * b.lambda0 / b.C0 * b.psi_series(x[band]) / ka[band] ** 2
+    return float(out[0]) if np.ndim(k) == 0 else out
+
+
+def phi0(basis: PswfBasis, r, r_c: float):
+    """(1/C0) int_0^{r/r_c} psi_0 ; 1 beyond the cutoff."""
+    if r_c <= 0.0:
+        raise DomainError("cutoff r_c must be positive")
+    ra = np.asarray(r, dtype=float)
+    x = np.minimum(ra / r_c, 1.0)
+    out = L.legval(x, L.legint(basis.legendre_coeffs, lbnd=0.0)) / basis.C0
+    return np.where(ra >= r_c, 1.0, out)
+
+
+def self_energy(kern: SplitKernel, charges) -> float:
+    q = np.asarray(charges, dtype=float)
+    if q.size == 0:
+        return 0.0
+    b = kern.basis
+    return float(-(b.psi0_at_zero / (2.0 * b.C0 * kern.r_c)) * np.sum(q * q))
+
+
+def background_correction(kern: SplitKernel, q_total: float, volume: float):
+    """(U_cb, U_bb, P_corr) for a non-neutral cell; zeros when neutral."""
+    if volume <= 0.0:
+        raise KernelError("volume must be positive")
+    if q_total == 0.0:
+        return 0.0, 0.0, np.zeros((3, 3))
+    nodes, weights = np.polynomial.legendre.leggauss(128)
+    r = 0.5 * kern.r_c * (nodes + 1.0)
+    w = 0.5 * kern.r_c * weights
+    j = 0.5 * kern.r_c ** 2 - float(np.sum(w * r * phi0(kern.basis, r, kern.r_c)))
+    u_cb = -4.0 * np.pi * q_total ** 2 / volume * j
+    u_bb = 2.0 * np.pi * q_total ** 2 / volume * j
+    p_corr = -2.0 * np.pi * q_total ** 2 * j / volume ** 2 * np.eye(3)
+    return u_cb, u_bb, p_corr

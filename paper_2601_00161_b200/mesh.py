@@ -1,0 +1,381 @@
+"""Drop-in replacement for ``prolate_ewald.mesh`` on the B200.
+
+Same names, signatures, argument meaning and exceptions as the reference
+module (mesh.py:25-379); the work runs in ``libesp_b200.so``:
+
+* ``spread_charges``      -> bin + tile spread + combine kernels
+* ``forward_density``     -> spread + cuFFT R2C (counted on the provider)
+* ``long_range_energy`` / ``long_range_pressure``
+                          -> ONE fused scale/reduce pass (cached per spectrum,
+                             so energy + pressure cost a single pass)
+* ``long_range_forces(mode="ik")`` -> ik spectra + 3 inverse FFTs + gather
+
+Inputs may be the reference's own dataclasses (duck-typed: ``positions``,
+``charges``, ``cell.h``; ``spec.M``, ``spec.P``, ``spec.window``) or this
+package's.  Fourier fields are kept on the device as the half spectrum;
+``GridField.full()`` materialises the reference's full (Mx, My, Mz) numpy
+spectrum for inspection.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .errors import MeshError, PlanningError
+from .kernel import SplitKernel
+from .plan import EspPlan, cell_tables, out7_to_tensor
+from .pswf import PswfBasis, WindowTable, build_pswf, solve_bandwidth, tabulate_window
+from .system import Cell
+
+
+class TransformProvider:
+    """FFT contract with call counters (mesh.py:33-55).
+
+    The pipeline functions below run the plan's cuFFT transforms and count
+    them here, so ``forward_count`` / ``inverse_count`` certify the transform
+    economy exactly as the reference's counters do.  ``forward`` /
+    ``inverse`` themselves transform CUDA tensors with cuFFT (torch.fft).
+    """
+
+    def __init__(self):
+        self.forward_count = 0
+        self.inverse_count = 0
+
+    def forward(self, values):
+        self.forward_count += 1
+        return torch.fft.fftn(_as_cuda(values))
+
+    def inverse(self, values):
+        self.inverse_count += 1
+        return torch.fft.ifftn(_as_cuda(values))
+
+    def reset(self):
+        self.forward_count = 0
+        self.inverse_count = 0
+
+
+def _as_cuda(x):
+    if isinstance(x, torch.Tensor):
+        return x if x.is_cuda else x.cuda()
+    return torch.as_tensor(np.asarray(x), device="cuda")
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Mesh geometry plus the spreading window (mesh.py:58-78)."""
+
+    M: tuple
+    spacing: tuple
+    P: int
+    omega: tuple
+    spread_basis: PswfBasis
+    window: WindowTable
+    delta_spread: float
+    oversampling: float
+    lengths: tuple
+    _plans: dict = field(default_factory=dict, compare=False, repr=False)
+
+    @property
+    def n_grid(self) -> int:
+        return int(np.prod(self.M))
+
+    @property
+    def cell_volume_element(self) -> float:
+        return float(np.prod(self.spacing))
+
+
+def plan_grid(cell, kern, delta_spread: float, P: int, oversampling: float = 1.0,
+              spread_basis: PswfBasis | None = None, fixed_M: tuple | None = None,
+              window: WindowTable | None = None, allow_triclinic: bool = False) -> GridSpec:
+    """Grid counts and window (mesh.py:81-142).  ``allow_triclinic`` enables
+    the fractional-coordinate lattice (the reference refuses such cells)."""
+    h = np.asarray(cell.h, dtype=float)
+    ortho = _is_ortho(h)
+    if not ortho and not allow_triclinic:
+        raise PlanningError("mesh pipeline requires an orthorhombic cell")
+    if oversampling < 1.0:
+        raise PlanningError("oversampling factor must be >= 1")
+    if P < 2:
+        raise PlanningError("spreading order P must be >= 2")
+    lengths = np.diag(h) if ortho else np.linalg.norm(h, axis=0)
+    kmax = kern.kmax
+    if fixed_M is not None:
+        M = np.asarray(fixed_M, dtype=int)
+    else:
+        M = np.ceil(oversampling * kmax * lengths / np.pi).astype(int)
+        M += M % 2
+        M = np.maximum(M, 2)
+    spacing = lengths / M
+    omega = P * spacing / 2.0
+    if spread_basis is None:
+        spread_basis = build_pswf(solve_bandwidth(delta_spread))
+    c_spread = spread_basis.c
+    for d in range(3):
+        if np.pi / spacing[d] < kmax * (1.0 - 1e-12):
+            raise PlanningError(f"Nyquist coverage violated in dimension {d}: "
+                                f"pi/h={np.pi / spacing[d]:.4g} < kmax={kmax:.4g}")
+        if c_spread / omega[d] < kmax * (1.0 - 1e-12):
+            raise PlanningError(
+                f"window band coverage violated in dimension {d}: "
+                f"c_spread/omega={c_spread / omega[d]:.4g} < kmax={kmax:.4g}; "
+                f"decrease P or delta_spread, or increase oversampling")
+        if 2.0 * omega[d] >= lengths[d]:
+            raise PlanningError(f"window support 2*omega={2 * omega[d]:.4g} not below box "
+                                f"length {lengths[d]:.4g} in dimension {d}")
+    if window is None:
+        window = tabulate_window(spread_basis, P)
+    elif window.P != P or window.basis_c != spread_basis.c:
+        raise PlanningError("supplied window table does not match P and basis")
+    spec = GridSpec(M=tuple(int(m) for m in M), spacing=tuple(float(s) for s in spacing),
+                    P=int(P), omega=tuple(float(w) for w in omega),
+                    spread_basis=spread_basis, window=window,
+                    delta_spread=float(delta_spread), oversampling=float(oversampling),
+                    lengths=tuple(float(x) for x in lengths))
+    object.__setattr__(spec, "_kern", kern)
+    object.__setattr__(spec, "_allow_triclinic", bool(allow_triclinic))
+    return spec
+
+
+def _is_ortho(h) -> bool:
+    off = h - np.diag(np.diag(h))
+    return bool(np.all(np.abs(off) <= 1e-12 * np.max(np.abs(h))))
+
+
+def _window_of(spec) -> WindowTable:
+    """Accept this package's WindowTable or the reference's (PPoly based)."""
+    w = spec.window
+    if isinstance(w, WindowTable):
+        return w
+    val, der = w.value, w.deriv
+    return WindowTable(P=int(w.P), degree=int(w.degree), table_tol=float(w.table_tol),
+                       coef=np.ascontiguousarray(val.c.T), deriv_coef=np.ascontiguousarray(der.c.T),
+                       breaks=np.asarray(val.x, dtype=float), basis_c=float(w.basis_c))
+
+
+_SPEC_KERNELS = {}
+
+
+def _get_plan(spec, kern, cell, precision="fp64") -> EspPlan:
+    """Device plan cached per (spec, kernel, cell, precision)."""
+    h = np.asarray(cell.h, dtype=float)
+    if kern is None:
+        # Spread/transform only: a kernel whose band covers the whole grid.
+        kern = _SPEC_KERNELS.get(id(spec))
+        if kern is None:
+            sb = spec.spread_basis
+            kmax = np.pi / min(spec.spacing)
+            kern = SplitKernel(basis=sb, r_c=sb.c / kmax)
+            _SPEC_KERNELS[id(spec)] = kern
+    plans = spec._plans if hasattr(spec, "_plans") else _SPEC_KERNELS.setdefault(("plans", id(spec)), {})
+    key = (id(kern), h.tobytes(), precision)
+    plan = plans.get(key)
+    if plan is None:
+        plan = EspPlan(spec.M, spec.P, _window_of(spec), kern.basis, kern.r_c,
+                       spread=spec.spread_basis, precision=precision)
+        plan.set_cell(h)
+        plan._kern = kern
+        plans[key] = plan
+    return plan
+
+
+@dataclass
+class GridField:
+    """Scalar field on the periodic mesh, real or Fourier (mesh.py:145-151).
+
+    Real fields: ``values`` is a CUDA tensor indexed [x, y, z] like the
+    reference (a view of the device [z][y][x] layout).  Fourier fields:
+    ``values`` is the CUDA half spectrum [kz, ky, kx<=Mx/2] already scaled by
+    the volume element; ``full()`` gives the reference's full spectrum.
+    """
+
+    values: object
+    spec: object
+    space: str = "real"
+    _plan: object = field(default=None, repr=False)
+    _version: int = field(default=-1, repr=False)
+
+    def numpy(self) -> np.ndarray:
+        if self.space == "real":
+            v = self.values
+            return v.detach().cpu().numpy() if isinstance(v, torch.Tensor) else np.asarray(v)
+        return self.full()
+
+    def full(self) -> np.ndarray:
+        """Full complex spectrum in the reference layout [mx, my, mz]."""
+        if self.space != "fourier":
+            raise MeshError("full() is defined for spectral fields only")
+        half = self.values.detach().cpu().numpy()      # [kz][ky][kx_h]
+        Mx, My, Mz = self.spec.M
+        out = np.empty((Mz, My, Mx), dtype=complex)
+        out[:, :, : half.shape[2]] = half
+        kx = np.arange(half.shape[2], Mx)
+        mirror_x = (-kx) % Mx
+        zz = (-np.arange(Mz)) % Mz
+        yy = (-np.arange(My)) % My
+        out[:, :, half.shape[2]:] = np.conj(half[zz][:, yy][:, :, mirror_x])
+        return np.transpose(out, (2, 1, 0))
+
+
+def _particles(sys):
+    pos = sys.positions
+    q = sys.charges
+    if not isinstance(pos, torch.Tensor):
+        pos = torch.as_tensor(np.ascontiguousarray(pos, dtype=float), device="cuda")
+    if not isinstance(q, torch.Tensor):
+        q = torch.as_tensor(np.ascontiguousarray(q, dtype=float), device="cuda")
+    return pos.to(torch.float64).contiguous(), q.to(torch.float64).contiguous()
+
+
+def spread_charges(sys, spec) -> GridField:
+    """Deposit q_j W(r_g - r_j) on the mesh (mesh.py:204-210)."""
+    plan = _get_plan(spec, getattr(spec, "_kern", None), sys.cell)
+    pos, q = _particles(sys)
+    grid = plan.spread(pos, q).clone()
+    plan._bins_for = id(sys)
+    return GridField(values=grid.permute(2, 1, 0), spec=spec, space="real")
+
+
+def forward_density(sys, spec, provider: TransformProvider) -> GridField:
+    """Spread and forward-transform with continuum normalisation
+    (mesh.py:221-226): one cuFFT R2C, counted on ``provider``."""
+    plan = _get_plan(spec, getattr(spec, "_kern", None), sys.cell)
+    pos, q = _particles(sys)
+    plan.spread(pos, q)
+    plan._bins_for = id(sys)
+    plan.forward()
+    provider.forward_count += 1
+    vals = plan.spectrum_view() * plan.tables.volume_element
+    return GridField(values=vals, spec=spec, space="fourier", _plan=plan,
+                     _version=plan.version)
+
+
+def _spectrum_plan(rho_hat: GridField, kern, spec, cell) -> EspPlan:
+    plan = _get_plan(spec, kern, cell)
+    if rho_hat._plan is plan and rho_hat._version == plan.version:
+        return plan
+    vals = rho_hat.values
+    if not isinstance(vals, torch.Tensor):
+        raise MeshError("spectral field must come from forward_density")
+    scale = plan.tables.volume_element
+    plan.set_spectrum((vals / scale).to(torch.complex128 if plan.precision == "fp64"
+                                        else torch.complex64))
+    rho_hat._plan = plan
+    rho_hat._version = plan.version
+    return plan
+
+
+def _reduce(rho_hat, kern, spec, cell):
+    plan = _spectrum_plan(rho_hat, kern, spec, cell)
+    cache = getattr(plan, "_reduce_cache", None)
+    if cache is not None and cache[0] == plan.version:
+        return cache[1]
+    out7 = plan.scale_reduce(write_ik=False)
+    res = out7_to_tensor(out7)
+    plan._reduce_cache = (plan.version, res)
+    return res
+
+
+class ModeWorkspace:
+    """Per-(spec, cell) mode data (mesh.py:229-282).
+
+    Builds the device plan and its retained-mode tables (mask, Fhat What^-2,
+    pressure kernel) once.  The host arrays ``mask``, ``kvec``, ``k2``,
+    ``w_inv2``, ``fhat`` and ``dterm`` are provided for inspection with the
+    reference's formulas (they are not used on the device path).
+    """
+
+    def __init__(self, spec, kern, cell):
+        h = np.asarray(cell.h, dtype=float)
+        if not _is_ortho(h) and not getattr(spec, "_allow_triclinic", False):
+            raise PlanningError("mesh pipeline requires an orthorhombic cell")
+        self.volume = float(np.linalg.det(h))
+        self._plan = _get_plan(spec, kern, cell)
+        self._spec, self._kern, self._h = spec, kern, h
+        self._host = None
+
+    def _host_arrays(self):
+        if self._host is None:
+            spec, kern = self._spec, self._kern
+            t = cell_tables(self._h, spec.M, spec.P, spec.spread_basis, kern.kmax)
+            kv = [t.axis_k[a][0][:, None, None] + t.axis_k[a][1][None, :, None]
+                  + t.axis_k[a][2][None, None, :] for a in range(3)]
+            kx, ky, kz = [np.broadcast_to(k, spec.M) for k in kv]
+            k2 = kx ** 2 + ky ** 2 + kz ** 2
+            kmag = np.sqrt(k2)
+            mask = (kmag <= kern.kmax) & (k2 > 0.0)
+            what = (t.axis_what[0][:, None, None] * t.axis_what[1][None, :, None]) \
+                * t.axis_what[2][None, None, :]
+            what = np.broadcast_to(what, spec.M)[mask]
+            b = kern.basis
+            x = np.clip(kmag[mask] * kern.r_c / b.c, 0.0, 1.0)
+            pref = 2.0 * np.pi * b.lambda0 / b.C0
+            k2m = k2[mask]
+            self._host = dict(mask=mask, kvec=[kx[mask], ky[mask], kz[mask]], k2=k2m,
+                              w_inv2=1.0 / (what * what),
+                              fhat=pref * b.psi_series(x) / k2m,
+                              dterm=pref * x * b.psi_series(x, derivative=1) / k2m ** 2)
+        return self._host
+
+    mask = property(lambda self: self._host_arrays()["mask"])
+    kvec = property(lambda self: self._host_arrays()["kvec"])
+    k2 = property(lambda self: self._host_arrays()["k2"])
+    w_inv2 = property(lambda self: self._host_arrays()["w_inv2"])
+    fhat = property(lambda self: self._host_arrays()["fhat"])
+    dterm = property(lambda self: self._host_arrays()["dterm"])
+
+    def pressure_kernel_component(self, a: int, b: int) -> np.ndarray:
+        kk = self.kvec[a] * self.kvec[b]
+        out = self.dterm * kk - 2.0 * self.fhat * kk / self.k2
+        return out + self.fhat if a == b else out
+
+
+def long_range_energy(rho_hat: GridField, kern: SplitKernel, spec, cell,
+                      modes: ModeWorkspace | None = None) -> float:
+    """U_F = (1/2V) sum_{k!=0} Fhat What^-2 |rho_hat|^2 (mesh.py:285-292)."""
+    if rho_hat.space != "fourier":
+        raise MeshError("long_range_energy expects a spectral density")
+    return _reduce(rho_hat, kern, spec, cell)[0]
+
+
+def long_range_pressure(rho_hat: GridField, kern: SplitKernel, spec, cell,
+                        modes: ModeWorkspace | None = None) -> np.ndarray:
+    """Global far-field pressure tensor; no inverse transform (mesh.py:295-312)."""
+    if rho_hat.space != "fourier":
+        raise MeshError("long_range_pressure expects a spectral density")
+    return _reduce(rho_hat, kern, spec, cell)[1].copy()
+
+
+def long_range_forces(rho_hat: GridField, sys, kern: SplitKernel, spec, cell,
+                      mode: str = "ik", provider: TransformProvider | None = None,
+                      modes: ModeWorkspace | None = None) -> np.ndarray:
+    """Far-field forces by ik differentiation and window gathering
+    (mesh.py:315-342): three inverse transforms, counted on ``provider``."""
+    if rho_hat.space != "fourier":
+        raise MeshError("long_range_forces expects a spectral density")
+    if mode not in ("ik", "analytic"):
+        raise MeshError(f"unknown differentiation mode {mode!r}")
+    if mode == "analytic":
+        raise MeshError("analytic-differentiation forces are not built in this release "
+                        "(SURVEY §8(f) f1)")
+    provider = provider or TransformProvider()
+    plan = _spectrum_plan(rho_hat, kern, spec, cell)
+    pos, q = _particles(sys)
+    version = plan.version
+    if getattr(plan, "_bins_for", None) != id(sys):
+        plan.spread(pos, q)        # re-bin these particles; the spectrum is untouched
+        plan._bins_for = id(sys)
+    plan.scale_reduce(write_ik=True)
+    F = plan.forces_ik(pos.shape[0])
+    provider.inverse_count += 3
+    plan.version = version
+    return F.cpu().numpy()
+
+
+def local_pressure(rho_hat: GridField, sys, kern, spec, cell, provider=None, modes=None):
+    """Per-particle pressure tensors (mesh.py:353-379) — SURVEY §8(f) f2."""
+    if rho_hat.space != "fourier":
+        raise MeshError("local_pressure expects a spectral density")
+    raise MeshError("per-particle pressure is not built in this release (SURVEY §8(f) f2)")

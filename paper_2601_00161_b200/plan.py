@@ -1,0 +1,369 @@
+"""EspPlan: one device plan (grid, window, basis, buffers, cuFFT plans).
+
+Python owner of the C-ABI ``esp_plan`` (include/esp_b200.h).  Setup-time
+tables (per-axis wavenumbers and window transforms — the separable inputs of
+the reference ModeWorkspace, mesh.py:237-275) are computed here on the host
+with the reference's exact arithmetic and uploaded once per cell; the mask,
+Fhat and dterm tables are then built on the device.  Every per-step
+operation is a CUDA launch on the caller's torch stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ParameterError, PlanningError
+from .pswf import PswfBasis, WindowTable
+
+_DT = {"fp64": _lib.ESP_FP64, "fp32": _lib.ESP_FP32}
+
+
+class _DevView:
+    """__cuda_array_interface__ shim to alias plan-owned device memory."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+@dataclass
+class CellTables:
+    """Per-cell inputs of the device mode setup."""
+    h: np.ndarray
+    hinv: np.ndarray
+    orthorhombic: bool
+    spacing: np.ndarray
+    volume: float
+    volume_element: float
+    axis_k: list          # axis_k[a][d] : (M_d,) f64
+    axis_what: list       # (M_d,) f64 per axis
+    what_zero: float
+    band: tuple
+    grad_scale: np.ndarray
+
+
+def cell_tables(h, M, P, spread: PswfBasis, kmax: float, orthorhombic=None) -> CellTables:
+    """Separable mode-workspace inputs.
+
+    Orthorhombic: k_d = 2 pi fftfreq(M_d, 1/M_d) / L_d (mesh.py:242) and
+    What_d = omega_d lambda0 psi(clip(omega_d k_d / c)) (mesh.py:258-261) with
+    omega_d = P h_d / 2 (mesh.py:109-110) — the same numpy expressions, so the
+    mask and deconvolution agree bit-for-bit with the reference.
+    Triclinic (fractional-coordinate lattice):
+    k = 2 pi h^-T m and What(m) = V prod_d (P/2M_d) lambda0 psi(pi P m_d/(M_d c)).
+    """
+    h = np.asarray(h, dtype=float).reshape(3, 3)
+    M = tuple(int(m) for m in M)
+    if orthorhombic is None:
+        off = h - np.diag(np.diag(h))
+        orthorhombic = bool(np.all(np.abs(off) <= 1e-12 * np.max(np.abs(h))))
+    volume = float(np.linalg.det(h))
+    hinv = np.linalg.inv(h)
+    freqs = [np.fft.fftfreq(M[d], d=1.0 / M[d]) for d in range(3)]
+    zeros = [np.zeros(M[d]) for d in range(3)]
+    axis_k = [[zeros[d] for d in range(3)] for _ in range(3)]
+    sb = spread
+    if orthorhombic:
+        lengths = np.diag(h)
+        spacing = lengths / np.asarray(M)
+        omega = P * spacing / 2.0
+        for d in range(3):
+            axis_k[d][d] = 2.0 * np.pi * np.fft.fftfreq(M[d], d=1.0 / M[d]) / lengths[d]
+        axis_what = [omega[d] * sb.lambda0 * sb.psi_series(
+            np.clip(omega[d] * axis_k[d][d] / sb.c, -1, 1)) for d in range(3)]
+        what_zero = float(np.prod([w * sb.lambda0 * sb.psi0_at_zero for w in omega]))
+        volume_element = float(np.prod(spacing))
+        band = []
+        for d in range(3):
+            inb = np.abs(axis_k[d][d]) <= kmax
+            band.append(int(np.max(np.abs(np.round(freqs[d][inb])))) if inb.any() else 0)
+        grad_scale = 1.0 / spacing
+    else:
+        norms = np.linalg.norm(h, axis=0)
+        spacing = norms / np.asarray(M)
+        B = 2.0 * np.pi * hinv.T
+        for a in range(3):
+            for d in range(3):
+                axis_k[a][d] = B[a, d] * freqs[d]
+        axis_what = []
+        for d in range(3):
+            arg = np.pi * P * freqs[d] / (M[d] * sb.c)
+            w = (P / (2.0 * M[d])) * sb.lambda0 * sb.psi_series(np.clip(arg, -1, 1))
+            axis_what.append(volume * w if d == 0 else w)
+        what_zero = volume * float(np.prod([(P / (2.0 * m)) * sb.lambda0 * sb.psi0_at_zero
+                                            for m in M]))
+        volume_element = volume / float(np.prod(M))
+        band = [min(M[d] // 2, int(np.floor(kmax * norms[d] / (2.0 * np.pi) * (1 + 1e-9))) + 1)
+                for d in range(3)]
+        grad_scale = np.zeros(3)
+    return CellTables(h=h, hinv=hinv, orthorhombic=orthorhombic, spacing=np.asarray(spacing),
+                      volume=volume, volume_element=volume_element,
+                      axis_k=[[np.ascontiguousarray(x, dtype=float) for x in row] for row in axis_k],
+                      axis_what=[np.ascontiguousarray(x, dtype=float) for x in axis_what],
+                      what_zero=what_zero, band=tuple(band), grad_scale=np.asarray(grad_scale))
+
+
+def _stream_handle(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class EspPlan:
+    """Device plan for one (M, P, window, splitting kernel, precision)."""
+
+    def __init__(self, M, P: int, window: WindowTable, split: PswfBasis, r_c: float,
+                 spread: PswfBasis | None = None, precision: str = "fp64",
+                 deterministic: bool = True, capacity: int = 1 << 16, tile=(0, 0, 0)):
+        if not torch.cuda.is_available():
+            raise RuntimeError("EspPlan needs a CUDA device (the B200 path has no CPU fallback)")
+        if precision not in _DT:
+            raise ParameterError(f"unknown precision {precision!r}")
+        if window.P != P:
+            raise PlanningError("supplied window table does not match P")
+        torch.cuda.current_device()
+        torch.empty(0, device="cuda")  # make torch's primary context current
+        self.M = tuple(int(m) for m in M)
+        self.P = int(P)
+        self.window = window
+        self.split = split
+        self.spread_basis = spread if spread is not None else split
+        self.r_c = float(r_c)
+        self.kmax = split.c / self.r_c
+        self.precision = precision
+        self.deterministic = bool(deterministic)
+        self.tile = tuple(int(t) for t in tile)
+        self.capacity = int(max(capacity, 1))
+        self._handle = None
+        self._cell = None
+        self.version = 0          # bumps on every forward transform
+        self._create()
+
+    # -- lifetime -----------------------------------------------------------
+    def _create(self):
+        L = _lib.lib()
+        w = self.window
+        self._coef = np.ascontiguousarray(w.coef, dtype=float)
+        self._dcoef = np.ascontiguousarray(w.deriv_coef, dtype=float)
+        self._breaks = np.ascontiguousarray(w.breaks, dtype=float)
+        self._leg = np.ascontiguousarray(self.split.legendre_coeffs, dtype=float)
+        self._legd = np.ascontiguousarray(self.split.derivative_coeffs, dtype=float)
+        d = _lib.PlanDesc()
+        d.M[:] = list(self.M)
+        d.P = self.P
+        d.precision = _DT[self.precision]
+        d.deterministic = int(self.deterministic)
+        d.max_particles = self.capacity
+        d.n_pieces = w.coef.shape[0]
+        d.degree = w.coef.shape[1] - 1
+        d.h_window_coef = _ptr(self._coef)
+        d.h_window_deriv_coef = _ptr(self._dcoef)
+        d.h_window_breaks = _ptr(self._breaks)
+        d.n_legendre = self._leg.size
+        d.h_legendre = _ptr(self._leg)
+        d.n_legendre_deriv = self._legd.size
+        d.h_legendre_deriv = _ptr(self._legd)
+        d.split_c = self.split.c
+        d.split_lambda0 = self.split.lambda0
+        d.split_C0 = self.split.C0
+        d.r_c = self.r_c
+        d.kmax = self.kmax
+        d.tile[:] = list(self.tile)
+        h = C.c_void_p()
+        _lib.check(L.esp_plan_create(C.byref(d), C.byref(h)), "esp_plan_create")
+        self._handle = h
+        info = self.info()
+        self.Hx = int(info[3])
+        self.n_tiles = int(info[6])
+
+    def close(self):
+        if self._handle is not None and self._handle.value:
+            torch.cuda.synchronize()
+            _lib.lib().esp_plan_destroy(self._handle)
+        self._handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def ensure_capacity(self, n: int):
+        if n <= self.capacity:
+            return
+        cell = self._cell
+        self.close()
+        self.capacity = max(int(n), 2 * self.capacity)
+        self._create()
+        if cell is not None:
+            self._cell = None
+            self.set_cell(cell)
+
+    # -- per cell -------------------------------------------------------------
+    def set_cell(self, h, orthorhombic=None, stream=None):
+        t = cell_tables(h, self.M, self.P, self.spread_basis, self.kmax, orthorhombic)
+        c = _lib.CellDesc()
+        c.h[:] = list(t.h.reshape(-1))
+        c.hinv[:] = list(t.hinv.reshape(-1))
+        c.orthorhombic = int(t.orthorhombic)
+        c.spacing[:] = list(t.spacing)
+        c.volume = t.volume
+        c.volume_element = t.volume_element
+        for a in range(3):
+            for dd in range(3):
+                c.h_axis_k[3 * a + dd] = _ptr(t.axis_k[a][dd])
+        for dd in range(3):
+            c.h_axis_what[dd] = _ptr(t.axis_what[dd])
+        c.what_zero = t.what_zero
+        c.band[:] = list(t.band)
+        c.grad_scale[:] = list(t.grad_scale)
+        _lib.check(_lib.lib().esp_plan_set_cell(self._handle, C.byref(c), _stream_handle(stream)),
+                   "esp_plan_set_cell")
+        self._cell = t.h.copy()
+        self.tables = t
+        return t
+
+    # -- introspection --------------------------------------------------------
+    def info(self):
+        buf = (C.c_int64 * 8)()
+        _lib.check(_lib.lib().esp_grid_info(self._handle, buf), "esp_grid_info")
+        return list(buf)
+
+    @property
+    def real_dtype(self):
+        return torch.float64 if self.precision == "fp64" else torch.float32
+
+    def counters(self):
+        f, i = C.c_int64(), C.c_int64()
+        _lib.check(_lib.lib().esp_counters(self._handle, C.byref(f), C.byref(i)))
+        return int(f.value), int(i.value)
+
+    def reset_counters(self):
+        _lib.lib().esp_reset_counters(self._handle)
+
+    def grid_view(self) -> torch.Tensor:
+        """Alias of the plan's real grid, shape (Mz, My, Mx) ([z][y][x])."""
+        ts = "<f8" if self.precision == "fp64" else "<f4"
+        ptr = _lib.lib().esp_grid_ptr(self._handle)
+        return torch.as_tensor(_DevView(ptr, (self.M[2], self.M[1], self.M[0]), ts),
+                               device="cuda")
+
+    def spectrum_view(self) -> torch.Tensor:
+        """Alias of the plan's half spectrum (Mz, My, Mx//2+1), unscaled."""
+        ts = "<f8" if self.precision == "fp64" else "<f4"
+        ptr = _lib.lib().esp_spectrum_ptr(self._handle)
+        raw = torch.as_tensor(_DevView(ptr, (self.M[2], self.M[1], self.Hx, 2), ts),
+                              device="cuda")
+        return torch.view_as_complex(raw)
+
+    # -- stages ---------------------------------------------------------------
+    @staticmethod
+    def _check_particles(pos, q):
+        if not (isinstance(pos, torch.Tensor) and pos.is_cuda and pos.dtype == torch.float64):
+            raise ParameterError("positions must be a CUDA float64 tensor of shape (N, 3)")
+        if not (isinstance(q, torch.Tensor) and q.is_cuda and q.dtype == torch.float64):
+            raise ParameterError("charges must be a CUDA float64 tensor of shape (N,)")
+        if pos.dim() != 2 or pos.shape[1] != 3 or q.numel() != pos.shape[0]:
+            raise ParameterError("positions (N,3) and charges (N,) shapes disagree")
+        return pos.contiguous(), q.contiguous()
+
+    def spread(self, pos: torch.Tensor, q: torch.Tensor, stream=None):
+        pos, q = self._check_particles(pos, q)
+        n = pos.shape[0]
+        self.ensure_capacity(n)
+        _lib.check(_lib.lib().esp_spread(self._handle, C.c_void_p(pos.data_ptr()),
+                                         C.c_void_p(q.data_ptr()), n, None,
+                                         _stream_handle(stream)), "esp_spread")
+        return self.grid_view()
+
+    def forward(self, grid: torch.Tensor | None = None, stream=None):
+        ptr = None
+        if grid is not None:
+            g = grid.contiguous()
+            if g.dtype != self.real_dtype or g.numel() != int(np.prod(self.M)):
+                raise ParameterError("grid shape/dtype does not match the plan")
+            ptr = C.c_void_p(g.data_ptr())
+        _lib.check(_lib.lib().esp_forward(self._handle, ptr, _stream_handle(stream)),
+                   "esp_forward")
+        self.version += 1
+
+    def set_spectrum(self, spec: torch.Tensor, stream=None):
+        s = torch.view_as_real(spec.contiguous()).contiguous()
+        _lib.check(_lib.lib().esp_set_spectrum(self._handle, C.c_void_p(s.data_ptr()),
+                                               _stream_handle(stream)), "esp_set_spectrum")
+        self.version += 1
+
+    def scale_reduce(self, write_ik: bool = False, out7: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+        if out7 is None:
+            out7 = torch.empty(7, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().esp_scale_reduce(self._handle, C.c_void_p(out7.data_ptr()),
+                                               int(bool(write_ik)), _stream_handle(stream)),
+                   "esp_scale_reduce")
+        return out7
+
+    def forces_ik(self, n: int, forces: torch.Tensor | None = None, stream=None):
+        if forces is None:
+            forces = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().esp_forces_ik(self._handle, C.c_void_p(forces.data_ptr()),
+                                            _stream_handle(stream)), "esp_forces_ik")
+        return forces
+
+    def evaluate(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool = True,
+                 out7: torch.Tensor | None = None, forces: torch.Tensor | None = None,
+                 stream=None):
+        """Whole step on the device: (out7[E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz], F)."""
+        pos, q = self._check_particles(pos, q)
+        n = pos.shape[0]
+        self.ensure_capacity(n)
+        if out7 is None:
+            out7 = torch.empty(7, dtype=torch.float64, device="cuda")
+        if want_forces and forces is None:
+            forces = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        flags = _lib.ESP_WANT_ENERGY_PRESSURE | (_lib.ESP_WANT_FORCES if want_forces else 0)
+        _lib.check(_lib.lib().esp_evaluate(
+            self._handle, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()), n, flags,
+            C.c_void_p(out7.data_ptr()),
+            C.c_void_p(forces.data_ptr()) if want_forces else None,
+            _stream_handle(stream)), "esp_evaluate")
+        self.version += 1
+        return out7, forces
+
+    def launches_last_step(self) -> int:
+        return int(self.info()[5])
+
+    def set_profiling(self, on: bool = True):
+        _lib.check(_lib.lib().esp_set_profiling(self._handle, int(bool(on))), "esp_set_profiling")
+
+    def profile(self):
+        """[(kernel name, ms)] of the last profiled esp_evaluate (synchronises)."""
+        names = C.create_string_buffer(2048)
+        ms = (C.c_double * 48)()
+        n = _lib.lib().esp_profile_read(self._handle, names, 2048, ms, 48)
+        if n < 0:
+            _lib.check(-n, "esp_profile_read")
+        labels = names.value.decode().split(",") if n else []
+        return list(zip(labels, [float(ms[i]) for i in range(n)]))
+
+
+def probe_fp64_tflops(stream=None) -> float:
+    """Measured FP64 FMA throughput of the current device (TFLOP/s)."""
+    out = C.c_double()
+    _lib.check(_lib.lib().esp_probe_fp64(C.byref(out), _stream_handle(stream)), "esp_probe_fp64")
+    return float(out.value)
+
+
+def out7_to_tensor(out7) -> np.ndarray:
+    """[E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz] -> (E, 3x3 symmetric)."""
+    v = out7.detach().cpu().numpy() if isinstance(out7, torch.Tensor) else np.asarray(out7)
+    P = np.array([[v[1], v[2], v[3]], [v[2], v[4], v[5]], [v[3], v[5], v[6]]])
+    return float(v[0]), P

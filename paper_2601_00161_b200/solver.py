@@ -1,0 +1,214 @@
+"""Solver composition on the B200 (reference: prolate_ewald/evaluate.py).
+
+:class:`KSpaceSolver` is the fused product entry point: positions and charges
+(CUDA tensors, or host arrays that are copied in) -> far-field energy, the
+full 3x3 pressure tensor and ik forces in one device pipeline (bin, spread,
+1 forward FFT, fused scale/reduce, and for forces 3 inverse FFTs + gather).
+:class:`CoulombSolver` mirrors ``evaluate.CoulombSolver`` (evaluate.py:81-152)
+for the terms this build owns: far field + self energy + uniform background.
+The real-space near field is outside this build's scope;
+pass its result in with ``near=`` to compose totals.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .cells import CellType, infer_cell_type
+from .errors import ParameterError
+from .kernel import SplitKernel, background_correction, self_energy
+from .mesh import plan_grid
+from .plan import EspPlan, out7_to_tensor
+from .pswf import build_pswf, solve_bandwidth
+from .system import Cell, check_cutoff
+
+
+@dataclass(frozen=True)
+class EwaldParameters:
+    """Accuracy knobs (evaluate.py:29-57) plus the B200 execution options."""
+
+    r_c: float
+    delta_split: float = 1e-6
+    delta_spread: float | None = None
+    P: int | None = None
+    oversampling: float = 1.0
+    prefactor: float = 1.0
+    force_mode: str = "ik"
+    fixed_M: tuple | None = None
+    precision: str = "fp64"
+    deterministic: bool = True
+    cell_type: str | None = None
+
+    def resolved(self):
+        if self.r_c <= 0:
+            raise ParameterError("cutoff r_c must be positive")
+        if self.force_mode not in ("ik", "analytic"):
+            raise ParameterError(f"unknown force mode {self.force_mode!r}")
+        if self.precision not in ("fp64", "fp32"):
+            raise ParameterError(f"unknown precision {self.precision!r}")
+        d_split = float(self.delta_split)
+        d_spread = d_split if self.delta_spread is None else float(self.delta_spread)
+        P = self.P if self.P is not None else int(np.ceil(-np.log10(d_split))) + 1
+        return d_split, d_spread, int(P)
+
+
+@dataclass
+class KSpaceResult:
+    energy: float
+    pressure: np.ndarray            # (3,3)
+    forces: object = None           # (N,3) tensor/array or None
+    cell_type: CellType | None = None
+
+    @property
+    def reported_pressure(self):
+        """The pressure quantities the cell type couples to."""
+        ct = self.cell_type or CellType.TRICLINIC
+        return ct.reduce(self.pressure)
+
+
+def _to_device(x, dtype=torch.float64):
+    if isinstance(x, torch.Tensor):
+        return x.to(device="cuda", dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device="cuda").to(dtype)
+
+
+class KSpaceSolver:
+    """Far-field solver bound to one cell (M pinned by ``fixed_M`` or planned)."""
+
+    def __init__(self, cell, params: EwaldParameters, capacity: int = 1 << 16):
+        d_split, d_spread, P = params.resolved()
+        self.params = params
+        h = np.asarray(cell.h if hasattr(cell, "h") else cell, dtype=float)
+        self.cell = Cell(h)
+        self.cell_type = CellType(params.cell_type) if params.cell_type else \
+            infer_cell_type(self.cell.h)
+        self.cell_type.validate(self.cell.h)
+        check_cutoff(self.cell, params.r_c)
+        basis = build_pswf(solve_bandwidth(d_split))
+        spread = basis if abs(d_spread - d_split) <= 1e-300 else build_pswf(solve_bandwidth(d_spread))
+        self.kern = SplitKernel(basis=basis, r_c=params.r_c)
+        self.spec = plan_grid(self.cell, self.kern, delta_spread=d_spread, P=P,
+                              oversampling=params.oversampling, spread_basis=spread,
+                              fixed_M=params.fixed_M,
+                              allow_triclinic=self.cell_type is CellType.TRICLINIC)
+        self.plan = EspPlan(self.spec.M, P, self.spec.window, basis, params.r_c,
+                            spread=spread, precision=params.precision,
+                            deterministic=params.deterministic, capacity=capacity)
+        self.plan.set_cell(self.cell.h)
+
+    @property
+    def M(self):
+        return self.spec.M
+
+    def rebind_cell(self, cell, fixed_M=None):
+        """NPT rebind with the grid pinned (evaluate.py:99-112)."""
+        h = np.asarray(cell.h if hasattr(cell, "h") else cell, dtype=float)
+        if fixed_M is not None and tuple(fixed_M) != tuple(self.spec.M):
+            raise ParameterError("the B200 plan keeps M pinned; build a new solver to re-grid")
+        new = Cell(h)
+        self.cell_type.validate(new.h)
+        check_cutoff(new, self.params.r_c)
+        self.spec = plan_grid(new, self.kern, delta_spread=self.spec.delta_spread,
+                              P=self.spec.P, spread_basis=self.spec.spread_basis,
+                              fixed_M=self.spec.M, window=self.spec.window,
+                              allow_triclinic=self.cell_type is CellType.TRICLINIC)
+        self.cell = new
+        self.plan.set_cell(new.h)
+
+    def evaluate_device(self, positions: torch.Tensor, charges: torch.Tensor,
+                        want_forces: bool = True, out7=None, forces=None, stream=None):
+        """Device-only step: returns (out7 tensor, forces tensor|None) without
+        synchronising.  out7 = [E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz] (prefactor 1)."""
+        return self.plan.evaluate(positions, charges, want_forces, out7, forces, stream)
+
+    def evaluate(self, positions, charges, want_forces: bool = True,
+                 want_pressure: bool = True) -> KSpaceResult:
+        host = not isinstance(positions, torch.Tensor)
+        pos = _to_device(positions)
+        q = _to_device(charges)
+        out7, F = self.plan.evaluate(pos, q, want_forces)
+        E, Pt = out7_to_tensor(out7)
+        pref = self.params.prefactor
+        if want_forces:
+            F = F * pref
+            if host:
+                F = F.cpu().numpy()
+        return KSpaceResult(energy=pref * E, pressure=pref * Pt if want_pressure else None,
+                            forces=F if want_forces else None, cell_type=self.cell_type)
+
+    def pressure_only(self, positions, charges):
+        r = self.evaluate(positions, charges, want_forces=False)
+        return r.energy, r.pressure
+
+
+@dataclass
+class EnergyBreakdown:
+    """Electrostatic outputs with per-term energies (evaluate.py:60-77)."""
+
+    u_near: float
+    u_far: float
+    u_self: float
+    u_background: float
+    forces: np.ndarray | None = None
+    pressure: np.ndarray | None = None
+    pair_count: int = 0
+
+    @property
+    def energy(self) -> float:
+        return self.u_near + self.u_far + self.u_self + self.u_background
+
+
+class CoulombSolver:
+    """evaluate.CoulombSolver with the far field on the B200.
+
+    ``near`` (optional) is any object with ``energy``, ``forces`` (N,3),
+    ``pressure`` (3,3) and ``pair_count`` — e.g. the reference's
+    ``short_range`` result — added to the totals exactly as evaluate.py:132-144.
+    """
+
+    def __init__(self, cell, params: EwaldParameters):
+        self.params = params
+        self.kspace = KSpaceSolver(cell, params)
+        self.kern = self.kspace.kern
+        self.cell = self.kspace.cell
+
+    @property
+    def spec(self):
+        return self.kspace.spec
+
+    def rebind_cell(self, cell, fixed_M=None):
+        self.kspace.rebind_cell(cell, fixed_M)
+        self.cell = self.kspace.cell
+
+    def evaluate(self, sys, want_forces: bool = True, want_pressure: bool = True,
+                 neighbors=None, near=None) -> EnergyBreakdown:
+        if not np.allclose(np.asarray(sys.cell.h), self.cell.h):
+            raise ParameterError("system cell differs from the solver's cell; "
+                                 "call rebind_cell first")
+        pref = self.params.prefactor
+        far = self.kspace.evaluate(sys.positions, sys.charges, want_forces=want_forces)
+        q = np.asarray(sys.charges, dtype=float)
+        u_self = self_energy(self.kern, q)
+        u_cb, u_bb, p_corr = background_correction(self.kern, float(q.sum()), self.cell.volume)
+        e_near = getattr(near, "energy", 0.0) if near is not None else 0.0
+        out = EnergyBreakdown(u_near=pref * e_near, u_far=far.energy,
+                              u_self=pref * u_self, u_background=pref * (u_cb + u_bb),
+                              pair_count=getattr(near, "pair_count", 0) if near is not None else 0)
+        if want_forces:
+            f = np.asarray(far.forces)
+            if near is not None:
+                f = f + pref * np.asarray(near.forces)
+            out.forces = f
+        if want_pressure:
+            p = far.pressure + pref * p_corr
+            if near is not None:
+                p = p + pref * np.asarray(near.pressure)
+            out.pressure = p
+        return out
+
+
+def evaluate_system(sys, params: EwaldParameters, want_forces=True, want_pressure=True):
+    return CoulombSolver(sys.cell, params).evaluate(sys, want_forces, want_pressure)

@@ -1,0 +1,175 @@
+"""Generate the golden fixtures by running the REFERENCE implementation.
+
+Run once in the build container (the reference tree exists only there):
+
+    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_golden.py
+
+It imports ``prolate_ewald`` from ``/root/reference/pkg/src`` and calls the
+reference API exactly as SURVEY.md §8(c) "Oracle call sequence" lists
+(``plan_grid(..., fixed_M=...)``, ``ModeWorkspace``, ``forward_density``,
+``long_range_energy``, ``long_range_pressure``, ``long_range_forces(mode=
+"ik")``), plus ``direct_ksum`` on small triclinic cells.  Outputs go to
+``tests/golden/*.npz`` together with the numpy/scipy versions used.
+Nothing under ``tests/`` reads ``/root/reference`` at run time; only these
+committed fixtures travel.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import scipy
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+from prolate_ewald import (Cell, ParticleSystem, SplitKernel, build_pswf,  # noqa: E402
+                           solve_bandwidth, tabulate_window)
+from prolate_ewald.mesh import (ModeWorkspace, TransformProvider,  # noqa: E402
+                                forward_density, local_pressure,
+                                long_range_energy, long_range_forces,
+                                long_range_pressure, plan_grid,
+                                spread_charges)
+from prolate_ewald.oracle import direct_ksum  # noqa: E402
+
+from paper_2601_00161_b200 import workloads  # noqa: E402
+
+VERSIONS = np.array([np.__version__, scipy.__version__])
+
+
+def run_reference(h, raw, q, M, P, delta, r_c, with_grid=False, with_local=False,
+                  with_analytic=False):
+    basis = build_pswf(solve_bandwidth(delta))
+    kern = SplitKernel(basis=basis, r_c=r_c)
+    cell = Cell(np.asarray(h, dtype=float))
+    sys_ = ParticleSystem(cell=cell, positions=raw, charges=q)
+    assert np.array_equal(sys_.positions, workloads.wrap_positions(h, raw))
+    spec = plan_grid(cell, kern, delta_spread=delta, P=P, spread_basis=basis,
+                     fixed_M=tuple(M))
+    modes = ModeWorkspace(spec, kern, cell)
+    prov = TransformProvider()
+    rho_hat = forward_density(sys_, spec, prov)
+    E = long_range_energy(rho_hat, kern, spec, cell, modes)
+    Pt = long_range_pressure(rho_hat, kern, spec, cell, modes)
+    assert prov.forward_count == 1 and prov.inverse_count == 0
+    F = long_range_forces(rho_hat, sys_, kern, spec, cell, "ik", prov, modes)
+    out = dict(E=E, Pt=Pt, F=F, c=basis.c, lambda0=basis.lambda0, C0=basis.C0,
+               psi0_at_zero=basis.psi0_at_zero, legendre=basis.legendre_coeffs,
+               window_c=spec.window.value.c, window_x=spec.window.value.x,
+               window_dc=spec.window.deriv.c, n_modes=int(modes.mask.sum()),
+               versions=VERSIONS)
+    if with_grid:
+        out["grid"] = spread_charges(sys_, spec).values
+        out["rho_hat_masked"] = rho_hat.values[modes.mask]
+    if with_local:
+        out["local"] = local_pressure(rho_hat, sys_, kern, spec, cell, prov, modes)
+    if with_analytic:
+        out["F_analytic"] = long_range_forces(rho_hat, sys_, kern, spec, cell,
+                                              "analytic", prov, modes)
+    return out
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
+def configs():
+    for idx in (0, 1, 2):
+        w, raw, q = workloads.generate(idx, wrap=False)
+        pos = workloads.wrap_positions(w.h, raw)
+        r = run_reference(w.h, raw, q, w.M, w.P, w.delta, w.r_c,
+                          with_grid=(idx == 0))
+        F = r.pop("F")
+        stride = 1 if idx == 0 else 97
+        sel = np.arange(0, w.n, stride)
+        save(f"cfg{idx}", pos_head=pos[:4], pos_sum=pos.sum(axis=0),
+             F_idx=sel, F_sel=F[sel], F_rms=np.sqrt(np.mean(np.sum(F * F, axis=1))),
+             F_sum=F.sum(axis=0), **r)
+
+
+SMALL = [
+    # (name, n, lengths, seed, delta, P, r_c, oversampling)
+    ("small_cube_p5", 32, (6.0, 6.0, 6.0), 0, 1e-4, 5, 1.0, 2.0),
+    ("small_cube_p6", 32, (6.0, 6.0, 6.0), 1, 1e-5, 6, 1.2, 2.0),
+    ("small_brick_p6", 48, (5.0, 6.0, 7.0), 4, 1e-5, 6, 1.2, 2.0),
+    ("small_brick_p8", 64, (6.2, 6.0, 6.4), 523, 1e-7, 8, 2.94, 2.0),
+    ("small_brick_p7", 40, (6.0, 7.0, 8.0), 9, 1e-6, 7, 1.2, 2.0),
+    ("small_cube_p4", 16, (6.0, 6.0, 6.0), 10, 1e-3, 4, 1.1, 2.0),
+    ("small_single", 1, (6.0, 6.0, 6.0), 3, 1e-4, 5, 1.0, 2.0),
+]
+
+
+def small_cases():
+    for (name, n, lengths, seed, delta, P, r_c, ovs) in SMALL:
+        raw, q = workloads.random_neutral_system(n, lengths, seed, wrap=False)
+        pos = workloads.wrap_positions(np.diag(lengths), raw)
+        if n == 1:
+            q = np.array([1.0])
+        basis = build_pswf(solve_bandwidth(delta))
+        kern = SplitKernel(basis=basis, r_c=r_c)
+        cell = Cell.orthorhombic(lengths)
+        spec = plan_grid(cell, kern, delta_spread=delta, P=P, oversampling=ovs,
+                         spread_basis=basis)
+        r = run_reference(np.diag(lengths), raw, q, spec.M, P, delta, r_c,
+                          with_grid=True, with_local=True, with_analytic=True)
+        e_d, f_d, p_d = direct_ksum(ParticleSystem(cell=cell, positions=raw, charges=q), kern)
+        save(name, pos=pos, q=q, h=np.diag(lengths), M=np.array(spec.M), P=P,
+             delta=delta, r_c=r_c, E_direct=e_d, F_direct=f_d, Pt_direct=p_d, **r)
+
+
+TRICLINIC = [
+    # (name, h columns, n, seed, delta, P, r_c, M)
+    ("tri_skew_p8", np.array([[20.0, 2.0, 1.0], [0.0, 19.0, 1.5], [0.0, 0.0, 25.0]]),
+     400, 11, 1e-7, 8, 4.0, (64, 64, 80)),
+    ("tri_skew_p6", np.array([[20.0, 2.0, 1.0], [0.0, 19.0, 1.5], [0.0, 0.0, 25.0]]),
+     400, 12, 1e-5, 6, 4.0, (48, 48, 60)),
+    ("tri_flex_p7", np.array([[6.0, 1.2, -0.8], [0.0, 6.5, 0.9], [0.0, 0.0, 7.0]]),
+     32, 13, 1e-6, 7, 1.5, (44, 48, 52)),
+]
+
+
+def triclinic_cases():
+    """Exact mode sums (reference direct_ksum, any cell) that pin the
+    triclinic mesh extension at the Delta level."""
+    for (name, h, n, seed, delta, P, r_c, M) in TRICLINIC:
+        rng = np.random.default_rng(seed)
+        raw = rng.uniform(0.0, 1.0, (n, 3)) @ h.T
+        pos = workloads.wrap_positions(h, raw)
+        q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+        basis = build_pswf(solve_bandwidth(delta))
+        kern = SplitKernel(basis=basis, r_c=r_c)
+        cell = Cell(h)
+        sys_ = ParticleSystem(cell=cell, positions=raw, charges=q)
+        assert np.array_equal(sys_.positions, pos)
+        e_d, f_d, p_d = direct_ksum(sys_, kern)
+        save(name, pos=pos, q=q, h=h, M=np.array(M), P=P, delta=delta, r_c=r_c,
+             E_direct=e_d, F_direct=f_d, Pt_direct=p_d, versions=VERSIONS)
+
+
+def window_tables():
+    """Reference window tables for P in 2..12 at a few tolerances."""
+    rows = {}
+    for delta in (1e-3, 1e-5, 1e-7, 1e-9):
+        basis = build_pswf(solve_bandwidth(delta))
+        for P in (2, 3, 4, 5, 6, 7, 8, 10, 12):
+            w = tabulate_window(basis, P)
+            rows[f"d{delta:g}_P{P}_c"] = w.value.c
+            rows[f"d{delta:g}_P{P}_x"] = w.value.x
+            rows[f"d{delta:g}_P{P}_dc"] = w.deriv.c
+        rows[f"d{delta:g}_legendre"] = basis.legendre_coeffs
+        rows[f"d{delta:g}_consts"] = np.array([basis.c, basis.lambda0, basis.C0,
+                                               basis.psi0_at_zero])
+    save("window_tables", versions=VERSIONS, **rows)
+
+
+if __name__ == "__main__":
+    window_tables()
+    small_cases()
+    triclinic_cases()
+    configs()

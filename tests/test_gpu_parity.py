@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference
+goldens and the CPU oracle.
+
+Tolerances (north star): fp64 energy / pressure (Frobenius) / forces (rms
+relative over atoms) within 1e-10; fp32 mode within 1e-5.  Spread grids
+are compared at 1e-13 of the grid's max.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import SMALL_CASES, TRI_CASES, golden
+from oracle import esp_oracle as O
+from paper_2601_00161_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+F64_TOL = 1e-10
+F32_TOL = 1e-5
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _plan_for(g, M=None, precision="fp64", deterministic=True, capacity=1 << 12):
+    from paper_2601_00161_b200 import EspPlan, build_pswf, tabulate_window
+    b = build_pswf(float(g["c"])) if "c" in g else None
+    if b is None:
+        from paper_2601_00161_b200 import solve_bandwidth
+        b = build_pswf(solve_bandwidth(float(g["delta"])))
+    P = int(g["P"])
+    w = tabulate_window(b, P)
+    plan = EspPlan(tuple(M if M is not None else g["M"]), P, w, b, float(g["r_c"]),
+                   precision=precision, deterministic=deterministic, capacity=capacity)
+    plan.set_cell(g["h"])
+    return plan
+
+
+def _dev(torch, a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
+
+
+def _run(plan, pos, q, want_forces=True):
+    torch = _torch()
+    from paper_2601_00161_b200.plan import out7_to_tensor
+    out7, F = plan.evaluate(_dev(torch, pos), _dev(torch, q), want_forces)
+    E, Pt = out7_to_tensor(out7)
+    return E, Pt, (F.cpu().numpy() if F is not None else None)
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_spread_grid_matches_reference(name):
+    torch = _torch()
+    g = golden(name)
+    plan = _plan_for(g)
+    grid = plan.spread(_dev(torch, g["pos"]), _dev(torch, g["q"]))
+    got = grid.permute(2, 1, 0).cpu().numpy()           # device [z][y][x] -> [x][y][z]
+    ref = g["grid"]
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_small_cases_energy_pressure_forces(name):
+    g = golden(name)
+    plan = _plan_for(g)
+    E, Pt, F = _run(plan, g["pos"], g["q"])
+    assert O.rel_scalar(E, g["E"]) <= F64_TOL
+    assert O.rel_frobenius(Pt, g["Pt"]) <= F64_TOL
+    if np.any(g["F"]):
+        assert O.rms_rel_forces(F, g["F"]) <= F64_TOL
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_configs_match_reference_goldens(idx):
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    g = golden(f"cfg{idx}")
+    w, pos, q = workloads.generate(idx)
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                          fixed_M=w.M, cell_type=w.cell_type))
+    r = s.evaluate(pos, q)
+    assert O.rel_scalar(r.energy, g["E"]) <= F64_TOL
+    assert O.rel_frobenius(r.pressure, g["Pt"]) <= F64_TOL
+    assert O.rms_rel_forces(r.forces[g["F_idx"]], g["F_sel"]) <= F64_TOL
+    if idx == 0:
+        plan = s.plan
+        torch = _torch()
+        grid = plan.spread(_dev(torch, pos), _dev(torch, q)).permute(2, 1, 0).cpu().numpy()
+        assert np.max(np.abs(grid - g["grid"])) <= 1e-13 * np.max(np.abs(g["grid"]))
+
+
+def test_pressure_only_path_is_one_forward_fft():
+    """Energy + full pressure tensor ride on one forward transform and no
+    inverse (test_mesh.py:163-172), through the drop-in mesh API."""
+    _torch()
+    from paper_2601_00161_b200 import (Cell, ParticleSystem, SplitKernel, TransformProvider,
+                                       build_pswf, forward_density, long_range_energy,
+                                       long_range_forces, long_range_pressure, plan_grid,
+                                       solve_bandwidth)
+    g = golden("small_brick_p6")
+    b = build_pswf(solve_bandwidth(float(g["delta"])))
+    kern = SplitKernel(basis=b, r_c=float(g["r_c"]))
+    cell = Cell(g["h"])
+    spec = plan_grid(cell, kern, delta_spread=float(g["delta"]), P=int(g["P"]),
+                     spread_basis=b, fixed_M=tuple(g["M"]))
+    sys = ParticleSystem(cell=cell, positions=g["pos"], charges=g["q"])
+    prov = TransformProvider()
+    rho_hat = forward_density(sys, spec, prov)
+    E = long_range_energy(rho_hat, kern, spec, cell)
+    Pt = long_range_pressure(rho_hat, kern, spec, cell)
+    assert prov.forward_count == 1 and prov.inverse_count == 0
+    assert O.rel_scalar(E, g["E"]) <= F64_TOL
+    assert O.rel_frobenius(Pt, g["Pt"]) <= F64_TOL
+    F = long_range_forces(rho_hat, sys, kern, spec, cell, provider=prov)
+    assert prov.forward_count == 1 and prov.inverse_count == 3
+    assert O.rms_rel_forces(F, g["F"]) <= F64_TOL
+    # the spectrum itself: masked full-spectrum values vs the reference
+    full = rho_hat.full()
+    plan = O.make_plan(g["h"], tuple(g["M"]), int(g["P"]), float(g["delta"]), float(g["r_c"]))
+    m = O.Modes(plan)
+    ref = g["rho_hat_masked"]
+    assert np.max(np.abs(full[m.mask] - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_wrong_space_rejected():
+    _torch()
+    from paper_2601_00161_b200 import (Cell, MeshError, ParticleSystem, SplitKernel,
+                                       build_pswf, long_range_energy, long_range_forces,
+                                       long_range_pressure, plan_grid, solve_bandwidth,
+                                       spread_charges)
+    b = build_pswf(solve_bandwidth(1e-4))
+    kern = SplitKernel(basis=b, r_c=1.0)
+    cell = Cell.orthorhombic([6.0, 6.0, 6.0])
+    spec = plan_grid(cell, kern, delta_spread=1e-4, P=5, oversampling=2.0, spread_basis=b)
+    pos, q = workloads.random_neutral_system(8, [6.0] * 3, seed=2)
+    sys = ParticleSystem(cell=cell, positions=pos, charges=q)
+    rho = spread_charges(sys, spec)
+    for fn in (long_range_energy, long_range_pressure):
+        with pytest.raises(MeshError):
+            fn(rho, kern, spec, cell)
+    with pytest.raises(MeshError):
+        long_range_forces(rho, sys, kern, spec, cell)
+
+
+def test_ik_forces_conserve_momentum():
+    g = golden("small_brick_p8")
+    plan = _plan_for(g)
+    _, _, F = _run(plan, g["pos"], g["q"])
+    assert np.linalg.norm(F.sum(axis=0)) < 1e-10 * np.linalg.norm(F, axis=1).max()
+    w, pos, q = workloads.generate(1)
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M))
+    F = s.evaluate(pos, q).forces
+    assert np.linalg.norm(F.sum(axis=0)) < 1e-10 * np.linalg.norm(F, axis=1).max()
+
+
+def test_deterministic_bitwise():
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    w, pos, q = workloads.generate(1)
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M))
+    P_, Q_ = _dev(torch, pos), _dev(torch, q)
+    a7, aF = s.evaluate_device(P_, Q_)
+    a7, aF = a7.clone(), aF.clone()
+    perm = torch.randperm(P_.shape[0], device="cuda")
+    for _ in range(3):
+        b7, bF = s.evaluate_device(P_, Q_)
+        assert torch.equal(a7, b7) and torch.equal(aF, bF)
+    # a permuted particle order gives the same physics to round-off
+    c7, cF = s.evaluate_device(P_[perm].contiguous(), Q_[perm].contiguous())
+    assert torch.allclose(c7, a7, rtol=1e-13, atol=0)
+    assert torch.allclose(cF, aF[perm], rtol=1e-11, atol=1e-15)
+
+
+def test_fp32_mode_within_1e5():
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    for idx in (0, 1):
+        g = golden(f"cfg{idx}")
+        w, pos, q = workloads.generate(idx)
+        s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                              fixed_M=w.M, precision="fp32"))
+        r = s.evaluate(pos, q)
+        assert O.rel_scalar(r.energy, g["E"]) <= F32_TOL
+        assert O.rel_frobenius(r.pressure, g["Pt"]) <= F32_TOL
+        assert O.rms_rel_forces(r.forces[g["F_idx"]], g["F_sel"]) <= F32_TOL
+
+
+@pytest.mark.parametrize("name,M", TRI_CASES)
+def test_triclinic_matches_oracle(name, M):
+    g = golden(name)
+    plan = _plan_for(g, M=M)
+    E, Pt, F = _run(plan, g["pos"], g["q"])
+    op = O.make_plan(g["h"], M, int(g["P"]), float(g["delta"]), float(g["r_c"]))
+    oE, oP, oF = O.kspace(op, g["pos"], g["q"])
+    assert O.rel_scalar(E, oE) <= F64_TOL
+    assert O.rel_frobenius(Pt, oP) <= F64_TOL
+    assert O.rms_rel_forces(F, oF) <= F64_TOL
+    tol = 50 * float(g["delta"])
+    assert O.rel_scalar(E, g["E_direct"]) <= tol
+    assert O.rms_rel_forces(F, g["F_direct"]) <= tol
+
+
+def test_edge_particles_on_faces_and_capacity_growth():
+    torch = _torch()
+    g = golden("small_brick_p7")           # odd P: round-half-even anchors
+    plan = _plan_for(g, capacity=4)
+    L = np.diag(g["h"])
+    h = L / np.asarray(g["M"])
+    pos = np.array([[0.0, 0.0, 0.0], [np.nextafter(L[0], 0), 1.0, 2.0],
+                    [2.5 * h[0], 3.5 * h[1], 0.5 * h[2]],      # exact .5: ties to even
+                    [L[0] / 2, L[1] / 2, np.nextafter(L[2], 0)]])
+    q = np.array([1.0, -0.5, 0.75, -1.25])
+    pos = workloads.wrap_positions(g["h"], pos)
+    E, Pt, F = _run(plan, pos, q)
+    op = O.make_plan(g["h"], tuple(g["M"]), int(g["P"]), float(g["delta"]), float(g["r_c"]))
+    oE, oP, oF = O.kspace(op, pos, q)
+    assert O.rel_scalar(E, oE) <= F64_TOL
+    assert O.rel_frobenius(Pt, oP) <= F64_TOL
+    assert O.rms_rel_forces(F, oF) <= F64_TOL
+    # grow past the initial capacity of 4
+    E2, P2, F2 = _run(plan, g["pos"], g["q"])
+    assert O.rel_scalar(E2, g["E"]) <= F64_TOL
+    # empty system: zero energy, pressure
+    empty = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    out7, _ = plan.evaluate(empty, torch.zeros(0, dtype=torch.float64, device="cuda"),
+                            want_forces=True)
+    assert torch.count_nonzero(out7).item() == 0
+
+
+def test_counters_and_launch_count():
+    g = golden("small_cube_p6")
+    plan = _plan_for(g)
+    plan.reset_counters()
+    _run(plan, g["pos"], g["q"], want_forces=False)
+    assert plan.counters() == (1, 0)
+    _run(plan, g["pos"], g["q"], want_forces=True)
+    assert plan.counters() == (2, 3)
+    assert plan.launches_last_step() >= 7
+
+
+@pytest.mark.slow
+def test_config4_geometry_subset_against_oracle():
+    """384^3 grid, P=8 (config 4 geometry) with a 60k-charge subset: the full
+    CUDA pipeline against the oracle at the north-star tolerances."""
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    w = workloads.workload(4)
+    rng = np.random.default_rng(44)
+    n = 60_000
+    pos = workloads.wrap_positions(w.h, rng.uniform(0, 300.0, (n, 3)))
+    q = np.where(np.arange(n) % 2 == 0, 0.7, -0.7)
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M))
+    r = s.evaluate(pos, q)
+    op = O.make_plan(w.h, w.M, w.P, w.delta, w.r_c)
+    oE, oP, oF = O.kspace(op, pos, q)
+    assert O.rel_scalar(r.energy, oE) <= F64_TOL
+    assert O.rel_frobenius(r.pressure, oP) <= F64_TOL
+    assert O.rms_rel_forces(r.forces, oF) <= F64_TOL
