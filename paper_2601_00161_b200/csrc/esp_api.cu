@@ -76,7 +76,7 @@ static void free_all(esp_plan* p) {
                   p->d_u_tmp,   p->d_q_tmp,    p->d_idx_tmp, p->d_cub,     p->d_scratch,
                   p->d_grid,    p->d_spec,     p->d_ikspec,  p->d_fields,  p->d_axis_k,
                   p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
-                  p->d_partials, p->d_err};
+                  p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_fwd) cufftDestroy(p->fwd);
@@ -84,6 +84,8 @@ static void free_all(esp_plan* p) {
   if (p->have_inv1) cufftDestroy(p->inv1);
   if (p->profiling)
     for (int i = 0; i < 48; ++i) cudaEventDestroy(p->ev[i]);
+  delete p->h_fast;
+  p->h_fast = nullptr;
 }
 
 extern "C" {
@@ -150,7 +152,7 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
     delete p;
     return ESP_ERR_PARAM;
   }
-  int tz = d->tile[2] > 0 ? d->tile[2] : (d->M[2] <= 128 ? 16 : 32);
+  int tz = d->tile[2] > 0 ? d->tile[2] : 8;
   p->TZ = std::min(tz, d->M[2]);
   p->PZ = p->TZ + d->P - 1;
   p->ntx = (d->M[0] + p->TX - 1) / p->TX;
@@ -221,6 +223,46 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(cudaMalloc(&p->d_ikspec, 3 * 2 * real_sz * (size_t)p->H));
   TRY(cudaMalloc(&p->d_fields, 3 * real_sz * (size_t)p->G));
   TRY(dalloc(&p->d_err, 4));
+  // fast window table (kernel parameter) and deterministic-combine tables
+  p->h_fast = new esp::FastTab;
+  std::memset(p->h_fast, 0, sizeof(esp::FastTab));
+  if (p->n_pieces == p->P && p->ncoef == esp::kFastNC && p->P <= esp::kFastMaxP) {
+    p->h_fast->enabled = 1;
+    for (size_t i = 0; i < nt; ++i) {
+      p->h_fast->c[i] = d->h_window_coef[i];
+      p->h_fast->cf[i] = (float)d->h_window_coef[i];
+    }
+    for (int i = 0; i <= p->n_pieces; ++i) p->h_fast->brk[i] = d->h_window_breaks[i];
+  }
+  {
+    std::vector<int> ent_all, cnt_all;
+    const int T[3] = {p->TX, p->TY, p->TZ};
+    const int E[3] = {esp::kPad, esp::kPad, p->PZ};
+    const int NT[3] = {p->ntx, p->nty, p->ntz};
+    long long off = 0;
+    for (int a = 0; a < 3; ++a) {
+      std::vector<int> ent, cnt;
+      esp::build_combine_axis(p->M[a], T[a], E[a], NT[a], p->lo, ent, cnt);
+      for (int c : cnt) {
+        if (c > esp::kCombW) {
+          set_error("grid too small for the tile decomposition (combine width)");
+          free_all(p);
+          delete p;
+          return ESP_ERR_PLANNING;
+        }
+      }
+      p->comb_off[a] = off;
+      off += p->M[a];
+      ent_all.insert(ent_all.end(), ent.begin(), ent.end());
+      cnt_all.insert(cnt_all.end(), cnt.begin(), cnt.end());
+    }
+    TRY(dalloc(&p->d_comb_ent, ent_all.size()));
+    TRY(dalloc(&p->d_comb_cnt, cnt_all.size()));
+    TRY(cudaMemcpy(p->d_comb_ent, ent_all.data(), sizeof(int) * ent_all.size(),
+                   cudaMemcpyHostToDevice));
+    TRY(cudaMemcpy(p->d_comb_cnt, cnt_all.data(), sizeof(int) * cnt_all.size(),
+                   cudaMemcpyHostToDevice));
+  }
 #undef TRY
   // cuFFT plans: [z][y][x] row-major, x fastest.
   const cufftType fwd_t = p->precision == ESP_FP64 ? CUFFT_D2Z : CUFFT_R2C;

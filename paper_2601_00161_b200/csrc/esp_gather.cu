@@ -1,16 +1,22 @@
 // esp_gather.cu — force interpolation (mesh.py:213-218 `_gather`, used by
 // long_range_forces ik mode, mesh.py:336-342).
 //
-// The transpose of the spread tile kernel: the same CTA/tile decomposition
-// and column ownership, but each thread holds a P-deep sliding window of the
-// three ik field values of its (x, y) column in registers.  For each particle
-// whose stencil touches the warp's 8 x 4 column block, a lane forms
-//   part_c = wx*wy * sum_s wz[s] * field_c[z_s]        (c = x, y, z)
-// and the warp reduces (part_x, part_y, part_z) with a transposed butterfly
-// (12 shuffles instead of 30).  Warp partials land in a per-(particle, warp)
-// shared-memory slot and are summed in fixed warp order, so forces are
-// bitwise reproducible.  F_c = -q * sum (the h3 factors of mesh.py:341-342
-// cancel; the 1/G of the inverse transform is folded into the spectrum).
+// k_gather_warp (P <= 8, the production path): CTA = one anchor tile (the
+// spread's decomposition).  The CTA stages the padded field tile — the three
+// ik fields on 16 x 16 columns x PZ planes — in shared memory once, then each
+// warp takes one particle at a time: lane (i, j) owns stencil columns
+// (i, j) and (i, j+4), dots the P z-values of the three fields with wz, and
+// the warp reduces (F_x, F_y, F_z) with a transposed butterfly.  Rows are
+// XOR-swizzled by 8 columns on odd y so every LDS phase is bank-conflict
+// free.  Each particle is owned by exactly one warp: no atomics, fixed
+// reduction order, bitwise reproducible.
+//
+// k_gather_ik (P > 8): column-owner variant — each thread holds a P-deep
+// sliding window of the three fields of one padded column in registers and
+// warps reduce per-particle partials.
+//
+// F_c = -q * sum (the h3 factors of mesh.py:341-342 cancel; the 1/G of the
+// inverse transform is folded into the spectrum).
 #include "esp_internal.cuh"
 
 namespace esp {
@@ -54,6 +60,145 @@ __device__ __forceinline__ real warp_reduce3(real v0, real v1, real v2, int lane
   k += __shfl_xor_sync(full, k, 2);
   k += __shfl_xor_sync(full, k, 1);
   return k;
+}
+
+
+template <typename real> struct Real2;
+template <> struct Real2<double> { using type = double2; };
+template <> struct Real2<float> { using type = float2; };
+
+template <typename real, int P>
+struct GatherLayout {
+  static size_t bytes(int PZ, int n_pieces, int ncoef) {
+    size_t b = sizeof(real) * (size_t)n_pieces * ncoef;
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(double) * (size_t)(n_pieces + 1);
+    b = (b + 15) & ~size_t(15);
+    b += 2 * sizeof(real) * (size_t)PZ * kPad * kPad;   // (f_x, f_y) pairs
+    b += sizeof(real) * (size_t)PZ * kPad * kPad;       // f_z
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(real) * (size_t)kGChunk * 24;           // weights [pl][3][8]
+    b += sizeof(int) * 3 * (size_t)kGChunk;             // anchors
+    return b;
+  }
+};
+
+__device__ __forceinline__ int swz(int x, int y) { return y * kPad + ((x + 8 * (y & 1)) & 15); }
+
+template <typename real, int P>
+__global__ void __launch_bounds__(kTileThreads, 2)
+k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
+              const double* __restrict__ brk, int n_pieces, int ncoef,
+              const int* __restrict__ offsets, const double* __restrict__ U,
+              const double* __restrict__ Q, const int* __restrict__ IDX, long long cap,
+              const real* __restrict__ fld, long long G, double* __restrict__ forces) {
+  static_assert(P <= 8, "warp gather covers at most 8 stencil columns per axis");
+  using R2 = typename Real2<real>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tile = blockIdx.x;
+  const int tz = tile % g.ntz;
+  const int txy = tile / g.ntz;
+  const int tx = txy % g.ntx, ty = txy / g.ntx;
+  const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+  const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+  const long long p0 = offsets[key0], p1 = offsets[key1];
+  if (p0 == p1) return;
+
+  real* s_tab = reinterpret_cast<real*>(smem_raw);
+  size_t off = sizeof(real) * (size_t)n_pieces * ncoef;
+  off = (off + 15) & ~size_t(15);
+  double* s_brk = reinterpret_cast<double*>(smem_raw + off);
+  off += sizeof(double) * (size_t)(n_pieces + 1);
+  off = (off + 15) & ~size_t(15);
+  const int plane = kPad * kPad;
+  R2* s_f01 = reinterpret_cast<R2*>(smem_raw + off);
+  off += 2 * sizeof(real) * (size_t)g.PZ * plane;
+  real* s_f2 = reinterpret_cast<real*>(smem_raw + off);
+  off += sizeof(real) * (size_t)g.PZ * plane;
+  off = (off + 15) & ~size_t(15);
+  real* s_w = reinterpret_cast<real*>(smem_raw + off);
+  off += sizeof(real) * (size_t)kGChunk * 24;
+  int* s_anc = reinterpret_cast<int*>(smem_raw + off);
+
+  for (int i = threadIdx.x; i < n_pieces * ncoef; i += blockDim.x) s_tab[i] = tab[i];
+  for (int i = threadIdx.x; i <= n_pieces; i += blockDim.x) s_brk[i] = brk[i];
+
+  // Stage the padded field tile (rows of 16 consecutive x: coalesced).
+  const real* f0 = fld;
+  const real* f1 = fld + G;
+  const real* f2 = fld + 2 * G;
+  const long long Mxy = (long long)g.M[0] * g.M[1];
+  for (int e = threadIdx.x; e < g.PZ * plane; e += blockDim.x) {
+    const int pz = e / plane, r = e - pz * plane;
+    const int y = r / kPad, x = r - y * kPad;
+    const int gx = wrap_index((long long)tx * g.TX + g.lo + x, g.M[0]);
+    const int gy = wrap_index((long long)ty * g.TY + g.lo + y, g.M[1]);
+    const int gz = wrap_index((long long)tz * g.TZ + g.lo + pz, g.M[2]);
+    const long long o = gz * Mxy + (long long)gy * g.M[0] + gx;
+    const int ph = pz * plane + swz(x, y);
+    R2 v;
+    v.x = f0[o];
+    v.y = f1[o];
+    s_f01[ph] = v;
+    s_f2[ph] = f2[o];
+  }
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int li = lane & 7, lj = lane >> 3;
+
+  for (long long c0 = p0; c0 < p1; c0 += kGChunk) {
+    const int n = (int)min((long long)kGChunk, p1 - c0);
+    __syncthreads();
+    for (int item = threadIdx.x; item < 3 * n; item += blockDim.x) {
+      const int d = item / n, pl = item - d * n;
+      const double u = U[d * cap + c0 + pl];
+      const double base = anchor_base(g, u);
+      const int a = wrap_index((long long)base, g.M[d]);
+      const int org = d == 0 ? tx * g.TX : (d == 1 ? ty * g.TY : tz * g.TZ);
+      s_anc[d * kGChunk + pl] = a - org;
+      real w[P];
+      stencil_weights<real, P>(ft, s_tab, s_brk, n_pieces, ncoef, u, base, g.lo, real(1), w);
+      real* dst = s_w + (size_t)pl * 24 + d * 8;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dst[s] = s < P ? w[s < P ? s : 0] : real(0);
+    }
+    __syncthreads();
+    for (int pl = warp; pl < n; pl += kTileThreads / 32) {
+      const int xl = s_anc[pl];
+      const int yl = s_anc[kGChunk + pl];
+      const int zl = s_anc[2 * kGChunk + pl];
+      const real* W = s_w + (size_t)pl * 24;
+      const real wx = W[li];
+      const real wy0 = W[8 + lj];
+      const real wy1 = W[8 + ((lj + 4) & 7)] * (real)(lj + 4 < P);
+      const int x = min(xl + li, kPad - 1);
+      const int ya = min(yl + lj, kPad - 1), yb = min(yl + lj + 4, kPad - 1);
+      const int ca = swz(x, ya), cb = swz(x, yb);
+      real ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const real wz = W[16 + s];
+        const int pb = (zl + s) * plane;
+        const R2 va = s_f01[pb + ca];
+        const R2 vb = s_f01[pb + cb];
+        const real za = s_f2[pb + ca];
+        const real zb = s_f2[pb + cb];
+        ax = fma(wz, va.x, ax);
+        ay = fma(wz, va.y, ay);
+        az = fma(wz, za, az);
+        bx = fma(wz, vb.x, bx);
+        by = fma(wz, vb.y, by);
+        bz = fma(wz, zb, bz);
+      }
+      const real ka = wx * wy0, kb = wx * wy1;
+      const real v = warp_reduce3<real>(fma(ka, ax, kb * bx), fma(ka, ay, kb * by),
+                                        fma(ka, az, kb * bz), lane);
+      if ((lane & 7) == 0 && lane < 24) {
+        const long long id = IDX[c0 + pl];
+        forces[id * 3 + (lane >> 3)] = -Q[c0 + pl] * (double)v;
+      }
+    }
+  }
 }
 
 template <typename real, int P>
@@ -190,14 +335,39 @@ static size_t gather_smem(int P, int n_pieces, int ncoef) {
 template <typename real, int P>
 static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   Geom g = make_geom(p);
+  if constexpr (P <= 8) {
+    const real* tab = std::is_same<real, double>::value
+                          ? reinterpret_cast<const real*>(p->d_tab)
+                          : reinterpret_cast<const real*>(p->d_tabf);
+    const size_t smem = GatherLayout<real, P>::bytes(p->PZ, p->n_pieces, p->ncoef);
+    static size_t attr_set = 0;  // set once per instantiation (capture-safe)
+    if (smem > attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(k_gather_warp<real, P>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_set = smem;
+    }
+    k_gather_warp<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
+        g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u,
+        p->d_q, p->d_idx, p->cap, reinterpret_cast<const real*>(p->d_fields), p->G,
+        d_forces);
+    p->launches++;
+    prof_mark(p, s, "gather");
+    return cudaGetLastError();
+  }
   const real* tab = std::is_same<real, double>::value
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
   const size_t smem = gather_smem<real>(P, p->n_pieces, p->ncoef);
-  cudaError_t e = cudaFuncSetAttribute(k_gather_ik<real, P>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+  static size_t attr_set = 0;  // set once per instantiation (capture-safe)
+  if (smem > attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gather_ik<real, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = smem;
+  }
   k_gather_ik<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
       g, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->d_q,
       p->d_idx, p->cap, reinterpret_cast<const real*>(p->d_fields), p->G, d_forces);

@@ -16,7 +16,8 @@ namespace esp {
 
 constexpr int kPad = 16;          // padded columns per tile along x and y
 constexpr int kTileThreads = 256; // kPad * kPad column owners per CTA
-constexpr int kChunk = 256;       // particles staged per CTA pass
+constexpr int kChunk = 256;       // particles staged per CTA pass (spread)
+constexpr int kGChunk = 64;       // particles staged per CTA pass (gather)
 constexpr int kMaxCoef = 25;      // window table degree + 1 (reference: 19)
 constexpr int kMaxPieces = 64;    // window pieces (P * pieces-per-unit)
 constexpr int kRedThreads = 256;
@@ -115,6 +116,67 @@ __device__ __forceinline__ double legval(double x, const double* c, int n) {
   return __dadd_rn(c0, __dmul_rn(c1, x));
 }
 
+// Fast path for the common table shape (one degree-18 piece per unit
+// interval, P <= 12): the coefficients travel as a kernel parameter, so the
+// unrolled Horner chains read them straight from the constant bank (no
+// shared-memory loads).  Stencil offset s always falls in piece P-1-s; the
+// rare tie on a piece boundary drops to the general search.
+constexpr int kFastNC = 19;
+constexpr int kFastMaxP = 12;
+struct FastTab {
+  double c[kFastMaxP * kFastNC];
+  float cf[kFastMaxP * kFastNC];
+  double brk[kFastMaxP + 1];
+  int enabled;
+};
+
+template <typename real> __device__ __forceinline__ const real* fast_coef(const FastTab& t);
+template <> __device__ __forceinline__ const double* fast_coef<double>(const FastTab& t) { return t.c; }
+template <> __device__ __forceinline__ const float* fast_coef<float>(const FastTab& t) { return t.cf; }
+
+// w[s] = qf * W(u - (base + lo + s)), s = 0..P-1.
+template <typename real, int P>
+__device__ __forceinline__ void stencil_weights(const FastTab& ft, const real* s_tab,
+                                                const double* s_brk, int n_pieces,
+                                                int ncoef, double u, double base, int lo,
+                                                real qf, real* w) {
+  if (ft.enabled) {
+    const real* C = fast_coef<real>(ft);
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const double t = u - (base + (double)(lo + s));
+      const int j = P - 1 - s;
+      const bool ok = t >= ft.brk[j] && t < ft.brk[j + 1];
+      real v;
+      if (ok) {
+        const real x = (real)(t - ft.brk[j]);
+        real acc = C[j * kFastNC];
+#pragma unroll
+        for (int m = 1; m < kFastNC; ++m) acc = fma(acc, x, C[j * kFastNC + m]);
+        v = acc;
+      } else {
+        v = window_eval<real>(s_tab, s_brk, n_pieces, ncoef, t);
+      }
+      w[s] = v * qf;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const double t = u - (base + (double)(lo + s));
+      w[s] = window_eval<real>(s_tab, s_brk, n_pieces, ncoef, t) * qf;
+    }
+  }
+}
+
+// Per-axis candidate (tile, padded index) pairs for the deterministic halo
+// combine, precomputed at plan creation: entry [c*kCombW + k] =
+// tile | pad << 16, count in cnt[c].
+constexpr int kCombW = 8;
+struct CombineTabs {
+  const int* ent[3];
+  const int* cnt[3];
+};
+
 template <typename T> struct Cplx;
 template <> struct Cplx<double> { using type = double2; };
 template <> struct Cplx<float> { using type = float2; };
@@ -167,6 +229,10 @@ struct esp_plan {
   double *d_modeA, *d_modeB;
   double* d_partials;
   int* d_err;
+  int* d_comb_ent;        // combine candidate tables (3 axes)
+  int* d_comb_cnt;
+  long long comb_off[3];
+  esp::FastTab* h_fast;   // host copy of the fast window table (kernel param)
   cufftHandle fwd, inv3, inv1;
   int have_fwd, have_inv3, have_inv1;
   long long fwd_count, inv_count;
@@ -192,6 +258,8 @@ cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
                                 cudaStream_t s);
 cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s);
 cudaError_t launch_mode_setup(esp_plan* p, double what_zero, cudaStream_t s);
+void build_combine_axis(int M, int T, int E, int nt, int lo, std::vector<int>& ent,
+                        std::vector<int>& cnt);
 
 void set_error(const std::string& msg);
 

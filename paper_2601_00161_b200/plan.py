@@ -341,6 +341,34 @@ class EspPlan:
     def launches_last_step(self) -> int:
         return int(self.info()[5])
 
+    # -- CUDA graphs ---------------------------------------------------------
+    def graph(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool,
+              out7: torch.Tensor, forces: torch.Tensor | None, pre=None, post=None):
+        """Capture one whole step (optionally with caller copies before/after)
+        into a CUDA graph and return it; ``g.replay()`` re-runs the step on the
+        same buffers with a single launch from the host."""
+        pos, q = self._check_particles(pos, q)
+        self.ensure_capacity(pos.shape[0])
+
+        def body():
+            if pre is not None:
+                pre()
+            self.evaluate(pos, q, want_forces, out7, forces)
+            if post is not None:
+                post()
+
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            body()                      # warm-up: kernel attributes, cuFFT work areas
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        torch.cuda.synchronize()
+        return g
+
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.lib().esp_set_profiling(self._handle, int(bool(on))), "esp_set_profiling")
 

@@ -124,6 +124,27 @@ class KSpaceSolver:
         synchronising.  out7 = [E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz] (prefactor 1)."""
         return self.plan.evaluate(positions, charges, want_forces, out7, forces, stream)
 
+    def graphed(self, positions: torch.Tensor, charges: torch.Tensor,
+                want_forces: bool = True, out7=None, forces=None):
+        """Capture the device step on fixed buffers into a CUDA graph.
+        Returns (graph, out7, forces); ``graph.replay()`` recomputes them after
+        the caller updates ``positions`` / ``charges`` in place."""
+        n = positions.shape[0]
+        out7 = out7 if out7 is not None else torch.empty(7, dtype=torch.float64,
+                                                         device=positions.device)
+        if want_forces and forces is None:
+            forces = torch.empty((n, 3), dtype=torch.float64, device=positions.device)
+        g = self.plan.graph(positions, charges, want_forces, out7, forces)
+        return g, out7, forces
+
+    def host_stepper(self, n: int, want_forces: bool = True):
+        """Public host-buffer path: pinned host inputs -> device step ->
+        pinned host outputs, captured as one CUDA graph (H2D copies, the
+        k-space step and D2H copies).  Returns an object with pinned
+        ``positions`` (N,3), ``charges`` (N,), ``forces`` (N,3), ``out7`` (7,)
+        and ``step()`` (replay + synchronise)."""
+        return _HostStepper(self, n, want_forces)
+
     def evaluate(self, positions, charges, want_forces: bool = True,
                  want_pressure: bool = True) -> KSpaceResult:
         host = not isinstance(positions, torch.Tensor)
@@ -142,6 +163,43 @@ class KSpaceSolver:
     def pressure_only(self, positions, charges):
         r = self.evaluate(positions, charges, want_forces=False)
         return r.energy, r.pressure
+
+
+class _HostStepper:
+    def __init__(self, solver: "KSpaceSolver", n: int, want_forces: bool):
+        f64 = torch.float64
+        self.positions = torch.empty((n, 3), dtype=f64).pin_memory()
+        self.charges = torch.empty(n, dtype=f64).pin_memory()
+        self.forces = torch.empty((n, 3), dtype=f64).pin_memory()
+        self.out7 = torch.empty(7, dtype=f64).pin_memory()
+        self._d_pos = torch.empty((n, 3), dtype=f64, device="cuda")
+        self._d_q = torch.empty(n, dtype=f64, device="cuda")
+        self._d_out7 = torch.empty(7, dtype=f64, device="cuda")
+        self._d_F = torch.empty((n, 3), dtype=f64, device="cuda") if want_forces else None
+        self.want_forces = want_forces
+        self.h2d_bytes = (3 * n + n) * 8
+        self.d2h_bytes = (3 * n * 8 if want_forces else 0) + 7 * 8
+
+        def pre():
+            self._d_pos.copy_(self.positions, non_blocking=True)
+            self._d_q.copy_(self.charges, non_blocking=True)
+
+        def post():
+            if want_forces:
+                self.forces.copy_(self._d_F, non_blocking=True)
+            self.out7.copy_(self._d_out7, non_blocking=True)
+
+        self.graph = solver.plan.graph(self._d_pos, self._d_q, want_forces, self._d_out7,
+                                       self._d_F, pre=pre, post=post)
+
+    def launch(self):
+        """Enqueue one step (no host synchronisation)."""
+        self.graph.replay()
+
+    def step(self):
+        self.graph.replay()
+        torch.cuda.current_stream().synchronize()
+        return self.out7, (self.forces if self.want_forces else None)
 
 
 @dataclass
