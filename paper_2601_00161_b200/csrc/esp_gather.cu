@@ -3,13 +3,12 @@
 //
 // k_gather_warp (P <= 8, the production path): CTA = one anchor tile (the
 // spread's decomposition).  The CTA stages the padded field tile — the three
-// ik fields on 16 x 16 columns x PZ planes — in shared memory once, then each
-// warp takes one particle at a time: lane (i, j) owns stencil columns
-// (i, j) and (i, j+4), dots the P z-values of the three fields with wz, and
-// the warp reduces (F_x, F_y, F_z) with a transposed butterfly.  Rows are
-// XOR-swizzled by 8 columns on odd y so every LDS phase is bank-conflict
-// free.  Each particle is owned by exactly one warp: no atomics, fixed
-// reduction order, bitwise reproducible.
+// ik fields on 16 x 16 columns x PZ planes — in shared memory once; a warp
+// then handles 4 particles at a time, lane (p, k) summing particle p's
+// stencil plane k (x rows at immediate offsets) and 8 lanes reducing with
+// 3 shuffle levels.  An odd plane stride keeps the 8 planes of a particle in
+// distinct bank groups.  Each particle is owned by one lane group: no
+// atomics, fixed reduction order, bitwise reproducible.
 //
 // k_gather_ik (P > 8): column-owner variant — each thread holds a P-deep
 // sliding window of the three fields of one padded column in registers and
@@ -69,22 +68,33 @@ template <> struct Real2<float> { using type = float2; };
 
 template <typename real, int P>
 struct GatherLayout {
+  // (f_x, f_y) pairs: rows of 16, plane stride 257 (odd): the 8 planes read by
+  // one LDS.128 phase fall in 8 distinct bank groups.
+  static constexpr int kPlane = kPad * kPad + 1;
+  // f_z: rows of 24 (= 8 mod 16), plane stride 385 (= 1 mod 16): the 16 lanes
+  // of one LDS.64 phase (8 planes x 2 adjacent rows) hit 16 distinct banks.
+  static constexpr int kRowZ = 24;
+  static constexpr int kPlaneZ = kPad * kRowZ + 1;
   static size_t bytes(int PZ, int n_pieces, int ncoef) {
     size_t b = sizeof(real) * (size_t)n_pieces * ncoef;
     b = (b + 15) & ~size_t(15);
     b += sizeof(double) * (size_t)(n_pieces + 1);
     b = (b + 15) & ~size_t(15);
-    b += 2 * sizeof(real) * (size_t)PZ * kPad * kPad;   // (f_x, f_y) pairs
-    b += sizeof(real) * (size_t)PZ * kPad * kPad;       // f_z
+    b += 2 * sizeof(real) * (size_t)PZ * kPlane;   // (f_x, f_y) pairs
+    b += sizeof(real) * (size_t)PZ * kPlaneZ;      // f_z
     b = (b + 15) & ~size_t(15);
-    b += sizeof(real) * (size_t)kGChunk * 24;           // weights [pl][3][8]
-    b += sizeof(int) * 3 * (size_t)kGChunk;             // anchors
+    b += sizeof(real) * (size_t)kGChunk * 24;      // weights [pl][3][8]
+    b += sizeof(double) * (size_t)kGChunk;         // charges
+    b += sizeof(int) * 5 * (size_t)kGChunk;        // anchors x,y,z + index
     return b;
   }
 };
 
-__device__ __forceinline__ int swz(int x, int y) { return y * kPad + ((x + 8 * (y & 1)) & 15); }
-
+// Warp = 2 particles x 8 stencil planes x 2 row parities.  Lane (p, h, k)
+// sums rows j = h, h+2, .. of particle p's stencil on plane zl+k (x contiguous,
+// immediate smem offsets), weights by wz[k], and the 16 lanes of a particle
+// reduce with 4 xor-shuffle levels.  Strides make every LDS phase
+// bank-conflict free (see GatherLayout).
 template <typename real, int P>
 __global__ void __launch_bounds__(kTileThreads, 2)
 k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
@@ -92,8 +102,11 @@ k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
               const int* __restrict__ offsets, const double* __restrict__ U,
               const double* __restrict__ Q, const int* __restrict__ IDX, long long cap,
               const real* __restrict__ fld, long long G, double* __restrict__ forces) {
-  static_assert(P <= 8, "warp gather covers at most 8 stencil columns per axis");
+  static_assert(P <= 8, "warp gather covers at most 8 stencil planes");
   using R2 = typename Real2<real>::type;
+  constexpr int kPlane = GatherLayout<real, P>::kPlane;
+  constexpr int kRowZ = GatherLayout<real, P>::kRowZ;
+  constexpr int kPlaneZ = GatherLayout<real, P>::kPlaneZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tile = blockIdx.x;
   const int tz = tile % g.ntz;
@@ -110,41 +123,46 @@ k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
   double* s_brk = reinterpret_cast<double*>(smem_raw + off);
   off += sizeof(double) * (size_t)(n_pieces + 1);
   off = (off + 15) & ~size_t(15);
-  const int plane = kPad * kPad;
   R2* s_f01 = reinterpret_cast<R2*>(smem_raw + off);
-  off += 2 * sizeof(real) * (size_t)g.PZ * plane;
+  off += 2 * sizeof(real) * (size_t)g.PZ * kPlane;
   real* s_f2 = reinterpret_cast<real*>(smem_raw + off);
-  off += sizeof(real) * (size_t)g.PZ * plane;
+  off += sizeof(real) * (size_t)g.PZ * kPlaneZ;
   off = (off + 15) & ~size_t(15);
   real* s_w = reinterpret_cast<real*>(smem_raw + off);
   off += sizeof(real) * (size_t)kGChunk * 24;
-  int* s_anc = reinterpret_cast<int*>(smem_raw + off);
+  double* s_q = reinterpret_cast<double*>(smem_raw + off);
+  off += sizeof(double) * (size_t)kGChunk;
+  int* s_anc = reinterpret_cast<int*>(smem_raw + off);   // [3][kGChunk]
+  int* s_id = s_anc + 3 * kGChunk;
 
   for (int i = threadIdx.x; i < n_pieces * ncoef; i += blockDim.x) s_tab[i] = tab[i];
   for (int i = threadIdx.x; i <= n_pieces; i += blockDim.x) s_brk[i] = brk[i];
 
-  // Stage the padded field tile (rows of 16 consecutive x: coalesced).
-  const real* f0 = fld;
-  const real* f1 = fld + G;
-  const real* f2 = fld + 2 * G;
-  const long long Mxy = (long long)g.M[0] * g.M[1];
-  for (int e = threadIdx.x; e < g.PZ * plane; e += blockDim.x) {
-    const int pz = e / plane, r = e - pz * plane;
-    const int y = r / kPad, x = r - y * kPad;
-    const int gx = wrap_index((long long)tx * g.TX + g.lo + x, g.M[0]);
-    const int gy = wrap_index((long long)ty * g.TY + g.lo + y, g.M[1]);
-    const int gz = wrap_index((long long)tz * g.TZ + g.lo + pz, g.M[2]);
-    const long long o = gz * Mxy + (long long)gy * g.M[0] + gx;
-    const int ph = pz * plane + swz(x, y);
-    R2 v;
-    v.x = f0[o];
-    v.y = f1[o];
-    s_f01[ph] = v;
-    s_f2[ph] = f2[o];
+  // Stage the padded field tile.  blockDim == 256 == one 16x16 plane, so
+  // each thread owns one (x, y) column: wrap it once, then walk the planes.
+  {
+    const real* f0 = fld;
+    const real* f1 = fld + G;
+    const real* f2 = fld + 2 * G;
+    const long long Mxy = (long long)g.M[0] * g.M[1];
+    const int r = threadIdx.x;
+    const int gx = wrap_near(tx * g.TX + g.lo + (r & 15), g.M[0]);
+    const int gy = wrap_near(ty * g.TY + g.lo + (r >> 4), g.M[1]);
+    const long long col = (long long)gy * g.M[0] + gx;
+    int gz = wrap_near(tz * g.TZ + g.lo, g.M[2]);
+    for (int pz = 0; pz < g.PZ; ++pz) {
+      const long long o = gz * Mxy + col;
+      R2 v;
+      v.x = f0[o];
+      v.y = f1[o];
+      s_f01[pz * kPlane + r] = v;
+      s_f2[pz * kPlaneZ + (r >> 4) * kRowZ + (r & 15)] = f2[o];
+      gz = gz + 1 == g.M[2] ? 0 : gz + 1;
+    }
   }
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int li = lane & 7, lj = lane >> 3;
+  const int slot = lane >> 4, h = (lane >> 3) & 1, k = lane & 7;
 
   for (long long c0 = p0; c0 < p1; c0 += kGChunk) {
     const int n = (int)min((long long)kGChunk, p1 - c0);
@@ -161,41 +179,62 @@ k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
       real* dst = s_w + (size_t)pl * 24 + d * 8;
 #pragma unroll
       for (int s = 0; s < 8; ++s) dst[s] = s < P ? w[s < P ? s : 0] : real(0);
+      if (d == 0) {
+        s_q[pl] = Q[c0 + pl];
+        s_id[pl] = IDX[c0 + pl];
+      }
     }
     __syncthreads();
-    for (int pl = warp; pl < n; pl += kTileThreads / 32) {
-      const int xl = s_anc[pl];
-      const int yl = s_anc[kGChunk + pl];
-      const int zl = s_anc[2 * kGChunk + pl];
-      const real* W = s_w + (size_t)pl * 24;
-      const real wx = W[li];
-      const real wy0 = W[8 + lj];
-      const real wy1 = W[8 + ((lj + 4) & 7)] * (real)(lj + 4 < P);
-      const int x = min(xl + li, kPad - 1);
-      const int ya = min(yl + lj, kPad - 1), yb = min(yl + lj + 4, kPad - 1);
-      const int ca = swz(x, ya), cb = swz(x, yb);
-      real ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    for (int pb = warp * 2; pb < n; pb += (kTileThreads / 32) * 2) {
+      const int pl = pb + slot;
+      const bool live = pl < n && k < P;
+      real ax = 0, ay = 0, az = 0;
+      if (live) {
+        const int xl = s_anc[pl];
+        const int yl = s_anc[kGChunk + pl];
+        const int zl = s_anc[2 * kGChunk + pl];
+        const real* W = s_w + (size_t)pl * 24;
+        real wx[P];
 #pragma unroll
-      for (int s = 0; s < P; ++s) {
-        const real wz = W[16 + s];
-        const int pb = (zl + s) * plane;
-        const R2 va = s_f01[pb + ca];
-        const R2 vb = s_f01[pb + cb];
-        const real za = s_f2[pb + ca];
-        const real zb = s_f2[pb + cb];
-        ax = fma(wz, va.x, ax);
-        ay = fma(wz, va.y, ay);
-        az = fma(wz, za, az);
-        bx = fma(wz, vb.x, bx);
-        by = fma(wz, vb.y, by);
-        bz = fma(wz, zb, bz);
+        for (int s = 0; s < P; ++s) wx[s] = W[s];
+        const real wzk = W[16 + k];
+        const R2* rowp = s_f01 + (zl + k) * kPlane + (yl + h) * kPad + xl;
+        const real* rowz = s_f2 + (zl + k) * kPlaneZ + (yl + h) * kRowZ + xl;
+#pragma unroll
+        for (int jj = 0; jj < (P + 1) / 2; ++jj) {
+          const int j = 2 * jj;                 // row j + h of the stencil
+          if (j + 1 < P || h == 0) {
+            const real wy = W[8 + j + h];
+            real rx = 0, ry = 0, rz = 0;
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+              const R2 v = rowp[j * kPad + i];
+              const real vz = rowz[j * kRowZ + i];
+              rx = fma(wx[i], v.x, rx);
+              ry = fma(wx[i], v.y, ry);
+              rz = fma(wx[i], vz, rz);
+            }
+            ax = fma(wy, rx, ax);
+            ay = fma(wy, ry, ay);
+            az = fma(wy, rz, az);
+          }
+        }
+        ax *= wzk;
+        ay *= wzk;
+        az *= wzk;
       }
-      const real ka = wx * wy0, kb = wx * wy1;
-      const real v = warp_reduce3<real>(fma(ka, ax, kb * bx), fma(ka, ay, kb * by),
-                                        fma(ka, az, kb * bz), lane);
-      if ((lane & 7) == 0 && lane < 24) {
-        const long long id = IDX[c0 + pl];
-        forces[id * 3 + (lane >> 3)] = -Q[c0 + pl] * (double)v;
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        ax += __shfl_xor_sync(0xffffffffu, ax, o);
+        ay += __shfl_xor_sync(0xffffffffu, ay, o);
+        az += __shfl_xor_sync(0xffffffffu, az, o);
+      }
+      if ((lane & 15) == 0 && pl < n) {
+        const double q = s_q[pl];
+        double* f = forces + (long long)s_id[pl] * 3;
+        f[0] = -q * (double)ax;
+        f[1] = -q * (double)ay;
+        f[2] = -q * (double)az;
       }
     }
   }

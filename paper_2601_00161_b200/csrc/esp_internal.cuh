@@ -15,7 +15,8 @@
 namespace esp {
 
 constexpr int kPad = 16;          // padded columns per tile along x and y
-constexpr int kTileThreads = 256; // kPad * kPad column owners per CTA
+constexpr int kTileThreads = 256; // threads per gather CTA
+constexpr int kSpreadThreads = 128; // spread CTA: 4 warps x 8x8 columns, 2 per lane
 constexpr int kChunk = 256;       // particles staged per CTA pass (spread)
 constexpr int kGChunk = 64;       // particles staged per CTA pass (gather)
 constexpr int kMaxCoef = 25;      // window table degree + 1 (reference: 19)
@@ -71,6 +72,13 @@ __device__ __forceinline__ double anchor_base(const Geom& g, double u) {
 __device__ __forceinline__ int wrap_index(long long v, int M) {
   long long r = v % M;
   return (int)(r < 0 ? r + M : r);
+}
+
+// Periodic wrap for indices a few periods from [0, M): no division.
+__device__ __forceinline__ int wrap_near(int v, int M) {
+  while (v < 0) v += M;
+  while (v >= M) v -= M;
+  return v;
 }
 
 // W(t) from the piecewise table (pswf.py:253-258 semantics: zero outside

@@ -6,11 +6,11 @@
 //    whose stencils cover a padded block of 16 x 16 columns x PZ = TZ+P-1
 //    planes.  Its particles are a contiguous, z-anchor-sorted range of the
 //    binned arrays (esp_bin.cu).
-//  * Each of the 256 threads owns one padded (x, y) column and keeps a
-//    P-deep sliding window of z accumulators in registers.  Particles are
+//  * Each of the 128 threads owns two padded (x, y) columns and keeps a
+//    P-deep sliding window of z accumulators for each in registers.  Particles are
 //    visited in z-anchor order; when the anchor advances the window slides
 //    and the finished plane is stored (plain store, exclusive owner).  Every
-//    multiply-add in the window is useful along z; along x/y a warp (8 x 4
+//    multiply-add in the window is useful along z; along x/y a warp (8 x 8
 //    columns) only visits the particles whose stencil touches it, found by a
 //    ballot over a per-particle 8-bit warp mask staged with the weights.
 //  * 1D weights are evaluated once per particle and dimension (unrolled
@@ -25,51 +25,40 @@
 
 namespace esp {
 
+// Per-particle staging record (reals): x weights and y weights each stored
+// in a zero-padded row of RL = P + 16 entries (weight s at offset 8 + s), so a
+// lane reads its column's weight at (cx - xl + 8) with no clamp or predicate;
+// then the P z weights.  The x row carries q.
+template <int P>
+struct SpreadRec {
+  static constexpr int RL = P + 16;
+  static constexpr int kX = 0, kY = RL, kZ = 2 * RL;
+  static constexpr int kLen = ((2 * RL + P) + 1) & ~1;   // keep 16B alignment
+};
+
+constexpr int kSChunk = 128;   // particles staged per spread pass
+
 template <typename real, int P>
 struct SpreadLayout {
-  static constexpr int kWRow = P;  // weights per (particle, dim)
   static size_t bytes(int n_pieces, int ncoef) {
     size_t b = sizeof(real) * (size_t)n_pieces * ncoef;
     b = (b + 15) & ~size_t(15);
     b += sizeof(double) * (size_t)(n_pieces + 1);
     b = (b + 15) & ~size_t(15);
-    b += sizeof(real) * 3 * (size_t)kChunk * P;
-    b += sizeof(int) * 4 * (size_t)kChunk;
+    b += sizeof(real) * (size_t)kSChunk * SpreadRec<P>::kLen;
+    b += sizeof(int) * (size_t)kSChunk * (3 + 1 + 4);   // anchors, packed, 4 warp lists
+    b += sizeof(int) * 8;                               // list lengths
     return b;
   }
 };
 
-// Stage anchors, weights and warp-overlap masks of particles [c0, c0+n).
 template <typename real, int P>
-__device__ __forceinline__ void stage_spread(const Geom& g, const FastTab& ft,
-                                             const real* s_tab, const double* s_brk,
-                                             int n_pieces, int ncoef,
-                                             const double* __restrict__ U,
-                                             const double* __restrict__ Q, long long cap,
-                                             long long c0, int n, int tx, int ty, int tz,
-                                             real* s_w, int* s_anc) {
-  for (int item = threadIdx.x; item < 3 * n; item += blockDim.x) {
-    const int d = item / n, pl = item - d * n;   // d-major: coalesced U reads
-    const double u = U[d * cap + c0 + pl];
-    const double base = anchor_base(g, u);
-    const int a = wrap_index((long long)base, g.M[d]);
-    const int org = d == 0 ? tx * g.TX : (d == 1 ? ty * g.TY : tz * g.TZ);
-    s_anc[d * kChunk + pl] = a - org;
-    const real qf = d == 0 ? (real)Q[c0 + pl] : real(1);
-    real w[P];
-    stencil_weights<real, P>(ft, s_tab, s_brk, n_pieces, ncoef, u, base, g.lo, qf, w);
-    real* dst = s_w + ((size_t)d * kChunk + pl) * P;
-#pragma unroll
-    for (int s = 0; s < P; ++s) dst[s] = w[s];
-  }
-}
-
-template <typename real, int P>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kSpreadThreads)
 k_spread_tiles(Geom g, FastTab ft, const real* __restrict__ tab,
                const double* __restrict__ brk, int n_pieces, int ncoef,
                const int* __restrict__ offsets, const double* __restrict__ U,
                const double* __restrict__ Q, long long cap, real* __restrict__ scratch) {
+  using Rec = SpreadRec<P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tile = blockIdx.x;
   const int tz = tile % g.ntz;
@@ -86,81 +75,134 @@ k_spread_tiles(Geom g, FastTab ft, const real* __restrict__ tab,
   double* s_brk = reinterpret_cast<double*>(smem_raw + off);
   off += sizeof(double) * (size_t)(n_pieces + 1);
   off = (off + 15) & ~size_t(15);
-  real* s_w = reinterpret_cast<real*>(smem_raw + off);
-  off += sizeof(real) * 3 * (size_t)kChunk * P;
-  int* s_anc = reinterpret_cast<int*>(smem_raw + off);   // [3][kChunk] + mask[kChunk]
-  int* s_mask = s_anc + 3 * kChunk;
+  real* s_rec = reinterpret_cast<real*>(smem_raw + off);
+  off += sizeof(real) * (size_t)kSChunk * Rec::kLen;
+  int* s_anc = reinterpret_cast<int*>(smem_raw + off);   // [3][kSChunk]
+  int* s_pk = s_anc + 3 * kSChunk;                       // packed x | y<<8 | z<<16
+  int* s_list = s_pk + kSChunk;                          // [4][kSChunk]
+  int* s_len = s_list + 4 * kSChunk;
 
   // General table (the fast path falls back to it on exact piece-boundary ties).
   for (int i = threadIdx.x; i < n_pieces * ncoef; i += blockDim.x) s_tab[i] = tab[i];
   for (int i = threadIdx.x; i <= n_pieces; i += blockDim.x) s_brk[i] = brk[i];
 
+  // Warp w owns the 8x8 column block (wx0.., wy0..); lane owns (cx, cy) and
+  // (cx, cy + 4).
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
+  const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 8;
   const int cx = wx0 + (lane & 7), cy = wy0 + (lane >> 3);
-  real* out = scratch + (size_t)tile * g.PZ * kPad * kPad + (size_t)cy * kPad + cx;
+  real* outA = scratch + (size_t)tile * g.PZ * kPad * kPad + (size_t)cy * kPad + cx;
+  real* outB = outA + 4 * kPad;
   const size_t plane = (size_t)kPad * kPad;
 
-  real win[P];
+  real winA[P], winB[P];
 #pragma unroll
-  for (int s = 0; s < P; ++s) win[s] = real(0);
+  for (int s = 0; s < P; ++s) {
+    winA[s] = real(0);
+    winB[s] = real(0);
+  }
   int zc = 0;
 
-  for (long long c0 = p0; c0 < p1; c0 += kChunk) {
-    const int n = (int)min((long long)kChunk, p1 - c0);
+  for (long long c0 = p0; c0 < p1; c0 += kSChunk) {
+    const int n = (int)min((long long)kSChunk, p1 - c0);
     __syncthreads();
-    stage_spread<real, P>(g, ft, s_tab, s_brk, n_pieces, ncoef, U, Q, cap, c0, n, tx, ty,
-                          tz, s_w, s_anc);
-    __syncthreads();
-    for (int pl = threadIdx.x; pl < n; pl += blockDim.x) {
-      const int xl = s_anc[pl], yl = s_anc[kChunk + pl];
-      int m = 0;
+    // (1) weights + anchors, one (particle, dim) per thread
+    for (int item = threadIdx.x; item < 3 * n; item += blockDim.x) {
+      const int d = item / n, pl = item - d * n;   // d-major: coalesced U reads
+      const double u = U[d * cap + c0 + pl];
+      const double base = anchor_base(g, u);
+      const int a = wrap_index((long long)base, g.M[d]);
+      const int org = d == 0 ? tx * g.TX : (d == 1 ? ty * g.TY : tz * g.TZ);
+      s_anc[d * kSChunk + pl] = a - org;
+      const real qf = d == 0 ? (real)Q[c0 + pl] : real(1);
+      real w[P];
+      stencil_weights<real, P>(ft, s_tab, s_brk, n_pieces, ncoef, u, base, g.lo, qf, w);
+      real* rec = s_rec + (size_t)pl * Rec::kLen;
+      if (d < 2) {
+        real* row = rec + (d == 0 ? Rec::kX : Rec::kY);
 #pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const int ax = (w & 1) * 8, ay = (w >> 1) * 4;
-        const bool hit = xl < ax + 8 && xl + P > ax && yl < ay + 4 && yl + P > ay;
-        m |= (int)hit << w;
+        for (int t = 0; t < 8; ++t) row[t] = real(0);
+#pragma unroll
+        for (int t = 0; t < P; ++t) row[8 + t] = w[t];
+#pragma unroll
+        for (int t = 8 + P; t < Rec::RL; ++t) row[t] = real(0);
+      } else {
+#pragma unroll
+        for (int t = 0; t < P; ++t) rec[Rec::kZ + t] = w[t];
       }
-      s_mask[pl] = m;
     }
     __syncthreads();
-    for (int base = 0; base < n; base += 32) {
-      const int pq = base + lane;
-      const bool mine = pq < n && ((s_mask[pq] >> warp) & 1);
-      unsigned bits = __ballot_sync(0xffffffffu, mine);
-      while (bits) {
-        const int pl = base + __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int xl = s_anc[pl];
-        const int yl = s_anc[kChunk + pl];
-        const int zl = s_anc[2 * kChunk + pl];
-        while (zc < zl) {  // slide: plane zc is final for this column
-          out[(size_t)zc * plane] = win[0];
-#pragma unroll
-          for (int s = 0; s < P - 1; ++s) win[s] = win[s + 1];
-          win[P - 1] = real(0);
-          ++zc;
+    // (2) packed anchors; (3) per-warp ordered lists of overlapping particles
+    for (int pl = threadIdx.x; pl < n; pl += blockDim.x)
+      s_pk[pl] = s_anc[pl] | (s_anc[kSChunk + pl] << 8) | (s_anc[2 * kSChunk + pl] << 16);
+    {
+      int cnt = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int pl = base + lane;
+        bool hit = false;
+        if (pl < n) {
+          const int xl = s_anc[pl], yl = s_anc[kSChunk + pl];
+          hit = xl < wx0 + 8 && xl + P > wx0 && yl < wy0 + 8 && yl + P > wy0;
         }
-        const int sx = cx - xl, sy = cy - yl;
-        const bool in = (unsigned)sx < (unsigned)P && (unsigned)sy < (unsigned)P;
-        const real* wxp = s_w + (size_t)pl * P;
-        const real* wyp = s_w + ((size_t)kChunk + pl) * P;
-        const real* wzp = s_w + ((size_t)2 * kChunk + pl) * P;
-        const int sxc = min(max(sx, 0), P - 1), syc = min(max(sy, 0), P - 1);
-        const real a = in ? wxp[sxc] * wyp[syc] : real(0);
-        real wz[P];
+        const unsigned bits = __ballot_sync(0xffffffffu, hit);
+        if (hit) s_list[warp * kSChunk + cnt + __popc(bits & ((1u << lane) - 1u))] = pl;
+        cnt += __popc(bits);
+      }
+      if (lane == 0) s_len[warp] = cnt;
+    }
+    __syncthreads();
+    const int cnt = s_len[warp];
+    const int* list = s_list + warp * kSChunk;
+    const int ofx = cx + 8, ofy = cy + 8;
+    // Particles arrive in z-anchor order: slide the window once per anchor
+    // plane (outer loop) and run a pure-FMA inner loop over the particles
+    // sharing that plane (no register rotation inside the hot loop).
+    int t = 0;
+    while (t < cnt) {
+      int pl = list[t];
+      int pk = s_pk[pl];
+      const int zl = pk >> 16;
+      while (zc < zl) {  // slide: plane zc is final for these columns
+        outA[(size_t)zc * plane] = winA[0];
+        outB[(size_t)zc * plane] = winB[0];
 #pragma unroll
-        for (int s = 0; s < P; ++s) wz[s] = wzp[s];
+        for (int s = 0; s < P - 1; ++s) {
+          winA[s] = winA[s + 1];
+          winB[s] = winB[s + 1];
+        }
+        winA[P - 1] = real(0);
+        winB[P - 1] = real(0);
+        ++zc;
+      }
+      for (;;) {
+        const real* rec = s_rec + (size_t)pl * Rec::kLen;
+        const int xl = pk & 0xff, yl = (pk >> 8) & 0xff;
+        const real wx = rec[Rec::kX + ofx - xl];
+        const real a = wx * rec[Rec::kY + ofy - yl];
+        const real b = wx * rec[Rec::kY + ofy + 4 - yl];
 #pragma unroll
-        for (int s = 0; s < P; ++s) win[s] = fma(a, wz[s], win[s]);
+        for (int s = 0; s < P; ++s) {
+          const real wz = rec[Rec::kZ + s];
+          winA[s] = fma(a, wz, winA[s]);
+          winB[s] = fma(b, wz, winB[s]);
+        }
+        if (++t >= cnt) break;
+        pl = list[t];
+        pk = s_pk[pl];
+        if ((pk >> 16) != zl) break;
       }
     }
   }
   while (zc < g.PZ) {
-    out[(size_t)zc * plane] = win[0];
+    outA[(size_t)zc * plane] = winA[0];
+    outB[(size_t)zc * plane] = winB[0];
 #pragma unroll
-    for (int s = 0; s < P - 1; ++s) win[s] = win[s + 1];
-    win[P - 1] = real(0);
+    for (int s = 0; s < P - 1; ++s) {
+      winA[s] = winA[s + 1];
+      winB[s] = winB[s + 1];
+    }
+    winA[P - 1] = real(0);
+    winB[P - 1] = real(0);
     ++zc;
   }
 }
@@ -212,7 +254,7 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = smem;
   }
-  k_spread_tiles<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
+  k_spread_tiles<real, P><<<(unsigned)p->n_tiles, kSpreadThreads, smem, s>>>(
       g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->d_q,
       p->cap, reinterpret_cast<real*>(p->d_scratch));
   p->launches++;
