@@ -288,3 +288,62 @@ def test_cuda_graph_replay_matches_eager():
     hs.charges.copy_(torch.as_tensor(q))
     h7, hF = hs.step()
     assert torch.equal(h7, e7.cpu()) and torch.equal(hF, eF.cpu())
+
+
+@pytest.mark.slow
+def test_config3_triclinic_against_oracle():
+    """Config 3 (1e6 charges, triclinic 192x192x256, P=8): E and the full
+    pressure tensor against the oracle; forces on a 20k-atom sample."""
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    w, pos, q = workloads.generate(3)
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M,
+                                          cell_type="triclinic"), capacity=w.n)
+    r = s.evaluate(pos, q)
+    op = O.make_plan(w.h, w.M, w.P, w.delta, w.r_c)
+    m = O.Modes(op)
+    rh = O.forward_density(op, pos, q)
+    assert O.rel_scalar(r.energy, O.energy(m, rh)) <= F64_TOL
+    assert O.rel_frobenius(r.pressure, O.pressure(m, rh)) <= F64_TOL
+    sel = np.random.default_rng(3).choice(w.n, 20_000, replace=False)
+    h3 = op.volume_element
+    scale = m.fhat * m.w_inv2 * rh[m.mask]
+    Fo = np.empty((sel.size, 3))
+    for d in range(3):
+        spec = np.zeros(op.M, dtype=complex)
+        spec[m.mask] = 1j * m.kvec[d] * scale
+        fld = np.fft.ifftn(spec).real / h3
+        Fo[:, d] = -q[sel] * h3 * O.gather(op, fld, pos[sel])
+    assert O.rms_rel_forces(r.forces[sel], Fo) <= F64_TOL
+    assert np.linalg.norm(r.forces.sum(axis=0)) < 1e-10 * np.linalg.norm(r.forces, axis=1).max() * 1e3
+
+
+@pytest.mark.slow
+def test_config4_size_independent_properties():
+    """Config 4 (8.1e6 charges, 384^3): momentum conservation, bitwise
+    determinism, invariance under a one-grid-spacing translation, charge
+    scaling (E, P ~ q^2; F ~ q^2), and fp32 mode within 1e-5."""
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    w, pos, q = workloads.generate(4)
+    prm = dict(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M)
+    s = KSpaceSolver(w.h, EwaldParameters(**prm), capacity=w.n)
+    P_, Q_ = _dev(torch, pos), _dev(torch, q)
+    a7, aF = s.evaluate_device(P_, Q_)
+    a7, aF = a7.clone(), aF.clone()
+    b7, bF = s.evaluate_device(P_, Q_)
+    assert torch.equal(a7, b7) and torch.equal(aF, bF)
+    F = aF.cpu().numpy()
+    assert np.linalg.norm(F.sum(axis=0)) < 1e-9 * np.linalg.norm(F, axis=1).max()
+    hx = 300.0 / 384
+    shifted = workloads.wrap_positions(w.h, pos + np.array([hx, 0.0, 0.0]))
+    c7, cF = s.evaluate_device(_dev(torch, shifted), Q_)
+    assert O.rel_scalar(c7[0].item(), a7[0].item()) <= F64_TOL
+    assert torch.allclose(c7, a7, rtol=1e-9, atol=1e-12 * a7.abs().max().item())
+    assert O.rms_rel_forces(cF.cpu().numpy(), F) <= F64_TOL
+    d7, dF = s.evaluate_device(P_, 2.0 * Q_)
+    assert torch.allclose(d7, 4.0 * a7, rtol=1e-12, atol=0)
+    assert O.rms_rel_forces(dF.cpu().numpy(), 4.0 * F) <= 1e-13
+    s32 = KSpaceSolver(w.h, EwaldParameters(precision="fp32", **prm), capacity=w.n)
+    e7, eF = s32.evaluate_device(P_, Q_)
+    assert O.rel_scalar(e7[0].item(), a7[0].item()) <= F32_TOL
+    assert O.rms_rel_forces(eF.cpu().numpy(), F) <= F32_TOL
