@@ -76,7 +76,8 @@ static void free_all(esp_plan* p) {
                   p->d_u_tmp,   p->d_q_tmp,    p->d_idx_tmp, p->d_cub,     p->d_scratch,
                   p->d_grid,    p->d_spec,     p->d_ikspec,  p->d_fields,  p->d_axis_k,
                   p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
-                  p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt};
+                  p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt,
+                  p->d_wrec,     p->d_pk};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_fwd) cufftDestroy(p->fwd);
@@ -213,6 +214,8 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(dalloc(&p->d_u_tmp, 3 * cap));
   TRY(dalloc(&p->d_q_tmp, cap));
   TRY(dalloc(&p->d_idx_tmp, cap));
+  TRY(cudaMalloc(&p->d_wrec, real_sz * 3 * esp::rec_stride(p->P) * cap));
+  TRY(dalloc(&p->d_pk, cap));
   p->cub_bytes = esp::scan_temp_bytes(p->n_keys + 1);
   TRY(cudaMalloc(&p->d_cub, std::max<size_t>(p->cub_bytes, 16)));
   TRY(cudaMalloc(&p->d_scratch,

@@ -17,6 +17,35 @@
 
 namespace esp {
 
+// Window weights and tile-local anchors of one binned particle, written once
+// per step and read by both the spread and the gather kernels.
+template <typename real, int P>
+__device__ __forceinline__ void write_record(const Geom& g, const FastTab& ft,
+                                             const real* __restrict__ tab,
+                                             const double* __restrict__ brk,
+                                             int n_pieces, int ncoef, int key,
+                                             const double u[3], long long dst,
+                                             real* __restrict__ wrec,
+                                             int* __restrict__ pk) {
+  const int az = key % g.M[2];
+  const int txy = key / g.M[2];
+  const int org[3] = {(txy % g.ntx) * g.TX, (txy / g.ntx) * g.TY, (az / g.TZ) * g.TZ};
+  constexpr int RS = rec_stride(P);
+  real* out = wrec + dst * (3 * RS);
+  int packed = 0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double base = anchor_base(g, u[d]);
+    const int a = wrap_index((long long)base, g.M[d]);
+    packed |= (a - org[d]) << (8 * d);
+    real w[P];
+    stencil_weights<real, P>(ft, tab, brk, n_pieces, ncoef, u[d], base, g.lo, real(1), w);
+#pragma unroll
+    for (int s = 0; s < RS; ++s) out[d * RS + s] = s < P ? w[s < P ? s : 0] : real(0);
+  }
+  pk[dst] = packed;
+}
+
 __global__ void k_bin_count(const double* __restrict__ pos, long long n, Geom g,
                             int* __restrict__ key, int* __restrict__ slot,
                             int* __restrict__ counts) {
@@ -63,15 +92,20 @@ __global__ void k_bin_scatter(const double* __restrict__ pos,
   if (key_out) key_out[dst] = k;
 }
 
-// Deterministic order inside each key segment: rank by original index.
-__global__ void k_bin_canon(long long n, long long cap,
+// Deterministic order inside each key segment: rank by original index; then
+// the particle's weight record at its final position.
+template <typename real, int P>
+__global__ void k_bin_canon(Geom g, FastTab ft, const real* __restrict__ tab,
+                            const double* __restrict__ brk, int n_pieces, int ncoef,
+                            long long n, long long cap,
                             const int* __restrict__ key_tmp,
                             const int* __restrict__ offsets,
                             const double* __restrict__ u_tmp,
                             const double* __restrict__ q_tmp,
                             const int* __restrict__ idx_tmp,
                             double* __restrict__ u_out, double* __restrict__ q_out,
-                            int* __restrict__ idx_out) {
+                            int* __restrict__ idx_out, real* __restrict__ wrec,
+                            int* __restrict__ pk) {
   long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int k = key_tmp[j];
@@ -80,11 +114,68 @@ __global__ void k_bin_canon(long long n, long long cap,
   int rank = 0;
   for (int t = s0; t < s1; ++t) rank += (idx_tmp[t] < me);
   const long long dst = (long long)s0 + rank;
-  u_out[dst] = u_tmp[j];
-  u_out[cap + dst] = u_tmp[cap + j];
-  u_out[2 * cap + dst] = u_tmp[2 * cap + j];
+  const double u[3] = {u_tmp[j], u_tmp[cap + j], u_tmp[2 * cap + j]};
+  u_out[dst] = u[0];
+  u_out[cap + dst] = u[1];
+  u_out[2 * cap + dst] = u[2];
   q_out[dst] = q_tmp[j];
   idx_out[dst] = me;
+  write_record<real, P>(g, ft, tab, brk, n_pieces, ncoef, k, u, dst, wrec, pk);
+}
+
+// Non-deterministic mode: records straight after the atomic-slot scatter.
+template <typename real, int P>
+__global__ void k_bin_records(Geom g, FastTab ft, const real* __restrict__ tab,
+                              const double* __restrict__ brk, int n_pieces, int ncoef,
+                              long long n, long long cap, const int* __restrict__ key,
+                              const int* __restrict__ slot, const int* __restrict__ offsets,
+                              const double* __restrict__ u_in, real* __restrict__ wrec,
+                              int* __restrict__ pk) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k = key[i];
+  const long long dst = (long long)offsets[k] + slot[i];
+  const double u[3] = {u_in[dst], u_in[cap + dst], u_in[2 * cap + dst]};
+  write_record<real, P>(g, ft, tab, brk, n_pieces, ncoef, k, u, dst, wrec, pk);
+}
+
+template <typename real, int P>
+static void launch_tail(esp_plan* p, const Geom& g, long long n, unsigned grid, int B,
+                        cudaStream_t s) {
+  const real* tab = std::is_same<real, double>::value
+                        ? reinterpret_cast<const real*>(p->d_tab)
+                        : reinterpret_cast<const real*>(p->d_tabf);
+  real* wrec = reinterpret_cast<real*>(p->d_wrec);
+  if (p->deterministic) {
+    k_bin_canon<real, P><<<grid, B, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
+                                           p->ncoef, n, p->cap, p->d_bkey, p->d_offsets,
+                                           p->d_u_tmp, p->d_q_tmp, p->d_idx_tmp, p->d_u,
+                                           p->d_q, p->d_idx, wrec, p->d_pk);
+  } else {
+    k_bin_records<real, P><<<grid, B, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
+                                             p->ncoef, n, p->cap, p->d_key, p->d_slot,
+                                             p->d_offsets, p->d_u, wrec, p->d_pk);
+  }
+}
+
+template <typename real>
+static cudaError_t launch_tail_r(esp_plan* p, const Geom& g, long long n, unsigned grid,
+                                 int B, cudaStream_t s) {
+  switch (p->P) {
+    case 2: launch_tail<real, 2>(p, g, n, grid, B, s); break;
+    case 3: launch_tail<real, 3>(p, g, n, grid, B, s); break;
+    case 4: launch_tail<real, 4>(p, g, n, grid, B, s); break;
+    case 5: launch_tail<real, 5>(p, g, n, grid, B, s); break;
+    case 6: launch_tail<real, 6>(p, g, n, grid, B, s); break;
+    case 7: launch_tail<real, 7>(p, g, n, grid, B, s); break;
+    case 8: launch_tail<real, 8>(p, g, n, grid, B, s); break;
+    case 9: launch_tail<real, 9>(p, g, n, grid, B, s); break;
+    case 10: launch_tail<real, 10>(p, g, n, grid, B, s); break;
+    case 11: launch_tail<real, 11>(p, g, n, grid, B, s); break;
+    case 12: launch_tail<real, 12>(p, g, n, grid, B, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
@@ -111,11 +202,7 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
                                      p->d_offsets, p->cap, p->d_u_tmp, p->d_q_tmp,
                                      p->d_idx_tmp, p->d_bkey);
     prof_mark(p, s, "bin_scatter");
-    k_bin_canon<<<grid, B, 0, s>>>(n, p->cap, p->d_bkey, p->d_offsets, p->d_u_tmp,
-                                   p->d_q_tmp, p->d_idx_tmp, p->d_u, p->d_q,
-                                   p->d_idx);
-    p->launches += 2;
-    prof_mark(p, s, "bin_canon");
+    p->launches += 1;
   } else {
     k_bin_scatter<<<grid, B, 0, s>>>(d_pos, d_q, n, g, p->d_key, p->d_slot,
                                      p->d_offsets, p->cap, p->d_u, p->d_q, p->d_idx,
@@ -123,6 +210,11 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
     p->launches++;
     prof_mark(p, s, "bin_scatter");
   }
+  e = p->precision == ESP_FP64 ? launch_tail_r<double>(p, g, n, grid, B, s)
+                               : launch_tail_r<float>(p, g, n, grid, B, s);
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, p->deterministic ? "bin_canon_weights" : "bin_weights");
   return cudaGetLastError();
 }
 

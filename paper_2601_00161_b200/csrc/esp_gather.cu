@@ -75,17 +75,10 @@ struct GatherLayout {
   // of one LDS.64 phase (8 planes x 2 adjacent rows) hit 16 distinct banks.
   static constexpr int kRowZ = 24;
   static constexpr int kPlaneZ = kPad * kRowZ + 1;
-  static size_t bytes(int PZ, int n_pieces, int ncoef) {
-    size_t b = sizeof(real) * (size_t)n_pieces * ncoef;
+  static size_t bytes(int PZ) {
+    size_t b = 2 * sizeof(real) * (size_t)PZ * kPlane;   // (f_x, f_y) pairs
     b = (b + 15) & ~size_t(15);
-    b += sizeof(double) * (size_t)(n_pieces + 1);
-    b = (b + 15) & ~size_t(15);
-    b += 2 * sizeof(real) * (size_t)PZ * kPlane;   // (f_x, f_y) pairs
-    b += sizeof(real) * (size_t)PZ * kPlaneZ;      // f_z
-    b = (b + 15) & ~size_t(15);
-    b += sizeof(real) * (size_t)kGChunk * 24;      // weights [pl][3][8]
-    b += sizeof(double) * (size_t)kGChunk;         // charges
-    b += sizeof(int) * 5 * (size_t)kGChunk;        // anchors x,y,z + index
+    b += sizeof(real) * (size_t)PZ * kPlaneZ;           // f_z
     return b;
   }
 };
@@ -93,20 +86,21 @@ struct GatherLayout {
 // Warp = 2 particles x 8 stencil planes x 2 row parities.  Lane (p, h, k)
 // sums rows j = h, h+2, .. of particle p's stencil on plane zl+k (x contiguous,
 // immediate smem offsets), weights by wz[k], and the 16 lanes of a particle
-// reduce with 4 xor-shuffle levels.  Strides make every LDS phase
-// bank-conflict free (see GatherLayout).
+// reduce with 4 xor-shuffle levels.  Weights and anchors come from the
+// per-particle records of the binning pass; the field tile is the only
+// shared-memory data.  Strides make every LDS phase bank-conflict free.
 template <typename real, int P>
 __global__ void __launch_bounds__(kTileThreads, 2)
-k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
-              const double* __restrict__ brk, int n_pieces, int ncoef,
-              const int* __restrict__ offsets, const double* __restrict__ U,
-              const double* __restrict__ Q, const int* __restrict__ IDX, long long cap,
-              const real* __restrict__ fld, long long G, double* __restrict__ forces) {
+k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ wrec,
+              const int* __restrict__ PK, const double* __restrict__ Q,
+              const int* __restrict__ IDX, const real* __restrict__ fld, long long G,
+              double* __restrict__ forces) {
   static_assert(P <= 8, "warp gather covers at most 8 stencil planes");
   using R2 = typename Real2<real>::type;
   constexpr int kPlane = GatherLayout<real, P>::kPlane;
   constexpr int kRowZ = GatherLayout<real, P>::kRowZ;
   constexpr int kPlaneZ = GatherLayout<real, P>::kPlaneZ;
+  constexpr int RS = rec_stride(P);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tile = blockIdx.x;
   const int tz = tile % g.ntz;
@@ -117,26 +111,10 @@ k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
   const long long p0 = offsets[key0], p1 = offsets[key1];
   if (p0 == p1) return;
 
-  real* s_tab = reinterpret_cast<real*>(smem_raw);
-  size_t off = sizeof(real) * (size_t)n_pieces * ncoef;
+  R2* s_f01 = reinterpret_cast<R2*>(smem_raw);
+  size_t off = 2 * sizeof(real) * (size_t)g.PZ * kPlane;
   off = (off + 15) & ~size_t(15);
-  double* s_brk = reinterpret_cast<double*>(smem_raw + off);
-  off += sizeof(double) * (size_t)(n_pieces + 1);
-  off = (off + 15) & ~size_t(15);
-  R2* s_f01 = reinterpret_cast<R2*>(smem_raw + off);
-  off += 2 * sizeof(real) * (size_t)g.PZ * kPlane;
   real* s_f2 = reinterpret_cast<real*>(smem_raw + off);
-  off += sizeof(real) * (size_t)g.PZ * kPlaneZ;
-  off = (off + 15) & ~size_t(15);
-  real* s_w = reinterpret_cast<real*>(smem_raw + off);
-  off += sizeof(real) * (size_t)kGChunk * 24;
-  double* s_q = reinterpret_cast<double*>(smem_raw + off);
-  off += sizeof(double) * (size_t)kGChunk;
-  int* s_anc = reinterpret_cast<int*>(smem_raw + off);   // [3][kGChunk]
-  int* s_id = s_anc + 3 * kGChunk;
-
-  for (int i = threadIdx.x; i < n_pieces * ncoef; i += blockDim.x) s_tab[i] = tab[i];
-  for (int i = threadIdx.x; i <= n_pieces; i += blockDim.x) s_brk[i] = brk[i];
 
   // Stage the padded field tile.  blockDim == 256 == one 16x16 plane, so
   // each thread owns one (x, y) column: wrap it once, then walk the planes.
@@ -160,82 +138,63 @@ k_gather_warp(Geom g, FastTab ft, const real* __restrict__ tab,
       gz = gz + 1 == g.M[2] ? 0 : gz + 1;
     }
   }
+  __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = lane >> 4, h = (lane >> 3) & 1, k = lane & 7;
-
-  for (long long c0 = p0; c0 < p1; c0 += kGChunk) {
-    const int n = (int)min((long long)kGChunk, p1 - c0);
-    __syncthreads();
-    for (int item = threadIdx.x; item < 3 * n; item += blockDim.x) {
-      const int d = item / n, pl = item - d * n;
-      const double u = U[d * cap + c0 + pl];
-      const double base = anchor_base(g, u);
-      const int a = wrap_index((long long)base, g.M[d]);
-      const int org = d == 0 ? tx * g.TX : (d == 1 ? ty * g.TY : tz * g.TZ);
-      s_anc[d * kGChunk + pl] = a - org;
-      real w[P];
-      stencil_weights<real, P>(ft, s_tab, s_brk, n_pieces, ncoef, u, base, g.lo, real(1), w);
-      real* dst = s_w + (size_t)pl * 24 + d * 8;
+  for (long long pb = p0 + warp * 2; pb < p1; pb += (kTileThreads / 32) * 2) {
+    const long long pl = pb + slot;
+    const bool live = pl < p1 && k < P;
+    real ax = 0, ay = 0, az = 0;
+    if (live) {
+      const int pk = PK[pl];
+      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = pk >> 16;
+      const real* W = wrec + pl * (3 * RS);
+      real wx[P], wy[P];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) dst[s] = s < P ? w[s < P ? s : 0] : real(0);
-      if (d == 0) {
-        s_q[pl] = Q[c0 + pl];
-        s_id[pl] = IDX[c0 + pl];
+      for (int s = 0; s < P; ++s) {
+        wx[s] = W[s];
+        wy[s] = W[RS + s];
       }
-    }
-    __syncthreads();
-    for (int pb = warp * 2; pb < n; pb += (kTileThreads / 32) * 2) {
-      const int pl = pb + slot;
-      const bool live = pl < n && k < P;
-      real ax = 0, ay = 0, az = 0;
-      if (live) {
-        const int xl = s_anc[pl];
-        const int yl = s_anc[kGChunk + pl];
-        const int zl = s_anc[2 * kGChunk + pl];
-        const real* W = s_w + (size_t)pl * 24;
-        real wx[P];
+      const real wzk = W[2 * RS + k];
+      const R2* rowp = s_f01 + (zl + k) * kPlane + (yl + h) * kPad + xl;
+      const real* rowz = s_f2 + (zl + k) * kPlaneZ + (yl + h) * kRowZ + xl;
 #pragma unroll
-        for (int s = 0; s < P; ++s) wx[s] = W[s];
-        const real wzk = W[16 + k];
-        const R2* rowp = s_f01 + (zl + k) * kPlane + (yl + h) * kPad + xl;
-        const real* rowz = s_f2 + (zl + k) * kPlaneZ + (yl + h) * kRowZ + xl;
+      for (int jj = 0; jj < (P + 1) / 2; ++jj) {
+        const int j = 2 * jj;                 // row j + h of the stencil
+        const bool odd_row = j + 1 < P;       // compile-time after unrolling
+        if (odd_row || h == 0) {
+          const real wy_ = (odd_row && h) ? wy[odd_row ? j + 1 : j] : wy[j];
+          real rx = 0, ry = 0, rz = 0;
 #pragma unroll
-        for (int jj = 0; jj < (P + 1) / 2; ++jj) {
-          const int j = 2 * jj;                 // row j + h of the stencil
-          if (j + 1 < P || h == 0) {
-            const real wy = W[8 + j + h];
-            real rx = 0, ry = 0, rz = 0;
-#pragma unroll
-            for (int i = 0; i < P; ++i) {
-              const R2 v = rowp[j * kPad + i];
-              const real vz = rowz[j * kRowZ + i];
-              rx = fma(wx[i], v.x, rx);
-              ry = fma(wx[i], v.y, ry);
-              rz = fma(wx[i], vz, rz);
-            }
-            ax = fma(wy, rx, ax);
-            ay = fma(wy, ry, ay);
-            az = fma(wy, rz, az);
+          for (int i = 0; i < P; ++i) {
+            const R2 v = rowp[j * kPad + i];
+            const real vz = rowz[j * kRowZ + i];
+            rx = fma(wx[i], v.x, rx);
+            ry = fma(wx[i], v.y, ry);
+            rz = fma(wx[i], vz, rz);
           }
+          ax = fma(wy_, rx, ax);
+          ay = fma(wy_, ry, ay);
+          az = fma(wy_, rz, az);
         }
-        ax *= wzk;
-        ay *= wzk;
-        az *= wzk;
       }
+      ax *= wzk;
+      ay *= wzk;
+      az *= wzk;
+    }
 #pragma unroll
-      for (int o = 1; o < 16; o <<= 1) {
-        ax += __shfl_xor_sync(0xffffffffu, ax, o);
-        ay += __shfl_xor_sync(0xffffffffu, ay, o);
-        az += __shfl_xor_sync(0xffffffffu, az, o);
-      }
-      if ((lane & 15) == 0 && pl < n) {
-        const double q = s_q[pl];
-        double* f = forces + (long long)s_id[pl] * 3;
-        f[0] = -q * (double)ax;
-        f[1] = -q * (double)ay;
-        f[2] = -q * (double)az;
-      }
+    for (int o = 1; o < 16; o <<= 1) {
+      ax += __shfl_xor_sync(0xffffffffu, ax, o);
+      ay += __shfl_xor_sync(0xffffffffu, ay, o);
+      az += __shfl_xor_sync(0xffffffffu, az, o);
+    }
+    if ((lane & 15) == 0 && pl < p1) {
+      const double q = Q[pl];
+      double* f = forces + (long long)IDX[pl] * 3;
+      f[0] = -q * (double)ax;
+      f[1] = -q * (double)ay;
+      f[2] = -q * (double)az;
     }
   }
 }
@@ -375,10 +334,7 @@ template <typename real, int P>
 static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   Geom g = make_geom(p);
   if constexpr (P <= 8) {
-    const real* tab = std::is_same<real, double>::value
-                          ? reinterpret_cast<const real*>(p->d_tab)
-                          : reinterpret_cast<const real*>(p->d_tabf);
-    const size_t smem = GatherLayout<real, P>::bytes(p->PZ, p->n_pieces, p->ncoef);
+    const size_t smem = GatherLayout<real, P>::bytes(p->PZ);
     static size_t attr_set = 0;  // set once per instantiation (capture-safe)
     if (smem > attr_set) {
       cudaError_t e = cudaFuncSetAttribute(k_gather_warp<real, P>,
@@ -388,9 +344,8 @@ static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s) {
       attr_set = smem;
     }
     k_gather_warp<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
-        g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u,
-        p->d_q, p->d_idx, p->cap, reinterpret_cast<const real*>(p->d_fields), p->G,
-        d_forces);
+        g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q, p->d_idx,
+        reinterpret_cast<const real*>(p->d_fields), p->G, d_forces);
     p->launches++;
     prof_mark(p, s, "gather");
     return cudaGetLastError();

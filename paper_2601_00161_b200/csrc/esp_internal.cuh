@@ -180,6 +180,8 @@ __device__ __forceinline__ void stencil_weights(const FastTab& ft, const real* s
 // combine, precomputed at plan creation: entry [c*kCombW + k] =
 // tile | pad << 16, count in cnt[c].
 constexpr int kCombW = 8;
+// Per-particle weight record: 3 dims x RS weights (RS = 8 for P <= 8, else 12).
+__host__ __device__ constexpr int rec_stride(int P) { return P <= 8 ? 8 : 12; }
 struct CombineTabs {
   const int* ent[3];
   const int* cnt[3];
@@ -222,6 +224,9 @@ struct esp_plan {
   int* d_idx;
   double *d_u_tmp, *d_q_tmp;
   int* d_idx_tmp;
+  void* d_wrec;           // per binned particle: 24 window weights (x|y|z, q folded
+                          // into x by the spread), precision of the plan
+  int* d_pk;              // per binned particle: tile-local anchor x | y<<8 | z<<16
   void* d_cub;
   size_t cub_bytes;
   void* d_scratch;

@@ -13,10 +13,10 @@
 //    multiply-add in the window is useful along z; along x/y a warp (8 x 8
 //    columns) only visits the particles whose stencil touches it, found by a
 //    ballot over a per-particle 8-bit warp mask staged with the weights.
-//  * 1D weights are evaluated once per particle and dimension (unrolled
-//    Horner on the reference's degree-18 piecewise table, pswf.py:238-293,
-//    coefficients in the constant bank) and staged in shared memory; q is
-//    folded into the x weights.
+//  * 1D weights come from the per-particle records written by the binning
+//    pass (unrolled Horner on the reference's degree-18 piecewise table,
+//    pswf.py:238-293) and are staged in shared memory as zero-padded rows;
+//    q is folded into the x weights.
 //  * The padded blocks go to a scratch buffer; k_combine sums, for every grid
 //    point, the contributions of the (at most 8) covering tiles in a fixed
 //    order read from precomputed per-axis tables.  No atomics: results are
@@ -40,12 +40,8 @@ constexpr int kSChunk = 128;   // particles staged per spread pass
 
 template <typename real, int P>
 struct SpreadLayout {
-  static size_t bytes(int n_pieces, int ncoef) {
-    size_t b = sizeof(real) * (size_t)n_pieces * ncoef;
-    b = (b + 15) & ~size_t(15);
-    b += sizeof(double) * (size_t)(n_pieces + 1);
-    b = (b + 15) & ~size_t(15);
-    b += sizeof(real) * (size_t)kSChunk * SpreadRec<P>::kLen;
+  static size_t bytes() {
+    size_t b = sizeof(real) * (size_t)kSChunk * SpreadRec<P>::kLen;
     b += sizeof(int) * (size_t)kSChunk * (3 + 1 + 4);   // anchors, packed, 4 warp lists
     b += sizeof(int) * 8;                               // list lengths
     return b;
@@ -54,10 +50,9 @@ struct SpreadLayout {
 
 template <typename real, int P>
 __global__ void __launch_bounds__(kSpreadThreads)
-k_spread_tiles(Geom g, FastTab ft, const real* __restrict__ tab,
-               const double* __restrict__ brk, int n_pieces, int ncoef,
-               const int* __restrict__ offsets, const double* __restrict__ U,
-               const double* __restrict__ Q, long long cap, real* __restrict__ scratch) {
+k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__ wrec,
+               const int* __restrict__ PK, const double* __restrict__ Q,
+               real* __restrict__ scratch) {
   using Rec = SpreadRec<P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tile = blockIdx.x;
@@ -69,22 +64,13 @@ k_spread_tiles(Geom g, FastTab ft, const real* __restrict__ tab,
   const long long p0 = offsets[key0], p1 = offsets[key1];
   if (p0 == p1) return;  // empty tile: k_combine skips it
 
-  real* s_tab = reinterpret_cast<real*>(smem_raw);
-  size_t off = sizeof(real) * (size_t)n_pieces * ncoef;
-  off = (off + 15) & ~size_t(15);
-  double* s_brk = reinterpret_cast<double*>(smem_raw + off);
-  off += sizeof(double) * (size_t)(n_pieces + 1);
-  off = (off + 15) & ~size_t(15);
+  size_t off = 0;
   real* s_rec = reinterpret_cast<real*>(smem_raw + off);
   off += sizeof(real) * (size_t)kSChunk * Rec::kLen;
   int* s_anc = reinterpret_cast<int*>(smem_raw + off);   // [3][kSChunk]
   int* s_pk = s_anc + 3 * kSChunk;                       // packed x | y<<8 | z<<16
   int* s_list = s_pk + kSChunk;                          // [4][kSChunk]
   int* s_len = s_list + 4 * kSChunk;
-
-  // General table (the fast path falls back to it on exact piece-boundary ties).
-  for (int i = threadIdx.x; i < n_pieces * ncoef; i += blockDim.x) s_tab[i] = tab[i];
-  for (int i = threadIdx.x; i <= n_pieces; i += blockDim.x) s_brk[i] = brk[i];
 
   // Warp w owns the 8x8 column block (wx0.., wy0..); lane owns (cx, cy) and
   // (cx, cy + 4).
@@ -106,35 +92,36 @@ k_spread_tiles(Geom g, FastTab ft, const real* __restrict__ tab,
   for (long long c0 = p0; c0 < p1; c0 += kSChunk) {
     const int n = (int)min((long long)kSChunk, p1 - c0);
     __syncthreads();
-    // (1) weights + anchors, one (particle, dim) per thread
+    // (1) padded weight rows from the per-particle records (esp_bin.cu),
+    //     one (particle, dim) per thread; q folded into the x row
+    constexpr int RS = rec_stride(P);
     for (int item = threadIdx.x; item < 3 * n; item += blockDim.x) {
-      const int d = item / n, pl = item - d * n;   // d-major: coalesced U reads
-      const double u = U[d * cap + c0 + pl];
-      const double base = anchor_base(g, u);
-      const int a = wrap_index((long long)base, g.M[d]);
-      const int org = d == 0 ? tx * g.TX : (d == 1 ? ty * g.TY : tz * g.TZ);
-      s_anc[d * kSChunk + pl] = a - org;
-      const real qf = d == 0 ? (real)Q[c0 + pl] : real(1);
+      const int d = item / n, pl = item - d * n;
+      const real* src = wrec + (c0 + pl) * (3 * RS) + d * RS;
       real w[P];
-      stencil_weights<real, P>(ft, s_tab, s_brk, n_pieces, ncoef, u, base, g.lo, qf, w);
+#pragma unroll
+      for (int t = 0; t < P; ++t) w[t] = src[t];
       real* rec = s_rec + (size_t)pl * Rec::kLen;
       if (d < 2) {
+        const real qf = d == 0 ? (real)Q[c0 + pl] : real(1);
         real* row = rec + (d == 0 ? Rec::kX : Rec::kY);
 #pragma unroll
         for (int t = 0; t < 8; ++t) row[t] = real(0);
 #pragma unroll
-        for (int t = 0; t < P; ++t) row[8 + t] = w[t];
+        for (int t = 0; t < P; ++t) row[8 + t] = w[t] * qf;
 #pragma unroll
         for (int t = 8 + P; t < Rec::RL; ++t) row[t] = real(0);
       } else {
 #pragma unroll
         for (int t = 0; t < P; ++t) rec[Rec::kZ + t] = w[t];
+        const int pk = PK[c0 + pl];
+        s_pk[pl] = pk;
+        s_anc[pl] = pk & 0xff;
+        s_anc[kSChunk + pl] = (pk >> 8) & 0xff;
       }
     }
     __syncthreads();
-    // (2) packed anchors; (3) per-warp ordered lists of overlapping particles
-    for (int pl = threadIdx.x; pl < n; pl += blockDim.x)
-      s_pk[pl] = s_anc[pl] | (s_anc[kSChunk + pl] << 8) | (s_anc[2 * kSChunk + pl] << 16);
+    // (2) per-warp ordered lists of overlapping particles
     {
       int cnt = 0;
       for (int base = 0; base < n; base += 32) {
@@ -242,10 +229,7 @@ __global__ void k_combine(Geom g, CombineTabs ct, const int* __restrict__ offset
 template <typename real, int P>
 static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
   Geom g = make_geom(p);
-  const real* tab = std::is_same<real, double>::value
-                        ? reinterpret_cast<const real*>(p->d_tab)
-                        : reinterpret_cast<const real*>(p->d_tabf);
-  const size_t smem = SpreadLayout<real, P>::bytes(p->n_pieces, p->ncoef);
+  const size_t smem = SpreadLayout<real, P>::bytes();
   static size_t attr_set = 0;  // set once per instantiation (capture-safe)
   if (smem > attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_spread_tiles<real, P>,
@@ -255,8 +239,8 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
     attr_set = smem;
   }
   k_spread_tiles<real, P><<<(unsigned)p->n_tiles, kSpreadThreads, smem, s>>>(
-      g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->d_q,
-      p->cap, reinterpret_cast<real*>(p->d_scratch));
+      g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
+      reinterpret_cast<real*>(p->d_scratch));
   p->launches++;
   prof_mark(p, s, "spread");
   CombineTabs ct;
