@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="run a few steps for ncu (no JSON contract line)")
+    ap.add_argument("--slab", action="store_true",
+                    help="multi-GPU z-slab decomposition of one system (strong "
+                         "scaling; default workload config 4)")
     return ap.parse_args()
 
 
@@ -423,10 +426,77 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_slab(args):
+    """Strong scaling: one config-4 system decomposed into z-slabs over the
+    ranks (NCCL halo send/recv, all-to-all transposes, 7-double all-gather)."""
+    import torch
+
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver, workloads
+    from paper_2601_00161_b200.mesh import plan_grid
+    from paper_2601_00161_b200.pswf import build_pswf, solve_bandwidth, tabulate_window
+    from paper_2601_00161_b200.slab import SlabKSpaceSolver
+
+    rank, world, local = dist_env()
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = args.config if args.config != CONFIG else 4
+    w, pos_np, q_np = workloads.generate(cfg)
+    basis = build_pswf(solve_bandwidth(w.delta))
+    window = tabulate_window(basis, w.P)
+    s = SlabKSpaceSolver(w.h, w.M, w.P, basis, window, w.r_c, precision=args.precision,
+                         capacity=w.n // max(world, 1) + w.n // 8)
+    mine = s.owned(pos_np)
+    pos = torch.as_tensor(pos_np[mine], device=dev)
+    q = torch.as_tensor(q_np[mine], device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(want_forces, K, W):
+        for _ in range(W):
+            s.evaluate(pos, q, want_forces)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(K)]
+        for i in range(K):
+            flush.zero_()
+            ev[i][0].record(stream)
+            s.evaluate(pos, q, want_forces)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / K, dist, dev)
+
+    with ClockSampler(local) as clk:
+        ms_fp = timed(True, args.steps, args.warmup)
+        ms_po = timed(False, args.steps, args.warmup)
+    line = {"metric": METRIC, "value": w.n / (ms_fp * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_fp,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic (seeded config recipe, SURVEY §8(d.1))",
+            "config": {"workload": w.name, "n_charges": w.n, "grid": list(w.M), "P": w.P,
+                       "parallelism": f"zslab{world}", "precision": args.precision,
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "pressure_only": {"value": w.n / (ms_po * 1e-3), "unit": UNIT,
+                              "ms_per_step": ms_po},
+            "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.slab:
+        run_slab(args)
     else:
         run_ours(args)
 

@@ -91,6 +91,11 @@ typedef struct esp_plan_desc {
   double kmax;             /* split_c / r_c (kernel.py:28-39)                */
   /* Tile shape override (0 = automatic).                                   */
   int32_t tile[3];
+  /* z-slab plans (multi-GPU slab decomposition): 0 = whole
+   * periodic grid.  Otherwise M[2] = owned planes + P - 1 ghost planes,
+   * slab_mz_global = global Mz and slab_z0 = first owned global plane.      */
+  int32_t slab_mz_global;
+  int32_t slab_z0;
 } esp_plan_desc;
 
 /* Per-cell data (ModeWorkspace inputs; re-sent on NPT rebind with M pinned,
@@ -137,6 +142,10 @@ int esp_scale_reduce(esp_plan* plan, double* d_out7, int32_t write_ik, void* str
  * preceding esp_spread on the same particles and esp_scale_reduce with
  * write_ik=1).  Counts three inverse transforms.                           */
 int esp_forces_ik(esp_plan* plan, double* d_forces, void* stream);
+/* Gather ik forces from caller-provided field grids [3][M2][M1][M0] (e.g. a
+ * slab with ghost planes) for the particles of the last esp_spread.        */
+int esp_gather_fields(esp_plan* plan, const void* d_fields, double* d_forces,
+                      void* stream);
 /* One inverse transform + window-gradient gather (orthorhombic only).      */
 int esp_forces_analytic(esp_plan* plan, double* d_forces, void* stream);
 /* Six inverse transforms + gathers -> per-particle tensors (N,3,3).        */
@@ -152,6 +161,7 @@ int esp_reset_counters(esp_plan* plan);
 /* Device pointers into the plan (valid until destroy / next set_cell).     */
 void* esp_grid_ptr(esp_plan* plan);       /* real grid, [z][y][x]          */
 void* esp_spectrum_ptr(esp_plan* plan);   /* complex half spectrum          */
+void* esp_fields_ptr(esp_plan* plan);     /* 3 ik force fields, [3][z][y][x] */
 int esp_grid_info(const esp_plan* plan, int64_t* info8);
 /* info8 = {Mx, My, Mz, Hx(=Mx/2+1), n_modes_retained(full spectrum),
  *          kernel_launches_last_step, n_tiles, precision}                   */

@@ -57,6 +57,8 @@ class PlanDesc(C.Structure):
         ("r_c", C.c_double),
         ("kmax", C.c_double),
         ("tile", C.c_int32 * 3),
+        ("slab_mz_global", C.c_int32),
+        ("slab_z0", C.c_int32),
     ]
 
 
@@ -101,6 +103,7 @@ def lib():
     L.esp_scale_reduce.argtypes = [vp, vp, C.c_int32, vp]
     L.esp_forces_ik.argtypes = [vp, vp, vp]
     L.esp_forces_analytic.argtypes = [vp, vp, vp]
+    L.esp_gather_fields.argtypes = [vp, vp, vp, vp]
     L.esp_local_pressure.argtypes = [vp, vp, vp]
     L.esp_evaluate.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp]
     L.esp_counters.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -109,6 +112,8 @@ def lib():
     L.esp_grid_ptr.restype = vp
     L.esp_spectrum_ptr.argtypes = [vp]
     L.esp_spectrum_ptr.restype = vp
+    L.esp_fields_ptr.argtypes = [vp]
+    L.esp_fields_ptr.restype = vp
     L.esp_grid_info.argtypes = [vp, C.POINTER(C.c_int64)]
     L.esp_set_spectrum.argtypes = [vp, vp, vp]
     L.esp_set_profiling.argtypes = [vp, C.c_int32]
@@ -124,6 +129,7 @@ EXPORTED = [
     "esp_forces_analytic", "esp_local_pressure", "esp_evaluate", "esp_counters",
     "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
+    "esp_gather_fields", "esp_fields_ptr",
 ]
 
 

@@ -20,8 +20,10 @@ Geom make_geom(const esp_plan* p) {
   Geom g;
   for (int d = 0; d < 3; ++d) {
     g.M[d] = p->M[d];
+    g.Mu[d] = p->Mu[d];
     g.spacing[d] = p->spacing[d];
   }
+  g.zshift = p->zshift;
   for (int i = 0; i < 9; ++i) g.hinv[i] = p->hinv[i];
   g.P = p->P;
   g.lo = p->lo;
@@ -126,7 +128,13 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   }
   esp_plan* p = new esp_plan;
   std::memset(p, 0, sizeof(esp_plan));
-  for (int k = 0; k < 3; ++k) p->M[k] = d->M[k];
+  for (int k = 0; k < 3; ++k) p->M[k] = p->Mu[k] = d->M[k];
+  if (d->slab_mz_global > 0) {
+    // z-slab plan: local planes [0, M[2]) hold global planes zshift + i
+    // (owned planes plus P-1 ghost planes); no periodic wrap inside the slab.
+    p->Mu[2] = d->slab_mz_global;
+    p->zshift = d->slab_z0 - ((d->P - 1) / 2);
+  }
   p->G = (long long)d->M[0] * d->M[1] * d->M[2];
   p->Hx = d->M[0] / 2 + 1;
   p->H = p->Hx * d->M[1] * d->M[2];
@@ -493,6 +501,18 @@ int esp_forces_ik(esp_plan* p, double* d_forces, void* stream) {
   return ESP_OK;
 }
 
+int esp_gather_fields(esp_plan* p, const void* d_fields, double* d_forces, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (!p->have_bins) {
+    set_error("esp_gather_fields needs a preceding esp_spread (particle bins)");
+    return ESP_ERR_MESH;
+  }
+  if (p->last_n > 0)
+    ESP_CUDA(esp::launch_gather_ik(p, d_forces, (cudaStream_t)stream, d_fields));
+  return ESP_OK;
+}
+
 int esp_forces_analytic(esp_plan* p, double* d_forces, void* stream) {
   (void)d_forces;
   (void)stream;
@@ -582,6 +602,7 @@ int esp_profile_read(esp_plan* p, char* names, int32_t names_len, double* ms, in
 
 void* esp_grid_ptr(esp_plan* p) { return p ? p->d_grid : nullptr; }
 void* esp_spectrum_ptr(esp_plan* p) { return p ? p->d_spec : nullptr; }
+void* esp_fields_ptr(esp_plan* p) { return p ? p->d_fields : nullptr; }
 
 int esp_grid_info(const esp_plan* p, int64_t* info) {
   if (!p || !info) return ESP_ERR_PARAM;

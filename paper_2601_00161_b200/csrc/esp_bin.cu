@@ -36,7 +36,7 @@ __device__ __forceinline__ void write_record(const Geom& g, const FastTab& ft,
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const double base = anchor_base(g, u[d]);
-    const int a = wrap_index((long long)base, g.M[d]);
+    const int a = local_anchor(g, d, base);
     packed |= (a - org[d]) << (8 * d);
     real w[P];
     stencil_weights<real, P>(ft, tab, brk, n_pieces, ncoef, u[d], base, g.lo, real(1), w);
@@ -60,7 +60,7 @@ __global__ void k_bin_count(const double* __restrict__ pos, long long n, Geom g,
     // Clamp pathological (non-finite / huge) coordinates into range; the
     // reference's int64 cast would be undefined there as well.
     b = fmin(fmax(b, -4.0e15), 4.0e15);
-    a[d] = wrap_index((long long)b, g.M[d]);
+    a[d] = local_anchor(g, d, b);
   }
   const int tx = a[0] / g.TX, ty = a[1] / g.TY;
   const int k = (ty * g.ntx + tx) * g.M[2] + a[2];

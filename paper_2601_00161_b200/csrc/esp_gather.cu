@@ -29,7 +29,7 @@ __device__ __forceinline__ void stage_weights_g(
     const int pl = item / 3, d = item - 3 * (item / 3);
     const double u = U[d * cap + c0 + pl];
     const double base = anchor_base(g, u);
-    const int a = wrap_index((long long)base, g.M[d]);
+    const int a = local_anchor(g, d, base);
     const int org = d == 0 ? tx * g.TX : (d == 1 ? ty * g.TY : tz * g.TZ);
     s_anc[d * kChunk + pl] = a - org;
     real* w = s_w + ((size_t)d * kChunk + pl) * P;
@@ -388,9 +388,14 @@ static cudaError_t gather_r(esp_plan* p, double* d_forces, cudaStream_t s) {
   }
 }
 
-cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s) {
-  return p->precision == ESP_FP64 ? gather_r<double>(p, d_forces, s)
-                                  : gather_r<float>(p, d_forces, s);
+cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s,
+                             const void* fields) {
+  void* saved = p->d_fields;
+  if (fields) p->d_fields = const_cast<void*>(fields);
+  cudaError_t e = p->precision == ESP_FP64 ? gather_r<double>(p, d_forces, s)
+                                           : gather_r<float>(p, d_forces, s);
+  p->d_fields = saved;
+  return e;
 }
 
 }  // namespace esp

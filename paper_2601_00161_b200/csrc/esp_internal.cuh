@@ -25,7 +25,9 @@ constexpr int kRedThreads = 256;
 
 // Grid/tile geometry passed by value to every kernel.
 struct Geom {
-  int M[3];
+  int M[3];             // local tile-grid counts (== Mu except for z slabs)
+  int Mu[3];            // global grid counts: coordinates and periodic wrap
+  int zshift;           // slab plans: local plane = global plane - zshift
   int P, lo, odd, ortho;
   double spacing[3];
   double hinv[9];       // row-major inverse cell matrix (triclinic u)
@@ -58,7 +60,7 @@ __device__ __forceinline__ void grid_coords(const Geom& g, double x, double y,
       double s = __dadd_rn(__dadd_rn(__dmul_rn(g.hinv[3 * d + 0], x),
                                      __dmul_rn(g.hinv[3 * d + 1], y)),
                            __dmul_rn(g.hinv[3 * d + 2], z));
-      u[d] = __dmul_rn(s, (double)g.M[d]);
+      u[d] = __dmul_rn(s, (double)g.Mu[d]);
     }
   }
 }
@@ -72,6 +74,13 @@ __device__ __forceinline__ double anchor_base(const Geom& g, double u) {
 __device__ __forceinline__ int wrap_index(long long v, int M) {
   long long r = v % M;
   return (int)(r < 0 ? r + M : r);
+}
+
+// Local anchor index of a stencil base along axis d: the periodic global
+// anchor, shifted into the slab's local planes for z.
+__device__ __forceinline__ int local_anchor(const Geom& g, int d, double base) {
+  const int a = wrap_index((long long)base, g.Mu[d]);
+  return d == 2 ? a - g.zshift : a;
 }
 
 // Periodic wrap for indices a few periods from [0, M): no division.
@@ -198,6 +207,8 @@ template <> struct Cplx<float> { using type = float2; };
 struct esp_plan {
   // static description
   int M[3];
+  int Mu[3];              // global grid counts (slab plans: Mu[2] != M[2])
+  int zshift;             // slab plans: z0 + lo
   long long G, Hx, H;
   int P, lo, odd, precision, deterministic;
   long long cap;
@@ -269,7 +280,8 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
 cudaError_t launch_spread(esp_plan* p, cudaStream_t s);
 cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
                                 cudaStream_t s);
-cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s);
+cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s,
+                             const void* fields = nullptr);
 cudaError_t launch_mode_setup(esp_plan* p, double what_zero, cudaStream_t s);
 void build_combine_axis(int M, int T, int E, int nt, int lo, std::vector<int>& ent,
                         std::vector<int>& cnt);

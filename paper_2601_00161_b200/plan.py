@@ -123,7 +123,11 @@ class EspPlan:
 
     def __init__(self, M, P: int, window: WindowTable, split: PswfBasis, r_c: float,
                  spread: PswfBasis | None = None, precision: str = "fp64",
-                 deterministic: bool = True, capacity: int = 1 << 16, tile=(0, 0, 0)):
+                 deterministic: bool = True, capacity: int = 1 << 16, tile=(0, 0, 0),
+                 slab: tuple | None = None):
+        """``slab=(Mz_global, z0, nz)``: a z-slab plan for the multi-GPU slab
+        decomposition — the local grid is (Mx, My, nz + P - 1) holding global
+        planes z0 + lo ... (owned planes plus ghost planes)."""
         if not torch.cuda.is_available():
             raise RuntimeError("EspPlan needs a CUDA device (the B200 path has no CPU fallback)")
         if precision not in _DT:
@@ -132,8 +136,15 @@ class EspPlan:
             raise PlanningError("supplied window table does not match P")
         torch.cuda.current_device()
         torch.empty(0, device="cuda")  # make torch's primary context current
-        self.M = tuple(int(m) for m in M)
         self.P = int(P)
+        self.slab = tuple(int(v) for v in slab) if slab is not None else None
+        if self.slab is not None:
+            Mz_glob, z0, nz = self.slab
+            self.M_global = (int(M[0]), int(M[1]), Mz_glob)
+            M = (int(M[0]), int(M[1]), nz + self.P - 1)
+        self.M = tuple(int(m) for m in M)
+        if self.slab is None:
+            self.M_global = self.M
         self.window = window
         self.split = split
         self.spread_basis = spread if spread is not None else split
@@ -178,6 +189,9 @@ class EspPlan:
         d.r_c = self.r_c
         d.kmax = self.kmax
         d.tile[:] = list(self.tile)
+        if self.slab is not None:
+            d.slab_mz_global = self.slab[0]
+            d.slab_z0 = self.slab[1]
         h = C.c_void_p()
         _lib.check(L.esp_plan_create(C.byref(d), C.byref(h)), "esp_plan_create")
         self._handle = h
@@ -210,7 +224,15 @@ class EspPlan:
 
     # -- per cell -------------------------------------------------------------
     def set_cell(self, h, orthorhombic=None, stream=None):
-        t = cell_tables(h, self.M, self.P, self.spread_basis, self.kmax, orthorhombic)
+        t = cell_tables(h, self.M_global, self.P, self.spread_basis, self.kmax, orthorhombic)
+        if self.slab is not None:
+            # slab plans spread/gather only: z axis arrays resized to the local
+            # plane count (their mode tables are never used)
+            nzl = self.M[2]
+            for a in range(3):
+                t.axis_k[a][2] = np.ascontiguousarray(np.resize(t.axis_k[a][2], nzl))
+            t.axis_what[2] = np.ascontiguousarray(np.resize(t.axis_what[2], nzl))
+            t.band = (t.band[0], t.band[1], min(t.band[2], nzl // 2))
         c = _lib.CellDesc()
         c.h[:] = list(t.h.reshape(-1))
         c.hinv[:] = list(t.hinv.reshape(-1))
@@ -255,6 +277,14 @@ class EspPlan:
         ts = "<f8" if self.precision == "fp64" else "<f4"
         ptr = _lib.lib().esp_grid_ptr(self._handle)
         return torch.as_tensor(_DevView(ptr, (self.M[2], self.M[1], self.M[0]), ts),
+                               device="cuda")
+
+    def fields_view(self) -> torch.Tensor:
+        """Alias of the plan's three ik force fields (3, Mz, My, Mx) of the last
+        force evaluation (diagnostics / slab tests)."""
+        ts = "<f8" if self.precision == "fp64" else "<f4"
+        ptr = _lib.lib().esp_fields_ptr(self._handle)
+        return torch.as_tensor(_DevView(ptr, (3, self.M[2], self.M[1], self.M[0]), ts),
                                device="cuda")
 
     def spectrum_view(self) -> torch.Tensor:
@@ -310,6 +340,20 @@ class EspPlan:
                                                int(bool(write_ik)), _stream_handle(stream)),
                    "esp_scale_reduce")
         return out7
+
+    def gather_fields(self, fields: torch.Tensor, n: int, forces: torch.Tensor | None = None,
+                      stream=None):
+        """ik forces from caller fields [3][M2][M1][M0] for the particles of the
+        last spread (slab plans: the owned planes plus ghost planes)."""
+        f = fields.contiguous()
+        if f.dtype != self.real_dtype or f.numel() != 3 * int(np.prod(self.M)):
+            raise ParameterError("fields shape/dtype does not match the plan")
+        if forces is None:
+            forces = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().esp_gather_fields(self._handle, C.c_void_p(f.data_ptr()),
+                                                C.c_void_p(forces.data_ptr()),
+                                                _stream_handle(stream)), "esp_gather_fields")
+        return forces
 
     def forces_ik(self, n: int, forces: torch.Tensor | None = None, stream=None):
         if forces is None:
