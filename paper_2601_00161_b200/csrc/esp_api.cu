@@ -79,7 +79,7 @@ static void free_all(esp_plan* p) {
                   p->d_grid,    p->d_spec,     p->d_ikspec,  p->d_fields,  p->d_axis_k,
                   p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
                   p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt,
-                  p->d_wrec,     p->d_pk};
+                  p->d_wrec,     p->d_pk,       p->d_drec,    p->d_err_out7};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_fwd) cufftDestroy(p->fwd);
@@ -223,6 +223,7 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(dalloc(&p->d_q_tmp, cap));
   TRY(dalloc(&p->d_idx_tmp, cap));
   TRY(cudaMalloc(&p->d_wrec, real_sz * 3 * esp::rec_stride(p->P) * cap));
+  TRY(cudaMalloc(&p->d_drec, real_sz * 3 * esp::rec_stride(p->P) * cap));
   TRY(dalloc(&p->d_pk, cap));
   p->cub_bytes = esp::scan_temp_bytes(p->n_keys + 1);
   TRY(cudaMalloc(&p->d_cub, std::max<size_t>(p->cub_bytes, 16)));
@@ -234,6 +235,7 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(cudaMalloc(&p->d_ikspec, 3 * 2 * real_sz * (size_t)p->H));
   TRY(cudaMalloc(&p->d_fields, 3 * real_sz * (size_t)p->G));
   TRY(dalloc(&p->d_err, 4));
+  TRY(dalloc(&p->d_err_out7, 8));
   // fast window table (kernel parameter) and deterministic-combine tables
   p->h_fast = new esp::FastTab;
   std::memset(p->h_fast, 0, sizeof(esp::FastTab));
@@ -514,21 +516,57 @@ int esp_gather_fields(esp_plan* p, const void* d_fields, double* d_forces, void*
 }
 
 int esp_forces_analytic(esp_plan* p, double* d_forces, void* stream) {
-  (void)d_forces;
-  (void)stream;
   int rc = check_ready(p);
   if (rc) return rc;
-  set_error("analytic-differentiation forces are not built in this release");
-  return ESP_ERR_MESH;
+  if (!p->have_spec || !p->have_bins) {
+    set_error("analytic forces need esp_spread and esp_forward first");
+    return ESP_ERR_MESH;
+  }
+  if (p->P > 8) {
+    set_error("analytic-differentiation gather supports P <= 8");
+    return ESP_ERR_PLANNING;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  ESP_CUDA(esp::launch_scale_reduce(p, p->d_err_out7, 2, s));
+  ESP_CUFFT(cufftSetStream(p->inv1, s));
+  if (p->precision == ESP_FP64) {
+    ESP_CUFFT(cufftExecZ2D(p->inv1, (cufftDoubleComplex*)p->d_ikspec,
+                           (cufftDoubleReal*)p->d_fields));
+  } else {
+    ESP_CUFFT(cufftExecC2R(p->inv1, (cufftComplex*)p->d_ikspec, (cufftReal*)p->d_fields));
+  }
+  esp::prof_mark(p, s, "fft_inverse_x1");
+  p->inv_count += 1;
+  p->have_ik = 0;
+  if (p->last_n > 0) ESP_CUDA(esp::launch_gather_grad(p, d_forces, s));
+  return ESP_OK;
 }
 
 int esp_local_pressure(esp_plan* p, double* d_tensors, void* stream) {
-  (void)d_tensors;
-  (void)stream;
   int rc = check_ready(p);
   if (rc) return rc;
-  set_error("per-particle pressure is not built in this release");
-  return ESP_ERR_MESH;
+  if (!p->have_spec || !p->have_bins) {
+    set_error("local pressure needs esp_spread and esp_forward first");
+    return ESP_ERR_MESH;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // (xx, xy, xz) -> tensor slots (0, 1, 2) + mirrors (-, 3, 6);
+  // (yy, yz, zz) -> (4, 5, 8) + mirrors (-, 7, -)   (mesh.py:371-378)
+  const esp::OutMap maps[2] = {{9, {0, 1, 2}, {-1, 3, 6}}, {9, {4, 5, 8}, {-1, 7, -1}}};
+  for (int half = 0; half < 2; ++half) {
+    ESP_CUDA(esp::launch_scale_reduce(p, p->d_err_out7, 3 + half, s));
+    ESP_CUFFT(cufftSetStream(p->inv3, s));
+    if (p->precision == ESP_FP64) {
+      ESP_CUFFT(cufftExecZ2D(p->inv3, (cufftDoubleComplex*)p->d_ikspec,
+                             (cufftDoubleReal*)p->d_fields));
+    } else {
+      ESP_CUFFT(cufftExecC2R(p->inv3, (cufftComplex*)p->d_ikspec, (cufftReal*)p->d_fields));
+    }
+    p->inv_count += 3;
+    if (p->last_n > 0) ESP_CUDA(esp::launch_gather_ik(p, d_tensors, s, nullptr, maps[half]));
+  }
+  p->have_ik = 0;
+  return ESP_OK;
 }
 
 int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
@@ -536,7 +574,7 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
   int rc = check_ready(p);
   if (rc) return rc;
   const int want_f = (flags & ESP_WANT_FORCES) != 0;
-  if (want_f && (flags & ESP_FORCES_ANALYTIC)) return esp_forces_analytic(p, d_forces, stream);
+  const int analytic = (flags & ESP_FORCES_ANALYTIC) != 0;
   p->launches = 0;
   p->n_ev = 0;
   esp::prof_mark(p, (cudaStream_t)stream, "start");
@@ -544,9 +582,10 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
   if (rc) return rc;
   rc = esp_forward(p, nullptr, stream);
   if (rc) return rc;
-  rc = esp_scale_reduce(p, d_out7, want_f, stream);
+  rc = esp_scale_reduce(p, d_out7, want_f && !analytic, stream);
   if (rc) return rc;
-  if (want_f) rc = esp_forces_ik(p, d_forces, stream);
+  if (want_f) rc = analytic ? esp_forces_analytic(p, d_forces, stream)
+                            : esp_forces_ik(p, d_forces, stream);
   return rc;
 }
 

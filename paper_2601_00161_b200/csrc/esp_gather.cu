@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
 k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ wrec,
               const int* __restrict__ PK, const double* __restrict__ Q,
               const int* __restrict__ IDX, const real* __restrict__ fld, long long G,
-              double* __restrict__ forces) {
+              double* __restrict__ forces, OutMap om) {
   static_assert(P <= 8, "warp gather covers at most 8 stencil planes");
   using R2 = typename Real2<real>::type;
   constexpr int kPlane = GatherLayout<real, P>::kPlane;
@@ -191,10 +191,139 @@ k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
     }
     if ((lane & 15) == 0 && pl < p1) {
       const double q = Q[pl];
+      double* f = forces + (long long)IDX[pl] * om.stride;
+      const double v[3] = {-q * (double)ax, -q * (double)ay, -q * (double)az};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        f[om.m[c]] = v[c];
+        if (om.m2[c] >= 0) f[om.m2[c]] = v[c];
+      }
+    }
+  }
+}
+
+// Window-gradient gather (analytic differentiation, mesh.py:343-349): one
+// field, three derivative sums G_d = sum w..w'_d..w f over the stencil (the
+// derivative on axis d), F_a = -q sum_d G_d J[d][a] with J = du/dr.
+// Same lane mapping and conflict-free strides as k_gather_warp's f_z tile.
+struct Jac {
+  double j[9];
+};
+
+template <typename real, int P>
+__global__ void __launch_bounds__(kTileThreads, 2)
+k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ wrec,
+              const real* __restrict__ drec, const int* __restrict__ PK,
+              const double* __restrict__ Q, const int* __restrict__ IDX,
+              const real* __restrict__ fld, Jac J, double* __restrict__ forces) {
+  static_assert(P <= 8, "gradient gather covers at most 8 stencil planes");
+  constexpr int kRowZ = GatherLayout<real, P>::kRowZ;
+  constexpr int kPlaneZ = GatherLayout<real, P>::kPlaneZ;
+  constexpr int RS = rec_stride(P);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tile = blockIdx.x;
+  const int tz = tile % g.ntz;
+  const int txy = tile / g.ntz;
+  const int tx = txy % g.ntx, ty = txy / g.ntx;
+  const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+  const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+  const long long p0 = offsets[key0], p1 = offsets[key1];
+  if (p0 == p1) return;
+  real* s_f = reinterpret_cast<real*>(smem_raw);
+  {
+    const long long Mxy = (long long)g.M[0] * g.M[1];
+    const int r = threadIdx.x;
+    const int gx = wrap_near(tx * g.TX + g.lo + (r & 15), g.M[0]);
+    const int gy = wrap_near(ty * g.TY + g.lo + (r >> 4), g.M[1]);
+    const long long col = (long long)gy * g.M[0] + gx;
+    int gz = wrap_near(tz * g.TZ + g.lo, g.M[2]);
+    for (int pz = 0; pz < g.PZ; ++pz) {
+      s_f[pz * kPlaneZ + (r >> 4) * kRowZ + (r & 15)] = fld[gz * Mxy + col];
+      gz = gz + 1 == g.M[2] ? 0 : gz + 1;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 4, h = (lane >> 3) & 1, k = lane & 7;
+  for (long long pb = p0 + warp * 2; pb < p1; pb += (kTileThreads / 32) * 2) {
+    const long long pl = pb + slot;
+    const bool live = pl < p1 && k < P;
+    real gx = 0, gy = 0, gz = 0;
+    if (live) {
+      const int pk = PK[pl];
+      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = pk >> 16;
+      const real* W = wrec + pl * (3 * RS);
+      const real* D = drec + pl * (3 * RS);
+      real wx[P], dx[P], wy[P], dy[P];
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        wx[s] = W[s];
+        dx[s] = D[s];
+        wy[s] = W[RS + s];
+        dy[s] = D[RS + s];
+      }
+      const real wzk = W[2 * RS + k], dzk = D[2 * RS + k];
+      const real* row = s_f + (zl + k) * kPlaneZ + (yl + h) * kRowZ + xl;
+      real ax = 0, ay = 0, az = 0;
+#pragma unroll
+      for (int jj = 0; jj < (P + 1) / 2; ++jj) {
+        const int j = 2 * jj;
+        const bool odd_row = j + 1 < P;
+        if (odd_row || h == 0) {
+          const real wy_ = (odd_row && h) ? wy[odd_row ? j + 1 : j] : wy[j];
+          const real dy_ = (odd_row && h) ? dy[odd_row ? j + 1 : j] : dy[j];
+          real r0 = 0, r1 = 0;
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const real v = row[j * kRowZ + i];
+            r0 = fma(wx[i], v, r0);
+            r1 = fma(dx[i], v, r1);
+          }
+          ax = fma(wy_, r1, ax);     // d/dx
+          ay = fma(dy_, r0, ay);     // d/dy
+          az = fma(wy_, r0, az);     // d/dz (plane weight below)
+        }
+      }
+      gx = ax * wzk;
+      gy = ay * wzk;
+      gz = az * dzk;
+    }
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      gx += __shfl_xor_sync(0xffffffffu, gx, o);
+      gy += __shfl_xor_sync(0xffffffffu, gy, o);
+      gz += __shfl_xor_sync(0xffffffffu, gz, o);
+    }
+    if ((lane & 15) == 0 && pl < p1) {
+      const double q = Q[pl];
+      const double G3[3] = {(double)gx, (double)gy, (double)gz};
       double* f = forces + (long long)IDX[pl] * 3;
-      f[0] = -q * (double)ax;
-      f[1] = -q * (double)ay;
-      f[2] = -q * (double)az;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        f[a] = -q * ((G3[0] * J.j[0 * 3 + a] + G3[1] * J.j[1 * 3 + a]) + G3[2] * J.j[2 * 3 + a]);
+    }
+  }
+}
+
+// Window-derivative records dW/dt of every binned particle (analytic mode).
+template <typename real, int P>
+__global__ void k_dweights(Geom g, const real* __restrict__ dtab,
+                           const double* __restrict__ brk, int n_pieces, int ncoef,
+                           long long n, long long cap, const double* __restrict__ U,
+                           real* __restrict__ drec) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  constexpr int RS = rec_stride(P);
+  real* out = drec + j * (3 * RS);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double u = U[d * cap + j];
+    const double base = anchor_base(g, u);
+#pragma unroll
+    for (int s = 0; s < RS; ++s) {
+      real v = real(0);
+      if (s < P) v = window_eval<real>(dtab, brk, n_pieces, ncoef, u - (base + (double)(g.lo + s)));
+      out[d * RS + s] = v;
     }
   }
 }
@@ -205,7 +334,7 @@ k_gather_ik(Geom g, const real* __restrict__ tab, const double* __restrict__ brk
             int n_pieces, int ncoef, const int* __restrict__ offsets,
             const double* __restrict__ U, const double* __restrict__ Q,
             const int* __restrict__ IDX, long long cap, const real* __restrict__ fld,
-            long long G, double* __restrict__ forces) {
+            long long G, double* __restrict__ forces, OutMap om) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tile = blockIdx.x;
   const int tz = tile % g.ntz;
@@ -311,7 +440,8 @@ k_gather_ik(Geom g, const real* __restrict__ tab, const double* __restrict__ brk
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += s_acc[((size_t)pl * 8 + w) * 3 + c];
-        forces[id * 3 + c] = -q * s;
+        forces[id * om.stride + om.m[c]] = -q * s;
+        if (om.m2[c] >= 0) forces[id * om.stride + om.m2[c]] = -q * s;
       }
     }
   }
@@ -331,7 +461,7 @@ static size_t gather_smem(int P, int n_pieces, int ncoef) {
 }
 
 template <typename real, int P>
-static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s, OutMap om) {
   Geom g = make_geom(p);
   if constexpr (P <= 8) {
     const size_t smem = GatherLayout<real, P>::bytes(p->PZ);
@@ -345,7 +475,7 @@ static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s) {
     }
     k_gather_warp<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
         g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q, p->d_idx,
-        reinterpret_cast<const real*>(p->d_fields), p->G, d_forces);
+        reinterpret_cast<const real*>(p->d_fields), p->G, d_forces, om);
     p->launches++;
     prof_mark(p, s, "gather");
     return cudaGetLastError();
@@ -364,38 +494,97 @@ static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   }
   k_gather_ik<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
       g, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->d_q,
-      p->d_idx, p->cap, reinterpret_cast<const real*>(p->d_fields), p->G, d_forces);
+      p->d_idx, p->cap, reinterpret_cast<const real*>(p->d_fields), p->G, d_forces, om);
   p->launches++;
   prof_mark(p, s, "gather");
   return cudaGetLastError();
 }
 
 template <typename real>
-static cudaError_t gather_r(esp_plan* p, double* d_forces, cudaStream_t s) {
+static cudaError_t gather_r(esp_plan* p, double* d_forces, cudaStream_t s, OutMap om) {
   switch (p->P) {
-    case 2: return gather_p<real, 2>(p, d_forces, s);
-    case 3: return gather_p<real, 3>(p, d_forces, s);
-    case 4: return gather_p<real, 4>(p, d_forces, s);
-    case 5: return gather_p<real, 5>(p, d_forces, s);
-    case 6: return gather_p<real, 6>(p, d_forces, s);
-    case 7: return gather_p<real, 7>(p, d_forces, s);
-    case 8: return gather_p<real, 8>(p, d_forces, s);
-    case 9: return gather_p<real, 9>(p, d_forces, s);
-    case 10: return gather_p<real, 10>(p, d_forces, s);
-    case 11: return gather_p<real, 11>(p, d_forces, s);
-    case 12: return gather_p<real, 12>(p, d_forces, s);
+    case 2: return gather_p<real, 2>(p, d_forces, s, om);
+    case 3: return gather_p<real, 3>(p, d_forces, s, om);
+    case 4: return gather_p<real, 4>(p, d_forces, s, om);
+    case 5: return gather_p<real, 5>(p, d_forces, s, om);
+    case 6: return gather_p<real, 6>(p, d_forces, s, om);
+    case 7: return gather_p<real, 7>(p, d_forces, s, om);
+    case 8: return gather_p<real, 8>(p, d_forces, s, om);
+    case 9: return gather_p<real, 9>(p, d_forces, s, om);
+    case 10: return gather_p<real, 10>(p, d_forces, s, om);
+    case 11: return gather_p<real, 11>(p, d_forces, s, om);
+    case 12: return gather_p<real, 12>(p, d_forces, s, om);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s,
-                             const void* fields) {
+                             const void* fields, OutMap om) {
   void* saved = p->d_fields;
   if (fields) p->d_fields = const_cast<void*>(fields);
-  cudaError_t e = p->precision == ESP_FP64 ? gather_r<double>(p, d_forces, s)
-                                           : gather_r<float>(p, d_forces, s);
+  cudaError_t e = p->precision == ESP_FP64 ? gather_r<double>(p, d_forces, s, om)
+                                           : gather_r<float>(p, d_forces, s, om);
   p->d_fields = saved;
   return e;
+}
+
+template <typename real, int P>
+static cudaError_t grad_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+  if constexpr (P > 8) {
+    return cudaErrorNotSupported;
+  } else {
+    Geom g = make_geom(p);
+    const real* dtab = std::is_same<real, double>::value
+                           ? reinterpret_cast<const real*>(p->d_dtab)
+                           : reinterpret_cast<const real*>(p->d_dtabf);
+    const int B = 256;
+    const long long n = p->last_n;
+    k_dweights<real, P><<<(unsigned)((n + B - 1) / B), B, 0, s>>>(
+        g, dtab, p->d_breaks, p->n_pieces, p->ncoef, n, p->cap, p->d_u,
+        reinterpret_cast<real*>(p->d_drec));
+    p->launches++;
+    prof_mark(p, s, "dweights");
+    Jac J;
+    for (int d = 0; d < 3; ++d)
+      for (int a = 0; a < 3; ++a)
+        J.j[d * 3 + a] = p->ortho ? (d == a ? 1.0 / p->spacing[d] : 0.0)
+                                  : (double)p->Mu[d] * p->hinv[d * 3 + a];
+    const size_t smem = sizeof(real) * (size_t)p->PZ * GatherLayout<real, P>::kPlaneZ;
+    static size_t attr_set = 0;
+    if (smem > attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(k_gather_grad<real, P>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_set = smem;
+    }
+    k_gather_grad<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
+        g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec),
+        reinterpret_cast<const real*>(p->d_drec), p->d_pk, p->d_q, p->d_idx,
+        reinterpret_cast<const real*>(p->d_fields), J, d_forces);
+    p->launches++;
+    prof_mark(p, s, "gather_grad");
+    return cudaGetLastError();
+  }
+}
+
+template <typename real>
+static cudaError_t grad_r(esp_plan* p, double* d_forces, cudaStream_t s) {
+  switch (p->P) {
+    case 2: return grad_p<real, 2>(p, d_forces, s);
+    case 3: return grad_p<real, 3>(p, d_forces, s);
+    case 4: return grad_p<real, 4>(p, d_forces, s);
+    case 5: return grad_p<real, 5>(p, d_forces, s);
+    case 6: return grad_p<real, 6>(p, d_forces, s);
+    case 7: return grad_p<real, 7>(p, d_forces, s);
+    case 8: return grad_p<real, 8>(p, d_forces, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s) {
+  return p->precision == ESP_FP64 ? grad_r<double>(p, d_forces, s)
+                                  : grad_r<float>(p, d_forces, s);
 }
 
 }  // namespace esp

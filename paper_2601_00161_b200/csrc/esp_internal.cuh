@@ -235,6 +235,7 @@ struct esp_plan {
   int* d_idx;
   double *d_u_tmp, *d_q_tmp;
   int* d_idx_tmp;
+  void* d_drec;           // per binned particle: window-derivative weights (analytic)
   void* d_wrec;           // per binned particle: 24 window weights (x|y|z, q folded
                           // into x by the spread), precision of the plan
   int* d_pk;              // per binned particle: tile-local anchor x | y<<8 | z<<16
@@ -253,6 +254,7 @@ struct esp_plan {
   double *d_modeA, *d_modeB;
   double* d_partials;
   int* d_err;
+  double* d_err_out7;     // sink for reductions run only to write spectra
   int* d_comb_ent;        // combine candidate tables (3 axes)
   int* d_comb_cnt;
   long long comb_off[3];
@@ -280,8 +282,17 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
 cudaError_t launch_spread(esp_plan* p, cudaStream_t s);
 cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
                                 cudaStream_t s);
+// Output placement of the 3 gathered values of particle id:
+// out[id*stride + m[c]] (and out[id*stride + m2[c]] when m2[c] >= 0).
+struct OutMap {
+  int stride;
+  int m[3];
+  int m2[3];
+};
 cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s,
-                             const void* fields = nullptr);
+                             const void* fields = nullptr,
+                             OutMap om = OutMap{3, {0, 1, 2}, {-1, -1, -1}});
+cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s);
 cudaError_t launch_mode_setup(esp_plan* p, double what_zero, cudaStream_t s);
 void build_combine_axis(int M, int T, int E, int nt, int lo, std::vector<int>& ent,
                         std::vector<int>& cnt);

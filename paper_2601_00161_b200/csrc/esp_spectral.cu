@@ -104,7 +104,8 @@ template <typename real>
 __global__ void __launch_bounds__(kRedThreads)
 k_scale_reduce(ModeArgs a, const typename Cplx<real>::type* __restrict__ spec,
                const double* __restrict__ modeA, const double* __restrict__ modeB,
-               double ik_scale, int write_ik, typename Cplx<real>::type* __restrict__ ik,
+               double ik_scale, double lp_scale, int write_ik,
+               typename Cplx<real>::type* __restrict__ ik,
                long long H, double* __restrict__ partials) {
   using C = typename Cplx<real>::type;
   double acc[7];
@@ -136,13 +137,32 @@ k_scale_reduce(ModeArgs a, const typename Cplx<real>::type* __restrict__ spec,
     acc[4] += t * ky * ky + wa;
     acc[5] += t * ky * kz;
     acc[6] += t * kz * kz + wa;
-    if (write_ik) {
+    if (write_ik == 1) {            // ik forces: i k_d A X h3/G
       const double c = A * ik_scale;
       const double cr = c * xr, ci = c * xi;
       C o;
       o.x = (real)(-kx * ci); o.y = (real)(kx * cr); ik[sidx] = o;
       o.x = (real)(-ky * ci); o.y = (real)(ky * cr); ik[H + sidx] = o;
       o.x = (real)(-kz * ci); o.y = (real)(kz * cr); ik[2 * H + sidx] = o;
+    } else if (write_ik == 2) {     // analytic forces: A X h3/G (mesh.py:344-346)
+      const double c = A * ik_scale;
+      C o;
+      o.x = (real)(c * xr); o.y = (real)(c * xi); ik[sidx] = o;
+    } else if (write_ik >= 3) {     // local pressure: -(B k_a k_b + d_ab A) X h3/(2 V G)
+      const double ka[3] = {kx, ky, kz};
+      const int bs[2][3] = {{0, 1, 2}, {1, 2, 2}};   // (xx,xy,xz) | (yy,yz,zz)
+      const int as[2][3] = {{0, 0, 0}, {1, 1, 2}};
+      const int m = write_ik - 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int aa = as[m][c], bb = bs[m][c];
+        const double kern = B * ka[aa] * ka[bb] + (aa == bb ? A : 0.0);
+        const double f = -kern * lp_scale;
+        C o;
+        o.x = (real)(f * xr);
+        o.y = (real)(f * xi);
+        ik[(long long)c * H + sidx] = o;
+      }
     }
   }
   block_reduce_store<7>(acc, partials + (size_t)blockIdx.x * 8);
@@ -202,22 +222,24 @@ cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
                                 cudaStream_t s) {
   ModeArgs a = mode_args(p);
   const double G = (double)p->G;
+  const double lp_scale = p->h3 / (2.0 * p->volume * G);
   cudaError_t e;
   const size_t cbytes = p->precision == ESP_FP64 ? sizeof(double2) : sizeof(float2);
   if (write_ik) {
-    e = cudaMemsetAsync(p->d_ikspec, 0, 3 * (size_t)p->H * cbytes, s);
+    const size_t nspec = write_ik == 2 ? 1 : 3;
+    e = cudaMemsetAsync(p->d_ikspec, 0, nspec * (size_t)p->H * cbytes, s);
     if (e != cudaSuccess) return e;
     prof_mark(p, s, "ik_memset");
   }
   if (p->precision == ESP_FP64) {
     k_scale_reduce<double><<<p->n_red_blocks, kRedThreads, 0, s>>>(
         a, reinterpret_cast<const double2*>(p->d_spec), p->d_modeA, p->d_modeB,
-        p->h3 / G, write_ik, reinterpret_cast<double2*>(p->d_ikspec), p->H,
+        p->h3 / G, lp_scale, write_ik, reinterpret_cast<double2*>(p->d_ikspec), p->H,
         p->d_partials);
   } else {
     k_scale_reduce<float><<<p->n_red_blocks, kRedThreads, 0, s>>>(
         a, reinterpret_cast<const float2*>(p->d_spec), p->d_modeA, p->d_modeB,
-        p->h3 / G, write_ik, reinterpret_cast<float2*>(p->d_ikspec), p->H,
+        p->h3 / G, lp_scale, write_ik, reinterpret_cast<float2*>(p->d_ikspec), p->H,
         p->d_partials);
   }
   p->launches++;

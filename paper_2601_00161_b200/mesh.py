@@ -357,9 +357,6 @@ def long_range_forces(rho_hat: GridField, sys, kern: SplitKernel, spec, cell,
         raise MeshError("long_range_forces expects a spectral density")
     if mode not in ("ik", "analytic"):
         raise MeshError(f"unknown differentiation mode {mode!r}")
-    if mode == "analytic":
-        raise MeshError("analytic-differentiation forces are not built in this release "
-                        "(SURVEY §8(f) f1)")
     provider = provider or TransformProvider()
     plan = _spectrum_plan(rho_hat, kern, spec, cell)
     pos, q = _particles(sys)
@@ -367,15 +364,31 @@ def long_range_forces(rho_hat: GridField, sys, kern: SplitKernel, spec, cell,
     if getattr(plan, "_bins_for", None) != id(sys):
         plan.spread(pos, q)        # re-bin these particles; the spectrum is untouched
         plan._bins_for = id(sys)
-    plan.scale_reduce(write_ik=True)
-    F = plan.forces_ik(pos.shape[0])
-    provider.inverse_count += 3
+    if mode == "analytic":
+        F = plan.forces_analytic(pos.shape[0])
+        provider.inverse_count += 1
+    else:
+        plan.scale_reduce(write_ik=True)
+        F = plan.forces_ik(pos.shape[0])
+        provider.inverse_count += 3
     plan.version = version
     return F.cpu().numpy()
 
 
-def local_pressure(rho_hat: GridField, sys, kern, spec, cell, provider=None, modes=None):
-    """Per-particle pressure tensors (mesh.py:353-379) — SURVEY §8(f) f2."""
+def local_pressure(rho_hat: GridField, sys, kern, spec, cell,
+                   provider: TransformProvider | None = None, modes=None) -> np.ndarray:
+    """Per-particle far-field pressure tensors (N,3,3) (mesh.py:353-379): six
+    inverse transforms (two batched C2R x3) and window gathers."""
     if rho_hat.space != "fourier":
         raise MeshError("local_pressure expects a spectral density")
-    raise MeshError("per-particle pressure is not built in this release (SURVEY §8(f) f2)")
+    provider = provider or TransformProvider()
+    plan = _spectrum_plan(rho_hat, kern, spec, cell)
+    pos, q = _particles(sys)
+    version = plan.version
+    if getattr(plan, "_bins_for", None) != id(sys):
+        plan.spread(pos, q)
+        plan._bins_for = id(sys)
+    out = plan.local_pressure(pos.shape[0])
+    provider.inverse_count += 6
+    plan.version = version
+    return out.cpu().numpy()

@@ -362,9 +362,25 @@ class EspPlan:
                                             _stream_handle(stream)), "esp_forces_ik")
         return forces
 
+    def forces_analytic(self, n: int, forces: torch.Tensor | None = None, stream=None):
+        """One inverse transform + window-gradient gather (mesh.py:343-349)."""
+        if forces is None:
+            forces = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().esp_forces_analytic(self._handle, C.c_void_p(forces.data_ptr()),
+                                                  _stream_handle(stream)), "esp_forces_analytic")
+        return forces
+
+    def local_pressure(self, n: int, out: torch.Tensor | None = None, stream=None):
+        """Per-particle far-field pressure tensors (N,3,3) (mesh.py:353-379)."""
+        if out is None:
+            out = torch.empty((n, 3, 3), dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().esp_local_pressure(self._handle, C.c_void_p(out.data_ptr()),
+                                                 _stream_handle(stream)), "esp_local_pressure")
+        return out
+
     def evaluate(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool = True,
                  out7: torch.Tensor | None = None, forces: torch.Tensor | None = None,
-                 stream=None):
+                 stream=None, analytic: bool = False):
         """Whole step on the device: (out7[E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz], F)."""
         pos, q = self._check_particles(pos, q)
         n = pos.shape[0]
@@ -374,6 +390,8 @@ class EspPlan:
         if want_forces and forces is None:
             forces = torch.empty((n, 3), dtype=torch.float64, device="cuda")
         flags = _lib.ESP_WANT_ENERGY_PRESSURE | (_lib.ESP_WANT_FORCES if want_forces else 0)
+        if analytic:
+            flags |= _lib.ESP_FORCES_ANALYTIC
         _lib.check(_lib.lib().esp_evaluate(
             self._handle, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()), n, flags,
             C.c_void_p(out7.data_ptr()),

@@ -122,7 +122,8 @@ class KSpaceSolver:
                         want_forces: bool = True, out7=None, forces=None, stream=None):
         """Device-only step: returns (out7 tensor, forces tensor|None) without
         synchronising.  out7 = [E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz] (prefactor 1)."""
-        return self.plan.evaluate(positions, charges, want_forces, out7, forces, stream)
+        return self.plan.evaluate(positions, charges, want_forces, out7, forces, stream,
+                                  analytic=self.params.force_mode == "analytic")
 
     def graphed(self, positions: torch.Tensor, charges: torch.Tensor,
                 want_forces: bool = True, out7=None, forces=None):
@@ -150,7 +151,8 @@ class KSpaceSolver:
         host = not isinstance(positions, torch.Tensor)
         pos = _to_device(positions)
         q = _to_device(charges)
-        out7, F = self.plan.evaluate(pos, q, want_forces)
+        out7, F = self.plan.evaluate(pos, q, want_forces,
+                                     analytic=self.params.force_mode == "analytic")
         E, Pt = out7_to_tensor(out7)
         pref = self.params.prefactor
         if want_forces:
@@ -159,6 +161,15 @@ class KSpaceSolver:
                 F = F.cpu().numpy()
         return KSpaceResult(energy=pref * E, pressure=pref * Pt if want_pressure else None,
                             forces=F if want_forces else None, cell_type=self.cell_type)
+
+    def local_pressure(self, positions, charges):
+        """Per-particle far-field pressure tensors (N,3,3), prefactored
+        (evaluate.py:147-152, mesh.py:353-379)."""
+        host = not isinstance(positions, torch.Tensor)
+        pos, q = _to_device(positions), _to_device(charges)
+        self.plan.evaluate(pos, q, want_forces=False)
+        out = self.plan.local_pressure(pos.shape[0]) * self.params.prefactor
+        return out.cpu().numpy() if host else out
 
     def pressure_only(self, positions, charges):
         r = self.evaluate(positions, charges, want_forces=False)
@@ -266,6 +277,13 @@ class CoulombSolver:
                 p = p + pref * np.asarray(near.pressure)
             out.pressure = p
         return out
+
+
+def _coulomb_local_pressure(self, sys):
+    return self.kspace.local_pressure(sys.positions, sys.charges)
+
+
+CoulombSolver.local_pressure = _coulomb_local_pressure
 
 
 def evaluate_system(sys, params: EwaldParameters, want_forces=True, want_pressure=True):

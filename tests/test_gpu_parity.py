@@ -400,3 +400,57 @@ def test_slab_solver_single_rank_on_gpu():
     assert O.rel_scalar(E, r.energy) <= 1e-12
     assert O.rel_frobenius(Pt, r.pressure) <= 1e-12
     assert O.rms_rel_forces(F.cpu().numpy(), r.forces) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["small_cube_p5", "small_brick_p6", "small_brick_p8",
+                                  "small_brick_p7", "small_cube_p4"])
+def test_analytic_forces_and_local_pressure_match_reference(name):
+    """f1 / f2 of SURVEY §8(f): analytic-differentiation forces
+    (mesh.py:343-349) and per-particle pressure tensors (mesh.py:353-379)."""
+    torch = _torch()
+    g = golden(name)
+    plan = _plan_for(g)
+    pos, q = _dev(torch, g["pos"]), _dev(torch, g["q"])
+    plan.evaluate(pos, q, want_forces=True, analytic=True)
+    Fa = plan.forces_analytic(pos.shape[0]).cpu().numpy()
+    assert O.rms_rel_forces(Fa, g["F_analytic"]) <= F64_TOL
+    plan.reset_counters()
+    plan.evaluate(pos, q, want_forces=False)
+    lp = plan.local_pressure(pos.shape[0]).cpu().numpy()
+    assert plan.counters() == (1, 6)
+    ref = g["local"]
+    assert np.max(np.abs(lp - ref)) <= F64_TOL * np.max(np.abs(ref))
+    np.testing.assert_array_equal(lp, np.swapaxes(lp, 1, 2))
+    # sum of local tensors ~ global pressure (test_mesh.py:279-287)
+    assert np.linalg.norm(lp.sum(0) - g["Pt"]) <= 1e-8 * np.linalg.norm(g["Pt"])
+
+
+def test_analytic_forces_through_mesh_api_and_triclinic():
+    torch = _torch()
+    from paper_2601_00161_b200 import (Cell, ParticleSystem, SplitKernel, TransformProvider,
+                                       build_pswf, forward_density, long_range_forces,
+                                       local_pressure, plan_grid, solve_bandwidth)
+    g = golden("small_brick_p8")
+    b = build_pswf(solve_bandwidth(float(g["delta"])))
+    kern = SplitKernel(basis=b, r_c=float(g["r_c"]))
+    cell = Cell(g["h"])
+    spec = plan_grid(cell, kern, delta_spread=float(g["delta"]), P=int(g["P"]),
+                     spread_basis=b, fixed_M=tuple(g["M"]))
+    sys = ParticleSystem(cell=cell, positions=g["pos"], charges=g["q"])
+    prov = TransformProvider()
+    rho_hat = forward_density(sys, spec, prov)
+    Fa = long_range_forces(rho_hat, sys, kern, spec, cell, mode="analytic", provider=prov)
+    assert prov.inverse_count == 1
+    assert O.rms_rel_forces(Fa, g["F_analytic"]) <= F64_TOL
+    lp = local_pressure(rho_hat, sys, kern, spec, cell, provider=prov)
+    assert prov.inverse_count == 7
+    assert np.max(np.abs(lp - g["local"])) <= F64_TOL * np.max(np.abs(g["local"]))
+    # triclinic: analytic and ik forces agree at the Delta level
+    gt = golden("tri_skew_p8")
+    plan = _plan_for(gt, M=(64, 64, 80))
+    pos, q = _dev(torch, gt["pos"]), _dev(torch, gt["q"])
+    _, Fik = plan.evaluate(pos, q, want_forces=True)
+    Fik = Fik.cpu().numpy()
+    _, Fan = plan.evaluate(pos, q, want_forces=True, analytic=True)
+    assert O.rms_rel_forces(Fan.cpu().numpy(), Fik) <= 50 * float(gt["delta"])
+    assert O.rms_rel_forces(Fan.cpu().numpy(), gt["F_direct"]) <= 50 * float(gt["delta"])
