@@ -36,6 +36,9 @@ Geom make_geom(const esp_plan* p) {
   g.ntx = p->ntx;
   g.nty = p->nty;
   g.ntz = p->ntz;
+  g.TZS = p->TZS;
+  g.PZS = p->PZS;
+  g.ntzs = p->ntzs;
   g.n_keys = p->n_keys;
   return g;
 }
@@ -168,6 +171,12 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   p->nty = (d->M[1] + p->TY - 1) / p->TY;
   p->ntz = (d->M[2] + p->TZ - 1) / p->TZ;
   p->n_tiles = (long long)p->ntx * p->nty * p->ntz;
+  // spread tiles share the x-y decomposition (and so the binning keys) but run
+  // deeper in z on large grids: the scratch halo shrinks from (TZ+P-1)/TZ.
+  p->TZS = std::min(d->M[2] <= 128 ? p->TZ : std::max(p->TZ, 32), d->M[2]);
+  p->PZS = p->TZS + d->P - 1;
+  p->ntzs = (d->M[2] + p->TZS - 1) / p->TZS;
+  p->n_tiles_s = (long long)p->ntx * p->nty * p->ntzs;
   p->n_keys = (long long)p->ntx * p->nty * d->M[2];
 
   const size_t real_sz = p->precision == ESP_FP64 ? sizeof(double) : sizeof(float);
@@ -228,7 +237,7 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   p->cub_bytes = esp::scan_temp_bytes(p->n_keys + 1);
   TRY(cudaMalloc(&p->d_cub, std::max<size_t>(p->cub_bytes, 16)));
   TRY(cudaMalloc(&p->d_scratch,
-                 real_sz * (size_t)p->n_tiles * p->PZ * esp::kPad * esp::kPad));
+                 real_sz * (size_t)p->n_tiles_s * p->PZS * esp::kPad * esp::kPad));
   TRY(cudaMalloc(&p->d_grid, real_sz * (size_t)p->G));
   TRY(cudaMemset(p->d_grid, 0, real_sz * (size_t)p->G));
   TRY(cudaMalloc(&p->d_spec, 2 * real_sz * (size_t)p->H));
@@ -249,9 +258,9 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   }
   {
     std::vector<int> ent_all, cnt_all;
-    const int T[3] = {p->TX, p->TY, p->TZ};
-    const int E[3] = {esp::kPad, esp::kPad, p->PZ};
-    const int NT[3] = {p->ntx, p->nty, p->ntz};
+    const int T[3] = {p->TX, p->TY, p->TZS};
+    const int E[3] = {esp::kPad, esp::kPad, p->PZS};
+    const int NT[3] = {p->ntx, p->nty, p->ntzs};
     long long off = 0;
     for (int a = 0; a < 3; ++a) {
       std::vector<int> ent, cnt;

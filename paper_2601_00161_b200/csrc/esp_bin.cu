@@ -29,7 +29,8 @@ __device__ __forceinline__ void write_record(const Geom& g, const FastTab& ft,
                                              int* __restrict__ pk) {
   const int az = key % g.M[2];
   const int txy = key / g.M[2];
-  const int org[3] = {(txy % g.ntx) * g.TX, (txy / g.ntx) * g.TY, (az / g.TZ) * g.TZ};
+  // x, y relative to the tile; z absolute (spread and gather tiles differ in z)
+  const int org[3] = {(txy % g.ntx) * g.TX, (txy / g.ntx) * g.TY, 0};
   constexpr int RS = rec_stride(P);
   real* out = wrec + dst * (3 * RS);
   int packed = 0;

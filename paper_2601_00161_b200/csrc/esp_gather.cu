@@ -75,12 +75,14 @@ struct GatherLayout {
   // of one LDS.64 phase (8 planes x 2 adjacent rows) hit 16 distinct banks.
   static constexpr int kRowZ = 24;
   static constexpr int kPlaneZ = kPad * kRowZ + 1;
-  static size_t bytes(int PZ) {
+  static constexpr int kRing = (kTileThreads / 32) * 2 * 2 * 3 * rec_stride(P);  // warps x bufs x pair
+  __host__ __device__ static size_t fields_bytes(int PZ) {
     size_t b = 2 * sizeof(real) * (size_t)PZ * kPlane;   // (f_x, f_y) pairs
     b = (b + 15) & ~size_t(15);
     b += sizeof(real) * (size_t)PZ * kPlaneZ;           // f_z
-    return b;
+    return (b + 15) & ~size_t(15);
   }
+  static size_t bytes(int PZ) { return fields_bytes(PZ) + sizeof(real) * (size_t)kRing; }
 };
 
 // Warp = 2 particles x 8 stencil planes x 2 row parities.  Lane (p, h, k)
@@ -142,14 +144,61 @@ k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = lane >> 4, h = (lane >> 3) & 1, k = lane & 7;
-  for (long long pb = p0 + warp * 2; pb < p1; pb += (kTileThreads / 32) * 2) {
+  constexpr int kStep = (kTileThreads / 32) * 2;
+  constexpr int kRec = 3 * RS;                              // reals per record
+  constexpr int kChunks = (2 * kRec * (int)sizeof(real)) / 16;   // 16 B pieces per pair
+  real* ring = reinterpret_cast<real*>(smem_raw + GatherLayout<real, P>::fields_bytes(g.PZ)) +
+               (size_t)warp * 2 * 2 * kRec;
+  // Records of particle pair `pb` -> ring buffer `b` (cp.async, 16 B pieces).
+  auto fetch = [&](long long pb, int b) {
+    if (lane < kChunks) {
+      const long long first = pb;
+      const int avail = (int)min((long long)2, p1 - first);
+      const int bytes_needed = avail * kRec * (int)sizeof(real);
+      if (lane * 16 < bytes_needed) {
+        const char* src = reinterpret_cast<const char*>(wrec + first * kRec) + lane * 16;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(
+            reinterpret_cast<char*>(ring + (size_t)b * 2 * kRec) + lane * 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  long long pb = p0 + warp * 2;
+  int buf = 0;
+  if (pb < p1) fetch(pb, 0);
+  int pk_n = 0;
+  double q_n = 0.0;
+  int id_n = 0;
+  if (pb + slot < p1) {
+    pk_n = PK[pb + slot];
+    q_n = Q[pb + slot];
+    id_n = IDX[pb + slot];
+  }
+  for (; pb < p1; pb += kStep, buf ^= 1) {
     const long long pl = pb + slot;
     const bool live = pl < p1 && k < P;
+    const int pk_c = pk_n;
+    const double q_c = q_n;
+    const int id_c = id_n;
+    const long long nx = pb + kStep;
+    if (nx < p1) {
+      fetch(nx, buf ^ 1);
+      if (nx + slot < p1) {          // scalars of the next pair, consumed next iteration
+        pk_n = PK[nx + slot];
+        q_n = Q[nx + slot];
+        id_n = IDX[nx + slot];
+      }
+      asm volatile("cp.async.wait_group 1;");
+    } else {
+      asm volatile("cp.async.wait_group 0;");
+    }
+    __syncwarp();
     real ax = 0, ay = 0, az = 0;
     if (live) {
-      const int pk = PK[pl];
-      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = pk >> 16;
-      const real* W = wrec + pl * (3 * RS);
+      const int pk = pk_c;
+      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = (pk >> 16) - tz * g.TZ;
+      const real* W = ring + ((size_t)buf * 2 + slot) * kRec;
       real wx[P], wy[P];
 #pragma unroll
       for (int s = 0; s < P; ++s) {
@@ -189,9 +238,10 @@ k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
       ay += __shfl_xor_sync(0xffffffffu, ay, o);
       az += __shfl_xor_sync(0xffffffffu, az, o);
     }
+    __syncwarp();   // the ring slot is refilled two iterations later
     if ((lane & 15) == 0 && pl < p1) {
-      const double q = Q[pl];
-      double* f = forces + (long long)IDX[pl] * om.stride;
+      const double q = q_c;
+      double* f = forces + (long long)id_c * om.stride;
       const double v[3] = {-q * (double)ax, -q * (double)ay, -q * (double)az};
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -251,7 +301,7 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
     real gx = 0, gy = 0, gz = 0;
     if (live) {
       const int pk = PK[pl];
-      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = pk >> 16;
+      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = (pk >> 16) - tz * g.TZ;
       const real* W = wrec + pl * (3 * RS);
       const real* D = drec + pl * (3 * RS);
       real wx[P], dx[P], wy[P], dy[P];

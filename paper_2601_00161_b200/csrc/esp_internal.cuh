@@ -31,8 +31,9 @@ struct Geom {
   int P, lo, odd, ortho;
   double spacing[3];
   double hinv[9];       // row-major inverse cell matrix (triclinic u)
-  int TX, TY, TZ, PZ;   // anchor-cell tile and padded z extent
+  int TX, TY, TZ, PZ;   // anchor-cell tile and padded z extent (gather tiles)
   int ntx, nty, ntz;
+  int TZS, PZS, ntzs;   // spread tiles: deeper in z (less scratch halo)
   long long n_keys;     // ntx * nty * Mz  (key = (ty*ntx+tx)*Mz + az)
 };
 
@@ -217,7 +218,8 @@ struct esp_plan {
   int n_leg, n_legd;
   // tiles
   int TX, TY, TZ, PZ, ntx, nty, ntz;
-  long long n_tiles, n_keys;
+  int TZS, PZS, ntzs;
+  long long n_tiles, n_tiles_s, n_keys;
   // cell
   int have_cell;
   int ortho;

@@ -42,7 +42,7 @@ template <typename real, int P>
 struct SpreadLayout {
   static size_t bytes() {
     size_t b = sizeof(real) * (size_t)kSChunk * SpreadRec<P>::kLen;
-    b += sizeof(int) * (size_t)kSChunk * (3 + 1 + 4);   // anchors, packed, 4 warp lists
+    b += sizeof(int) * (size_t)kSChunk * (3 + 1 + 8);   // anchors, packed, 4 warp lists x2
     b += sizeof(int) * 8;                               // list lengths
     return b;
   }
@@ -56,11 +56,11 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
   using Rec = SpreadRec<P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tile = blockIdx.x;
-  const int tz = tile % g.ntz;
-  const int txy = tile / g.ntz;
+  const int tz = tile % g.ntzs;
+  const int txy = tile / g.ntzs;
   const int tx = txy % g.ntx, ty = txy / g.ntx;
-  const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
-  const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+  const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZS;
+  const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZS);
   const long long p0 = offsets[key0], p1 = offsets[key1];
   if (p0 == p1) return;  // empty tile: k_combine skips it
 
@@ -70,14 +70,15 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
   int* s_anc = reinterpret_cast<int*>(smem_raw + off);   // [3][kSChunk]
   int* s_pk = s_anc + 3 * kSChunk;                       // packed x | y<<8 | z<<16
   int* s_list = s_pk + kSChunk;                          // [4][kSChunk]
-  int* s_len = s_list + 4 * kSChunk;
+  int* s_lpk = s_list + 4 * kSChunk;                     // packed anchors, list order
+  int* s_len = s_lpk + 4 * kSChunk;
 
   // Warp w owns the 8x8 column block (wx0.., wy0..); lane owns (cx, cy) and
   // (cx, cy + 4).
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 8;
   const int cx = wx0 + (lane & 7), cy = wy0 + (lane >> 3);
-  real* outA = scratch + (size_t)tile * g.PZ * kPad * kPad + (size_t)cy * kPad + cx;
+  real* outA = scratch + (size_t)tile * g.PZS * kPad * kPad + (size_t)cy * kPad + cx;
   real* outB = outA + 4 * kPad;
   const size_t plane = (size_t)kPad * kPad;
 
@@ -132,7 +133,11 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
           hit = xl < wx0 + 8 && xl + P > wx0 && yl < wy0 + 8 && yl + P > wy0;
         }
         const unsigned bits = __ballot_sync(0xffffffffu, hit);
-        if (hit) s_list[warp * kSChunk + cnt + __popc(bits & ((1u << lane) - 1u))] = pl;
+        if (hit) {
+          const int at = warp * kSChunk + cnt + __popc(bits & ((1u << lane) - 1u));
+          s_list[at] = pl;
+          s_lpk[at] = s_pk[pl];
+        }
         cnt += __popc(bits);
       }
       if (lane == 0) s_len[warp] = cnt;
@@ -140,16 +145,35 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
     __syncthreads();
     const int cnt = s_len[warp];
     const int* list = s_list + warp * kSChunk;
+    const int* lpk = s_lpk + warp * kSChunk;
     const int ofx = cx + 8, ofy = cy + 8;
-    // Particles arrive in z-anchor order: slide the window once per anchor
-    // plane (outer loop) and run a pure-FMA inner loop over the particles
-    // sharing that plane (no register rotation inside the hot loop).
-    int t = 0;
-    while (t < cnt) {
-      int pl = list[t];
-      int pk = s_pk[pl];
-      const int zl = pk >> 16;
-      while (zc < zl) {  // slide: plane zc is final for these columns
+    // Particles arrive in z-anchor order.  The loop is software-pipelined
+    // with two register sets (A/B ping-pong, no copies): the shared-memory
+    // loads of particle t+1 are in flight while particle t's FMAs issue.
+    // The window slides (register rotation + plane store) only when the
+    // z anchor advances.
+    struct Ld {
+      real wx, wa, wb;
+      real wz[P];
+      int zl;
+    };
+    // loads only: nothing here consumes a pending shared-memory load, so the
+    // in-order warp goes on to the previous particle's FMAs while they land
+    auto load = [&](int tt, Ld& L) {
+      const int pl = list[tt];
+      const int pk = lpk[tt];
+      const real* rec = s_rec + (size_t)pl * Rec::kLen;
+      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff;
+      L.wx = rec[Rec::kX + ofx - xl];
+      L.wa = rec[Rec::kY + ofy - yl];
+      L.wb = rec[Rec::kY + ofy + 4 - yl];
+#pragma unroll
+      for (int s = 0; s < P; ++s) L.wz[s] = rec[Rec::kZ + s];
+      L.zl = (pk >> 16) - tz * g.TZS;
+    };
+    auto proc = [&](const Ld& L) {
+      const real a = L.wx * L.wa, b = L.wx * L.wb;
+      while (zc < L.zl) {  // slide: plane zc is final for these columns
         outA[(size_t)zc * plane] = winA[0];
         outB[(size_t)zc * plane] = winB[0];
 #pragma unroll
@@ -161,26 +185,25 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
         winB[P - 1] = real(0);
         ++zc;
       }
-      for (;;) {
-        const real* rec = s_rec + (size_t)pl * Rec::kLen;
-        const int xl = pk & 0xff, yl = (pk >> 8) & 0xff;
-        const real wx = rec[Rec::kX + ofx - xl];
-        const real a = wx * rec[Rec::kY + ofy - yl];
-        const real b = wx * rec[Rec::kY + ofy + 4 - yl];
 #pragma unroll
-        for (int s = 0; s < P; ++s) {
-          const real wz = rec[Rec::kZ + s];
-          winA[s] = fma(a, wz, winA[s]);
-          winB[s] = fma(b, wz, winB[s]);
-        }
-        if (++t >= cnt) break;
-        pl = list[t];
-        pk = s_pk[pl];
-        if ((pk >> 16) != zl) break;
+      for (int s = 0; s < P; ++s) {
+        winA[s] = fma(a, L.wz[s], winA[s]);
+        winB[s] = fma(b, L.wz[s], winB[s]);
       }
+    };
+    Ld LA, LB;
+    int t = 0;
+    if (cnt > 0) load(0, LA);
+    while (t < cnt) {
+      if (t + 1 < cnt) load(t + 1, LB);
+      proc(LA);
+      if (++t >= cnt) break;
+      if (t + 1 < cnt) load(t + 1, LA);
+      proc(LB);
+      ++t;
     }
   }
-  while (zc < g.PZ) {
+  while (zc < g.PZS) {
     outA[(size_t)zc * plane] = winA[0];
     outB[(size_t)zc * plane] = winB[0];
 #pragma unroll
@@ -215,11 +238,11 @@ __global__ void k_combine(Geom g, CombineTabs ct, const int* __restrict__ offset
         const int ex = ct.ent[0][x * kCombW + c];
         const int tx = ex & 0xffff, px = ex >> 16;
         const int txy = ty * g.ntx + tx;
-        const long long k0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
-        const long long k1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+        const long long k0 = (long long)txy * g.M[2] + (long long)tz * g.TZS;
+        const long long k1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZS);
         if (offsets[k0] == offsets[k1]) continue;
-        const long long tile = (long long)txy * g.ntz + tz;
-        acc += (double)scratch[((tile * g.PZ + pz) * kPad + py) * kPad + px];
+        const long long tile = (long long)txy * g.ntzs + tz;
+        acc += (double)scratch[((tile * g.PZS + pz) * kPad + py) * kPad + px];
       }
     }
   }
@@ -238,7 +261,7 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = smem;
   }
-  k_spread_tiles<real, P><<<(unsigned)p->n_tiles, kSpreadThreads, smem, s>>>(
+  k_spread_tiles<real, P><<<(unsigned)p->n_tiles_s, kSpreadThreads, smem, s>>>(
       g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
       reinterpret_cast<real*>(p->d_scratch));
   p->launches++;
