@@ -11,6 +11,7 @@
 namespace esp {
 
 size_t scan_temp_bytes(long long n_items);
+size_t sort_temp_bytes(long long cap, long long n_keys);
 
 static thread_local std::string g_last_error;
 
@@ -82,7 +83,8 @@ static void free_all(esp_plan* p) {
                   p->d_grid,    p->d_spec,     p->d_ikspec,  p->d_fields,  p->d_axis_k,
                   p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
                   p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt,
-                  p->d_wrec,     p->d_pk,       p->d_drec,    p->d_err_out7};
+                  p->d_wrec,     p->d_pk,       p->d_drec,    p->d_err_out7,
+                  p->d_sort_tmp};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_fwd) cufftDestroy(p->fwd);
@@ -236,6 +238,10 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(dalloc(&p->d_pk, cap));
   p->cub_bytes = esp::scan_temp_bytes(p->n_keys + 1);
   TRY(cudaMalloc(&p->d_cub, std::max<size_t>(p->cub_bytes, 16)));
+  if (p->cap >= esp::kSortThreshold) {
+    p->sort_bytes = esp::sort_temp_bytes(p->cap, p->n_keys);
+    TRY(cudaMalloc(&p->d_sort_tmp, std::max<size_t>(p->sort_bytes, 16)));
+  }
   TRY(cudaMalloc(&p->d_scratch,
                  real_sz * (size_t)p->n_tiles_s * p->PZS * esp::kPad * esp::kPad));
   TRY(cudaMalloc(&p->d_grid, real_sz * (size_t)p->G));

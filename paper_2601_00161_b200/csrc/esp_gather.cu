@@ -104,9 +104,11 @@ k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
   constexpr int kPlaneZ = GatherLayout<real, P>::kPlaneZ;
   constexpr int RS = rec_stride(P);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tile = blockIdx.x;
-  const int tz = tile % g.ntz;
-  const int txy = tile / g.ntz;
+  // z-slab-major tile order: CTAs running together cover one slab of tiles,
+  // whose halo planes (3 fields x PZ planes x the whole x-y plane) stay in L2
+  const int nxy = g.ntx * g.nty;
+  const int tz = blockIdx.x / nxy;
+  const int txy = blockIdx.x - tz * nxy;
   const int tx = txy % g.ntx, ty = txy / g.ntx;
   const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
   const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
@@ -271,9 +273,9 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
   constexpr int kPlaneZ = GatherLayout<real, P>::kPlaneZ;
   constexpr int RS = rec_stride(P);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tile = blockIdx.x;
-  const int tz = tile % g.ntz;
-  const int txy = tile / g.ntz;
+  const int nxy = g.ntx * g.nty;                    // z-slab-major (see k_gather_warp)
+  const int tz = blockIdx.x / nxy;
+  const int txy = blockIdx.x - tz * nxy;
   const int tx = txy % g.ntx, ty = txy / g.ntx;
   const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
   const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);

@@ -22,6 +22,7 @@ constexpr int kGChunk = 64;       // particles staged per CTA pass (gather)
 constexpr int kMaxCoef = 25;      // window table degree + 1 (reference: 19)
 constexpr int kMaxPieces = 64;    // window pieces (P * pieces-per-unit)
 constexpr int kRedThreads = 256;
+constexpr long long kSortThreshold = 500000;   // radix-sort binning above this N
 
 // Grid/tile geometry passed by value to every kernel.
 struct Geom {
@@ -243,6 +244,8 @@ struct esp_plan {
   int* d_pk;              // per binned particle: tile-local anchor x | y<<8 | z<<16
   void* d_cub;
   size_t cub_bytes;
+  void* d_sort_tmp;       // CUB radix-sort temp (large-N binning path)
+  size_t sort_bytes;
   void* d_scratch;
   void* d_grid;
   void* d_spec;
