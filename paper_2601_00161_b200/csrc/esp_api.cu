@@ -176,6 +176,10 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   // spread tiles share the x-y decomposition (and so the binning keys) but run
   // deeper in z on large grids: the scratch halo shrinks from (TZ+P-1)/TZ.
   p->TZS = std::min(d->M[2] <= 128 ? p->TZ : std::max(p->TZ, 32), d->M[2]);
+  if (const char* env = getenv("ESP_TILE_ZS")) {   // diagnostic override (tuning sweeps)
+    const int v = atoi(env);
+    if (v > 0) p->TZS = std::min(v, d->M[2]);
+  }
   p->PZS = p->TZS + d->P - 1;
   p->ntzs = (d->M[2] + p->TZS - 1) / p->TZS;
   p->n_tiles_s = (long long)p->ntx * p->nty * p->ntzs;

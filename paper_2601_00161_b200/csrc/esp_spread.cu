@@ -62,7 +62,11 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
   const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZS;
   const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZS);
   const long long p0 = offsets[key0], p1 = offsets[key1];
-  if (p0 == p1) return;  // empty tile: k_combine skips it
+  if (p0 == p1) {  // empty tile: a zero block keeps k_combine branch-free
+    real* blk = scratch + (size_t)tile * g.PZS * kPad * kPad;
+    for (int i = threadIdx.x; i < g.PZS * kPad * kPad; i += blockDim.x) blk[i] = real(0);
+    return;
+  }
 
   size_t off = 0;
   real* s_rec = reinterpret_cast<real*>(smem_raw + off);
@@ -218,8 +222,8 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
 }
 
 template <typename real>
-__global__ void k_combine(Geom g, CombineTabs ct, const int* __restrict__ offsets,
-                          const real* __restrict__ scratch, real* __restrict__ grid) {
+__global__ void __launch_bounds__(256)
+k_combine(Geom g, CombineTabs ct, const real* __restrict__ scratch, real* __restrict__ grid) {
   const long long G = (long long)g.M[0] * g.M[1] * g.M[2];
   const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (gid >= G) return;
@@ -228,21 +232,46 @@ __global__ void k_combine(Geom g, CombineTabs ct, const int* __restrict__ offset
   const int z = (int)(gid / ((long long)g.M[0] * g.M[1]));
   const int nx = ct.cnt[0][x], ny = ct.cnt[1][y], nz = ct.cnt[2][z];
   double acc = 0.0;
-  for (int a = 0; a < nz; ++a) {
-    const int ez = ct.ent[2][z * kCombW + a];
-    const int tz = ez & 0xffff, pz = ez >> 16;
-    for (int b = 0; b < ny; ++b) {
-      const int ey = ct.ent[1][y * kCombW + b];
-      const int ty = ey & 0xffff, py = ey >> 16;
-      for (int c = 0; c < nx; ++c) {
-        const int ex = ct.ent[0][x * kCombW + c];
-        const int tx = ex & 0xffff, px = ex >> 16;
-        const int txy = ty * g.ntx + tx;
-        const long long k0 = (long long)txy * g.M[2] + (long long)tz * g.TZS;
-        const long long k1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZS);
-        if (offsets[k0] == offsets[k1]) continue;
-        const long long tile = (long long)txy * g.ntzs + tz;
-        acc += (double)scratch[((tile * g.PZS + pz) * kPad + py) * kPad + px];
+  if (nx <= 2 && ny <= 2 && nz <= 2) {
+    // common case (each axis covered by <= 2 tiles): issue all <= 8 loads
+    // before summing, in the same fixed (z, y, x) order
+    long long addr[8];
+    bool use[8];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int ez = ct.ent[2][z * kCombW + (a < nz ? a : 0)];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int ey = ct.ent[1][y * kCombW + (b < ny ? b : 0)];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int ex = ct.ent[0][x * kCombW + (c < nx ? c : 0)];
+          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
+                                 (ez & 0xffff);
+          const int i = (a * 2 + b) * 2 + c;
+          addr[i] = ((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad + (ex >> 16);
+          use[i] = a < nz && b < ny && c < nx;
+        }
+      }
+    }
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = use[i] ? (double)scratch[addr[i]] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (use[i]) acc += v[i];
+  } else {
+    for (int a = 0; a < nz; ++a) {
+      const int ez = ct.ent[2][z * kCombW + a];
+      for (int b = 0; b < ny; ++b) {
+        const int ey = ct.ent[1][y * kCombW + b];
+        for (int c = 0; c < nx; ++c) {
+          const int ex = ct.ent[0][x * kCombW + c];
+          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
+                                 (ez & 0xffff);
+          acc += (double)scratch[((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad +
+                                 (ex >> 16)];
+        }
       }
     }
   }
@@ -273,8 +302,7 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
   }
   const int B = 256;
   k_combine<real><<<(unsigned)((p->G + B - 1) / B), B, 0, s>>>(
-      g, ct, p->d_offsets, reinterpret_cast<const real*>(p->d_scratch),
-      reinterpret_cast<real*>(p->d_grid));
+      g, ct, reinterpret_cast<const real*>(p->d_scratch), reinterpret_cast<real*>(p->d_grid));
   p->launches++;
   prof_mark(p, s, "combine");
   return cudaGetLastError();
