@@ -153,6 +153,15 @@ template <typename real> __device__ __forceinline__ const real* fast_coef(const 
 template <> __device__ __forceinline__ const double* fast_coef<double>(const FastTab& t) { return t.c; }
 template <> __device__ __forceinline__ const float* fast_coef<float>(const FastTab& t) { return t.cf; }
 
+// Out-of-line general table evaluation: only reached on exact piece-boundary
+// ties, so it must not bloat the unrolled fast path (I-cache).
+template <typename real>
+__device__ __noinline__ real window_eval_slow(const real* __restrict__ coef,
+                                              const double* __restrict__ breaks,
+                                              int n_pieces, int ncoef, double t) {
+  return window_eval<real>(coef, breaks, n_pieces, ncoef, t);
+}
+
 // w[s] = qf * W(u - (base + lo + s)), s = 0..P-1.
 template <typename real, int P>
 __device__ __forceinline__ void stencil_weights(const FastTab& ft, const real* s_tab,
@@ -174,7 +183,7 @@ __device__ __forceinline__ void stencil_weights(const FastTab& ft, const real* s
         for (int m = 1; m < kFastNC; ++m) acc = fma(acc, x, C[j * kFastNC + m]);
         v = acc;
       } else {
-        v = window_eval<real>(s_tab, s_brk, n_pieces, ncoef, t);
+        v = window_eval_slow<real>(s_tab, s_brk, n_pieces, ncoef, t);
       }
       w[s] = v * qf;
     }
