@@ -18,35 +18,37 @@
 
 namespace esp {
 
-// Window weights and tile-local anchors of one binned particle, written once
-// per step and read by both the spread and the gather kernels.
+// One dimension of a particle's record (three threads per particle: the
+// binning kernels run 96-thread blocks = 32 particles x 3 dimensions, so each
+// thread carries one copy of the 8 unrolled Horner chains).  The packed
+// anchor is written bytewise: x -> byte 0, y -> byte 1, z -> bytes 2-3.
 template <typename real, int P>
-__device__ __forceinline__ void write_record(const Geom& g, const FastTab& ft,
-                                             const real* __restrict__ tab,
-                                             const double* __restrict__ brk,
-                                             int n_pieces, int ncoef, int key,
-                                             const double u[3], long long dst,
-                                             real* __restrict__ wrec,
-                                             int* __restrict__ pk) {
-  const int az = key % g.M[2];
-  const int txy = key / g.M[2];
-  // x, y relative to the tile; z absolute (spread and gather tiles differ in z)
-  const int org[3] = {(txy % g.ntx) * g.TX, (txy / g.ntx) * g.TY, 0};
+__device__ __forceinline__ void write_record_dim(const Geom& g, const FastTab& ft,
+                                                 const real* __restrict__ tab,
+                                                 const double* __restrict__ brk,
+                                                 int n_pieces, int ncoef, int key, int d,
+                                                 double u, long long dst,
+                                                 real* __restrict__ wrec,
+                                                 int* __restrict__ pk) {
   constexpr int RS = rec_stride(P);
-  real* out = wrec + dst * (3 * RS);
-  int packed = 0;
+  const double base = anchor_base(g, u);
+  real w[P];
+  stencil_weights<real, P>(ft, tab, brk, n_pieces, ncoef, u, base, g.lo, real(1), w);
+  real* out = wrec + dst * (3 * RS) + d * RS;
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double base = anchor_base(g, u[d]);
-    const int a = local_anchor(g, d, base);
-    packed |= (a - org[d]) << (8 * d);
-    real w[P];
-    stencil_weights<real, P>(ft, tab, brk, n_pieces, ncoef, u[d], base, g.lo, real(1), w);
-#pragma unroll
-    for (int s = 0; s < RS; ++s) out[d * RS + s] = s < P ? w[s < P ? s : 0] : real(0);
+  for (int s = 0; s < RS; ++s) out[s] = s < P ? w[s < P ? s : 0] : real(0);
+  const int a = local_anchor(g, d, base);
+  unsigned char* pb = reinterpret_cast<unsigned char*>(pk + dst);
+  if (d == 2) {
+    *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
+  } else {
+    const int txy = key / g.M[2];
+    const int org = d == 0 ? (txy % g.ntx) * g.TX : (txy / g.ntx) * g.TY;
+    pb[d] = (unsigned char)(a - org);
   }
-  pk[dst] = packed;
 }
+
+constexpr int kBinPerBlock = 32;   // particles per 96-thread binning block
 
 __global__ void k_bin_count(const double* __restrict__ pos, long long n, Geom g,
                             int* __restrict__ key, int* __restrict__ slot,
@@ -95,25 +97,25 @@ __global__ void k_bin_keys(const double* __restrict__ pos, long long n, Geom g,
 // After the stable radix sort: gather each particle into its binned slot and
 // write its weight record.  Reads are random, writes coalesced.
 template <typename real, int P>
-__global__ void k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab,
-                             const double* __restrict__ brk, int n_pieces, int ncoef,
-                             long long n, long long cap, const int* __restrict__ skey,
-                             const int* __restrict__ sval, const double* __restrict__ pos,
-                             const double* __restrict__ q, double* __restrict__ u_out,
-                             double* __restrict__ q_out, int* __restrict__ idx_out,
-                             real* __restrict__ wrec, int* __restrict__ pk) {
-  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(3 * kBinPerBlock)
+k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __restrict__ brk,
+             int n_pieces, int ncoef, long long n, long long cap,
+             const int* __restrict__ skey, const int* __restrict__ sval,
+             const double* __restrict__ pos, const double* __restrict__ q,
+             double* __restrict__ u_out, double* __restrict__ q_out,
+             int* __restrict__ idx_out, real* __restrict__ wrec, int* __restrict__ pk) {
+  const int d = threadIdx.x / kBinPerBlock;
+  const long long j = (long long)blockIdx.x * kBinPerBlock + (threadIdx.x % kBinPerBlock);
   if (j >= n) return;
   const int i = sval[j];
-  double u[3];
-  grid_coords(g, pos[3 * (long long)i + 0], pos[3 * (long long)i + 1],
-              pos[3 * (long long)i + 2], u);
-  u_out[j] = u[0];
-  u_out[cap + j] = u[1];
-  u_out[2 * cap + j] = u[2];
-  q_out[j] = q[i];
-  idx_out[j] = i;
-  write_record<real, P>(g, ft, tab, brk, n_pieces, ncoef, skey[j], u, j, wrec, pk);
+  const long long i3 = 3 * (long long)i;
+  const double u = grid_coord(g, d, pos[i3], pos[i3 + 1], pos[i3 + 2]);
+  u_out[d * cap + j] = u;
+  if (d == 0) {
+    q_out[j] = q[i];
+    idx_out[j] = i;
+  }
+  write_record_dim<real, P>(g, ft, tab, brk, n_pieces, ncoef, skey[j], d, u, j, wrec, pk);
 }
 
 // Scatter to key segments.  Writes grid coordinates u (SoA), charge and the
@@ -141,50 +143,53 @@ __global__ void k_bin_scatter(const double* __restrict__ pos,
 }
 
 // Deterministic order inside each key segment: rank by original index; then
-// the particle's weight record at its final position.
+// the particle's record at its final position (3 threads per particle).
 template <typename real, int P>
-__global__ void k_bin_canon(Geom g, FastTab ft, const real* __restrict__ tab,
-                            const double* __restrict__ brk, int n_pieces, int ncoef,
-                            long long n, long long cap,
-                            const int* __restrict__ key_tmp,
-                            const int* __restrict__ offsets,
-                            const double* __restrict__ u_tmp,
-                            const double* __restrict__ q_tmp,
-                            const int* __restrict__ idx_tmp,
-                            double* __restrict__ u_out, double* __restrict__ q_out,
-                            int* __restrict__ idx_out, real* __restrict__ wrec,
-                            int* __restrict__ pk) {
-  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(3 * kBinPerBlock)
+k_bin_canon(Geom g, FastTab ft, const real* __restrict__ tab, const double* __restrict__ brk,
+            int n_pieces, int ncoef, long long n, long long cap,
+            const int* __restrict__ key_tmp, const int* __restrict__ offsets,
+            const double* __restrict__ u_tmp, const double* __restrict__ q_tmp,
+            const int* __restrict__ idx_tmp, double* __restrict__ u_out,
+            double* __restrict__ q_out, int* __restrict__ idx_out, real* __restrict__ wrec,
+            int* __restrict__ pk) {
+  __shared__ long long s_dst[kBinPerBlock];
+  const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
+  const long long j = (long long)blockIdx.x * kBinPerBlock + l;
+  if (d == 0 && j < n) {
+    const int k = key_tmp[j];
+    const int s0 = offsets[k], s1 = offsets[k + 1];
+    const int me = idx_tmp[j];
+    int rank = 0;
+    for (int t = s0; t < s1; ++t) rank += (idx_tmp[t] < me);
+    const long long dst = (long long)s0 + rank;
+    s_dst[l] = dst;
+    q_out[dst] = q_tmp[j];
+    idx_out[dst] = me;
+  }
+  __syncthreads();
   if (j >= n) return;
-  const int k = key_tmp[j];
-  const int s0 = offsets[k], s1 = offsets[k + 1];
-  const int me = idx_tmp[j];
-  int rank = 0;
-  for (int t = s0; t < s1; ++t) rank += (idx_tmp[t] < me);
-  const long long dst = (long long)s0 + rank;
-  const double u[3] = {u_tmp[j], u_tmp[cap + j], u_tmp[2 * cap + j]};
-  u_out[dst] = u[0];
-  u_out[cap + dst] = u[1];
-  u_out[2 * cap + dst] = u[2];
-  q_out[dst] = q_tmp[j];
-  idx_out[dst] = me;
-  write_record<real, P>(g, ft, tab, brk, n_pieces, ncoef, k, u, dst, wrec, pk);
+  const long long dst = s_dst[l];
+  const double u = u_tmp[d * cap + j];
+  u_out[d * cap + dst] = u;
+  write_record_dim<real, P>(g, ft, tab, brk, n_pieces, ncoef, key_tmp[j], d, u, dst, wrec, pk);
 }
 
 // Non-deterministic mode: records straight after the atomic-slot scatter.
 template <typename real, int P>
-__global__ void k_bin_records(Geom g, FastTab ft, const real* __restrict__ tab,
-                              const double* __restrict__ brk, int n_pieces, int ncoef,
-                              long long n, long long cap, const int* __restrict__ key,
-                              const int* __restrict__ slot, const int* __restrict__ offsets,
-                              const double* __restrict__ u_in, real* __restrict__ wrec,
-                              int* __restrict__ pk) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(3 * kBinPerBlock)
+k_bin_records(Geom g, FastTab ft, const real* __restrict__ tab, const double* __restrict__ brk,
+              int n_pieces, int ncoef, long long n, long long cap,
+              const int* __restrict__ key, const int* __restrict__ slot,
+              const int* __restrict__ offsets, const double* __restrict__ u_in,
+              real* __restrict__ wrec, int* __restrict__ pk) {
+  const int d = threadIdx.x / kBinPerBlock;
+  const long long i = (long long)blockIdx.x * kBinPerBlock + (threadIdx.x % kBinPerBlock);
   if (i >= n) return;
   const int k = key[i];
   const long long dst = (long long)offsets[k] + slot[i];
-  const double u[3] = {u_in[dst], u_in[cap + dst], u_in[2 * cap + dst]};
-  write_record<real, P>(g, ft, tab, brk, n_pieces, ncoef, k, u, dst, wrec, pk);
+  write_record_dim<real, P>(g, ft, tab, brk, n_pieces, ncoef, k, d, u_in[d * cap + dst], dst,
+                            wrec, pk);
 }
 
 template <typename real, int P>
@@ -194,13 +199,14 @@ static void launch_tail(esp_plan* p, const Geom& g, long long n, unsigned grid, 
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
   real* wrec = reinterpret_cast<real*>(p->d_wrec);
+  const unsigned g3 = (unsigned)((n + kBinPerBlock - 1) / kBinPerBlock);
   if (p->deterministic) {
-    k_bin_canon<real, P><<<grid, B, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
+    k_bin_canon<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
                                            p->ncoef, n, p->cap, p->d_bkey, p->d_offsets,
                                            p->d_u_tmp, p->d_q_tmp, p->d_idx_tmp, p->d_u,
                                            p->d_q, p->d_idx, wrec, p->d_pk);
   } else {
-    k_bin_records<real, P><<<grid, B, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
+    k_bin_records<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
                                              p->ncoef, n, p->cap, p->d_key, p->d_slot,
                                              p->d_offsets, p->d_u, wrec, p->d_pk);
   }
@@ -232,7 +238,8 @@ static void launch_sorted(esp_plan* p, const Geom& g, const double* d_pos, const
   const real* tab = std::is_same<real, double>::value
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
-  k_bin_sorted<real, P><<<grid, B, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
+  const unsigned g3 = (unsigned)((n + kBinPerBlock - 1) / kBinPerBlock);
+  k_bin_sorted<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
                                           p->ncoef, n, p->cap, p->d_bkey, p->d_idx_tmp, d_pos,
                                           d_q, p->d_u, p->d_q, p->d_idx,
                                           reinterpret_cast<real*>(p->d_wrec), p->d_pk);

@@ -67,6 +67,16 @@ __device__ __forceinline__ void grid_coords(const Geom& g, double x, double y,
   }
 }
 
+// One component u_d of grid_coords (same operations, same order).
+__device__ __forceinline__ double grid_coord(const Geom& g, int d, double x, double y,
+                                             double z) {
+  if (g.ortho) return __ddiv_rn(d == 0 ? x : (d == 1 ? y : z), g.spacing[d]);
+  const double s = __dadd_rn(__dadd_rn(__dmul_rn(g.hinv[3 * d + 0], x),
+                                       __dmul_rn(g.hinv[3 * d + 1], y)),
+                             __dmul_rn(g.hinv[3 * d + 2], z));
+  return __dmul_rn(s, (double)g.Mu[d]);
+}
+
 // Stencil anchor: np.round (half-to-even) for odd P, np.floor for even P
 // (mesh.py:161-168).
 __device__ __forceinline__ double anchor_base(const Geom& g, double u) {
