@@ -92,6 +92,11 @@ static void free_all(esp_plan* p) {
   if (p->have_inv1) cufftDestroy(p->inv1);
   if (p->profiling)
     for (int i = 0; i < 48; ++i) cudaEventDestroy(p->ev[i]);
+  if (p->have_side) {
+    cudaEventDestroy(p->ev_fork);
+    cudaEventDestroy(p->ev_join);
+    cudaStreamDestroy(p->side);
+  }
   delete p->h_fast;
   p->h_fast = nullptr;
 }
@@ -254,6 +259,11 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(cudaMalloc(&p->d_ikspec, 3 * 2 * real_sz * (size_t)p->H));
   TRY(cudaMalloc(&p->d_fields, 3 * real_sz * (size_t)p->G));
   TRY(dalloc(&p->d_err, 4));
+  TRY(cudaMemset(p->d_err, 0, 4 * sizeof(int)));
+  TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+  TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  p->have_side = 1;
   TRY(dalloc(&p->d_err_out7, 8));
   // fast window table (kernel parameter) and deterministic-combine tables
   p->h_fast = new esp::FastTab;
@@ -596,11 +606,26 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
   const int analytic = (flags & ESP_FORCES_ANALYTIC) != 0;
   p->launches = 0;
   p->n_ev = 0;
-  esp::prof_mark(p, (cudaStream_t)stream, "start");
+  cudaStream_t s0 = (cudaStream_t)stream;
+  esp::prof_mark(p, s0, "start");
+  const int ikmode = want_f ? (analytic ? 2 : 1) : 0;
+  if (ikmode && !p->profiling) {
+    // zero the force spectra on a side stream while binning/spreading run
+    ESP_CUDA(cudaEventRecord(p->ev_fork, s0));
+    ESP_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    const size_t cbytes = p->precision == ESP_FP64 ? sizeof(double2) : sizeof(float2);
+    ESP_CUDA(cudaMemsetAsync(p->d_ikspec, 0, (ikmode == 2 ? 1 : 3) * (size_t)p->H * cbytes,
+                             p->side));
+    ESP_CUDA(cudaEventRecord(p->ev_join, p->side));
+  }
   rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
   if (rc) return rc;
   rc = esp_forward(p, nullptr, stream);
   if (rc) return rc;
+  if (ikmode && !p->profiling) {
+    ESP_CUDA(cudaStreamWaitEvent(s0, p->ev_join, 0));
+    p->ik_zeroed = 1;
+  }
   rc = esp_scale_reduce(p, d_out7, want_f && !analytic, stream);
   if (rc) return rc;
   if (want_f) rc = analytic ? esp_forces_analytic(p, d_forces, stream)

@@ -288,6 +288,10 @@ struct esp_plan {
   long long fwd_count, inv_count;
   long long last_n;
   int have_bins, have_spec, have_ik;
+  int ik_zeroed;          // ik spectra already zeroed on the side stream
+  cudaStream_t side;      // fork/join stream (captured as a parallel graph branch)
+  cudaEvent_t ev_fork, ev_join;
+  int have_side;
   int launches;
   // profiling: events recorded after each stage kernel when enabled
   int profiling;

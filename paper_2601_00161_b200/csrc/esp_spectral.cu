@@ -106,7 +106,8 @@ k_scale_reduce(ModeArgs a, const typename Cplx<real>::type* __restrict__ spec,
                const double* __restrict__ modeA, const double* __restrict__ modeB,
                double ik_scale, double lp_scale, int write_ik,
                typename Cplx<real>::type* __restrict__ ik,
-               long long H, double* __restrict__ partials) {
+               long long H, double* __restrict__ partials, int* __restrict__ done,
+               double escale, double pscale, double* __restrict__ out7) {
   using C = typename Cplx<real>::type;
   double acc[7];
 #pragma unroll
@@ -166,25 +167,33 @@ k_scale_reduce(ModeArgs a, const typename Cplx<real>::type* __restrict__ spec,
     }
   }
   block_reduce_store<7>(acc, partials + (size_t)blockIdx.x * 8);
-}
-
-__global__ void k_final_reduce(const double* __restrict__ partials, int nblocks,
-                               double escale, double pscale, double* __restrict__ out7) {
+  // Last block to finish sums the per-block partials in a fixed order (same
+  // tree as a separate final kernel would use): deterministic, one launch.
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
   double v[7];
 #pragma unroll
   for (int i = 0; i < 7; ++i) v[i] = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
 #pragma unroll
-    for (int i = 0; i < 7; ++i) v[i] += partials[(size_t)b * 8 + i];
+    for (int i = 0; i < 7; ++i) v[i] += __ldcg(partials + (size_t)b * 8 + i);
   }
   __shared__ double res[8];
+  __syncthreads();   // block_reduce_store's scratch is reused
   block_reduce_store<7>(v, res);
   __syncthreads();
   if (threadIdx.x == 0) {
     out7[0] = res[0] * escale;
     for (int i = 1; i < 7; ++i) out7[i] = res[i] * pscale;
+    *done = 0;       // re-arm for the next launch (graph replays)
   }
 }
+
 
 static ModeArgs mode_args(const esp_plan* p) {
   ModeArgs a;
@@ -225,31 +234,30 @@ cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
   const double lp_scale = p->h3 / (2.0 * p->volume * G);
   cudaError_t e;
   const size_t cbytes = p->precision == ESP_FP64 ? sizeof(double2) : sizeof(float2);
-  if (write_ik) {
+  if (write_ik && !p->ik_zeroed) {
     const size_t nspec = write_ik == 2 ? 1 : 3;
     e = cudaMemsetAsync(p->d_ikspec, 0, nspec * (size_t)p->H * cbytes, s);
     if (e != cudaSuccess) return e;
     prof_mark(p, s, "ik_memset");
   }
+  if (write_ik) p->ik_zeroed = 0;
+  const double h3sq = p->h3 * p->h3;
+  const double escale = h3sq / (2.0 * p->volume);
+  const double pscale = h3sq / (2.0 * p->volume * p->volume);
+  int* done = p->d_err + 1;
   if (p->precision == ESP_FP64) {
     k_scale_reduce<double><<<p->n_red_blocks, kRedThreads, 0, s>>>(
         a, reinterpret_cast<const double2*>(p->d_spec), p->d_modeA, p->d_modeB,
         p->h3 / G, lp_scale, write_ik, reinterpret_cast<double2*>(p->d_ikspec), p->H,
-        p->d_partials);
+        p->d_partials, done, escale, pscale, d_out7);
   } else {
     k_scale_reduce<float><<<p->n_red_blocks, kRedThreads, 0, s>>>(
         a, reinterpret_cast<const float2*>(p->d_spec), p->d_modeA, p->d_modeB,
         p->h3 / G, lp_scale, write_ik, reinterpret_cast<float2*>(p->d_ikspec), p->H,
-        p->d_partials);
+        p->d_partials, done, escale, pscale, d_out7);
   }
   p->launches++;
   prof_mark(p, s, "scale_reduce");
-  const double h3sq = p->h3 * p->h3;
-  k_final_reduce<<<1, kRedThreads, 0, s>>>(p->d_partials, p->n_red_blocks,
-                                           h3sq / (2.0 * p->volume),
-                                           h3sq / (2.0 * p->volume * p->volume), d_out7);
-  p->launches++;
-  prof_mark(p, s, "final_reduce");
   return cudaGetLastError();
 }
 
