@@ -247,7 +247,9 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(dalloc(&p->d_pk, cap));
   p->cub_bytes = esp::scan_temp_bytes(p->n_keys + 1);
   TRY(cudaMalloc(&p->d_cub, std::max<size_t>(p->cub_bytes, 16)));
-  if (p->cap >= esp::kSortThreshold) {
+  p->sort_threshold = esp::kSortThreshold;
+  if (const char* env = getenv("ESP_SORT_THRESHOLD")) p->sort_threshold = atoll(env);
+  if (p->cap >= p->sort_threshold) {
     p->sort_bytes = esp::sort_temp_bytes(p->cap, p->n_keys);
     TRY(cudaMalloc(&p->d_sort_tmp, std::max<size_t>(p->sort_bytes, 16)));
   }

@@ -287,7 +287,7 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
   if (e != cudaSuccess) return e;
   const int B = 256;
   const unsigned grid = (unsigned)((n + B - 1) / B);
-  if (n >= kSortThreshold && p->d_sort_tmp) {
+  if (n >= p->sort_threshold && p->d_sort_tmp) {
     // stable LSD radix sort of (key, index): deterministic intra-key order
     k_bin_keys<<<grid, B, 0, s>>>(d_pos, n, g, p->d_key, p->d_slot, p->d_counts);
     p->launches++;

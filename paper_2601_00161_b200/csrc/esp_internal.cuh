@@ -265,6 +265,7 @@ struct esp_plan {
   size_t cub_bytes;
   void* d_sort_tmp;       // CUB radix-sort temp (large-N binning path)
   size_t sort_bytes;
+  long long sort_threshold;
   void* d_scratch;
   void* d_grid;
   void* d_spec;

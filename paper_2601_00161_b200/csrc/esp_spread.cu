@@ -36,11 +36,12 @@ struct SpreadRec {
   static constexpr int kLen = ((2 * RL + P) + 1) & ~1;   // keep 16B alignment
 };
 
-constexpr int kSChunk = 128;   // particles staged per spread pass
+// Particles staged per spread pass: 128 on small grids (few, dense tiles),
+// 64 on large grids (halves the CTA's shared memory: more CTAs per SM).
 
 template <typename real, int P>
 struct SpreadLayout {
-  static size_t bytes() {
+  static size_t bytes(int kSChunk) {
     size_t b = sizeof(real) * (size_t)kSChunk * SpreadRec<P>::kLen;
     b += sizeof(int) * (size_t)kSChunk * (3 + 1 + 8);   // anchors, packed, 4 warp lists x2
     b += sizeof(int) * 8;                               // list lengths
@@ -52,7 +53,7 @@ template <typename real, int P>
 __global__ void __launch_bounds__(kSpreadThreads)
 k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__ wrec,
                const int* __restrict__ PK, const double* __restrict__ Q,
-               real* __restrict__ scratch) {
+               real* __restrict__ scratch, int kSChunk) {
   using Rec = SpreadRec<P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tile = blockIdx.x;
@@ -281,7 +282,8 @@ k_combine(Geom g, CombineTabs ct, const real* __restrict__ scratch, real* __rest
 template <typename real, int P>
 static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
   Geom g = make_geom(p);
-  const size_t smem = SpreadLayout<real, P>::bytes();
+  const int chunk = p->M[2] <= 128 ? 128 : 64;
+  const size_t smem = SpreadLayout<real, P>::bytes(chunk);
   static size_t attr_set = 0;  // set once per instantiation (capture-safe)
   if (smem > attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_spread_tiles<real, P>,
@@ -292,7 +294,7 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
   }
   k_spread_tiles<real, P><<<(unsigned)p->n_tiles_s, kSpreadThreads, smem, s>>>(
       g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
-      reinterpret_cast<real*>(p->d_scratch));
+      reinterpret_cast<real*>(p->d_scratch), chunk);
   p->launches++;
   prof_mark(p, s, "spread");
   CombineTabs ct;
