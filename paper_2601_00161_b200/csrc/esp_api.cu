@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -84,9 +85,11 @@ static void free_all(esp_plan* p) {
                   p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
                   p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt,
                   p->d_wrec,     p->d_pk,       p->d_drec,    p->d_err_out7,
-                  p->d_sort_tmp};
+                  p->d_sort_tmp, p->d_partials_fft};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  esp_fused_fft_destroy(p->fused);
+  p->fused = nullptr;
   if (p->have_fwd) cufftDestroy(p->fwd);
   if (p->have_inv3) cufftDestroy(p->inv3);
   if (p->have_inv1) cufftDestroy(p->inv1);
@@ -403,6 +406,26 @@ int esp_plan_set_cell(esp_plan* p, const esp_cell_desc* c, void* stream) {
   p->n_red_blocks = (int)std::max<long long>(
       1, std::min<long long>((p->nbox + esp::kRedThreads - 1) / esp::kRedThreads, 148 * 4));
   ESP_CUDA(dalloc(&p->d_partials, (size_t)p->n_red_blocks * 8));
+  // band-pruned fused transforms for esp_evaluate (full-grid plans whose
+  // lengths factor into 2s and 3s; ESP_FFT=cufft keeps the cuFFT path)
+  esp_fused_fft_destroy(p->fused);
+  p->fused = nullptr;
+  if (p->d_partials_fft) cudaFree(p->d_partials_fft);
+  p->d_partials_fft = nullptr;
+  {
+    const char* env = std::getenv("ESP_FFT");
+    const bool want = !(env && std::string(env) == "cufft");
+    if (want && p->Mu[2] == p->M[2] && p->zshift == 0) {
+      p->fused = esp_fused_fft_create(p);
+      if (p->fused) {
+        p->n_red_blocks_fft = esp::fused_reduce_blocks(p);
+        const long long nb = p->n_red_blocks_fft, ng = (nb + 31) / 32;
+        const size_t nd = (size_t)(nb + ng) * 8 + (size_t)(ng + 2) / 2 + 1;
+        ESP_CUDA(dalloc(&p->d_partials_fft, nd));
+        ESP_CUDA(cudaMemset(p->d_partials_fft, 0, nd * sizeof(double)));
+      }
+    }
+  }
   std::vector<double> hk(3 * msum), hw(msum);
   for (int a = 0; a < 3; ++a)
     for (int d = 0; d < 3; ++d)
@@ -611,6 +634,21 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
   cudaStream_t s0 = (cudaStream_t)stream;
   esp::prof_mark(p, s0, "start");
   const int ikmode = want_f ? (analytic ? 2 : 1) : 0;
+  if (p->fused && !analytic) {
+    // spread -> fused band-pruned transforms (+ scale/reduce, ik spectra and
+    // inverse transforms) -> gather
+    rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
+    if (rc) return rc;
+    ESP_CUDA(esp::launch_fused_fft(p, want_f, d_out7, s0));
+    p->fwd_count++;
+    p->have_spec = 1;   // in-band box of d_spec is current
+    p->have_ik = 0;
+    if (want_f) {
+      p->inv_count += 3;
+      if (p->last_n > 0) ESP_CUDA(esp::launch_gather_ik(p, d_forces, s0));
+    }
+    return ESP_OK;
+  }
   if (ikmode && !p->profiling) {
     // zero the force spectra on a side stream while binning/spreading run
     ESP_CUDA(cudaEventRecord(p->ev_fork, s0));

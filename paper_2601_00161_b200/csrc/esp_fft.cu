@@ -1,0 +1,1039 @@
+// esp_fft.cu — band-pruned, fused 3D transforms for the k-space step.
+//
+// The far field only ever uses modes inside the box |m_d| <= band_d (the
+// mask |k| <= kmax lies inside it, mesh.py:248-249).  The forward transform
+// therefore keeps only in-band outputs after each 1D stage, and its last
+// stage (along z) is fused with the deconvolution scaling + energy/pressure
+// reduction (mesh.py:285-312), the ik spectra (mesh.py:333-341) and the
+// first inverse stage:
+//
+//   P1  x rows:  real -> complex (two rows per complex FFT), keep kx <= band
+//   P2  y lines: C2C, keep |ky| <= band
+//   P3a z lines: C2C; reduce E, P_ab over the retained modes; write the box
+//                spectrum
+//   P3b z lines: build i k_d A X h3/G on the box, inverse C2C along z
+//   P4  y lines: inverse C2C of the three ik pencils, zero-padded in ky
+//   P5  x rows:  complex -> real (two rows per complex FFT), zero-padded in kx
+//
+// The pressure-only path is P1-P3a: one forward transform whose last pass is
+// the fused scaling/reduction.  Intermediate arrays keep kx in a column pitch
+// `ldx` rounded up to 8 so that every 8 (fp64) / 16 (fp32) consecutive lines
+// a CTA reads form full 128-byte segments.
+//
+// Line transforms: compile-time length N, mixed-radix (8, 6, 4, 3, 2)
+// Stockham auto-sort stages executed in place in shared memory through
+// registers (load R inputs -> barrier -> twiddle, DFT, store).  Shared rows
+// use pitch N + N/8 + 1 and index i + i/8 so that strided butterflies and
+// the line-transposing loads are bank-conflict free; per-stage twiddle
+// tables are laid out [t-1][k] so a warp reads consecutive entries.
+// Grids whose lengths are not in ESP_FFT_SIZES use the cuFFT path.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "esp_internal.cuh"
+
+#define ESP_FFT_SIZES(X) X(32) X(48) X(64) X(96) X(128) X(192) X(256) X(384)
+
+namespace esp {
+namespace fft {
+
+template <typename real> struct Cx;
+template <> struct Cx<double> { using t = double2; };
+template <> struct Cx<float> { using t = float2; };
+
+__host__ __device__ constexpr int pick_radix(int n) {
+  return n % 8 == 0 ? 8 : n % 6 == 0 ? 6 : n % 4 == 0 ? 4 : n % 3 == 0 ? 3 : 2;
+}
+// twiddle entries needed by the stages that start at span Ns
+__host__ __device__ constexpr int tw_from(int N, int Ns) {
+  return Ns >= N ? 0
+                 : (Ns > 1 ? (pick_radix(N / Ns) - 1) * Ns : 0) +
+                       tw_from(N, Ns * pick_radix(N / Ns));
+}
+__host__ __device__ constexpr int tw_total(int N) { return tw_from(N, 1); }
+__host__ __device__ constexpr int tw_offset(int N, int Ns) { return tw_total(N) - tw_from(N, Ns); }
+__host__ __device__ constexpr int pitch(int N) { return N + N / 8 + 1; }
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 3); }
+
+__host__ __device__ constexpr int pow2_floor(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+// CTA shapes.  x rows: kThreadsX threads transform pairs_x(N) row pairs.
+// y/z lines: lines_yz consecutive kx columns (one 128-byte segment per row)
+// with threads_yz(N) threads, so that small grids still launch several CTAs
+// per SM.
+constexpr int kThreadsX = 128;
+// x rows: ~1024 elements per CTA on large grids; small grids (L2-resident)
+// take fewer rows per CTA so that every SM gets work.
+__host__ __device__ constexpr int pairs_x(int N) {
+  return N >= 128 ? (N >= 1024 ? 1 : 1024 / N) : 256 / N;
+}
+// y/z lines: one 128-byte segment of consecutive kx per row on large grids;
+// 2 lines on small grids.
+template <typename real>
+__host__ __device__ constexpr int lines_yz(int N) {
+  return N > 128 ? 128 / (2 * (int)sizeof(real)) : 2;
+}
+template <typename real>
+__host__ __device__ constexpr int threads_yz(int N) {
+  return lines_yz<real>(N) * N / 8 < 32 ? 32
+         : lines_yz<real>(N) * N / 8 > 256 ? 256
+                                           : lines_yz<real>(N) * N / 8;
+}
+
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) {
+  C r;
+  r.x = a.x * b.x - a.y * b.y;
+  r.y = a.x * b.y + a.y * b.x;
+  return r;
+}
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) {
+  C r;
+  r.x = a.x + b.x;
+  r.y = a.y + b.y;
+  return r;
+}
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) {
+  C r;
+  r.x = a.x - b.x;
+  r.y = a.y - b.y;
+  return r;
+}
+// a * (SIGN i): -i for the forward sign, +i for the inverse
+template <int SIGN, typename C>
+__device__ __forceinline__ C cmuli(C a) {
+  C r;
+  if (SIGN < 0) {
+    r.x = a.y;
+    r.y = -a.x;
+  } else {
+    r.x = -a.y;
+    r.y = a.x;
+  }
+  return r;
+}
+
+// In-register DFT of radix R with kernel e^{SIGN 2 pi i jk/R}.
+template <int R, int SIGN, typename C>
+__device__ __forceinline__ void dft(C* v) {
+  using real = decltype(v[0].x);
+  if constexpr (R == 2) {
+    const C a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 3) {
+    const real c1 = real(-0.5), s1 = real(SIGN) * real(0.86602540378443864676);
+    const C a = v[0], b = v[1], c = v[2];
+    const C t1 = cadd(b, c), t2 = csub(b, c);
+    C m1, m2;
+    m1.x = a.x + c1 * t1.x;
+    m1.y = a.y + c1 * t1.y;
+    m2.x = -s1 * t2.y;
+    m2.y = s1 * t2.x;
+    v[0] = cadd(a, t1);
+    v[1] = cadd(m1, m2);
+    v[2] = csub(m1, m2);
+  } else if constexpr (R == 4) {
+    const C a = v[0], b = v[1], c = v[2], d = v[3];
+    const C t0 = cadd(a, c), t1 = csub(a, c), t2 = cadd(b, d), t3 = cmuli<SIGN>(csub(b, d));
+    v[0] = cadd(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[2] = csub(t0, t2);
+    v[3] = csub(t1, t3);
+  } else if constexpr (R == 6) {
+    C e[3] = {v[0], v[2], v[4]}, o[3] = {v[1], v[3], v[5]};
+    dft<3, SIGN>(e);
+    dft<3, SIGN>(o);
+    const real h = real(0.86602540378443864676) * real(SIGN);
+    C w1, w2;
+    w1.x = real(0.5);
+    w1.y = h;
+    w2.x = real(-0.5);
+    w2.y = h;
+    o[1] = cmul(o[1], w1);
+    o[2] = cmul(o[2], w2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      v[k] = cadd(e[k], o[k]);
+      v[k + 3] = csub(e[k], o[k]);
+    }
+  } else if constexpr (R == 8) {
+    C e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    dft<4, SIGN>(e);
+    dft<4, SIGN>(o);
+    const real h = real(0.70710678118654752440);
+    C w1, w3;
+    w1.x = h;
+    w1.y = real(SIGN) * h;
+    w3.x = -h;
+    w3.y = real(SIGN) * h;
+    o[1] = cmul(o[1], w1);
+    o[2] = cmuli<SIGN>(o[2]);
+    o[3] = cmul(o[3], w3);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = cadd(e[k], o[k]);
+      v[k + 4] = csub(e[k], o[k]);
+    }
+  }
+}
+
+// One Stockham stage over L lines of length N, in place through registers.
+// Enters with the buffer complete; leaves after a barrier.
+template <int R, int N, int Ns, int L, int NT, int SIGN, typename C>
+__device__ __forceinline__ void stage_ip(C* buf, const C* __restrict__ tw) {
+  constexpr int nb = N / R, total = L * nb, iters = (total + NT - 1) / NT, LP = pitch(N);
+  constexpr int toff = tw_offset(N, Ns);
+  C v[iters][R];
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int idx = threadIdx.x + it * NT;
+    if (total % NT == 0 || idx < total) {
+      const int line = idx / nb, j = idx - line * nb;
+      const C* in = buf + line * LP;
+#pragma unroll
+      for (int t = 0; t < R; ++t) v[it][t] = in[pidx(j + t * nb)];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int idx = threadIdx.x + it * NT;
+    if (total % NT == 0 || idx < total) {
+      const int line = idx / nb, j = idx - line * nb;
+      const int k = j % Ns;
+      if constexpr (Ns > 1) {
+#pragma unroll
+        for (int t = 1; t < R; ++t) {
+          C w = __ldg(tw + toff + (t - 1) * Ns + k);
+          if (SIGN > 0) w.y = -w.y;
+          v[it][t] = cmul(v[it][t], w);
+        }
+      }
+      dft<R, SIGN>(v[it]);
+      C* out = buf + line * LP;
+      const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+      for (int t = 0; t < R; ++t) out[pidx(base + t * Ns)] = v[it][t];
+    }
+  }
+  __syncthreads();
+}
+
+template <int N, int Ns, int L, int NT, int SIGN, typename C>
+__device__ __forceinline__ void fft_ip(C* buf, const C* tw) {
+  if constexpr (Ns < N) {
+    constexpr int R = pick_radix(N / Ns);
+    stage_ip<R, N, Ns, L, NT, SIGN>(buf, tw);
+    fft_ip<N, Ns * R, L, NT, SIGN>(buf, tw);
+  }
+}
+
+// Twiddle tables live in global memory in the plan's precision and are read
+// through L1 (a warp reads consecutive entries).
+
+// in-band index -> mode and mode -> in-band index along y/z (band box is
+// [0..b] U [N-b..N-1], or the whole axis when nb == N)
+__device__ __forceinline__ int band_mode(int bi, int nb, int N) {
+  return (nb == N || bi <= (nb - 1) / 2) ? bi : bi + N - nb;
+}
+__device__ __forceinline__ int band_index(int m, int nb, int N) {
+  if (nb == N) return m;
+  const int b = (nb - 1) / 2;
+  return m <= b ? m : (m >= N - b ? m - (N - nb) : -1);
+}
+
+// ---------------------------------------------------------------------------
+// P1: x rows, real -> complex, two rows per transform; out[row][kx], kx < ldx
+// (zeros for kx >= nbx).
+template <typename real, int N>
+__global__ void __launch_bounds__(kThreadsX, 6)
+k_x_r2c(const real* __restrict__ grid, typename Cx<real>::t* __restrict__ out,
+        const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx) {
+  using C = typename Cx<real>::t;
+  constexpr int PP = pairs_x(N), LP = pitch(N), NT = kThreadsX;
+  __shared__ C buf[PP * LP];
+  const long long r0 = 2LL * blockIdx.x * PP;
+  constexpr int nld = (PP * N + NT - 1) / NT;
+  real va[nld], vb[nld];
+#pragma unroll
+  for (int it = 0; it < nld; ++it) {
+    const int e = threadIdx.x + it * NT;
+    const int l = e / N, i = e - l * N;
+    const long long ra = r0 + 2 * l;
+    const bool in = (PP * N) % NT == 0 || e < PP * N;
+    va[it] = in && ra < nrows ? __ldcs(grid + ra * N + i) : real(0);
+    vb[it] = in && ra + 1 < nrows ? __ldcs(grid + (ra + 1) * N + i) : real(0);
+  }
+#pragma unroll
+  for (int it = 0; it < nld; ++it) {
+    const int e = threadIdx.x + it * NT;
+    if ((PP * N) % NT == 0 || e < PP * N) {
+      const int l = e / N, i = e - l * N;
+      C z;
+      z.x = va[it];
+      z.y = vb[it];
+      buf[l * LP + pidx(i)] = z;
+    }
+  }
+  __syncthreads();
+  fft_ip<N, 1, PP, NT, -1>(buf, tw);
+  for (int e = threadIdx.x; e < PP * ldx; e += NT) {
+    const int l = e / ldx, k = e - l * ldx;
+    const long long ra = r0 + 2 * l;
+    C A, B;
+    A.x = A.y = B.x = B.y = real(0);
+    if (k < nbx) {
+      const C zk = buf[l * LP + pidx(k)], zm = buf[l * LP + pidx((N - k) % N)];
+      A.x = real(0.5) * (zk.x + zm.x);   // (Zk + conj Zm) / 2
+      A.y = real(0.5) * (zk.y - zm.y);
+      B.x = real(0.5) * (zk.y + zm.y);   // (Zk - conj Zm) / 2i
+      B.y = real(-0.5) * (zk.x - zm.x);
+    }
+    if (ra < nrows) out[ra * ldx + k] = A;
+    if (ra + 1 < nrows) out[(ra + 1) * ldx + k] = B;
+  }
+}
+
+// P2: y lines (z, kx) for kx < ldx: forward C2C, keep the nby in-band ky.
+// in[(z*N + y)*ldx + kx] -> out[(z*nby + by)*ldx + kx].
+template <typename real, int N>
+__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+k_y_fwd(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ out,
+        const typename Cx<real>::t* __restrict__ tw, long long nlines, int ldx, int nby) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
+  constexpr int YS = NT / L, nld = N / YS;
+  static_assert(NT % L == 0 && N % YS == 0, "CTA shape");
+  extern __shared__ __align__(16) unsigned char sm[];
+  C* buf = reinterpret_cast<C*>(sm);
+  const int l = threadIdx.x % L;           // fixed line per thread
+  const long long line = (long long)blockIdx.x * L + l;
+  const bool valid = line < nlines;
+  const long long z = valid ? line / ldx : 0, kx = valid ? line - z * ldx : 0;
+  const C* src = in + z * N * ldx + kx;
+  C v[nld];
+#pragma unroll
+  for (int it = 0; it < nld; ++it) {
+    const int y = threadIdx.x / L + it * YS;
+    if (valid) v[it] = __ldcs(src + (long long)y * ldx);
+    else v[it].x = v[it].y = real(0);
+  }
+#pragma unroll
+  for (int it = 0; it < nld; ++it) buf[l * LP + pidx(threadIdx.x / L + it * YS)] = v[it];
+  __syncthreads();
+  fft_ip<N, 1, L, NT, -1>(buf, tw);
+  if (!valid) return;
+  C* dst = out + z * (long long)nby * ldx + kx;
+  for (int by = threadIdx.x / L; by < nby; by += YS)
+    dst[(long long)by * ldx] = buf[l * LP + pidx(band_mode(by, nby, N))];
+}
+
+struct FusedArgs {
+  int M[3];
+  int nbx, nby, nbz, ldx;
+  long long Hx;
+  long long Msum;
+  long long koff[3];
+  const double* axis_k;
+  const double* modeA;
+  const double* modeB;
+  double ik_scale;
+  double escale, pscale;
+};
+
+// Deterministic two-level completion of a per-block reduction: block b has
+// written partials[b][0..6].  The last block to finish in each group of 32
+// sums the group's partials in block order (lane j <- block 32g + j, then a
+// fixed xor tree) into the group slot; the last group to finish sums the
+// group slots the same way and writes out7.  Counters re-arm themselves.
+// Layout: partials [nblk][8] | group sums [ng][8]; counters [ng + 1].
+__device__ __forceinline__ void tree_finish(double* partials, int* counters, double* out7,
+                                            double escale, double pscale) {
+  __shared__ int s_flag;
+  const int nb = gridDim.x, g = blockIdx.x >> 5, ng = (nb + 31) >> 5;
+  const int gsize = min(32, nb - (g << 5));
+  double* gsum = partials + (size_t)nb * 8;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_flag = atomicAdd(counters + g, 1) == gsize - 1;
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  const int lane = threadIdx.x;
+  if (lane < 32) {
+    double v[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i)
+      v[i] = lane < gsize ? __ldcg(partials + (size_t)((g << 5) + lane) * 8 + i) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < 7; ++i) gsum[(size_t)g * 8 + i] = v[i];
+      counters[g] = 0;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_flag = atomicAdd(counters + ng, 1) == ng - 1;
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  if (lane < 32) {
+    double v[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) v[i] = 0.0;
+    for (int j = lane; j < ng; j += 32) {
+#pragma unroll
+      for (int i = 0; i < 7; ++i) v[i] += __ldcg(gsum + (size_t)j * 8 + i);
+    }
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    }
+    if (lane == 0) {
+      out7[0] = v[0] * escale;
+      for (int i = 1; i < 7; ++i) out7[i] = v[i] * pscale;
+      counters[ng] = 0;
+    }
+  }
+}
+
+// P3a: z pencils line = by*ldx + kx: forward C2C; the in-band kz box goes to
+// spec (cuFFT half-spectrum layout) and into the fixed-order energy/pressure
+// reduction (warp shuffle -> block -> per-block partials -> last block).
+template <typename real, int N>
+__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ spec,
+           const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines,
+           double* __restrict__ partials, int* __restrict__ counters,
+           double* __restrict__ out7) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
+  constexpr int ZS = NT / L, nld = N / ZS;
+  static_assert(NT % L == 0 && N % ZS == 0, "CTA shape");
+  extern __shared__ __align__(16) unsigned char sm[];
+  C* X = reinterpret_cast<C*>(sm);
+  const int ldx = fa.ldx, nbx = fa.nbx, nby = fa.nby, nbz = fa.nbz;
+  const long long zstride = (long long)nby * ldx;
+  const int l = threadIdx.x % L;
+  const long long line = (long long)blockIdx.x * L + l;
+  const bool valid = line < nlines;
+  int by = 0, mx = 0, my = 0;
+  bool live = false;
+  auto pencil = [&]() {   // (by, kx) of this thread's line
+    by = valid ? (int)(line / ldx) : 0;
+    mx = valid ? (int)(line - (long long)by * ldx) : 0;
+    live = valid && mx < nbx;
+    my = band_mode(by, nby, fa.M[1]);
+  };
+  // Mode tables: A, B and k_c = (K_c,x[mx] + K_c,y[my]) + K_c,z[mz] (the
+  // order of mesh.py:242).  Masked modes have A = B = 0 and add exact zeros.
+  // Small pencils (short latency chains, few CTAs) issue every table load
+  // before the transform so that they overlap the input loads; large ones
+  // load A, B, K_z after it (register budget).
+  constexpr bool PF = nld <= 6;
+  constexpr int NP = PF ? nld : 1;
+  double pA[NP], pB[NP], pk[3][NP], kxy[3];
+  if constexpr (PF) {
+    pencil();
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double* K = fa.axis_k + c * fa.Msum;
+      kxy[c] = live ? __dadd_rn(__ldg(K + fa.koff[0] + mx), __ldg(K + fa.koff[1] + my)) : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < NP; ++it) {
+      const int bz = threadIdx.x / L + it * ZS;
+      pA[it] = pB[it] = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) pk[c][it] = 0.0;
+      if (live && bz < nbz) {
+        const long long be = ((long long)bz * nby + by) * nbx + mx;
+        const int mz = band_mode(bz, nbz, N);
+        pA[it] = __ldg(fa.modeA + be);
+        pB[it] = __ldg(fa.modeB + be);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pk[c][it] = __ldg(fa.axis_k + c * fa.Msum + fa.koff[2] + mz);
+      }
+    }
+  }
+  {
+    C v[nld];
+#pragma unroll
+    for (int it = 0; it < nld; ++it) {
+      const int z = threadIdx.x / L + it * ZS;
+      if (valid) v[it] = __ldcs(in + (long long)z * zstride + line);
+      else v[it].x = v[it].y = real(0);
+    }
+#pragma unroll
+    for (int it = 0; it < nld; ++it) X[l * LP + pidx(threadIdx.x / L + it * ZS)] = v[it];
+  }
+  __syncthreads();
+  fft_ip<N, 1, L, NT, -1>(X, tw);
+  if constexpr (!PF) pencil();
+  double acc[7];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) acc[i] = 0.0;
+  if (live) {
+    const double wx = (mx == 0 || 2 * mx == fa.M[0]) ? 1.0 : 2.0;
+    if constexpr (PF) {
+#pragma unroll
+      for (int it = 0; it < NP; ++it) {
+        const int bz = threadIdx.x / L + it * ZS;
+        if (bz >= nbz) continue;
+        const int mz = band_mode(bz, nbz, N);
+        const C Xv = X[l * LP + pidx(mz)];
+        spec[((long long)mz * fa.M[1] + my) * fa.Hx + mx] = Xv;
+        const double A = pA[it], B = pB[it];
+        if (A == 0.0) continue;
+        const double xr = (double)Xv.x, xi = (double)Xv.y;
+        const double w = wx * (xr * xr + xi * xi);
+        const double kx = __dadd_rn(kxy[0], pk[0][it]), ky = __dadd_rn(kxy[1], pk[1][it]),
+                     kz = __dadd_rn(kxy[2], pk[2][it]);
+        const double wa = w * A, t = w * B;
+        acc[0] += wa;
+        acc[1] += t * kx * kx + wa;
+        acc[2] += t * kx * ky;
+        acc[3] += t * kx * kz;
+        acc[4] += t * ky * ky + wa;
+        acc[5] += t * ky * kz;
+        acc[6] += t * kz * kz + wa;
+      }
+    } else {
+      const double* Kz[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double* K = fa.axis_k + c * fa.Msum;
+        kxy[c] = __dadd_rn(__ldg(K + fa.koff[0] + mx), __ldg(K + fa.koff[1] + my));
+        Kz[c] = K + fa.koff[2];
+      }
+      for (int bz = threadIdx.x / L; bz < nbz; bz += ZS) {
+        const int mz = band_mode(bz, nbz, N);
+        const C Xv = X[l * LP + pidx(mz)];
+        spec[((long long)mz * fa.M[1] + my) * fa.Hx + mx] = Xv;
+        const long long be = ((long long)bz * nby + by) * nbx + mx;
+        const double A = __ldg(fa.modeA + be);
+        if (A == 0.0) continue;
+        const double B = __ldg(fa.modeB + be);
+        const double xr = (double)Xv.x, xi = (double)Xv.y;
+        const double w = wx * (xr * xr + xi * xi);
+        const double kx = __dadd_rn(kxy[0], __ldg(Kz[0] + mz)),
+                     ky = __dadd_rn(kxy[1], __ldg(Kz[1] + mz)),
+                     kz = __dadd_rn(kxy[2], __ldg(Kz[2] + mz));
+        const double wa = w * A, t = w * B;
+        acc[0] += wa;
+        acc[1] += t * kx * kx + wa;
+        acc[2] += t * kx * ky;
+        acc[3] += t * kx * kz;
+        acc[4] += t * ky * ky + wa;
+        acc[5] += t * ky * kz;
+        acc[6] += t * kz * kz + wa;
+      }
+    }
+  }
+  constexpr int NW = (NT + 31) / 32;
+  __shared__ double red[NW][7];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 7; ++i) red[warp][i] = acc[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
+    partials[(size_t)blockIdx.x * 8 + threadIdx.x] = s;
+  }
+  tree_finish(partials, counters, out7, fa.escale, fa.pscale);
+}
+
+// P3b: ik pencils, one force component per blockIdx.y: i k_c A X h3/G on the
+// retained modes (zero elsewhere, mesh.py:333-341), inverse C2C along z ->
+// ik[c][z][by][kx].  X is the box spectrum P3a wrote.
+template <typename real, int N>
+__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __restrict__ ik,
+       const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
+  constexpr int ZS = NT / L, nld = N / ZS;
+  extern __shared__ __align__(16) unsigned char sm[];
+  C* T = reinterpret_cast<C*>(sm);
+  const int comp = blockIdx.y;
+  const int ldx = fa.ldx, nbx = fa.nbx, nby = fa.nby, nbz = fa.nbz;
+  const long long zstride = (long long)nby * ldx;
+  const int l = threadIdx.x % L;
+  const long long line = (long long)blockIdx.x * L + l;
+  const bool valid = line < nlines;
+  const int by = valid ? (int)(line / ldx) : 0;
+  const int mx = valid ? (int)(line - (long long)by * ldx) : 0;
+  const bool live = valid && mx < nbx;
+  const int my = band_mode(by, nby, fa.M[1]);
+  const double* K = fa.axis_k + comp * fa.Msum;
+  const double kxy = live ? __dadd_rn(K[fa.koff[0] + mx], K[fa.koff[1] + my]) : 0.0;
+  {
+    C v[nld];
+#pragma unroll
+    for (int it = 0; it < nld; ++it) {
+      const int mz = threadIdx.x / L + it * ZS;
+      v[it].x = v[it].y = real(0);
+      const int bz = band_index(mz, nbz, N);
+      if (live && bz >= 0) {
+        const double A = __ldg(fa.modeA + ((long long)bz * nby + by) * nbx + mx);
+        const C Xv = __ldg(spec + ((long long)mz * fa.M[1] + my) * fa.Hx + mx);
+        const double cf = A * fa.ik_scale * __dadd_rn(kxy, __ldg(K + fa.koff[2] + mz));
+        v[it].x = (real)(-cf * (double)Xv.y);
+        v[it].y = (real)(cf * (double)Xv.x);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < nld; ++it) T[l * LP + pidx(threadIdx.x / L + it * ZS)] = v[it];
+  }
+  __syncthreads();
+  fft_ip<N, 1, L, NT, +1>(T, tw);
+  if (!valid) return;
+  C* dst = ik + (long long)comp * N * zstride + line;
+#pragma unroll
+  for (int it = 0; it < nld; ++it) {
+    const int z = threadIdx.x / L + it * ZS;
+    __stcs(dst + (long long)z * zstride, T[l * LP + pidx(z)]);
+  }
+}
+
+// P4: y lines (c, z, kx): inverse C2C from the nby in-band ky rows (zero
+// elsewhere).  in[(cz*nby + by)*ldx + kx] -> out[(cz*N + y)*ldx + kx].
+template <typename real, int N>
+__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+k_y_inv(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ out,
+        const typename Cx<real>::t* __restrict__ tw, long long nlines, int ldx, int nby) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
+  constexpr int YS = NT / L, nld = N / YS;
+  static_assert(NT % L == 0 && N % YS == 0, "CTA shape");
+  extern __shared__ __align__(16) unsigned char sm[];
+  C* buf = reinterpret_cast<C*>(sm);
+  const int l = threadIdx.x % L;
+  const long long line = (long long)blockIdx.x * L + l;
+  const bool valid = line < nlines;
+  const long long cz = valid ? line / ldx : 0, kx = valid ? line - cz * ldx : 0;
+  const C* src = in + cz * (long long)nby * ldx + kx;
+  C v[nld];
+#pragma unroll
+  for (int it = 0; it < nld; ++it) {
+    const int y = threadIdx.x / L + it * YS;
+    const int by = band_index(y, nby, N);
+    if (valid && by >= 0) v[it] = __ldcs(src + (long long)by * ldx);
+    else v[it].x = v[it].y = real(0);
+  }
+#pragma unroll
+  for (int it = 0; it < nld; ++it) buf[l * LP + pidx(threadIdx.x / L + it * YS)] = v[it];
+  __syncthreads();
+  fft_ip<N, 1, L, NT, +1>(buf, tw);
+  if (!valid) return;
+  C* dst = out + cz * (long long)N * ldx + kx;
+#pragma unroll
+  for (int it = 0; it < nld; ++it) {
+    const int y = threadIdx.x / L + it * YS;
+    dst[(long long)y * ldx] = buf[l * LP + pidx(y)];
+  }
+}
+
+// P5: x rows, complex -> real, two rows per transform; columns kx < nbx
+// (zero-padded to the half spectrum; kx = 0 and Nyquist taken as real, as a
+// C2R transform does).  Each in-band column is read once and placed at k and
+// N - k (conjugate-symmetric extension).
+template <typename real, int N>
+__global__ void __launch_bounds__(kThreadsX, 6)
+k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
+        const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx) {
+  using C = typename Cx<real>::t;
+  constexpr int PP = pairs_x(N), LP = pitch(N), NT = kThreadsX;
+  constexpr int half = N / 2, NH = half + 1;
+  __shared__ C buf[PP * LP];
+  const long long r0 = 2LL * blockIdx.x * PP;
+  constexpr int nhl = (PP * NH + NT - 1) / NT;
+  C va[nhl], vb[nhl];
+#pragma unroll
+  for (int it = 0; it < nhl; ++it) {
+    const int e = threadIdx.x + it * NT;
+    const int l = e / NH, k = e - l * NH;
+    const long long ra = r0 + 2 * l;
+    va[it].x = va[it].y = vb[it].x = vb[it].y = real(0);
+    if (e < PP * NH && k < nbx) {
+      if (ra < nrows) va[it] = __ldcs(in + ra * ldx + k);
+      if (ra + 1 < nrows) vb[it] = __ldcs(in + (ra + 1) * ldx + k);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < nhl; ++it) {
+    const int e = threadIdx.x + it * NT;
+    if (e < PP * NH) {
+      const int l = e / NH, k = e - l * NH;
+      C A = va[it], B = vb[it];
+      if (k == 0 || k == half) {
+        A.y = real(0);
+        B.y = real(0);
+      }
+      C z;   // Z_k = A + i B
+      z.x = A.x - B.y;
+      z.y = A.y + B.x;
+      buf[l * LP + pidx(k)] = z;
+      if (k != 0 && k != half) {   // Z_{N-k} = conj A + i conj B
+        z.x = A.x + B.y;
+        z.y = B.x - A.y;
+        buf[l * LP + pidx(N - k)] = z;
+      }
+    }
+  }
+  __syncthreads();
+  fft_ip<N, 1, PP, NT, +1>(buf, tw);
+  constexpr int nld = (PP * N + NT - 1) / NT;
+#pragma unroll 4
+  for (int it = 0; it < nld; ++it) {
+    const int e = threadIdx.x + it * NT;
+    if ((PP * N) % NT == 0 || e < PP * N) {
+      const int l = e / N, i = e - l * N;
+      const long long ra = r0 + 2 * l;
+      const C z = buf[l * LP + pidx(i)];
+      if (ra < nrows) __stcs(fld + ra * N + i, z.x);
+      if (ra + 1 < nrows) __stcs(fld + (ra + 1) * N + i, z.y);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+
+static bool supported(int n) {
+  switch (n) {
+#define ESP_CASE(v) case v:
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+    return true;
+    default:
+      return false;
+  }
+}
+
+// Per-stage twiddles in the kernels' order: for each stage with span Ns > 1
+// and radix R, entries [(t-1)*Ns + k] = e^{-2 pi i t k / (Ns R)}.
+static std::vector<double2> twiddles(int n) {
+  std::vector<double2> h;
+  int Ns = 1;
+  while (Ns < n) {
+    const int R = pick_radix(n / Ns);
+    if (Ns > 1)
+      for (int t = 1; t < R; ++t)
+        for (int k = 0; k < Ns; ++k) {
+          const double a = -2.0 * 3.14159265358979323846 * (double)(t * k) / (double)(Ns * R);
+          h.push_back(make_double2(std::cos(a), std::sin(a)));
+        }
+    Ns *= R;
+  }
+  if (h.empty()) h.push_back(make_double2(1.0, 0.0));
+  return h;
+}
+
+template <typename real, int N>
+static cudaError_t launch_x_r2c(const esp_plan* p, const void* grid, void* out, const void* tw,
+                                int ldx, cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  constexpr int PP = pairs_x(N);
+  const long long nrows = (long long)p->M[1] * p->M[2];
+  const long long nblk = (nrows + 2 * PP - 1) / (2 * PP);
+  k_x_r2c<real, N><<<(unsigned)nblk, kThreadsX, 0, s>>>(
+      reinterpret_cast<const real*>(grid), reinterpret_cast<C*>(out),
+      reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx);
+  return cudaGetLastError();
+}
+
+template <typename real, int N>
+static cudaError_t launch_y_fwd(const esp_plan* p, const void* in, void* out, const void* tw,
+                                int ldx, cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N);
+  const long long nlines = (long long)p->M[2] * ldx;
+  const size_t smem = sizeof(C) * L * pitch(N);
+  cudaError_t e = cudaFuncSetAttribute(k_y_fwd<real, N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_y_fwd<real, N><<<(unsigned)((nlines + L - 1) / L), threads_yz<real>(N), smem, s>>>(
+      reinterpret_cast<const C*>(in), reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw),
+      nlines, ldx, p->nby);
+  return cudaGetLastError();
+}
+
+template <typename real, int N>
+static cudaError_t launch_z_reduce(const esp_plan* p, const void* in, const void* tw,
+                                   const FusedArgs& fa, double* partials, long long nblk_cap,
+                                   double* out7, cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N);
+  const size_t smem = sizeof(C) * L * pitch(N);
+  cudaError_t e = cudaFuncSetAttribute(k_z_reduce<real, N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long nlines = (long long)p->nby * fa.ldx;
+  const long long nblk = (nlines + L - 1) / L;
+  if (nblk > nblk_cap) return cudaErrorInvalidConfiguration;
+  k_z_reduce<real, N><<<(unsigned)nblk, threads_yz<real>(N), smem, s>>>(
+      reinterpret_cast<const C*>(in), reinterpret_cast<C*>(p->d_spec),
+      reinterpret_cast<const C*>(tw), fa, nlines, partials,
+      reinterpret_cast<int*>(partials + (nblk + (nblk + 31) / 32) * 8), out7);
+  return cudaGetLastError();
+}
+
+template <typename real, int N>
+static cudaError_t launch_z_ik(const esp_plan* p, void* ik, const void* tw, const FusedArgs& fa,
+                               cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N);
+  const size_t smem = sizeof(C) * L * pitch(N);
+  cudaError_t e = cudaFuncSetAttribute(k_z_ik<real, N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long nlines = (long long)p->nby * fa.ldx;
+  const dim3 grid((unsigned)((nlines + L - 1) / L), 3);
+  k_z_ik<real, N><<<grid, threads_yz<real>(N), smem, s>>>(
+      reinterpret_cast<const C*>(p->d_spec), reinterpret_cast<C*>(ik),
+      reinterpret_cast<const C*>(tw), fa, nlines);
+  return cudaGetLastError();
+}
+
+template <typename real, int N>
+static cudaError_t launch_y_inv(const esp_plan* p, const void* in, void* out, const void* tw,
+                                int ldx, cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  constexpr int L = lines_yz<real>(N);
+  const long long nlines = 3LL * p->M[2] * ldx;
+  const size_t smem = sizeof(C) * L * pitch(N);
+  cudaError_t e = cudaFuncSetAttribute(k_y_inv<real, N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_y_inv<real, N><<<(unsigned)((nlines + L - 1) / L), threads_yz<real>(N), smem, s>>>(
+      reinterpret_cast<const C*>(in), reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw),
+      nlines, ldx, p->nby);
+  return cudaGetLastError();
+}
+
+template <typename real, int N>
+static cudaError_t launch_x_c2r(const esp_plan* p, const void* in, void* fld, const void* tw,
+                                int ldx, cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  constexpr int PP = pairs_x(N);
+  const long long nrows = 3LL * p->M[1] * p->M[2];
+  const long long nblk = (nrows + 2 * PP - 1) / (2 * PP);
+  k_x_c2r<real, N><<<(unsigned)nblk, kThreadsX, 0, s>>>(
+      reinterpret_cast<const C*>(in), reinterpret_cast<real*>(fld),
+      reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx);
+  return cudaGetLastError();
+}
+
+}  // namespace fft
+
+struct FusedFft {
+  void* tw[3];   // per-axis twiddles in the plan's precision
+  void* bufA;   // x-pass output [Mz][My][ldx]
+  void* bufB;   // y-pass output [Mz][nby][ldx]
+  void* bufC;   // ik pencils    [3][Mz][nby][ldx]
+  void* bufD;   // y-inverse     [3][Mz][My][ldx]
+  int ldx, nbx, nby, nbz;
+};
+
+}  // namespace esp
+
+using esp::FusedFft;
+
+void esp_fused_fft_destroy(void* h) {
+  auto* f = reinterpret_cast<FusedFft*>(h);
+  if (!f) return;
+  for (int d = 0; d < 3; ++d)
+    if (f->tw[d]) cudaFree(f->tw[d]);
+  if (f->bufA) cudaFree(f->bufA);
+  if (f->bufB) cudaFree(f->bufB);
+  if (f->bufC) cudaFree(f->bufC);
+  if (f->bufD) cudaFree(f->bufD);
+  delete f;
+}
+
+// Build the fused transform for the plan's grid and current box; nullptr if a
+// grid length is not one of ESP_FFT_SIZES (the plan then uses cuFFT).
+void* esp_fused_fft_create(esp_plan* p) {
+  for (int d = 0; d < 3; ++d)
+    if (!esp::fft::supported(p->M[d])) return nullptr;
+  auto* f = new FusedFft;
+  std::memset(f, 0, sizeof(FusedFft));
+  for (int d = 0; d < 3; ++d) {
+    const std::vector<double2> h = esp::fft::twiddles(p->M[d]);
+    std::vector<float2> hf(h.size());
+    for (size_t i = 0; i < h.size(); ++i) hf[i] = make_float2((float)h[i].x, (float)h[i].y);
+    const bool dp = p->precision == ESP_FP64;
+    const size_t bytes = (dp ? sizeof(double2) : sizeof(float2)) * h.size();
+    const void* src = dp ? (const void*)h.data() : (const void*)hf.data();
+    if (cudaMalloc(&f->tw[d], bytes) != cudaSuccess ||
+        cudaMemcpy(f->tw[d], src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+      esp_fused_fft_destroy(f);
+      return nullptr;
+    }
+  }
+  const size_t cs = p->precision == ESP_FP64 ? sizeof(double2) : sizeof(float2);
+  f->nbx = p->nbx;
+  f->nby = p->nby;
+  f->nbz = p->nbz;
+  f->ldx = (p->nbx + 7) / 8 * 8;
+  const long long My = p->M[1], Mz = p->M[2], ldx = f->ldx;
+  if (cudaMalloc(&f->bufA, cs * Mz * My * ldx) != cudaSuccess ||
+      cudaMalloc(&f->bufB, cs * Mz * p->nby * ldx) != cudaSuccess ||
+      cudaMalloc(&f->bufC, cs * 3 * Mz * p->nby * ldx) != cudaSuccess ||
+      cudaMalloc(&f->bufD, cs * 3 * Mz * My * ldx) != cudaSuccess) {
+    cudaGetLastError();
+    esp_fused_fft_destroy(f);
+    return nullptr;
+  }
+  return f;
+}
+
+namespace esp {
+
+// Upper bound on the blocks of the fused reduction (the plan sizes its
+// partials | group sums | counters buffer from it, see tree_finish).
+int fused_reduce_blocks(const esp_plan* p) {
+  const int ldx = (p->nbx + 7) / 8 * 8;
+  const int L = p->precision == ESP_FP64 ? fft::lines_yz<double>(p->M[2])
+                                         : fft::lines_yz<float>(p->M[2]);
+  return (int)(((long long)p->nby * ldx + L - 1) / L);
+}
+
+// ESP_FFT_DEBUG=1: synchronize after every pass and name the failing one.
+static cudaError_t debug_check(cudaStream_t s, const char* what) {
+  static const bool on = std::getenv("ESP_FFT_DEBUG") != nullptr;
+  if (!on) return cudaSuccess;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) std::fprintf(stderr, "esp_fft: %s failed: %s\n", what, cudaGetErrorString(e));
+  return e;
+}
+
+template <typename real>
+static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_out7,
+                             cudaStream_t s) {
+  using namespace fft;
+  cudaError_t e = cudaErrorInvalidValue;
+  const int ldx = f->ldx;
+  switch (p->M[0]) {
+#define ESP_CASE(v) \
+  case v: e = launch_x_r2c<real, v>(p, p->d_grid, f->bufA, f->tw[0], ldx, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, "fft_x");
+  if ((e = debug_check(s, "fft_x")) != cudaSuccess) return e;
+  e = cudaErrorInvalidValue;
+  switch (p->M[1]) {
+#define ESP_CASE(v) \
+  case v: e = launch_y_fwd<real, v>(p, f->bufA, f->bufB, f->tw[1], ldx, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, "fft_y");
+  if ((e = debug_check(s, "fft_y")) != cudaSuccess) return e;
+  FusedArgs fa;
+  for (int d = 0; d < 3; ++d) {
+    fa.M[d] = p->M[d];
+    fa.koff[d] = p->koff[d];
+  }
+  fa.nbx = p->nbx;
+  fa.nby = p->nby;
+  fa.nbz = p->nbz;
+  fa.ldx = ldx;
+  fa.Hx = p->Hx;
+  fa.Msum = (long long)p->M[0] + p->M[1] + p->M[2];
+  fa.axis_k = p->d_axis_k;
+  fa.modeA = p->d_modeA;
+  fa.modeB = p->d_modeB;
+  fa.ik_scale = p->h3 / (double)p->G;
+  const double h3sq = p->h3 * p->h3;
+  fa.escale = h3sq / (2.0 * p->volume);
+  fa.pscale = h3sq / (2.0 * p->volume * p->volume);
+  e = cudaErrorInvalidValue;
+  switch (p->M[2]) {
+#define ESP_CASE(v)                                                                       \
+  case v:                                                                                 \
+    e = launch_z_reduce<real, v>(p, f->bufB, f->tw[2], fa, p->d_partials_fft,            \
+                                 p->n_red_blocks_fft, d_out7, s);                         \
+    break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, "fft_z_scale_reduce");
+  if ((e = debug_check(s, "fft_z_scale_reduce")) != cudaSuccess) return e;
+  if (!want_ik) return cudaSuccess;
+  e = cudaErrorInvalidValue;
+  switch (p->M[2]) {
+#define ESP_CASE(v) \
+  case v: e = launch_z_ik<real, v>(p, f->bufC, f->tw[2], fa, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, "ifft_z_ik");
+  if ((e = debug_check(s, "ifft_z_ik")) != cudaSuccess) return e;
+  e = cudaErrorInvalidValue;
+  switch (p->M[1]) {
+#define ESP_CASE(v) \
+  case v: e = launch_y_inv<real, v>(p, f->bufC, f->bufD, f->tw[1], ldx, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, "ifft_y");
+  if ((e = debug_check(s, "ifft_y")) != cudaSuccess) return e;
+  e = cudaErrorInvalidValue;
+  switch (p->M[0]) {
+#define ESP_CASE(v) \
+  case v: e = launch_x_c2r<real, v>(p, f->bufD, p->d_fields, f->tw[0], ldx, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  p->launches++;
+  prof_mark(p, s, "ifft_x");
+  if ((e = debug_check(s, "ifft_x")) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
+cudaError_t launch_fused_fft(esp_plan* p, int want_ik, double* d_out7, cudaStream_t s) {
+  auto* f = reinterpret_cast<FusedFft*>(p->fused);
+  return p->precision == ESP_FP64 ? fused_run<double>(p, f, want_ik, d_out7, s)
+                                  : fused_run<float>(p, f, want_ik, d_out7, s);
+}
+
+}  // namespace esp

@@ -248,6 +248,10 @@ struct esp_plan {
   int nbx, nby, nbz;
   long long nbox, n_modes;
   int n_red_blocks;
+  // band-pruned fused transforms (esp_fft.cu); null -> cuFFT path
+  void* fused;
+  double* d_partials_fft;
+  int n_red_blocks_fft;
   // device buffers
   double *d_tab, *d_dtab, *d_breaks;
   float *d_tabf, *d_dtabf;
@@ -322,6 +326,10 @@ cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s,
                              const void* fields = nullptr,
                              OutMap om = OutMap{3, {0, 1, 2}, {-1, -1, -1}});
 cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s);
+// Fused band-pruned forward transform + scale/reduce (+ ik spectra and the
+// inverse transforms into d_fields when want_ik).  Requires p->fused.
+cudaError_t launch_fused_fft(esp_plan* p, int want_ik, double* d_out7, cudaStream_t s);
+int fused_reduce_blocks(const esp_plan* p);
 cudaError_t launch_mode_setup(esp_plan* p, double what_zero, cudaStream_t s);
 void build_combine_axis(int M, int T, int E, int nt, int lo, std::vector<int>& ent,
                         std::vector<int>& cnt);
@@ -337,3 +345,8 @@ inline void prof_mark(esp_plan* p, cudaStream_t s, const char* name) {
 }
 
 }  // namespace esp
+
+// esp_fft.cu: fused transform state (nullptr when a grid length has a prime
+// factor other than 2 or 3, or for slab plans).
+void* esp_fused_fft_create(esp_plan* p);
+void esp_fused_fft_destroy(void* f);
