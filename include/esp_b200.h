@@ -166,6 +166,10 @@ int esp_grid_info(const esp_plan* plan, int64_t* info8);
 /* info8 = {Mx, My, Mz, Hx(=Mx/2+1), n_modes_retained(full spectrum),
  *          kernel_launches_last_step, n_tiles, precision}                   */
 int esp_set_spectrum(esp_plan* plan, const void* d_spectrum, void* stream);
+/* Transform path esp_evaluate uses: 1 = band-pruned fused transforms
+ * (grid lengths in {32,48,64,96,128,192,256,384}, full-grid plans),
+ * 0 = cuFFT.  ESP_FFT=cufft in the environment forces 0 at set_cell. */
+int esp_fft_path(const esp_plan* plan);
 
 /* --- diagnostics (bench / roofline) ----------------------------------------- */
 /* Record a CUDA event after every stage kernel of esp_evaluate.            */

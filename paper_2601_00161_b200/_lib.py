@@ -115,6 +115,7 @@ def lib():
     L.esp_fields_ptr.argtypes = [vp]
     L.esp_fields_ptr.restype = vp
     L.esp_grid_info.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.esp_fft_path.argtypes = [vp]
     L.esp_set_spectrum.argtypes = [vp, vp, vp]
     L.esp_set_profiling.argtypes = [vp, C.c_int32]
     L.esp_profile_read.argtypes = [vp, C.c_char_p, C.c_int32, C.POINTER(C.c_double), C.c_int32]
@@ -129,7 +130,7 @@ EXPORTED = [
     "esp_forces_analytic", "esp_local_pressure", "esp_evaluate", "esp_counters",
     "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
-    "esp_gather_fields", "esp_fields_ptr",
+    "esp_gather_fields", "esp_fields_ptr", "esp_fft_path",
 ]
 
 

@@ -727,6 +727,8 @@ void* esp_grid_ptr(esp_plan* p) { return p ? p->d_grid : nullptr; }
 void* esp_spectrum_ptr(esp_plan* p) { return p ? p->d_spec : nullptr; }
 void* esp_fields_ptr(esp_plan* p) { return p ? p->d_fields : nullptr; }
 
+int esp_fft_path(const esp_plan* p) { return p && p->fused ? 1 : 0; }
+
 int esp_grid_info(const esp_plan* p, int64_t* info) {
   if (!p || !info) return ESP_ERR_PARAM;
   info[0] = p->M[0];

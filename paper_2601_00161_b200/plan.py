@@ -261,6 +261,11 @@ class EspPlan:
         return list(buf)
 
     @property
+    def fft_path(self) -> str:
+        """"fused" (band-pruned transforms, esp_fft.cu) or "cufft"."""
+        return "fused" if _lib.lib().esp_fft_path(self._handle) else "cufft"
+
+    @property
     def real_dtype(self):
         return torch.float64 if self.precision == "fp64" else torch.float32
 

@@ -454,3 +454,68 @@ def test_analytic_forces_through_mesh_api_and_triclinic():
     _, Fan = plan.evaluate(pos, q, want_forces=True, analytic=True)
     assert O.rms_rel_forces(Fan.cpu().numpy(), Fik) <= 50 * float(gt["delta"])
     assert O.rms_rel_forces(Fan.cpu().numpy(), gt["F_direct"]) <= 50 * float(gt["delta"])
+
+
+# --- band-pruned fused transforms (esp_fft.cu) ---------------------------------
+# Grids whose lengths are all in {32,48,64,96,128,192,256,384} run esp_evaluate
+# through the fused transform pipeline; others (and ESP_FFT=cufft) use cuFFT.
+FUSED_CASES = [
+    ("tri_skew_p8", (64, 64, 96)),     # triclinic, P=8
+    ("tri_flex_p7", (48, 48, 64)),     # triclinic, odd P
+    ("small_brick_p6", (48, 64, 64)),  # orthorhombic
+    ("small_brick_p7", (64, 64, 96)),  # orthorhombic, odd P
+    ("small_cube_p5", (48, 48, 48)),   # odd P, cubic
+]
+
+
+@pytest.mark.parametrize("name,M", FUSED_CASES)
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_fused_fft_path_matches_oracle(name, M, precision):
+    g = golden(name)
+    plan = _plan_for(g, M=M, precision=precision)
+    assert plan.fft_path == "fused"
+    E, Pt, F = _run(plan, g["pos"], g["q"])
+    op = O.make_plan(g["h"], M, int(g["P"]), float(g["delta"]), float(g["r_c"]))
+    oE, oP, oF = O.kspace(op, g["pos"], g["q"])
+    tol = F64_TOL if precision == "fp64" else F32_TOL
+    assert O.rel_scalar(E, oE) <= tol
+    assert O.rel_frobenius(Pt, oP) <= tol
+    assert O.rms_rel_forces(F, oF) <= tol
+    # pressure-only step: one forward transform, no inverse, same E and P
+    plan.reset_counters()
+    E2, P2, _ = _run(plan, g["pos"], g["q"], want_forces=False)
+    assert plan.counters() == (1, 0)
+    assert O.rel_scalar(E2, oE) <= tol and O.rel_frobenius(P2, oP) <= tol
+
+
+def test_fused_and_cufft_paths_agree(monkeypatch):
+    g = golden("tri_skew_p8")
+    M = (64, 64, 96)
+    fused = _plan_for(g, M=M)
+    monkeypatch.setenv("ESP_FFT", "cufft")
+    ref = _plan_for(g, M=M)
+    assert fused.fft_path == "fused" and ref.fft_path == "cufft"
+    Ea, Pa, Fa = _run(fused, g["pos"], g["q"])
+    Eb, Pb, Fb = _run(ref, g["pos"], g["q"])
+    assert O.rel_scalar(Ea, Eb) <= 1e-13
+    assert O.rel_frobenius(Pa, Pb) <= 1e-13
+    assert O.rms_rel_forces(Fa, Fb) <= 1e-13
+    # the in-band spectrum box the fused forward pass leaves in the plan
+    # feeds the stage-level API (scale/reduce on the same spectrum)
+    torch = _torch()
+    out7 = torch.empty(7, dtype=torch.float64, device="cuda")
+    fused.scale_reduce(False, out7)
+    from paper_2601_00161_b200.plan import out7_to_tensor
+    E3, P3 = out7_to_tensor(out7)
+    assert O.rel_scalar(E3, Ea) <= 1e-14 and O.rel_frobenius(P3, Pa) <= 1e-14
+
+
+def test_unsupported_lengths_fall_back_to_cufft():
+    g = golden("tri_skew_p8")                  # M = (64, 64, 80): 80 not a fused length
+    plan = _plan_for(g)
+    assert plan.fft_path == "cufft"
+    E, Pt, F = _run(plan, g["pos"], g["q"])
+    op = O.make_plan(g["h"], tuple(g["M"]), int(g["P"]), float(g["delta"]), float(g["r_c"]))
+    oE, oP, oF = O.kspace(op, g["pos"], g["q"])
+    assert O.rel_scalar(E, oE) <= F64_TOL
+    assert O.rms_rel_forces(F, oF) <= F64_TOL
