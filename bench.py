@@ -148,21 +148,53 @@ class ClockSampler:
 # algorithmic bytes / flops (stated in DESIGN.md)
 
 
-def algorithmic(w, n, real_bytes=8):
+def box_counts(M, band):
+    """In-band box of the half spectrum: nbx (kx >= 0), nby, nbz (esp_api.cu
+    set_cell), and the fused path's padded kx pitch."""
+    nbx = min(band[0], M[0] // 2) + 1
+    nb = [M[d] if 2 * band[d] + 1 >= M[d] else 2 * band[d] + 1 for d in (1, 2)]
+    return nbx, nb[0], nb[1], (nbx + 7) // 8 * 8
+
+
+def algorithmic(w, n, band, real_bytes=8):
+    """Compulsory HBM bytes and flops per launch of each stage kernel."""
     Mx, My, Mz = w.M
     G = Mx * My * Mz
     H = (Mx // 2 + 1) * My * Mz
     r, c, pb = real_bytes, 2 * real_bytes, 32
     P, D = w.P, 18
+    nbx, nby, nbz, _ = box_counts(w.M, band)
+    nbox = nbx * nby * nbz
+    lg = np.log2
     return {
         "spread": dict(bytes=pb * n + r * G, flops=2 * (3 * P * D + P * P + P + P ** 3) * n),
         "combine": dict(bytes=r * G, flops=0),
-        "fft_forward": dict(bytes=r * G + c * H, flops=2.5 * G * np.log2(G)),
+        # cuFFT path
+        "fft_forward": dict(bytes=r * G + c * H, flops=2.5 * G * lg(G)),
         "scale_reduce": dict(bytes=c * H, flops=40 * H),
-        "fft_inverse_x3": dict(bytes=3 * (c * H + r * G), flops=3 * 2.5 * G * np.log2(G)),
+        "fft_inverse_x3": dict(bytes=3 * (c * H + r * G), flops=3 * 2.5 * G * lg(G)),
+        # band-pruned fused path (esp_fft.cu)
+        "fft_x": dict(bytes=r * G + c * My * Mz * nbx, flops=2.5 * G * lg(Mx)),
+        "fft_y": dict(bytes=c * Mz * nbx * (My + nby), flops=5 * Mz * nbx * My * lg(My)),
+        "fft_z_scale_reduce": dict(bytes=c * Mz * nby * nbx + (c + 16) * nbox,
+                                   flops=5 * nby * nbx * Mz * lg(Mz) + 40 * nbox),
+        "ifft_z_ik": dict(bytes=(c + 8) * nbox + 3 * c * Mz * nby * nbx,
+                          flops=3 * 5 * nby * nbx * Mz * lg(Mz)),
+        "ifft_y": dict(bytes=3 * c * Mz * nbx * (nby + My), flops=3 * 5 * Mz * nbx * My * lg(My)),
+        "ifft_x": dict(bytes=3 * (c * My * Mz * nbx + r * G), flops=3 * 2.5 * G * lg(Mx)),
         "gather": dict(bytes=pb * n + 3 * r * G + 3 * r * n,
                        flops=2 * (3 * P * D + P * P + 3 * P ** 3) * n),
     }
+
+
+def dram_traffic(workload, precision):
+    """Per-launch DRAM bytes (read + write) of each stage kernel, from the
+    ncu capture summarised by profiles/traffic.py."""
+    try:
+        with open(os.path.join(REPO, "profiles", "dram_traffic.json")) as f:
+            return json.load(f).get(f"{workload}/{precision}", {})
+    except Exception:
+        return {}
 
 
 def measured_peaks():
@@ -265,11 +297,12 @@ def run_ours(args):
     fp64_tflops = probe_fp64_tflops()
     hbm_peak, peak_kind = measured_peaks()
     real_b = 8 if args.precision == "fp64" else 4
-    alg = algorithmic(w, n, real_b)
+    alg = algorithmic(w, n, solver.plan.tables.band, real_b)
     kern = {k: v for k, v in prof.items() if k in alg}
     dom = max(kern, key=kern.get) if kern else None
     roof = None
     roof_fp = None
+    line_smem = None
     if dom:
         t = kern[dom] * 1e-3
         ach = alg[dom]["bytes"] / t / 1e9
@@ -283,6 +316,24 @@ def run_ours(args):
                        "achieved": round(fl, 3), "peak": round(fp64_tflops, 2),
                        "unit": "TFLOP/s", "frac": round(fl / fp64_tflops, 4),
                        "peak_source": "measured DFMA-chain probe (esp_probe_fp64)"}
+
+        # measured DRAM bytes of the same kernel from the committed ncu capture
+        tr = dram_traffic(w.name, args.precision).get(dom)
+        if tr is not None:
+            roof["traffic"] = tr
+            roof["traffic_source"] = "profiles/dram_traffic.json (ncu --set full)"
+        if dom == "gather" and clocks.get("sm_mhz"):
+            # the gather is bound by shared-memory reads of the field tile:
+            # 3 fields x P^3 points x real bytes per charge
+            sm_bytes = 3 * w.P ** 3 * real_b * n
+            peak_sm = 148 * 128 * clocks["sm_mhz"] * 1e6 / 1e9
+            ach_sm = sm_bytes / t / 1e9
+            line_smem = {"kernel": dom, "bound": "smem", "achieved": round(ach_sm, 1),
+                         "peak": round(peak_sm, 1), "unit": "GB/s",
+                         "frac": round(ach_sm / peak_sm, 4),
+                         "peak_source": "148 SMs x 128 B/clk x median SM clock"}
+        else:
+            line_smem = None
 
     value = world * n / (ms_fp * 1e-3)
     line = {
@@ -306,6 +357,7 @@ def run_ours(args):
         "clocks": clocks,
         "roofline": roof,
         "roofline_fp": roof_fp,
+        "roofline_smem": line_smem,
         "kernel_ms": {k: round(v, 5) for k, v in prof.items()},
         "fp64_peak_tflops_measured": round(fp64_tflops, 2),
     }
