@@ -183,7 +183,9 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   p->n_tiles = (long long)p->ntx * p->nty * p->ntz;
   // spread tiles share the x-y decomposition (and so the binning keys) but run
   // deeper in z on large grids: the scratch halo shrinks from (TZ+P-1)/TZ.
-  p->TZS = std::min(d->M[2] <= 128 ? p->TZ : std::max(p->TZ, 32), d->M[2]);
+  // small grids: shallow spread tiles (more tiles in flight; the extra
+  // scratch halo is L2-resident)
+  p->TZS = std::min(d->M[2] <= 128 ? 4 : std::max(p->TZ, 32), d->M[2]);
   if (const char* env = getenv("ESP_TILE_ZS")) {   // diagnostic override (tuning sweeps)
     const int v = atoi(env);
     if (v > 0) p->TZS = std::min(v, d->M[2]);

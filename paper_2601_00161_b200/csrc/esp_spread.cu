@@ -21,6 +21,8 @@
 //    point, the contributions of the (at most 8) covering tiles in a fixed
 //    order read from precomputed per-axis tables.  No atomics: results are
 //    bitwise reproducible.
+#include <cstdlib>
+
 #include "esp_internal.cuh"
 
 namespace esp {
@@ -222,6 +224,141 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_spread_warp (P <= 8, the production path): CTA = one tile, two warps.
+// Thread (x = t & 15, q = t >> 4) owns the 4 padded columns (x, 4q..4q+3)
+// and keeps a P-deep sliding z window for each (4 x P accumulators in
+// registers); warp w covers rows 8w..8w+7.  A charge is one visit of each
+// warp its stencil rows touch (a warp-uniform test, no lists): 4 products
+// wx * wy[r] and 4 x P independent FMAs per thread (columns the stencil
+// misses add exact zeros), so the instruction stream is dominated by FMAs.
+// Raw weight records are double-buffered in shared memory with cp.async; the
+// x/y weights are re-laid as zero-padded rows (weight s at OFF + s), so each
+// thread's weights are immediate-offset loads from one base.  Column owners
+// write each finished plane once: no atomics, bitwise reproducible.
+template <int P>
+struct WarpRow {
+  static constexpr int OFF = 16 - P;   // cx - xl + OFF >= 0 for every anchor of the tile
+  static constexpr int RL = 32 - P;    // covers cx - xl + OFF <= 31 - P
+};
+// ROWS = 4: 64 threads per tile (large grids); ROWS = 2: 128 threads per
+// tile, for grids with few tiles (more warps in flight per SM).
+__host__ __device__ constexpr int spread_warp_threads(int rows) { return 16 * (16 / rows); }
+
+template <typename real, int P, int ROWS>
+__global__ void __launch_bounds__(spread_warp_threads(ROWS))
+k_spread_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ wrec,
+              const int* __restrict__ PK, const double* __restrict__ Q,
+              real* __restrict__ scratch) {
+  static_assert(P <= 8, "warp spread: at most 8 stencil rows");
+  constexpr int NT = spread_warp_threads(ROWS);
+  constexpr int C = 32;                       // charges per staged chunk
+  constexpr int RS = rec_stride(P), KREC = 3 * RS;
+  constexpr int OFF = WarpRow<P>::OFF, RL = WarpRow<P>::RL;
+  __shared__ __align__(16) real s_raw[2][C * KREC];
+  __shared__ __align__(16) real s_row[C][2 * RL];
+  __shared__ int s_pk[2][C];
+  __shared__ __align__(16) double s_q[2][C];
+
+  const int tile = blockIdx.x;
+  const int tz = tile % g.ntzs;
+  const int txy = tile / g.ntzs;
+  const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZS;
+  const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZS);
+  const long long p0 = offsets[key0], p1 = offsets[key1];
+  const int tid = threadIdx.x;
+  real* blk = scratch + (size_t)tile * g.PZS * kPad * kPad;
+  if (p0 == p1) {  // empty tile: a zero block keeps k_combine branch-free
+    for (int i = tid; i < g.PZS * kPad * kPad; i += NT) blk[i] = real(0);
+    return;
+  }
+  // zero padding of the x/y rows is written once; chunks overwrite only the
+  // P weight slots
+  for (int i = tid; i < C * 2 * RL; i += NT) (&s_row[0][0])[i] = real(0);
+
+  auto fetch = [&](long long c0, int b) {
+    const int n = (int)min((long long)C, p1 - c0);
+    const int pieces = n * KREC * (int)sizeof(real) / 16;
+    const char* src = reinterpret_cast<const char*>(wrec + c0 * KREC);
+    for (int i = tid; i < pieces; i += NT) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(
+          reinterpret_cast<char*>(&s_raw[b][0]) + 16 * i);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 16 * i));
+    }
+    if (tid < n) {
+      const unsigned dpk = (unsigned)__cvta_generic_to_shared(&s_pk[b][tid]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dpk), "l"(PK + c0 + tid));
+    } else if (tid >= 32 && tid < 64 && tid - 32 < n) {
+      const unsigned dq = (unsigned)__cvta_generic_to_shared(&s_q[b][tid - 32]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dq),
+                   "l"(Q + c0 + tid - 32));
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+
+  // warp w covers rows [w * 2 ROWS, (w + 1) * 2 ROWS)
+  const int cx = tid & 15, ry0 = (tid >> 4) * ROWS, wy0 = (tid >> 5) * 2 * ROWS;
+  real* out = blk + (size_t)ry0 * kPad + cx;
+  constexpr size_t plane = (size_t)kPad * kPad;
+  real win[ROWS][P];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int s2 = 0; s2 < P; ++s2) win[r][s2] = real(0);
+  int zc = 0;
+  auto slide_to = [&](int zl) {   // planes < zl are final for these columns
+    while (zc < zl) {
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) out[(size_t)zc * plane + r * kPad] = win[r][0];
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+#pragma unroll
+        for (int s2 = 0; s2 < P - 1; ++s2) win[r][s2] = win[r][s2 + 1];
+        win[r][P - 1] = real(0);
+      }
+      ++zc;
+    }
+  };
+
+  int b = 0;
+  fetch(p0, 0);
+  for (long long c0 = p0; c0 < p1; c0 += C, b ^= 1) {
+    const int n = (int)min((long long)C, p1 - c0);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // padded x (q folded) and y rows of this chunk
+    for (int i = tid; i < n * 2 * P; i += NT) {
+      const int t = i / (2 * P), e = i - t * (2 * P);
+      const int d = e / P, sidx = e - d * P;
+      real v = s_raw[b][t * KREC + d * RS + sidx];
+      if (d == 0) v = (real)((double)v * s_q[b][t]);
+      s_row[t][d * RL + OFF + sidx] = v;
+    }
+    __syncthreads();
+    if (c0 + C < p1) fetch(c0 + C, b ^ 1);   // next chunk lands during this one
+    for (int t = 0; t < n; ++t) {
+      const int pk = s_pk[b][t];
+      const int xl = pk & 0xff, yl = (pk >> 8) & 0xff;
+      if (yl >= wy0 + 2 * ROWS || yl + P <= wy0) continue;   // warp-uniform: rows untouched
+      slide_to((pk >> 16) - tz * g.TZS);
+      const real wx = s_row[t][cx - xl + OFF];
+      const real* ry = &s_row[t][RL + ry0 - yl + OFF];
+      const real* rz = &s_raw[b][t * KREC + 2 * RS];
+      real wz[P];
+#pragma unroll
+      for (int s2 = 0; s2 < P; ++s2) wz[s2] = rz[s2];
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const real a = wx * ry[r];
+#pragma unroll
+        for (int s2 = 0; s2 < P; ++s2) win[r][s2] = fma(a, wz[s2], win[r][s2]);
+      }
+    }
+    __syncthreads();   // s_row / s_raw[b] are rewritten by the next chunks
+  }
+  slide_to(g.PZS);
+}
+
 template <typename real>
 __global__ void __launch_bounds__(256)
 k_combine(Geom g, CombineTabs ct, const real* __restrict__ scratch, real* __restrict__ grid) {
@@ -282,19 +419,35 @@ k_combine(Geom g, CombineTabs ct, const real* __restrict__ scratch, real* __rest
 template <typename real, int P>
 static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
   Geom g = make_geom(p);
-  const int chunk = p->M[2] <= 128 ? 128 : 64;
-  const size_t smem = SpreadLayout<real, P>::bytes(chunk);
-  static size_t attr_set = 0;  // set once per instantiation (capture-safe)
-  if (smem > attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_spread_tiles<real, P>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = smem;
+  static const bool legacy = std::getenv("ESP_SPREAD_LEGACY") != nullptr;   // A/B diagnostics
+  // k_spread_warp needs enough tiles to fill the SMs; tiny grids keep the
+  // 4-warp column-block kernel
+  if (P <= 8 && !legacy && p->n_tiles_s * 2 >= 148 * 4) {
+    constexpr int PW = P <= 8 ? P : 8;
+    if (p->n_tiles_s * 2 >= 148 * 12) {
+      k_spread_warp<real, PW, 4><<<(unsigned)p->n_tiles_s, spread_warp_threads(4), 0, s>>>(
+          g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
+          reinterpret_cast<real*>(p->d_scratch));
+    } else {
+      k_spread_warp<real, PW, 2><<<(unsigned)p->n_tiles_s, spread_warp_threads(2), 0, s>>>(
+          g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
+          reinterpret_cast<real*>(p->d_scratch));
+    }
+  } else {
+    const int chunk = p->M[2] <= 128 ? 128 : 64;
+    const size_t smem = SpreadLayout<real, P>::bytes(chunk);
+    static size_t attr_set = 0;  // set once per instantiation (capture-safe)
+    if (smem > attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(k_spread_tiles<real, P>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_set = smem;
+    }
+    k_spread_tiles<real, P><<<(unsigned)p->n_tiles_s, kSpreadThreads, smem, s>>>(
+        g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
+        reinterpret_cast<real*>(p->d_scratch), chunk);
   }
-  k_spread_tiles<real, P><<<(unsigned)p->n_tiles_s, kSpreadThreads, smem, s>>>(
-      g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
-      reinterpret_cast<real*>(p->d_scratch), chunk);
   p->launches++;
   prof_mark(p, s, "spread");
   CombineTabs ct;
