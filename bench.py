@@ -156,7 +156,18 @@ def box_counts(M, band):
     return nbx, nb[0], nb[1], (nbx + 7) // 8 * 8
 
 
-def algorithmic(w, n, band, real_bytes=8):
+def scratch_elems(w):
+    """Spread scratch blocks (esp_api.cu plan create): tiles of TX = TY = 17-P
+    anchors, TZS planes (4 on grids with Mz <= 128, else 32), padded 16 x 16
+    x (TZS + P - 1)."""
+    Mx, My, Mz = w.M
+    T = 17 - w.P
+    tzs = min(4 if Mz <= 128 else 32, Mz)
+    ntx, nty, ntz = -(-Mx // T), -(-My // T), -(-Mz // tzs)
+    return ntx * nty * ntz * (tzs + w.P - 1) * 256
+
+
+def algorithmic(w, n, band, real_bytes=8, n_scratch=None):
     """Compulsory HBM bytes and flops per launch of each stage kernel."""
     Mx, My, Mz = w.M
     G = Mx * My * Mz
@@ -165,10 +176,11 @@ def algorithmic(w, n, band, real_bytes=8):
     P, D = w.P, 18
     nbx, nby, nbz, _ = box_counts(w.M, band)
     nbox = nbx * nby * nbz
+    scratch = n_scratch if n_scratch is not None else G
     lg = np.log2
     return {
         "spread": dict(bytes=pb * n + r * G, flops=2 * (3 * P * D + P * P + P + P ** 3) * n),
-        "combine": dict(bytes=r * G, flops=0),
+        "combine": dict(bytes=r * (scratch + G), flops=0),   # tile blocks in, grid out
         # cuFFT path
         "fft_forward": dict(bytes=r * G + c * H, flops=2.5 * G * lg(G)),
         "scale_reduce": dict(bytes=c * H, flops=40 * H),
@@ -297,7 +309,7 @@ def run_ours(args):
     fp64_tflops = probe_fp64_tflops()
     hbm_peak, peak_kind = measured_peaks()
     real_b = 8 if args.precision == "fp64" else 4
-    alg = algorithmic(w, n, solver.plan.tables.band, real_b)
+    alg = algorithmic(w, n, solver.plan.tables.band, real_b, n_scratch=scratch_elems(w))
     kern = {k: v for k, v in prof.items() if k in alg}
     dom = max(kern, key=kern.get) if kern else None
     roof = None

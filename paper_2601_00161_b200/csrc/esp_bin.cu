@@ -23,21 +23,25 @@ namespace esp {
 // thread carries one copy of the 8 unrolled Horner chains).  The packed
 // anchor is written bytewise: x -> byte 0, y -> byte 1, z -> bytes 2-3.
 template <typename real, int P>
-__device__ __forceinline__ void write_record_dim(const Geom& g, const FastTab& ft,
-                                                 const real* __restrict__ tab,
-                                                 const double* __restrict__ brk,
-                                                 int n_pieces, int ncoef, int key, int d,
-                                                 double u, long long dst,
+__device__ __forceinline__ void record_dim_compute(const Geom& g, const FastTab& ft,
+                                                   const real* __restrict__ tab,
+                                                   const double* __restrict__ brk,
+                                                   int n_pieces, int ncoef, int d, double u,
+                                                   real (&w)[P], int& a) {
+  const double base = anchor_base(g, u);
+  stencil_weights<real, P>(ft, tab, brk, n_pieces, ncoef, u, base, g.lo, real(1), w);
+  a = local_anchor(g, d, base);
+}
+
+template <typename real, int P>
+__device__ __forceinline__ void record_dim_store(const Geom& g, int key, int d,
+                                                 const real (&w)[P], int a, long long dst,
                                                  real* __restrict__ wrec,
                                                  int* __restrict__ pk) {
   constexpr int RS = rec_stride(P);
-  const double base = anchor_base(g, u);
-  real w[P];
-  stencil_weights<real, P>(ft, tab, brk, n_pieces, ncoef, u, base, g.lo, real(1), w);
   real* out = wrec + dst * (3 * RS) + d * RS;
 #pragma unroll
   for (int s = 0; s < RS; ++s) out[s] = s < P ? w[s < P ? s : 0] : real(0);
-  const int a = local_anchor(g, d, base);
   unsigned char* pb = reinterpret_cast<unsigned char*>(pk + dst);
   if (d == 2) {
     *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
@@ -46,6 +50,20 @@ __device__ __forceinline__ void write_record_dim(const Geom& g, const FastTab& f
     const int org = d == 0 ? (txy % g.ntx) * g.TX : (txy / g.ntx) * g.TY;
     pb[d] = (unsigned char)(a - org);
   }
+}
+
+template <typename real, int P>
+__device__ __forceinline__ void write_record_dim(const Geom& g, const FastTab& ft,
+                                                 const real* __restrict__ tab,
+                                                 const double* __restrict__ brk,
+                                                 int n_pieces, int ncoef, int key, int d,
+                                                 double u, long long dst,
+                                                 real* __restrict__ wrec,
+                                                 int* __restrict__ pk) {
+  real w[P];
+  int a;
+  record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
+  record_dim_store<real, P>(g, key, d, w, a, dst, wrec, pk);
 }
 
 constexpr int kBinPerBlock = 32;   // particles per 96-thread binning block
@@ -156,23 +174,42 @@ k_bin_canon(Geom g, FastTab ft, const real* __restrict__ tab, const double* __re
   __shared__ long long s_dst[kBinPerBlock];
   const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
   const long long j = (long long)blockIdx.x * kBinPerBlock + l;
-  if (d == 0 && j < n) {
+  const bool live = j < n;
+  // rank by original index (warp 0); its loads are issued in batches of 8
+  if (d == 0 && live) {
     const int k = key_tmp[j];
     const int s0 = offsets[k], s1 = offsets[k + 1];
     const int me = idx_tmp[j];
     int rank = 0;
-    for (int t = s0; t < s1; ++t) rank += (idx_tmp[t] < me);
+    int t = s0;
+    for (; t + 8 <= s1; t += 8) {
+      int v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = idx_tmp[t + i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rank += (v[i] < me);
+    }
+    for (; t < s1; ++t) rank += (idx_tmp[t] < me);
     const long long dst = (long long)s0 + rank;
     s_dst[l] = dst;
     q_out[dst] = q_tmp[j];
     idx_out[dst] = me;
   }
+  // the record (weights, anchor) does not depend on the rank: warps 1-2 and
+  // warp 0 after its rank compute it before the barrier
+  double u = 0.0;
+  int key = 0, a = 0;
+  real w[P];
+  if (live) {
+    u = u_tmp[d * cap + j];
+    key = key_tmp[j];
+    record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
+  }
   __syncthreads();
-  if (j >= n) return;
+  if (!live) return;
   const long long dst = s_dst[l];
-  const double u = u_tmp[d * cap + j];
   u_out[d * cap + dst] = u;
-  write_record_dim<real, P>(g, ft, tab, brk, n_pieces, ncoef, key_tmp[j], d, u, dst, wrec, pk);
+  record_dim_store<real, P>(g, key, d, w, a, dst, wrec, pk);
 }
 
 // Non-deterministic mode: records straight after the atomic-slot scatter.

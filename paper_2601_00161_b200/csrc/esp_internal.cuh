@@ -217,6 +217,61 @@ struct CombineTabs {
   const int* cnt[3];
 };
 
+// Grid value at (x, y, z): the sum of the (at most 8) spread tile blocks
+// covering it, in a fixed (z, y, x) order (bitwise reproducible).  Used by
+// k_combine and, on the fused-transform path, by the x transform's loads.
+template <typename real>
+__device__ __forceinline__ double combine_at(const Geom& g, const CombineTabs& ct,
+                                             const real* __restrict__ scratch, int x, int y,
+                                             int z) {
+  const int nx = ct.cnt[0][x], ny = ct.cnt[1][y], nz = ct.cnt[2][z];
+  double acc = 0.0;
+  if (nx <= 2 && ny <= 2 && nz <= 2) {
+    // common case (each axis covered by <= 2 tiles): issue all <= 8 loads
+    // before summing, in the same fixed (z, y, x) order
+    long long addr[8];
+    bool use[8];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int ez = ct.ent[2][z * kCombW + (a < nz ? a : 0)];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int ey = ct.ent[1][y * kCombW + (b < ny ? b : 0)];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int ex = ct.ent[0][x * kCombW + (c < nx ? c : 0)];
+          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
+                                 (ez & 0xffff);
+          const int i = (a * 2 + b) * 2 + c;
+          addr[i] = ((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad + (ex >> 16);
+          use[i] = a < nz && b < ny && c < nx;
+        }
+      }
+    }
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = use[i] ? (double)scratch[addr[i]] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (use[i]) acc += v[i];
+  } else {
+    for (int a = 0; a < nz; ++a) {
+      const int ez = ct.ent[2][z * kCombW + a];
+      for (int b = 0; b < ny; ++b) {
+        const int ey = ct.ent[1][y * kCombW + b];
+        for (int c = 0; c < nx; ++c) {
+          const int ex = ct.ent[0][x * kCombW + c];
+          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
+                                 (ez & 0xffff);
+          acc += (double)scratch[((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad +
+                                 (ex >> 16)];
+        }
+      }
+    }
+  }
+  return acc;
+}
+
 template <typename T> struct Cplx;
 template <> struct Cplx<double> { using type = double2; };
 template <> struct Cplx<float> { using type = float2; };
@@ -312,7 +367,10 @@ Geom make_geom(const esp_plan* p);
 // Launchers (each returns cudaError_t of the launch).
 cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
                        long long n, cudaStream_t s);
-cudaError_t launch_spread(esp_plan* p, cudaStream_t s);
+// Tiles into the scratch blocks, then (with_combine) the halo combine into
+// d_grid.
+cudaError_t launch_spread(esp_plan* p, cudaStream_t s, bool with_combine = true);
+CombineTabs combine_tabs(const esp_plan* p);
 cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
                                 cudaStream_t s);
 // Output placement of the 3 gathered values of particle id:

@@ -368,56 +368,20 @@ k_combine(Geom g, CombineTabs ct, const real* __restrict__ scratch, real* __rest
   const int x = (int)(gid % g.M[0]);
   const int y = (int)((gid / g.M[0]) % g.M[1]);
   const int z = (int)(gid / ((long long)g.M[0] * g.M[1]));
-  const int nx = ct.cnt[0][x], ny = ct.cnt[1][y], nz = ct.cnt[2][z];
-  double acc = 0.0;
-  if (nx <= 2 && ny <= 2 && nz <= 2) {
-    // common case (each axis covered by <= 2 tiles): issue all <= 8 loads
-    // before summing, in the same fixed (z, y, x) order
-    long long addr[8];
-    bool use[8];
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int ez = ct.ent[2][z * kCombW + (a < nz ? a : 0)];
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const int ey = ct.ent[1][y * kCombW + (b < ny ? b : 0)];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int ex = ct.ent[0][x * kCombW + (c < nx ? c : 0)];
-          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
-                                 (ez & 0xffff);
-          const int i = (a * 2 + b) * 2 + c;
-          addr[i] = ((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad + (ex >> 16);
-          use[i] = a < nz && b < ny && c < nx;
-        }
-      }
-    }
-    double v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = use[i] ? (double)scratch[addr[i]] : 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (use[i]) acc += v[i];
-  } else {
-    for (int a = 0; a < nz; ++a) {
-      const int ez = ct.ent[2][z * kCombW + a];
-      for (int b = 0; b < ny; ++b) {
-        const int ey = ct.ent[1][y * kCombW + b];
-        for (int c = 0; c < nx; ++c) {
-          const int ex = ct.ent[0][x * kCombW + c];
-          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
-                                 (ez & 0xffff);
-          acc += (double)scratch[((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad +
-                                 (ex >> 16)];
-        }
-      }
-    }
+  grid[gid] = (real)combine_at(g, ct, scratch, x, y, z);
+}
+
+CombineTabs combine_tabs(const esp_plan* p) {
+  CombineTabs ct;
+  for (int d = 0; d < 3; ++d) {
+    ct.ent[d] = p->d_comb_ent + kCombW * p->comb_off[d];
+    ct.cnt[d] = p->d_comb_cnt + p->comb_off[d];
   }
-  grid[gid] = (real)acc;
+  return ct;
 }
 
 template <typename real, int P>
-static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
+static cudaError_t spread_p(esp_plan* p, cudaStream_t s, bool with_combine) {
   Geom g = make_geom(p);
   static const bool legacy = std::getenv("ESP_SPREAD_LEGACY") != nullptr;   // A/B diagnostics
   // k_spread_warp needs enough tiles to fill the SMs; tiny grids keep the
@@ -450,11 +414,8 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
   }
   p->launches++;
   prof_mark(p, s, "spread");
-  CombineTabs ct;
-  for (int d = 0; d < 3; ++d) {
-    ct.ent[d] = p->d_comb_ent + kCombW * p->comb_off[d];
-    ct.cnt[d] = p->d_comb_cnt + p->comb_off[d];
-  }
+  if (!with_combine) return cudaGetLastError();
+  const CombineTabs ct = combine_tabs(p);
   const int B = 256;
   k_combine<real><<<(unsigned)((p->G + B - 1) / B), B, 0, s>>>(
       g, ct, reinterpret_cast<const real*>(p->d_scratch), reinterpret_cast<real*>(p->d_grid));
@@ -464,25 +425,26 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s) {
 }
 
 template <typename real>
-static cudaError_t spread_r(esp_plan* p, cudaStream_t s) {
+static cudaError_t spread_r(esp_plan* p, cudaStream_t s, bool with_combine) {
   switch (p->P) {
-    case 2: return spread_p<real, 2>(p, s);
-    case 3: return spread_p<real, 3>(p, s);
-    case 4: return spread_p<real, 4>(p, s);
-    case 5: return spread_p<real, 5>(p, s);
-    case 6: return spread_p<real, 6>(p, s);
-    case 7: return spread_p<real, 7>(p, s);
-    case 8: return spread_p<real, 8>(p, s);
-    case 9: return spread_p<real, 9>(p, s);
-    case 10: return spread_p<real, 10>(p, s);
-    case 11: return spread_p<real, 11>(p, s);
-    case 12: return spread_p<real, 12>(p, s);
+    case 2: return spread_p<real, 2>(p, s, with_combine);
+    case 3: return spread_p<real, 3>(p, s, with_combine);
+    case 4: return spread_p<real, 4>(p, s, with_combine);
+    case 5: return spread_p<real, 5>(p, s, with_combine);
+    case 6: return spread_p<real, 6>(p, s, with_combine);
+    case 7: return spread_p<real, 7>(p, s, with_combine);
+    case 8: return spread_p<real, 8>(p, s, with_combine);
+    case 9: return spread_p<real, 9>(p, s, with_combine);
+    case 10: return spread_p<real, 10>(p, s, with_combine);
+    case 11: return spread_p<real, 11>(p, s, with_combine);
+    case 12: return spread_p<real, 12>(p, s, with_combine);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_spread(esp_plan* p, cudaStream_t s) {
-  return p->precision == ESP_FP64 ? spread_r<double>(p, s) : spread_r<float>(p, s);
+cudaError_t launch_spread(esp_plan* p, cudaStream_t s, bool with_combine) {
+  return p->precision == ESP_FP64 ? spread_r<double>(p, s, with_combine)
+                                  : spread_r<float>(p, s, with_combine);
 }
 
 // Host-side construction of the combine tables: for each coordinate c along
