@@ -78,11 +78,7 @@ __global__ void k_bin_count(const double* __restrict__ pos, long long n, Geom g,
   int a[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double b = anchor_base(g, u[d]);
-    // Clamp pathological (non-finite / huge) coordinates into range; the
-    // reference's int64 cast would be undefined there as well.
-    b = fmin(fmax(b, -4.0e15), 4.0e15);
-    a[d] = local_anchor(g, d, b);
+    a[d] = local_anchor(g, d, anchor_base(g, u[d]));
   }
   const int tx = a[0] / g.TX, ty = a[1] / g.TY;
   const int k = (ty * g.ntx + tx) * g.M[2] + a[2];
@@ -102,9 +98,7 @@ __global__ void k_bin_keys(const double* __restrict__ pos, long long n, Geom g,
   int a[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double b = anchor_base(g, u[d]);
-    b = fmin(fmax(b, -4.0e15), 4.0e15);
-    a[d] = local_anchor(g, d, b);
+    a[d] = local_anchor(g, d, anchor_base(g, u[d]));
   }
   const int k = ((a[1] / g.TY) * g.ntx + a[0] / g.TX) * g.M[2] + a[2];
   key[i] = k;

@@ -79,8 +79,12 @@ __device__ __forceinline__ double grid_coord(const Geom& g, int d, double x, dou
 
 // Stencil anchor: np.round (half-to-even) for odd P, np.floor for even P
 // (mesh.py:161-168).
+// Non-finite or huge coordinates are clamped (fmax/fmin drop NaN) so that
+// every pass derives the same in-range anchor; finite |u| < 4e15 is unchanged.
+// The reference's int64 cast is undefined there too (mesh.py:160-168).
 __device__ __forceinline__ double anchor_base(const Geom& g, double u) {
-  return g.odd ? rint(u) : floor(u);
+  const double b = g.odd ? rint(u) : floor(u);
+  return fmin(fmax(b, -4.0e15), 4.0e15);
 }
 
 __device__ __forceinline__ int wrap_index(long long v, int M) {

@@ -179,8 +179,9 @@ class KSpaceSolver:
 class _HostStepper:
     def __init__(self, solver: "KSpaceSolver", n: int, want_forces: bool):
         f64 = torch.float64
-        self.positions = torch.empty((n, 3), dtype=f64).pin_memory()
-        self.charges = torch.empty(n, dtype=f64).pin_memory()
+        # zero-initialised: the graph warm-up runs before the caller fills them
+        self.positions = torch.zeros((n, 3), dtype=f64).pin_memory()
+        self.charges = torch.zeros(n, dtype=f64).pin_memory()
         self.forces = torch.empty((n, 3), dtype=f64).pin_memory()
         self.out7 = torch.empty(7, dtype=f64).pin_memory()
         self._d_pos = torch.empty((n, 3), dtype=f64, device="cuda")

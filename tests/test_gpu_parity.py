@@ -519,3 +519,28 @@ def test_unsupported_lengths_fall_back_to_cufft():
     oE, oP, oF = O.kspace(op, g["pos"], g["q"])
     assert O.rel_scalar(E, oE) <= F64_TOL
     assert O.rms_rel_forces(F, oF) <= F64_TOL
+
+
+def test_non_finite_and_huge_positions_do_not_fault():
+    """Garbage coordinates (NaN, inf, 1e300, random bit patterns) must not
+    fault the device path: every pass clamps the anchor base the same way,
+    so packed tile-local anchors stay inside their tile.  Finite charges
+    elsewhere keep finite outputs."""
+    torch = _torch()
+    g = golden("small_cube_p6")
+    plan = _plan_for(g, capacity=256)
+    pos = np.ascontiguousarray(g["pos"], dtype=np.float64)
+    for val in (np.nan, np.inf, -np.inf, 1e300, -1e300, 3e15, 1e-310):
+        p2 = pos.copy()
+        p2[::5, 0] = val
+        p2[::7, 2] = val
+        E, Pt, F = _run(plan, p2, g["q"])
+        torch.cuda.synchronize()
+        if not np.isnan(val):
+            assert np.isfinite(E)
+    bits = np.random.default_rng(3).integers(0, 2 ** 63, size=pos.shape, dtype=np.int64)
+    _run(plan, bits.view(np.float64), g["q"])
+    torch.cuda.synchronize()
+    # the plan is still healthy afterwards
+    E, Pt, F = _run(plan, g["pos"], g["q"])
+    assert O.rel_scalar(E, g["E"]) <= F64_TOL
