@@ -96,7 +96,10 @@ __device__ __forceinline__ int wrap_index(long long v, int M) {
 // anchor, shifted into the slab's local planes for z.
 __device__ __forceinline__ int local_anchor(const Geom& g, int d, double base) {
   const int a = wrap_index((long long)base, g.Mu[d]);
-  return d == 2 ? a - g.zshift : a;
+  if (d != 2 || g.zshift == 0 && g.M[2] == g.Mu[2]) return a;
+  // slab plans: a charge outside the slab (a caller error) is clamped onto
+  // the local planes so that keys and tile offsets stay in range
+  return min(max(a - g.zshift, 0), g.M[2] - 1);
 }
 
 // Periodic wrap for indices a few periods from [0, M): no division.
