@@ -62,6 +62,18 @@ __device__ __forceinline__ real warp_reduce3(real v0, real v1, real v2, int lane
 }
 
 
+template <typename real> struct Vec16;
+template <> struct Vec16<double> {
+  using type = double2;
+  __device__ static void split(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
+};
+template <> struct Vec16<float> {
+  using type = float4;
+  __device__ static void split(const float4& v, float* o) {
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+};
+
 template <typename real> struct Real2;
 template <> struct Real2<double> { using type = double2; };
 template <> struct Real2<float> { using type = float2; };
@@ -201,11 +213,16 @@ k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
       const int pk = pk_c;
       const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = (pk >> 16) - tz * g.TZ;
       const real* W = ring + ((size_t)buf * 2 + slot) * kRec;
-      real wx[P], wy[P];
+      real wx[RS], wy[RS];
+      // 16-byte loads of the x and y weight rows (records are 16 B aligned)
+      using V = typename Vec16<real>::type;
+      constexpr int kPer = 16 / (int)sizeof(real);
 #pragma unroll
-      for (int s = 0; s < P; ++s) {
-        wx[s] = W[s];
-        wy[s] = W[RS + s];
+      for (int c = 0; c < RS / kPer; ++c) {
+        const V a = reinterpret_cast<const V*>(W)[c];
+        const V b = reinterpret_cast<const V*>(W + RS)[c];
+        Vec16<real>::split(a, wx + c * kPer);
+        Vec16<real>::split(b, wy + c * kPer);
       }
       const real wzk = W[2 * RS + k];
       const R2* rowp = s_f01 + (zl + k) * kPlane + (yl + h) * kPad + xl;
