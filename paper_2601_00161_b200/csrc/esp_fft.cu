@@ -723,6 +723,107 @@ k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
 }
 
 // ---------------------------------------------------------------------------
+// Small square planes (Mx == My <= 64): the x and y passes of one z plane in
+// ONE CTA (the whole plane fits in shared memory), forward and inverse.  Two
+// passes and two global round trips fewer on the latency-bound small grids.
+
+// P1+P2: plane z -> out[(z*nby + by)*ldx + kx] (kx >= nbx written as zero).
+template <typename real, int N>
+__global__ void __launch_bounds__(256)
+k_xy_fwd(const real* __restrict__ grid, typename Cx<real>::t* __restrict__ out,
+         const typename Cx<real>::t* __restrict__ tw, int ldx, int nbx, int nby) {
+  using C = typename Cx<real>::t;
+  constexpr int LP = pitch(N), NH = N / 2 + 1, NP = N / 2, NT = 256;
+  extern __shared__ __align__(16) unsigned char sm[];
+  C* A = reinterpret_cast<C*>(sm);          // NP row pairs x N (x along the line)
+  C* B = A + NP * LP;                       // NH kx columns x N (y along the line)
+  const real* g = grid + (long long)blockIdx.x * N * N;
+  for (int e = threadIdx.x; e < NP * N; e += NT) {
+    const int pr = e / N, x = e - pr * N;
+    C z;
+    z.x = __ldcs(g + (2 * pr) * N + x);
+    z.y = __ldcs(g + (2 * pr + 1) * N + x);
+    A[pr * LP + pidx(x)] = z;
+  }
+  __syncthreads();
+  fft_ip<N, 1, NP, NT, -1>(A, tw);
+  for (int e = threadIdx.x; e < NP * NH; e += NT) {
+    const int pr = e / NH, k = e - pr * NH;
+    C a, b;
+    a.x = a.y = b.x = b.y = real(0);
+    if (k < nbx) {
+      const C zk = A[pr * LP + pidx(k)], zm = A[pr * LP + pidx((N - k) % N)];
+      a.x = real(0.5) * (zk.x + zm.x);
+      a.y = real(0.5) * (zk.y - zm.y);
+      b.x = real(0.5) * (zk.y + zm.y);
+      b.y = real(-0.5) * (zk.x - zm.x);
+    }
+    B[k * LP + pidx(2 * pr)] = a;
+    B[k * LP + pidx(2 * pr + 1)] = b;
+  }
+  __syncthreads();
+  fft_ip<N, 1, NH, NT, -1>(B, tw);
+  C* dst = out + (long long)blockIdx.x * nby * ldx;
+  for (int e = threadIdx.x; e < nby * ldx; e += NT) {
+    const int by = e / ldx, kx = e - by * ldx;
+    C v;
+    v.x = v.y = real(0);
+    if (kx < nbx) v = B[kx * LP + pidx(band_mode(by, nby, N))];
+    dst[e] = v;
+  }
+}
+
+// P4+P5: plane cz = comp*Mz + z: in[(cz*nby + by)*ldx + kx] -> real rows of
+// field comp.
+template <typename real, int N>
+__global__ void __launch_bounds__(256)
+k_yx_inv(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
+         const typename Cx<real>::t* __restrict__ tw, int ldx, int nbx, int nby) {
+  using C = typename Cx<real>::t;
+  constexpr int LP = pitch(N), NH = N / 2 + 1, NP = N / 2, NT = 256, half = N / 2;
+  extern __shared__ __align__(16) unsigned char sm[];
+  C* A = reinterpret_cast<C*>(sm);
+  C* B = A + NP * LP;
+  const C* src = in + (long long)blockIdx.x * nby * ldx;
+  for (int e = threadIdx.x; e < NH * N; e += NT) {   // B[kx][y], zero outside the band
+    const int k = e / N, y = e - k * N;
+    const int by = band_index(y, nby, N);
+    C v;
+    v.x = v.y = real(0);
+    if (k < nbx && by >= 0) v = src[by * ldx + k];
+    B[k * LP + pidx(y)] = v;
+  }
+  __syncthreads();
+  fft_ip<N, 1, NH, NT, +1>(B, tw);
+  for (int e = threadIdx.x; e < NP * N; e += NT) {   // Z = A + i B rows, Hermitian extension
+    const int pr = e / N, k = e - pr * N;
+    const int kk = k <= half ? k : N - k;
+    C a = B[kk * LP + pidx(2 * pr)], b = B[kk * LP + pidx(2 * pr + 1)];
+    if (kk == 0 || kk == half) {
+      a.y = real(0);
+      b.y = real(0);
+    }
+    if (k > half) {
+      a.y = -a.y;
+      b.y = -b.y;
+    }
+    C z;
+    z.x = a.x - b.y;
+    z.y = a.y + b.x;
+    A[pr * LP + pidx(k)] = z;
+  }
+  __syncthreads();
+  fft_ip<N, 1, NP, NT, +1>(A, tw);
+  real* f = fld + (long long)blockIdx.x * N * N;
+  for (int e = threadIdx.x; e < NP * N; e += NT) {
+    const int pr = e / N, x = e - pr * N;
+    const C z = A[pr * LP + pidx(x)];
+    __stcs(f + (2 * pr) * N + x, z.x);
+    __stcs(f + (2 * pr + 1) * N + x, z.y);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host side
 
 static bool supported(int n) {
@@ -850,6 +951,40 @@ static cudaError_t launch_x_c2r(const esp_plan* p, const void* in, void* fld, co
   return cudaGetLastError();
 }
 
+template <typename real, int N>
+static size_t plane_smem() {
+  using C = typename Cx<real>::t;
+  return sizeof(C) * (size_t)(N / 2 + N / 2 + 1) * pitch(N);
+}
+
+template <typename real, int N>
+static cudaError_t launch_xy_fwd(const esp_plan* p, void* out, const void* tw, int ldx,
+                                 cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  const size_t smem = plane_smem<real, N>();
+  cudaError_t e = cudaFuncSetAttribute(k_xy_fwd<real, N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_xy_fwd<real, N><<<(unsigned)p->M[2], 256, smem, s>>>(
+      reinterpret_cast<const real*>(p->d_grid), reinterpret_cast<C*>(out),
+      reinterpret_cast<const C*>(tw), ldx, p->nbx, p->nby);
+  return cudaGetLastError();
+}
+
+template <typename real, int N>
+static cudaError_t launch_yx_inv(const esp_plan* p, const void* in, const void* tw, int ldx,
+                                 cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  const size_t smem = plane_smem<real, N>();
+  cudaError_t e = cudaFuncSetAttribute(k_yx_inv<real, N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_yx_inv<real, N><<<(unsigned)(3 * p->M[2]), 256, smem, s>>>(
+      reinterpret_cast<const C*>(in), reinterpret_cast<real*>(p->d_fields),
+      reinterpret_cast<const C*>(tw), ldx, p->nbx, p->nby);
+  return cudaGetLastError();
+}
+
 }  // namespace fft
 
 struct FusedFft {
@@ -940,27 +1075,43 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   using namespace fft;
   cudaError_t e = cudaErrorInvalidValue;
   const int ldx = f->ldx;
-  switch (p->M[0]) {
+  // small square planes: x and y in one kernel per plane
+  static const bool no_plane = std::getenv("ESP_FFT_NO_PLANE") != nullptr;   // A/B diagnostics
+  const bool plane = !no_plane && p->M[0] == p->M[1] &&
+                     (p->M[0] == 32 || p->M[0] == 48 || p->M[0] == 64);
+  if (plane) {
+    switch (p->M[0]) {
+      case 32: e = launch_xy_fwd<real, 32>(p, f->bufB, f->tw[0], ldx, s); break;
+      case 48: e = launch_xy_fwd<real, 48>(p, f->bufB, f->tw[0], ldx, s); break;
+      case 64: e = launch_xy_fwd<real, 64>(p, f->bufB, f->tw[0], ldx, s); break;
+    }
+    if (e != cudaSuccess) return e;
+    p->launches++;
+    prof_mark(p, s, "fft_xy");
+    if ((e = debug_check(s, "fft_xy")) != cudaSuccess) return e;
+  } else {
+    switch (p->M[0]) {
 #define ESP_CASE(v) \
   case v: e = launch_x_r2c<real, v>(p, p->d_grid, f->bufA, f->tw[0], ldx, s); break;
-    ESP_FFT_SIZES(ESP_CASE)
+      ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
-  }
-  if (e != cudaSuccess) return e;
-  p->launches++;
-  prof_mark(p, s, "fft_x");
-  if ((e = debug_check(s, "fft_x")) != cudaSuccess) return e;
-  e = cudaErrorInvalidValue;
-  switch (p->M[1]) {
+    }
+    if (e != cudaSuccess) return e;
+    p->launches++;
+    prof_mark(p, s, "fft_x");
+    if ((e = debug_check(s, "fft_x")) != cudaSuccess) return e;
+    e = cudaErrorInvalidValue;
+    switch (p->M[1]) {
 #define ESP_CASE(v) \
   case v: e = launch_y_fwd<real, v>(p, f->bufA, f->bufB, f->tw[1], ldx, s); break;
-    ESP_FFT_SIZES(ESP_CASE)
+      ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
+    }
+    if (e != cudaSuccess) return e;
+    p->launches++;
+    prof_mark(p, s, "fft_y");
+    if ((e = debug_check(s, "fft_y")) != cudaSuccess) return e;
   }
-  if (e != cudaSuccess) return e;
-  p->launches++;
-  prof_mark(p, s, "fft_y");
-  if ((e = debug_check(s, "fft_y")) != cudaSuccess) return e;
   FusedArgs fa;
   for (int d = 0; d < 3; ++d) {
     fa.M[d] = p->M[d];
@@ -1005,6 +1156,18 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   p->launches++;
   prof_mark(p, s, "ifft_z_ik");
   if ((e = debug_check(s, "ifft_z_ik")) != cudaSuccess) return e;
+  if (plane) {
+    e = cudaErrorInvalidValue;
+    switch (p->M[0]) {
+      case 32: e = launch_yx_inv<real, 32>(p, f->bufC, f->tw[0], ldx, s); break;
+      case 48: e = launch_yx_inv<real, 48>(p, f->bufC, f->tw[0], ldx, s); break;
+      case 64: e = launch_yx_inv<real, 64>(p, f->bufC, f->tw[0], ldx, s); break;
+    }
+    if (e != cudaSuccess) return e;
+    p->launches++;
+    prof_mark(p, s, "ifft_yx");
+    return debug_check(s, "ifft_yx");
+  }
   e = cudaErrorInvalidValue;
   switch (p->M[1]) {
 #define ESP_CASE(v) \
