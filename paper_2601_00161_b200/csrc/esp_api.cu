@@ -410,14 +410,19 @@ int esp_plan_set_cell(esp_plan* p, const esp_cell_desc* c, void* stream) {
   ESP_CUDA(dalloc(&p->d_partials, (size_t)p->n_red_blocks * 8));
   // band-pruned fused transforms for esp_evaluate (full-grid plans whose
   // lengths factor into 2s and 3s; ESP_FFT=cufft keeps the cuFFT path)
-  esp_fused_fft_destroy(p->fused);
-  p->fused = nullptr;
-  if (p->d_partials_fft) cudaFree(p->d_partials_fft);
-  p->d_partials_fft = nullptr;
+  // (a cell change that keeps the in-band box keeps the buffers: NPT loops
+  // rebind the cell every step)
   {
     const char* env = std::getenv("ESP_FFT");
     const bool want = !(env && std::string(env) == "cufft");
-    if (want && p->Mu[2] == p->M[2] && p->zshift == 0) {
+    const bool keep = want && p->fused && esp_fused_fft_matches(p->fused, p);
+    if (!keep) {
+      esp_fused_fft_destroy(p->fused);
+      p->fused = nullptr;
+      if (p->d_partials_fft) cudaFree(p->d_partials_fft);
+      p->d_partials_fft = nullptr;
+    }
+    if (!keep && want && p->Mu[2] == p->M[2] && p->zshift == 0) {
       p->fused = esp_fused_fft_create(p);
       if (p->fused) {
         p->n_red_blocks_fft = esp::fused_reduce_blocks(p);

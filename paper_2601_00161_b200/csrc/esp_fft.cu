@@ -994,6 +994,7 @@ struct FusedFft {
   void* bufC;   // ik pencils    [3][Mz][nby][ldx]
   void* bufD;   // y-inverse     [3][Mz][My][ldx]
   int ldx, nbx, nby, nbz;
+  bool fp64;
 };
 
 }  // namespace esp
@@ -1010,6 +1011,12 @@ void esp_fused_fft_destroy(void* h) {
   if (f->bufC) cudaFree(f->bufC);
   if (f->bufD) cudaFree(f->bufD);
   delete f;
+}
+
+bool esp_fused_fft_matches(const void* h, const esp_plan* p) {
+  const auto* f = reinterpret_cast<const FusedFft*>(h);
+  return f && f->nbx == p->nbx && f->nby == p->nby && f->nbz == p->nbz &&
+         f->fp64 == (p->precision == ESP_FP64);
 }
 
 // Build the fused transform for the plan's grid and current box; nullptr if a
@@ -1036,6 +1043,7 @@ void* esp_fused_fft_create(esp_plan* p) {
   f->nbx = p->nbx;
   f->nby = p->nby;
   f->nbz = p->nbz;
+  f->fp64 = p->precision == ESP_FP64;
   f->ldx = (p->nbx + 7) / 8 * 8;
   const long long My = p->M[1], Mz = p->M[2], ldx = f->ldx;
   if (cudaMalloc(&f->bufA, cs * Mz * My * ldx) != cudaSuccess ||

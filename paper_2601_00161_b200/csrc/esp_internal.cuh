@@ -415,3 +415,4 @@ inline void prof_mark(esp_plan* p, cudaStream_t s, const char* name) {
 // factor other than 2 or 3, or for slab plans).
 void* esp_fused_fft_create(esp_plan* p);
 void esp_fused_fft_destroy(void* f);
+bool esp_fused_fft_matches(const void* f, const esp_plan* p);   // same in-band box

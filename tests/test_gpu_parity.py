@@ -544,3 +544,30 @@ def test_non_finite_and_huge_positions_do_not_fault():
     # the plan is still healthy afterwards
     E, Pt, F = _run(plan, g["pos"], g["q"])
     assert O.rel_scalar(E, g["E"]) <= F64_TOL
+
+
+def test_fused_path_empty_system_and_cell_rebind():
+    """Fused / plane transform path (48^3): an empty system gives zeros, and
+    NPT-style rebinds (same band: buffers kept; new band: rebuilt) match the
+    oracle for each new cell."""
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    g = golden("small_cube_p6")
+    M = tuple(int(m) for m in g["M"])
+    s = KSpaceSolver(g["h"], EwaldParameters(r_c=float(g["r_c"]), delta_split=float(g["delta"]),
+                                             P=int(g["P"]), fixed_M=M), capacity=256)
+    assert s.plan.fft_path == "fused"
+    empty = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    out7, _ = s.plan.evaluate(empty, torch.zeros(0, dtype=torch.float64, device="cuda"),
+                              want_forces=True)
+    assert torch.count_nonzero(out7).item() == 0
+    for scale in (1.0, 1.002, 0.97, 1.05):
+        h = np.asarray(g["h"]) * scale
+        s.rebind_cell(h)
+        pos = np.asarray(g["pos"]) * scale
+        r = s.evaluate(pos, g["q"])
+        op = O.make_plan(h, M, int(g["P"]), float(g["delta"]), float(g["r_c"]))
+        oE, oP, oF = O.kspace(op, pos, g["q"])
+        assert O.rel_scalar(r.energy, oE) <= F64_TOL
+        assert O.rel_frobenius(r.pressure, oP) <= F64_TOL
+        assert O.rms_rel_forces(r.forces, oF) <= F64_TOL
