@@ -171,6 +171,37 @@ int esp_set_spectrum(esp_plan* plan, const void* d_spectrum, void* stream);
  * 0 = cuFFT.  ESP_FFT=cufft in the environment forces 0 at set_cell. */
 int esp_fft_path(const esp_plan* plan);
 
+/* --- distributed z-slab transforms --------------------------- */
+/* Rank `rank` of `nranks` (<= 8) slabs of a full-grid plan whose
+ * esp_fft_path() is 1.  Planes are split by z_start (nranks+1 entries); the
+ * in-band ky rows are split evenly (esp_slab_layout).  The forward and
+ * backward transposes are fused into the transform kernels: they store
+ * straight into the destination rank's receive buffer, so fwd_peers[r] /
+ * back_peers[r] must be rank r's buffers mapped into this process (NVLink
+ * peer memory; on one GPU, plain device buffers).  Between the stages the
+ * caller orders the ranks (a stream-ordered barrier): forward ->
+ * barrier -> reduce -> barrier -> inverse.  Replaces the rfft2 /
+ * all_to_all / fft sequence of the slab orchestration. */
+typedef struct {
+  int32_t nranks, rank;
+  int32_t z_start[9];
+  void* fwd_peers[8];    /* rank r: [Mz][ny_r][ldx] complex (plan precision) */
+  void* back_peers[8];   /* rank r: [3][nz_r][nby][ldx] complex              */
+} esp_slab_desc;
+/* by_start (nranks+1 entries) and info4 = {ldx, nby, nbx, complex bytes}.  */
+int esp_slab_layout(const esp_plan* plan, int32_t nranks, int32_t* by_start, int64_t* info4);
+/* own planes [nz][My][Mx] (real) -> x, y passes -> every rank's fwd buffer */
+int esp_slab_forward(esp_plan* plan, const esp_slab_desc* d, const void* d_own, void* stream);
+/* this rank's fwd buffer -> z pass, this rank's share of [E, P_ab] into
+ * d_out7 (sum the ranks' out7 in rank order); want_ik: ik + inverse z ->
+ * every rank's back buffer */
+int esp_slab_reduce(esp_plan* plan, const esp_slab_desc* d, const void* d_recv_fwd,
+                    int32_t want_ik, double* d_out7, void* stream);
+/* this rank's back buffer -> inverse y, x -> the rank's three field slabs
+ * [3][nz][My][Mx] (unghosted)                                             */
+int esp_slab_inverse(esp_plan* plan, const esp_slab_desc* d, const void* d_recv_back,
+                     void* d_fields, void* stream);
+
 /* --- diagnostics (bench / roofline) ----------------------------------------- */
 /* Record a CUDA event after every stage kernel of esp_evaluate.            */
 int esp_set_profiling(esp_plan* plan, int32_t on);

@@ -35,6 +35,12 @@ ESP_FORCES_ANALYTIC = 4
 _dp = C.POINTER(C.c_double)
 
 
+class SlabDesc(C.Structure):
+    """esp_slab_desc (include/esp_b200.h)."""
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("z_start", C.c_int32 * 9),
+                ("fwd_peers", C.c_void_p * 8), ("back_peers", C.c_void_p * 8)]
+
+
 class PlanDesc(C.Structure):
     _fields_ = [
         ("M", C.c_int32 * 3),
@@ -116,6 +122,10 @@ def lib():
     L.esp_fields_ptr.restype = vp
     L.esp_grid_info.argtypes = [vp, C.POINTER(C.c_int64)]
     L.esp_fft_path.argtypes = [vp]
+    L.esp_slab_layout.argtypes = [vp, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+    L.esp_slab_forward.argtypes = [vp, C.POINTER(SlabDesc), vp, vp]
+    L.esp_slab_reduce.argtypes = [vp, C.POINTER(SlabDesc), vp, C.c_int32, vp, vp]
+    L.esp_slab_inverse.argtypes = [vp, C.POINTER(SlabDesc), vp, vp, vp]
     L.esp_set_spectrum.argtypes = [vp, vp, vp]
     L.esp_set_profiling.argtypes = [vp, C.c_int32]
     L.esp_profile_read.argtypes = [vp, C.c_char_p, C.c_int32, C.POINTER(C.c_double), C.c_int32]
@@ -131,6 +141,7 @@ EXPORTED = [
     "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
     "esp_gather_fields", "esp_fields_ptr", "esp_fft_path",
+    "esp_slab_layout", "esp_slab_forward", "esp_slab_reduce", "esp_slab_inverse",
 ]
 
 

@@ -736,6 +736,76 @@ void* esp_fields_ptr(esp_plan* p) { return p ? p->d_fields : nullptr; }
 
 int esp_fft_path(const esp_plan* p) { return p && p->fused ? 1 : 0; }
 
+static int check_slab(esp_plan* p, const esp_slab_desc* d) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (!d || d->nranks < 1 || d->nranks > 8 || d->rank < 0 || d->rank >= d->nranks) {
+    set_error("slab descriptor: 1..8 ranks and 0 <= rank < nranks");
+    return ESP_ERR_PARAM;
+  }
+  if (!p->fused) {
+    set_error("slab transforms need the fused transform path (esp_fft_path() == 1)");
+    return ESP_ERR_PLANNING;
+  }
+  if (d->z_start[0] != 0 || d->z_start[d->nranks] != p->M[2]) {
+    set_error("slab z_start must run from 0 to Mz");
+    return ESP_ERR_PARAM;
+  }
+  for (int r = 0; r < d->nranks; ++r)
+    if (d->z_start[r + 1] <= d->z_start[r]) {
+      set_error("slab z_start must be increasing");
+      return ESP_ERR_PARAM;
+    }
+  return ESP_OK;
+}
+
+int esp_slab_layout(const esp_plan* p, int32_t nranks, int32_t* by_start, int64_t* info4) {
+  if (!p || nranks < 1 || nranks > 8) {
+    set_error("slab layout: 1..8 ranks");
+    return ESP_ERR_PARAM;
+  }
+  if (!p->have_cell || !p->fused) {
+    set_error("slab layout needs a cell and the fused transform path");
+    return ESP_ERR_PLANNING;
+  }
+  int bs[9];
+  esp::slab_by_split(p->nby, nranks, bs);
+  if (by_start)
+    for (int r = 0; r <= nranks; ++r) by_start[r] = bs[r];
+  if (info4) {
+    info4[0] = esp::fused_ldx(p);
+    info4[1] = p->nby;
+    info4[2] = p->nbx;
+    info4[3] = p->precision == ESP_FP64 ? 16 : 8;
+  }
+  return ESP_OK;
+}
+
+int esp_slab_forward(esp_plan* p, const esp_slab_desc* d, const void* d_own, void* stream) {
+  int rc = check_slab(p, d);
+  if (rc) return rc;
+  ESP_CUDA(esp::slab_forward(p, d, d_own, (cudaStream_t)stream));
+  p->fwd_count++;
+  return ESP_OK;
+}
+
+int esp_slab_reduce(esp_plan* p, const esp_slab_desc* d, const void* d_recv_fwd, int32_t want_ik,
+                    double* d_out7, void* stream) {
+  int rc = check_slab(p, d);
+  if (rc) return rc;
+  ESP_CUDA(esp::slab_reduce(p, d, d_recv_fwd, want_ik, d_out7, (cudaStream_t)stream));
+  if (want_ik) p->inv_count += 3;
+  return ESP_OK;
+}
+
+int esp_slab_inverse(esp_plan* p, const esp_slab_desc* d, const void* d_recv_back, void* d_fields,
+                     void* stream) {
+  int rc = check_slab(p, d);
+  if (rc) return rc;
+  ESP_CUDA(esp::slab_inverse(p, d, d_recv_back, d_fields, (cudaStream_t)stream));
+  return ESP_OK;
+}
+
 int esp_grid_info(const esp_plan* p, int64_t* info) {
   if (!p || !info) return ESP_ERR_PARAM;
   info[0] = p->M[0];

@@ -304,12 +304,34 @@ k_x_r2c(const real* __restrict__ grid, typename Cx<real>::t* __restrict__ out,
   }
 }
 
+// Distributed (z-slab) layout of the fused transforms.  R == 0: one GPU.
+// Otherwise the in-band ky rows are split over the R ranks (by_start) and
+// the z planes too (z_start); the forward y pass and the ik pass store
+// straight into the destination rank's receive buffer (peers[r], reachable
+// over NVLink peer memory): forward buffers are [Mz][ny_r][ldx], backward
+// buffers [3][nz_r][nby][ldx].
+constexpr int kMaxRanks = 8;
+struct SlabMap {
+  int R;
+  int z0;                          // this rank's first global plane (forward pass)
+  int by_start[kMaxRanks + 1];
+  int z_start[kMaxRanks + 1];
+  void* peers[kMaxRanks];
+};
+
+__device__ __forceinline__ int slab_owner(const int* start, int R, int v) {
+  int r = 0;
+  while (r + 1 < R && v >= start[r + 1]) ++r;
+  return r;
+}
+
 // P2: y lines (z, kx) for kx < ldx: forward C2C, keep the nby in-band ky.
 // in[(z*N + y)*ldx + kx] -> out[(z*nby + by)*ldx + kx].
 template <typename real, int N>
 __global__ void __launch_bounds__(threads_yz<real>(N), 3)
 k_y_fwd(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ out,
-        const typename Cx<real>::t* __restrict__ tw, long long nlines, int ldx, int nby) {
+        const typename Cx<real>::t* __restrict__ tw, long long nlines, int ldx, int nby,
+        SlabMap smap) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
   constexpr int YS = NT / L, nld = N / YS;
@@ -333,9 +355,20 @@ k_y_fwd(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __res
   __syncthreads();
   fft_ip<N, 1, L, NT, -1>(buf, tw);
   if (!valid) return;
-  C* dst = out + z * (long long)nby * ldx + kx;
-  for (int by = threadIdx.x / L; by < nby; by += YS)
-    dst[(long long)by * ldx] = buf[l * LP + pidx(band_mode(by, nby, N))];
+  if (smap.R == 0) {
+    C* dst = out + z * (long long)nby * ldx + kx;
+    for (int by = threadIdx.x / L; by < nby; by += YS)
+      dst[(long long)by * ldx] = buf[l * LP + pidx(band_mode(by, nby, N))];
+  } else {   // transpose into the ky owner's buffer: [Mz][ny_r][ldx]
+    const long long zg = smap.z0 + z;
+    for (int by = threadIdx.x / L; by < nby; by += YS) {
+      const int r = slab_owner(smap.by_start, smap.R, by);
+      const int ny_r = smap.by_start[r + 1] - smap.by_start[r];
+      C* dst = reinterpret_cast<C*>(smap.peers[r]);
+      dst[(zg * ny_r + (by - smap.by_start[r])) * ldx + kx] =
+          buf[l * LP + pidx(band_mode(by, nby, N))];
+    }
+  }
 }
 
 struct FusedArgs {
@@ -349,6 +382,7 @@ struct FusedArgs {
   const double* modeB;
   double ik_scale;
   double escale, pscale;
+  int by0, npy;        // pencil rows by0 .. by0+npy-1 of the in-band box (one GPU: 0, nby)
 };
 
 // Deterministic two-level completion of a per-block reduction: block b has
@@ -356,13 +390,13 @@ struct FusedArgs {
 // sums the group's partials in block order (lane j <- block 32g + j, then a
 // fixed xor tree) into the group slot; the last group to finish sums the
 // group slots the same way and writes out7.  Counters re-arm themselves.
-// Layout: partials [nblk][8] | group sums [ng][8]; counters [ng + 1].
-__device__ __forceinline__ void tree_finish(double* partials, int* counters, double* out7,
-                                            double escale, double pscale) {
+// Layout (fixed by the allocated capacity, so launches of any size share
+// it): partials [cap][8] | group sums [cap_groups][8] | counters.
+__device__ __forceinline__ void tree_finish(double* partials, double* gsum, int* counters,
+                                            double* out7, double escale, double pscale) {
   __shared__ int s_flag;
   const int nb = gridDim.x, g = blockIdx.x >> 5, ng = (nb + 31) >> 5;
   const int gsize = min(32, nb - (g << 5));
-  double* gsum = partials + (size_t)nb * 8;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_flag = atomicAdd(counters + g, 1) == gsize - 1;
@@ -420,8 +454,8 @@ template <typename real, int N>
 __global__ void __launch_bounds__(threads_yz<real>(N), 3)
 k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ spec,
            const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines,
-           double* __restrict__ partials, int* __restrict__ counters,
-           double* __restrict__ out7) {
+           double* __restrict__ partials, double* __restrict__ gsum,
+           int* __restrict__ counters, double* __restrict__ out7) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
   constexpr int ZS = NT / L, nld = N / ZS;
@@ -429,15 +463,16 @@ k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __
   extern __shared__ __align__(16) unsigned char sm[];
   C* X = reinterpret_cast<C*>(sm);
   const int ldx = fa.ldx, nbx = fa.nbx, nby = fa.nby, nbz = fa.nbz;
-  const long long zstride = (long long)nby * ldx;
+  const long long zstride = (long long)fa.npy * ldx;
   const int l = threadIdx.x % L;
   const long long line = (long long)blockIdx.x * L + l;
   const bool valid = line < nlines;
   int by = 0, mx = 0, my = 0;
   bool live = false;
   auto pencil = [&]() {   // (by, kx) of this thread's line
-    by = valid ? (int)(line / ldx) : 0;
-    mx = valid ? (int)(line - (long long)by * ldx) : 0;
+    const int byl = valid ? (int)(line / ldx) : 0;
+    mx = valid ? (int)(line - (long long)byl * ldx) : 0;
+    by = fa.by0 + byl;
     live = valid && mx < nbx;
     my = band_mode(by, nby, fa.M[1]);
   };
@@ -565,7 +600,7 @@ k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __
     for (int w = 0; w < NW; ++w) s += red[w][threadIdx.x];
     partials[(size_t)blockIdx.x * 8 + threadIdx.x] = s;
   }
-  tree_finish(partials, counters, out7, fa.escale, fa.pscale);
+  tree_finish(partials, gsum, counters, out7, fa.escale, fa.pscale);
 }
 
 // P3b: ik pencils, one force component per blockIdx.y: i k_c A X h3/G on the
@@ -574,7 +609,8 @@ k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __
 template <typename real, int N>
 __global__ void __launch_bounds__(threads_yz<real>(N), 3)
 k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __restrict__ ik,
-       const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines) {
+       const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines,
+       SlabMap smap) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
   constexpr int ZS = NT / L, nld = N / ZS;
@@ -582,12 +618,13 @@ k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __re
   C* T = reinterpret_cast<C*>(sm);
   const int comp = blockIdx.y;
   const int ldx = fa.ldx, nbx = fa.nbx, nby = fa.nby, nbz = fa.nbz;
-  const long long zstride = (long long)nby * ldx;
+  const long long zstride = (long long)fa.npy * ldx;
   const int l = threadIdx.x % L;
   const long long line = (long long)blockIdx.x * L + l;
   const bool valid = line < nlines;
-  const int by = valid ? (int)(line / ldx) : 0;
-  const int mx = valid ? (int)(line - (long long)by * ldx) : 0;
+  const int byl = valid ? (int)(line / ldx) : 0;
+  const int mx = valid ? (int)(line - (long long)byl * ldx) : 0;
+  const int by = fa.by0 + byl;
   const bool live = valid && mx < nbx;
   const int my = band_mode(by, nby, fa.M[1]);
   const double* K = fa.axis_k + comp * fa.Msum;
@@ -613,11 +650,23 @@ k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __re
   __syncthreads();
   fft_ip<N, 1, L, NT, +1>(T, tw);
   if (!valid) return;
-  C* dst = ik + (long long)comp * N * zstride + line;
+  if (smap.R == 0) {
+    C* dst = ik + (long long)comp * N * zstride + line;
 #pragma unroll
-  for (int it = 0; it < nld; ++it) {
-    const int z = threadIdx.x / L + it * ZS;
-    __stcs(dst + (long long)z * zstride, T[l * LP + pidx(z)]);
+    for (int it = 0; it < nld; ++it) {
+      const int z = threadIdx.x / L + it * ZS;
+      __stcs(dst + (long long)z * zstride, T[l * LP + pidx(z)]);
+    }
+  } else {   // transpose back into the plane owner's buffer: [3][nz_r][nby][ldx]
+#pragma unroll 4
+    for (int it = 0; it < nld; ++it) {
+      const int z = threadIdx.x / L + it * ZS;
+      const int r = slab_owner(smap.z_start, smap.R, z);
+      const int nz_r = smap.z_start[r + 1] - smap.z_start[r];
+      C* dst = reinterpret_cast<C*>(smap.peers[r]);
+      dst[(((long long)comp * nz_r + (z - smap.z_start[r])) * nby + by) * ldx + mx] =
+          T[l * LP + pidx(z)];
+    }
   }
 }
 
@@ -858,10 +907,10 @@ static std::vector<double2> twiddles(int n) {
 
 template <typename real, int N>
 static cudaError_t launch_x_r2c(const esp_plan* p, const void* grid, void* out, const void* tw,
-                                int ldx, cudaStream_t s) {
+                                int ldx, int nz, cudaStream_t s) {
   using C = typename Cx<real>::t;
   constexpr int PP = pairs_x(N);
-  const long long nrows = (long long)p->M[1] * p->M[2];
+  const long long nrows = (long long)p->M[1] * nz;
   const long long nblk = (nrows + 2 * PP - 1) / (2 * PP);
   k_x_r2c<real, N><<<(unsigned)nblk, kThreadsX, 0, s>>>(
       reinterpret_cast<const real*>(grid), reinterpret_cast<C*>(out),
@@ -871,17 +920,17 @@ static cudaError_t launch_x_r2c(const esp_plan* p, const void* grid, void* out, 
 
 template <typename real, int N>
 static cudaError_t launch_y_fwd(const esp_plan* p, const void* in, void* out, const void* tw,
-                                int ldx, cudaStream_t s) {
+                                int ldx, int nz, const SlabMap& smap, cudaStream_t s) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N);
-  const long long nlines = (long long)p->M[2] * ldx;
+  const long long nlines = (long long)nz * ldx;
   const size_t smem = sizeof(C) * L * pitch(N);
   cudaError_t e = cudaFuncSetAttribute(k_y_fwd<real, N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_y_fwd<real, N><<<(unsigned)((nlines + L - 1) / L), threads_yz<real>(N), smem, s>>>(
       reinterpret_cast<const C*>(in), reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw),
-      nlines, ldx, p->nby);
+      nlines, ldx, p->nby, smap);
   return cudaGetLastError();
 }
 
@@ -895,39 +944,39 @@ static cudaError_t launch_z_reduce(const esp_plan* p, const void* in, const void
   cudaError_t e = cudaFuncSetAttribute(k_z_reduce<real, N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long nlines = (long long)p->nby * fa.ldx;
+  const long long nlines = (long long)fa.npy * fa.ldx;
   const long long nblk = (nlines + L - 1) / L;
   if (nblk > nblk_cap) return cudaErrorInvalidConfiguration;
   k_z_reduce<real, N><<<(unsigned)nblk, threads_yz<real>(N), smem, s>>>(
       reinterpret_cast<const C*>(in), reinterpret_cast<C*>(p->d_spec),
-      reinterpret_cast<const C*>(tw), fa, nlines, partials,
-      reinterpret_cast<int*>(partials + (nblk + (nblk + 31) / 32) * 8), out7);
+      reinterpret_cast<const C*>(tw), fa, nlines, partials, partials + nblk_cap * 8,
+      reinterpret_cast<int*>(partials + (nblk_cap + (nblk_cap + 31) / 32) * 8), out7);
   return cudaGetLastError();
 }
 
 template <typename real, int N>
 static cudaError_t launch_z_ik(const esp_plan* p, void* ik, const void* tw, const FusedArgs& fa,
-                               cudaStream_t s) {
+                               const SlabMap& smap, cudaStream_t s) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N);
   const size_t smem = sizeof(C) * L * pitch(N);
   cudaError_t e = cudaFuncSetAttribute(k_z_ik<real, N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long nlines = (long long)p->nby * fa.ldx;
+  const long long nlines = (long long)fa.npy * fa.ldx;
   const dim3 grid((unsigned)((nlines + L - 1) / L), 3);
   k_z_ik<real, N><<<grid, threads_yz<real>(N), smem, s>>>(
       reinterpret_cast<const C*>(p->d_spec), reinterpret_cast<C*>(ik),
-      reinterpret_cast<const C*>(tw), fa, nlines);
+      reinterpret_cast<const C*>(tw), fa, nlines, smap);
   return cudaGetLastError();
 }
 
 template <typename real, int N>
 static cudaError_t launch_y_inv(const esp_plan* p, const void* in, void* out, const void* tw,
-                                int ldx, cudaStream_t s) {
+                                int ldx, int nz, cudaStream_t s) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N);
-  const long long nlines = 3LL * p->M[2] * ldx;
+  const long long nlines = 3LL * nz * ldx;
   const size_t smem = sizeof(C) * L * pitch(N);
   cudaError_t e = cudaFuncSetAttribute(k_y_inv<real, N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -940,10 +989,10 @@ static cudaError_t launch_y_inv(const esp_plan* p, const void* in, void* out, co
 
 template <typename real, int N>
 static cudaError_t launch_x_c2r(const esp_plan* p, const void* in, void* fld, const void* tw,
-                                int ldx, cudaStream_t s) {
+                                int ldx, int nz, cudaStream_t s) {
   using C = typename Cx<real>::t;
   constexpr int PP = pairs_x(N);
-  const long long nrows = 3LL * p->M[1] * p->M[2];
+  const long long nrows = 3LL * p->M[1] * nz;
   const long long nblk = (nrows + 2 * PP - 1) / (2 * PP);
   k_x_c2r<real, N><<<(unsigned)nblk, kThreadsX, 0, s>>>(
       reinterpret_cast<const C*>(in), reinterpret_cast<real*>(fld),
@@ -1083,6 +1132,8 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   using namespace fft;
   cudaError_t e = cudaErrorInvalidValue;
   const int ldx = f->ldx;
+  SlabMap one;   // single-GPU layout
+  std::memset(&one, 0, sizeof(one));
   // small square planes: x and y in one kernel per plane
   static const bool no_plane = std::getenv("ESP_FFT_NO_PLANE") != nullptr;   // A/B diagnostics
   const bool plane = !no_plane && p->M[0] == p->M[1] &&
@@ -1100,7 +1151,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   } else {
     switch (p->M[0]) {
 #define ESP_CASE(v) \
-  case v: e = launch_x_r2c<real, v>(p, p->d_grid, f->bufA, f->tw[0], ldx, s); break;
+  case v: e = launch_x_r2c<real, v>(p, p->d_grid, f->bufA, f->tw[0], ldx, p->M[2], s); break;
       ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
     }
@@ -1111,7 +1162,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
     e = cudaErrorInvalidValue;
     switch (p->M[1]) {
 #define ESP_CASE(v) \
-  case v: e = launch_y_fwd<real, v>(p, f->bufA, f->bufB, f->tw[1], ldx, s); break;
+  case v: e = launch_y_fwd<real, v>(p, f->bufA, f->bufB, f->tw[1], ldx, p->M[2], one, s); break;
       ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
     }
@@ -1138,6 +1189,8 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   const double h3sq = p->h3 * p->h3;
   fa.escale = h3sq / (2.0 * p->volume);
   fa.pscale = h3sq / (2.0 * p->volume * p->volume);
+  fa.by0 = 0;
+  fa.npy = p->nby;
   e = cudaErrorInvalidValue;
   switch (p->M[2]) {
 #define ESP_CASE(v)                                                                       \
@@ -1156,7 +1209,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   e = cudaErrorInvalidValue;
   switch (p->M[2]) {
 #define ESP_CASE(v) \
-  case v: e = launch_z_ik<real, v>(p, f->bufC, f->tw[2], fa, s); break;
+  case v: e = launch_z_ik<real, v>(p, f->bufC, f->tw[2], fa, one, s); break;
     ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
   }
@@ -1179,7 +1232,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   e = cudaErrorInvalidValue;
   switch (p->M[1]) {
 #define ESP_CASE(v) \
-  case v: e = launch_y_inv<real, v>(p, f->bufC, f->bufD, f->tw[1], ldx, s); break;
+  case v: e = launch_y_inv<real, v>(p, f->bufC, f->bufD, f->tw[1], ldx, p->M[2], s); break;
     ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
   }
@@ -1190,7 +1243,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   e = cudaErrorInvalidValue;
   switch (p->M[0]) {
 #define ESP_CASE(v) \
-  case v: e = launch_x_c2r<real, v>(p, f->bufD, p->d_fields, f->tw[0], ldx, s); break;
+  case v: e = launch_x_c2r<real, v>(p, f->bufD, p->d_fields, f->tw[0], ldx, p->M[2], s); break;
     ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
   }
@@ -1199,6 +1252,153 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   prof_mark(p, s, "ifft_x");
   if ((e = debug_check(s, "ifft_x")) != cudaSuccess) return e;
   return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Distributed (z-slab) steps on a full-grid plan's fused transforms.
+
+static void slab_map(const esp_slab_desc* d, const int* by_start, int z0, void* const* peers,
+                     fft::SlabMap& m) {
+  std::memset(&m, 0, sizeof(m));
+  m.R = d->nranks;
+  m.z0 = z0;
+  for (int r = 0; r <= d->nranks; ++r) {
+    m.by_start[r] = by_start[r];
+    m.z_start[r] = d->z_start[r];
+  }
+  for (int r = 0; r < d->nranks; ++r) m.peers[r] = peers[r];
+}
+
+void slab_by_split(int nby, int R, int* by_start) {
+  by_start[0] = 0;
+  for (int r = 0; r < R; ++r) by_start[r + 1] = by_start[r] + nby / R + (r < nby % R ? 1 : 0);
+}
+
+template <typename real>
+static cudaError_t slab_forward_t(esp_plan* p, const esp_slab_desc* d, const void* own,
+                                  cudaStream_t s) {
+  using namespace fft;
+  auto* f = reinterpret_cast<FusedFft*>(p->fused);
+  const int r = d->rank, z0 = d->z_start[r], nz = d->z_start[r + 1] - z0;
+  int by_start[kMaxRanks + 1];
+  slab_by_split(p->nby, d->nranks, by_start);
+  SlabMap m;
+  slab_map(d, by_start, z0, d->fwd_peers, m);
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (p->M[0]) {
+#define ESP_CASE(v) \
+  case v: e = launch_x_r2c<real, v>(p, own, f->bufA, f->tw[0], f->ldx, nz, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  e = cudaErrorInvalidValue;
+  switch (p->M[1]) {
+#define ESP_CASE(v) \
+  case v: e = launch_y_fwd<real, v>(p, f->bufA, nullptr, f->tw[1], f->ldx, nz, m, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  p->launches += 2;
+  return e;
+}
+
+template <typename real>
+static cudaError_t slab_reduce_t(esp_plan* p, const esp_slab_desc* d, const void* recv,
+                                 int want_ik, double* d_out7, cudaStream_t s) {
+  using namespace fft;
+  auto* f = reinterpret_cast<FusedFft*>(p->fused);
+  int by_start[kMaxRanks + 1];
+  slab_by_split(p->nby, d->nranks, by_start);
+  FusedArgs fa;
+  for (int k = 0; k < 3; ++k) {
+    fa.M[k] = p->M[k];
+    fa.koff[k] = p->koff[k];
+  }
+  fa.nbx = p->nbx;
+  fa.nby = p->nby;
+  fa.nbz = p->nbz;
+  fa.ldx = f->ldx;
+  fa.Hx = p->Hx;
+  fa.Msum = (long long)p->M[0] + p->M[1] + p->M[2];
+  fa.axis_k = p->d_axis_k;
+  fa.modeA = p->d_modeA;
+  fa.modeB = p->d_modeB;
+  fa.ik_scale = p->h3 / (double)p->G;
+  const double h3sq = p->h3 * p->h3;
+  fa.escale = h3sq / (2.0 * p->volume);
+  fa.pscale = h3sq / (2.0 * p->volume * p->volume);
+  fa.by0 = by_start[d->rank];
+  fa.npy = by_start[d->rank + 1] - by_start[d->rank];
+  cudaError_t e = cudaErrorInvalidValue;
+  if (fa.npy == 0) {   // no ky rows on this rank: zero partial sums
+    e = cudaMemsetAsync(d_out7, 0, 7 * sizeof(double), s);
+  } else {
+    switch (p->M[2]) {
+#define ESP_CASE(v)                                                                        \
+  case v:                                                                                  \
+    e = launch_z_reduce<real, v>(p, recv, f->tw[2], fa, p->d_partials_fft,                \
+                                 p->n_red_blocks_fft, d_out7, s);                          \
+    break;
+      ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+    }
+  }
+  if (e != cudaSuccess || !want_ik || fa.npy == 0) return e;
+  SlabMap m;
+  slab_map(d, by_start, 0, d->back_peers, m);
+  e = cudaErrorInvalidValue;
+  switch (p->M[2]) {
+#define ESP_CASE(v) \
+  case v: e = launch_z_ik<real, v>(p, nullptr, f->tw[2], fa, m, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  p->launches += 2;
+  return e;
+}
+
+template <typename real>
+static cudaError_t slab_inverse_t(esp_plan* p, const esp_slab_desc* d, const void* recv,
+                                  void* fields, cudaStream_t s) {
+  using namespace fft;
+  auto* f = reinterpret_cast<FusedFft*>(p->fused);
+  const int r = d->rank, nz = d->z_start[r + 1] - d->z_start[r];
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (p->M[1]) {
+#define ESP_CASE(v) \
+  case v: e = launch_y_inv<real, v>(p, recv, f->bufD, f->tw[1], f->ldx, nz, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  if (e != cudaSuccess) return e;
+  e = cudaErrorInvalidValue;
+  switch (p->M[0]) {
+#define ESP_CASE(v) \
+  case v: e = launch_x_c2r<real, v>(p, f->bufD, fields, f->tw[0], f->ldx, nz, s); break;
+    ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+  }
+  p->launches += 2;
+  return e;
+}
+
+cudaError_t slab_forward(esp_plan* p, const esp_slab_desc* d, const void* own, cudaStream_t s) {
+  return p->precision == ESP_FP64 ? slab_forward_t<double>(p, d, own, s)
+                                  : slab_forward_t<float>(p, d, own, s);
+}
+cudaError_t slab_reduce(esp_plan* p, const esp_slab_desc* d, const void* recv, int want_ik,
+                        double* d_out7, cudaStream_t s) {
+  return p->precision == ESP_FP64 ? slab_reduce_t<double>(p, d, recv, want_ik, d_out7, s)
+                                  : slab_reduce_t<float>(p, d, recv, want_ik, d_out7, s);
+}
+cudaError_t slab_inverse(esp_plan* p, const esp_slab_desc* d, const void* recv, void* fields,
+                         cudaStream_t s) {
+  return p->precision == ESP_FP64 ? slab_inverse_t<double>(p, d, recv, fields, s)
+                                  : slab_inverse_t<float>(p, d, recv, fields, s);
+}
+int fused_ldx(const esp_plan* p) {
+  return p->fused ? reinterpret_cast<const FusedFft*>(p->fused)->ldx : 0;
 }
 
 cudaError_t launch_fused_fft(esp_plan* p, int want_ik, double* d_out7, cudaStream_t s) {

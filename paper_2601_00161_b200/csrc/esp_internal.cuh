@@ -395,6 +395,13 @@ cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s);
 // inverse transforms into d_fields when want_ik).  Requires p->fused.
 cudaError_t launch_fused_fft(esp_plan* p, int want_ik, double* d_out7, cudaStream_t s);
 int fused_reduce_blocks(const esp_plan* p);
+cudaError_t slab_forward(esp_plan* p, const esp_slab_desc* d, const void* own, cudaStream_t s);
+cudaError_t slab_reduce(esp_plan* p, const esp_slab_desc* d, const void* recv, int want_ik,
+                        double* d_out7, cudaStream_t s);
+cudaError_t slab_inverse(esp_plan* p, const esp_slab_desc* d, const void* recv, void* fields,
+                         cudaStream_t s);
+void slab_by_split(int nby, int R, int* by_start);
+int fused_ldx(const esp_plan* p);
 cudaError_t launch_mode_setup(esp_plan* p, double what_zero, cudaStream_t s);
 void build_combine_axis(int M, int T, int E, int nt, int lo, std::vector<int>& ent,
                         std::vector<int>& cnt);

@@ -260,6 +260,62 @@ class EspPlan:
         _lib.check(_lib.lib().esp_grid_info(self._handle, buf), "esp_grid_info")
         return list(buf)
 
+    # -- distributed z-slab transforms (esp_slab_*) -----------------------------
+    def slab_layout(self, nranks: int):
+        """(by_start, info): the in-band ky rows owned per rank and
+        {ldx, nby, nbx, cbytes} of the fused transforms."""
+        by = (C.c_int32 * (nranks + 1))()
+        info = (C.c_int64 * 4)()
+        _lib.check(_lib.lib().esp_slab_layout(self._handle, int(nranks), by, info),
+                   "esp_slab_layout")
+        return [int(v) for v in by], dict(ldx=int(info[0]), nby=int(info[1]),
+                                           nbx=int(info[2]), cbytes=int(info[3]))
+
+    def slab_buffers(self, nranks: int, rank: int, z_start):
+        """Receive buffers of one rank: forward [Mz][ny_r][ldx] and backward
+        [3][nz_r][nby][ldx], complex in the plan precision."""
+        by, info = self.slab_layout(nranks)
+        ct = torch.complex128 if self.precision == "fp64" else torch.complex64
+        ny = by[rank + 1] - by[rank]
+        nz = z_start[rank + 1] - z_start[rank]
+        fwd = torch.zeros((self.M[2], max(ny, 1), info["ldx"]), dtype=ct, device="cuda")
+        back = torch.zeros((3, nz, info["nby"], info["ldx"]), dtype=ct, device="cuda")
+        return fwd, back
+
+    @staticmethod
+    def slab_desc(nranks: int, rank: int, z_start, fwd_peers, back_peers):
+        d = _lib.SlabDesc()
+        d.nranks, d.rank = int(nranks), int(rank)
+        for i, v in enumerate(z_start):
+            d.z_start[i] = int(v)
+        for i in range(nranks):
+            d.fwd_peers[i] = int(fwd_peers[i].data_ptr())
+            d.back_peers[i] = int(back_peers[i].data_ptr())
+        return d
+
+    def slab_forward(self, desc, own: torch.Tensor, stream=None):
+        own = own.contiguous()
+        _lib.check(_lib.lib().esp_slab_forward(self._handle, C.byref(desc),
+                                               C.c_void_p(own.data_ptr()),
+                                               _stream_handle(stream)), "esp_slab_forward")
+
+    def slab_reduce(self, desc, recv_fwd: torch.Tensor, want_ik: bool,
+                    out7: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if out7 is None:
+            out7 = torch.empty(7, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().esp_slab_reduce(self._handle, C.byref(desc),
+                                              C.c_void_p(recv_fwd.data_ptr()),
+                                              int(bool(want_ik)), C.c_void_p(out7.data_ptr()),
+                                              _stream_handle(stream)), "esp_slab_reduce")
+        return out7
+
+    def slab_inverse(self, desc, recv_back: torch.Tensor, fields: torch.Tensor, stream=None):
+        _lib.check(_lib.lib().esp_slab_inverse(self._handle, C.byref(desc),
+                                               C.c_void_p(recv_back.data_ptr()),
+                                               C.c_void_p(fields.data_ptr()),
+                                               _stream_handle(stream)), "esp_slab_inverse")
+        return fields
+
     @property
     def fft_path(self) -> str:
         """"fused" (band-pruned transforms, esp_fft.cu) or "cufft"."""

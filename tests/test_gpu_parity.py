@@ -571,3 +571,45 @@ def test_fused_path_empty_system_and_cell_rebind():
         assert O.rel_scalar(r.energy, oE) <= F64_TOL
         assert O.rel_frobenius(r.pressure, oP) <= F64_TOL
         assert O.rms_rel_forces(r.forces, oF) <= F64_TOL
+
+
+@pytest.mark.parametrize("R", [1, 2, 3])
+def test_fused_slab_transforms_emulated_on_one_gpu(R):
+    """Distributed z-slab transforms (esp_slab_*): R ranks run one after
+    another on one device, each storing its transpose output straight into
+    the other ranks' receive buffers (what NVLink peer stores do on a box).
+    The ranks' energy/pressure shares add up to the single-plan result and
+    each rank's field slab equals the single-plan fields on its planes."""
+    torch = _torch()
+    g = golden("tri_skew_p8")
+    M = (64, 64, 96)
+    plan = _plan_for(g, M=M)
+    assert plan.fft_path == "fused"
+    pos, q = _dev(torch, g["pos"]), _dev(torch, g["q"])
+    out7, _ = plan.evaluate(pos, q, True)
+    ref7 = out7.cpu().numpy().copy()
+    ref_fields = plan.fields_view().clone()
+    grid = plan.spread(pos, q).clone()                   # (Mz, My, Mx)
+    zc = [M[2] // R + (r < M[2] % R) for r in range(R)]
+    z_start = [0] + list(np.cumsum(zc))
+    bufs = [plan.slab_buffers(R, r, z_start) for r in range(R)]
+    fwd = [b[0] for b in bufs]
+    back = [b[1] for b in bufs]
+    descs = [plan.slab_desc(R, r, z_start, fwd, back) for r in range(R)]
+    for r in range(R):
+        plan.slab_forward(descs[r], grid[z_start[r]:z_start[r + 1]])
+    torch.cuda.synchronize()
+    parts = [plan.slab_reduce(descs[r], fwd[r], True).cpu().numpy().copy() for r in range(R)]
+    torch.cuda.synchronize()
+    tot = parts[0]
+    for r in range(1, R):
+        tot = tot + parts[r]
+    assert abs(tot[0] - ref7[0]) <= 1e-12 * abs(ref7[0])
+    assert np.linalg.norm(tot[1:] - ref7[1:]) <= 1e-12 * np.linalg.norm(ref7[1:])
+    for r in range(R):
+        nz = z_start[r + 1] - z_start[r]
+        f = torch.empty((3, nz, M[1], M[0]), dtype=torch.float64, device="cuda")
+        plan.slab_inverse(descs[r], back[r], f)
+        refp = ref_fields[:, z_start[r]:z_start[r + 1]]
+        err = (f - refp).abs().max().item()
+        assert err <= 1e-12 * refp.abs().max().item()
