@@ -84,6 +84,11 @@ class CudaSlabOps:
         self.plan = EspPlan(M, P, window, split, r_c, precision=precision, capacity=capacity,
                             slab=(M[2], z0, nz))
         self.plan.set_cell(h)
+        # full-grid plan whose band-pruned transforms run the distributed
+        # transposes (esp_slab_*): only its mode tables and transform buffers
+        # are used
+        self.spectral = EspPlan(M, P, window, split, r_c, precision=precision, capacity=1)
+        self.spectral.set_cell(h)
         self._n = 0
 
     def spread(self, pos: torch.Tensor, q: torch.Tensor) -> torch.Tensor:
@@ -121,6 +126,53 @@ class SlabKSpaceSolver:
         self.ops = ops if ops is not None else CudaSlabOps(
             self.M, self.P, window, split, r_c, self.h, self.z0, self.nz, precision, capacity)
         self._build_modes()
+        self._fused = self._setup_fused()
+
+    # -- fused transposes over peer memory (esp_slab_*) ---------------------------
+    def _setup_fused(self) -> bool:
+        """Receive buffers for the distributed transforms: forward
+        [Mz][ny_r][ldx] and backward [3][nz_r][nby][ldx] per rank, in one
+        symmetric-memory allocation per rank whose peers' base pointers are
+        the transpose targets.  False (torch/NCCL transposes) when the
+        backend is not the CUDA one, the grid has no fused transforms, or
+        peer memory is unavailable."""
+        spec = getattr(self.ops, "spectral", None)
+        if spec is None or spec.fft_path != "fused" or self.R > 8:
+            return False
+        R, lay = self.R, self.layout
+        z_start = list(lay.zstart) + [self.M[2]]
+        by, info = spec.slab_layout(R)
+        cb, ldx, nby = info["cbytes"], info["ldx"], info["nby"]
+        fwd_bytes = [self.M[2] * max(by[r + 1] - by[r], 1) * ldx * cb for r in range(R)]
+        back_bytes = [3 * lay.zcount[r] * nby * ldx * cb for r in range(R)]
+        off_back = (max(fwd_bytes) + 255) // 256 * 256
+        total = off_back + max(back_bytes)
+        try:
+            if R == 1:
+                raw = torch.zeros(total, dtype=torch.uint8, device=self.device)
+                bases, self._symm = [raw.data_ptr()], None
+            else:
+                import torch.distributed._symmetric_memory as symm_mem
+                raw = symm_mem.empty(total, dtype=torch.uint8, device=self.device)
+                raw.zero_()
+                self._symm = symm_mem.rendezvous(raw, self.group or dist.group.WORLD)
+                bases = list(self._symm.buffer_ptrs)
+        except Exception:
+            return False
+        self._raw = raw
+        ct = torch.complex128 if spec.precision == "fp64" else torch.complex64
+        me = self.rank
+        self._recv_fwd = raw[:fwd_bytes[me]].view(ct)
+        self._recv_back = raw[off_back:off_back + back_bytes[me]].view(ct)
+        d = _SlabPeers(R, me, z_start, [b for b in bases], [b + off_back for b in bases])
+        self._desc = d.desc()
+        return True
+
+    def _rank_barrier(self):
+        """Stream-ordered barrier between the transpose stages."""
+        if self.R == 1:
+            return
+        self._symm.barrier()
 
     # -- per-cell mode tables for this rank's ky chunk -----------------------
     def _build_modes(self):
@@ -217,6 +269,8 @@ class SlabKSpaceSolver:
         from_prev, from_next = self._p2p(upper, lower, upper.shape, lower.shape)
         own[:nup] += from_prev                             # prev's upper ghosts
         own[nz - nlo:] += from_next                        # next's lower ghosts
+        if self._fused:
+            return self._evaluate_fused(own, pos, q, want_forces)
         # forward transform: (y, x) per plane, transpose, z
         X = torch.fft.rfft2(own, dim=(-2, -1))             # (nz, My, Hx)
         Hx = X.shape[-1]
@@ -279,6 +333,57 @@ class SlabKSpaceSolver:
                                       "fp64") == "fp64" else torch.float32
         F = self.ops.gather(ext.to(dt).contiguous(), pos, q)
         return E, Pt, F
+
+    def _evaluate_fused(self, own: torch.Tensor, pos, q, want_forces: bool):
+        """The spectral part on the band-pruned kernels with the transposes
+        fused into them (peer stores), NCCL only for the 7-double reduction
+        and the ghost planes."""
+        spec = self.ops.spectral
+        lay, M, nz, nlo, nup = self.layout, self.M, self.nz, self.layout.nlo, self.layout.nup
+        spec.slab_forward(self._desc, own.to(spec.real_dtype))
+        self._rank_barrier()
+        part = spec.slab_reduce(self._desc, self._recv_fwd, want_forces)
+        if self.R > 1:
+            allp = [torch.empty_like(part) for _ in range(self.R)]
+            dist.all_gather(allp, part, group=self.group)
+            tot = allp[0].clone()
+            for r in range(1, self.R):
+                tot = tot + allp[r]
+        else:
+            tot = part
+        v = tot.cpu().numpy()
+        E = float(v[0])
+        pp = v[1:]
+        Pt = np.array([[pp[0], pp[1], pp[2]], [pp[1], pp[3], pp[4]], [pp[2], pp[4], pp[5]]])
+        if not want_forces:
+            return E, Pt, None
+        self._rank_barrier()
+        fields = torch.empty((3, nz, M[1], M[0]), dtype=spec.real_dtype, device=own.device)
+        spec.slab_inverse(self._desc, self._recv_back, fields)
+        top, bottom = fields[:, nz - nlo:], fields[:, :nup]
+        from_prev_f, from_next_f = self._p2p(top, bottom, (3, nlo) + tuple(fields.shape[2:]),
+                                             (3, nup) + tuple(fields.shape[2:]))
+        ext = torch.cat([from_prev_f, fields, from_next_f], dim=1)
+        F = self.ops.gather(ext.contiguous(), pos, q)
+        return E, Pt, F
+
+
+class _SlabPeers:
+    """esp_slab_desc of one rank from raw peer base addresses."""
+
+    def __init__(self, R, rank, z_start, fwd, back):
+        self.R, self.rank, self.z_start, self.fwd, self.back = R, rank, z_start, fwd, back
+
+    def desc(self):
+        from . import _lib
+        d = _lib.SlabDesc()
+        d.nranks, d.rank = self.R, self.rank
+        for i, v in enumerate(self.z_start):
+            d.z_start[i] = int(v)
+        for i in range(self.R):
+            d.fwd_peers[i] = int(self.fwd[i])
+            d.back_peers[i] = int(self.back[i])
+        return d
 
 
 def check_slab_geometry(M, R, P):
