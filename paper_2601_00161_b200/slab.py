@@ -153,9 +153,13 @@ class SlabKSpaceSolver:
                 bases, self._symm = [raw.data_ptr()], None
             else:
                 import torch.distributed._symmetric_memory as symm_mem
+                group = self.group or dist.group.WORLD
+                if not symm_mem.is_symm_mem_enabled_for_group(group.group_name):
+                    symm_mem.enable_symm_mem_for_group(group.group_name)
+                # same size on every rank (collective allocation)
                 raw = symm_mem.empty(total, dtype=torch.uint8, device=self.device)
                 raw.zero_()
-                self._symm = symm_mem.rendezvous(raw, self.group or dist.group.WORLD)
+                self._symm = symm_mem.rendezvous(raw, group)
                 bases = list(self._symm.buffer_ptrs)
         except Exception:
             return False
