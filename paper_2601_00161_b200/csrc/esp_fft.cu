@@ -27,6 +27,11 @@
 // the line-transposing loads are bank-conflict free; per-stage twiddle
 // tables are laid out [t-1][k] so a warp reads consecutive entries.
 // Grids whose lengths are not in ESP_FFT_SIZES use the cuFFT path.
+//
+// Small square planes (Mx == My <= 64) run P1+P2 and P4+P5 as one kernel
+// per z plane (k_xy_fwd, k_yx_inv).  The distributed z-slab decomposition
+// (esp_slab_*) reuses P1-P5 with the transposes fused into P2 and P3b: their
+// stores go straight into the destination rank's receive buffer (SlabMap).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

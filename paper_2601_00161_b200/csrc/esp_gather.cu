@@ -4,11 +4,12 @@
 // k_gather_warp (P <= 8, the production path): CTA = one anchor tile (the
 // spread's decomposition).  The CTA stages the padded field tile — the three
 // ik fields on 16 x 16 columns x PZ planes — in shared memory once; a warp
-// then handles 4 particles at a time, lane (p, k) summing particle p's
-// stencil plane k (x rows at immediate offsets) and 8 lanes reducing with
-// 3 shuffle levels.  An odd plane stride keeps the 8 planes of a particle in
-// distinct bank groups.  Each particle is owned by one lane group: no
-// atomics, fixed reduction order, bitwise reproducible.
+// then handles 2 particles at a time, lane (p, h, k) summing the rows of
+// parity h of particle p's stencil plane k (x rows at immediate offsets),
+// and the 16 lanes of a particle reduce with 4 xor-shuffle levels.  Odd
+// plane strides keep every LDS phase bank-conflict free; weight records
+// arrive through a per-warp cp.async ring.  Each particle is owned by one
+// lane group: no atomics, fixed reduction order, bitwise reproducible.
 //
 // k_gather_ik (P > 8): column-owner variant — each thread holds a P-deep
 // sliding window of the three fields of one padded column in registers and

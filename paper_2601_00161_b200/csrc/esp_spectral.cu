@@ -1,5 +1,7 @@
 // esp_spectral.cu — mode workspace setup and the fused deconvolution-scaling
-// + energy/pressure reduction pass.
+// + energy/pressure reduction pass of the cuFFT path (grids without fused
+// transforms, the stage-level API, analytic forces and local pressure; the
+// fused-transform path does the same sums inside k_z_reduce, esp_fft.cu).
 //
 // Reference: ModeWorkspace (mesh.py:229-282), long_range_energy
 // (mesh.py:285-292), long_range_pressure (mesh.py:295-312) and the spectrum

@@ -1,18 +1,20 @@
 // esp_spread.cu — PSWF charge spreading (mesh.py:204-210) as a tile kernel
 // plus a deterministic halo combine.
 //
-// Design (DESIGN.md §"spread"):
-//  * CTA = one anchor tile of TX x TY columns x TZ planes (TX = TY = 17 - P),
-//    whose stencils cover a padded block of 16 x 16 columns x PZ = TZ+P-1
+// Design:
+//  * CTA = one anchor tile of TX x TY columns x TZS planes (TX = TY = 17 - P),
+//    whose stencils cover a padded block of 16 x 16 columns x PZS = TZS+P-1
 //    planes.  Its particles are a contiguous, z-anchor-sorted range of the
 //    binned arrays (esp_bin.cu).
-//  * Each of the 128 threads owns two padded (x, y) columns and keeps a
-//    P-deep sliding window of z accumulators for each in registers.  Particles are
-//    visited in z-anchor order; when the anchor advances the window slides
-//    and the finished plane is stored (plain store, exclusive owner).  Every
-//    multiply-add in the window is useful along z; along x/y a warp (8 x 8
-//    columns) only visits the particles whose stencil touches it, found by a
-//    ballot over a per-particle 8-bit warp mask staged with the weights.
+//  * Threads own padded (x, y) columns and keep a P-deep sliding window of z
+//    accumulators for each in registers.  Particles are visited in z-anchor
+//    order; when the anchor advances the window slides and the finished
+//    plane is stored (plain store, exclusive owner).
+//      k_spread_warp (P <= 8, production): 2 or 4 warps per tile, a thread
+//        owns a strip of 4 (or 2) columns along y; every charge is one visit
+//        of each warp whose rows it touches.
+//      k_spread_tiles (tiny grids, P > 8): 4 warps of 8 x 8 column blocks,
+//        2 columns per lane, per-warp ballot-compacted particle lists.
 //  * 1D weights come from the per-particle records written by the binning
 //    pass (unrolled Horner on the reference's degree-18 piecewise table,
 //    pswf.py:238-293) and are staged in shared memory as zero-padded rows;
