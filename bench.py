@@ -492,11 +492,11 @@ def run_reference(args):
 
 def run_slab(args):
     """Strong scaling: one config-4 system decomposed into z-slabs over the
-    ranks (NCCL halo send/recv, all-to-all transposes, 7-double all-gather)."""
+    ranks (NCCL halo send/recv, transposes stored over peer memory by the
+    band-pruned transform kernels, 7-double all-gather)."""
     import torch
 
     from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver, workloads
-    from paper_2601_00161_b200.mesh import plan_grid
     from paper_2601_00161_b200.pswf import build_pswf, solve_bandwidth, tabulate_window
     from paper_2601_00161_b200.slab import SlabKSpaceSolver
 

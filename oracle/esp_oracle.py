@@ -24,7 +24,6 @@ Array conventions follow the reference: grids are C-order [x][y][z]
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import numpy as np

@@ -28,7 +28,7 @@ from .errors import MeshError, PlanningError
 from .kernel import SplitKernel
 from .plan import EspPlan, cell_tables, out7_to_tensor
 from .pswf import PswfBasis, WindowTable, build_pswf, solve_bandwidth, tabulate_window
-from .system import Cell
+from .system import Cell  # noqa: F401  (re-exported like the reference module)
 
 
 class TransformProvider:
