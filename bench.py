@@ -104,6 +104,26 @@ class ClockSampler:
         self._th = None
 
     def _run(self):
+        # NVML polls every 2 ms (the timed regions are tens of ms); nvidia-smi
+        # every 200 ms when NVML is unavailable
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+                    "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                act = ["Active" if r & b else "Not Active" for b in
+                       (bits["hw_slowdown"], bits["hw_thermal_slowdown"],
+                        bits["sw_thermal_slowdown"], bits["sw_power_cap"])]
+                self.samples.append([str(sm), str(mx), hex(r)] + act)
+                self._stop.wait(0.002)
+            return
+        except Exception:
+            pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
