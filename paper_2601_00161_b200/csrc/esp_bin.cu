@@ -107,7 +107,7 @@ __global__ void k_bin_keys(const double* __restrict__ pos, long long n, Geom g,
 }
 
 // After the stable radix sort: gather each particle into its binned slot and
-// write its weight record.  Reads are random, writes coalesced.
+// write its weight record.  Reads are random, writes contiguous per block.
 template <typename real, int P>
 __global__ void __launch_bounds__(3 * kBinPerBlock)
 k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __restrict__ brk,
@@ -116,18 +116,42 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
              const double* __restrict__ pos, const double* __restrict__ q,
              double* __restrict__ u_out, double* __restrict__ q_out,
              int* __restrict__ idx_out, real* __restrict__ wrec, int* __restrict__ pk) {
-  const int d = threadIdx.x / kBinPerBlock;
-  const long long j = (long long)blockIdx.x * kBinPerBlock + (threadIdx.x % kBinPerBlock);
-  if (j >= n) return;
-  const int i = sval[j];
-  const long long i3 = 3 * (long long)i;
-  const double u = grid_coord(g, d, pos[i3], pos[i3 + 1], pos[i3 + 2]);
-  u_out[d * cap + j] = u;
-  if (d == 0) {
-    q_out[j] = q[i];
-    idx_out[j] = i;
+  // The block's 32 records (and packed anchors) are assembled in shared
+  // memory and written out as one contiguous run.
+  constexpr int RS = rec_stride(P);
+  __shared__ __align__(16) real s_rec[kBinPerBlock * 3 * RS];
+  __shared__ int s_pk[kBinPerBlock];
+  const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
+  const long long j0 = (long long)blockIdx.x * kBinPerBlock;
+  const long long j = j0 + l;
+  const int nb = (int)min((long long)kBinPerBlock, n - j0);
+  if (l < nb) {
+    const int i = sval[j];
+    const long long i3 = 3 * (long long)i;
+    const double u = grid_coord(g, d, pos[i3], pos[i3 + 1], pos[i3 + 2]);
+    u_out[d * cap + j] = u;
+    if (d == 0) {
+      q_out[j] = q[i];
+      idx_out[j] = i;
+    }
+    real w[P];
+    int a;
+    record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
+#pragma unroll
+    for (int t = 0; t < RS; ++t) s_rec[(l * 3 + d) * RS + t] = t < P ? w[t < P ? t : 0] : real(0);
+    unsigned char* pb = reinterpret_cast<unsigned char*>(s_pk + l);
+    if (d == 2) {
+      *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
+    } else {
+      const int txy = skey[j] / g.M[2];
+      const int org = d == 0 ? (txy % g.ntx) * g.TX : (txy / g.ntx) * g.TY;
+      pb[d] = (unsigned char)(a - org);
+    }
   }
-  write_record_dim<real, P>(g, ft, tab, brk, n_pieces, ncoef, skey[j], d, u, j, wrec, pk);
+  __syncthreads();
+  real* dst = wrec + j0 * (3 * RS);
+  for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) dst[t] = s_rec[t];
+  for (int t = threadIdx.x; t < nb; t += 3 * kBinPerBlock) pk[j0 + t] = s_pk[t];
 }
 
 // Scatter to key segments.  Writes grid coordinates u (SoA), charge and the
