@@ -212,6 +212,74 @@ int esp_profile_read(esp_plan* plan, char* names, int32_t names_len, double* ms,
 /* Measured FP64 FMA throughput of this device (TFLOP/s), DFMA-chain probe. */
 int esp_probe_fp64(double* tflops, void* stream);
 
+/* --- near field (real-space pair sum) ---------------------
+ *
+ *   esp_near_evaluate        <- build_cell_list + short_range
+ *                               (system.py:144-222, realspace.py:115-157)
+ *   esp_near_evaluate_pairs  <- short_range with a caller NeighborList
+ *                               (realspace.py:115-157, system.py:123-135)
+ *   esp_near_desc tables     <- PairTable / build_pair_table (realspace.py:29-112)
+ *                               or, use_table = 0, kernel.near_field / fn_weight
+ *                               (kernel.py:41-97) from the Legendre series
+ *
+ * out7 = [E_near, P_xx, P_xy, P_xz, P_yy, P_yz, P_zz] (pressure = virial / V,
+ * realspace.py:155-156); forces (N,3) in the caller's order (overwritten, or
+ * added to with ESP_NEAR_ACCUMULATE); stats (device int64[3]) = {pair count
+ * within r_c, first coincident pair (i << 32 | j) or -1, first pair with an
+ * index outside [0, N) or -1}.  A coincident pair (r < 1e-12 r_c) is the
+ * reference's SingularPairError (realspace.py:20-21, 134-137).            */
+enum esp_near_flags { ESP_NEAR_ACCUMULATE = 1 };
+
+typedef struct esp_near esp_near;
+
+typedef struct esp_near_desc {
+  double r_c;               /* cutoff (SplitKernel.r_c)                      */
+  double reach;             /* cell-list reach, >= r_c (r_c + skin)          */
+  int32_t use_table;        /* 1: PairTable values, 0: exact series          */
+  /* PairTable (realspace.py:29-40): polynomial pieces on [0, r_in],
+   * ascending powers; cubic splines on [r_in, r_c] as scipy PPoly: knots
+   * (n_knots) and c[4][n_knots-1], highest power first.                     */
+  double r_in;
+  int32_t poly_order;
+  const double* h_smooth_poly;
+  const double* h_fn_poly;
+  int32_t n_knots;
+  const double* h_knots;
+  const double* h_smooth_spline;
+  const double* h_fn_spline;
+  /* psi_0 Legendre series and its integral from 0 (pswf.py:123-160),
+   * C0 = int_0^1 psi_0                                                      */
+  int32_t n_legendre;
+  const double* h_legendre;
+  int32_t n_cumint;
+  const double* h_cumint;
+  double C0;
+  int64_t max_particles;
+  int32_t cell_div;         /* cells per reach along each axis (0 = 2)       */
+} esp_near_desc;
+
+int esp_near_create(const esp_near_desc* desc, esp_near** out);
+int esp_near_destroy(esp_near* plan);
+/* Grow the particle / pair-list capacity (allocates; call outside graphs). */
+int esp_near_reserve(esp_near* plan, int64_t n_particles, int64_t n_pairs);
+/* Bind a cell: h and h^-1 row-major (columns of h = cell vectors).  Checks
+ * reach < half the minimum perpendicular width (system.py:137-141,
+ * GeometryError) and builds the cell lattice and stencil.                  */
+int esp_near_set_cell(esp_near* plan, const double* h_h, const double* h_hinv,
+                      int32_t orthorhombic, double volume);
+int esp_near_evaluate(esp_near* plan, const double* d_pos, const double* d_q, int64_t n,
+                      int32_t flags, double* d_out7, double* d_forces, int64_t* d_stats,
+                      void* stream);
+/* Pairs (d_i[k], d_j[k]) as given (int64 device arrays), separation by
+ * minimum_image.                                                           */
+int esp_near_evaluate_pairs(esp_near* plan, const double* d_pos, const double* d_q,
+                            int64_t n, const int64_t* d_i, const int64_t* d_j,
+                            int64_t n_pairs, int32_t flags, double* d_out7,
+                            double* d_forces, int64_t* d_stats, void* stream);
+/* info8 = {nc_x, nc_y, nc_z, stencil cells, capacity, launches last call,
+ *          cells per reach, use_table}                                      */
+int esp_near_info(const esp_near* plan, int64_t* info8);
+
 #ifdef __cplusplus
 }
 #endif

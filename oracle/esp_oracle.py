@@ -3,7 +3,8 @@
 This module is a numpy/scipy restatement of the reference package's
 long-range (k-space) pipeline, arXiv 2601.00161, ``prolate_ewald``
 (``/root/reference/pkg/src/prolate_ewald``).  It is the parity checker for
-the CUDA product path and the timed CPU leg of ``bench.py``
+the CUDA product path (k-space, and the near-field pair sum of
+realspace.py / system.py, L3 below) and the timed CPU leg of ``bench.py``
 (``cpu_baseline`` / ``--impl reference``, ``kind: "port"``).  Only
 ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU leg may
 import it; the product package never does.
@@ -498,6 +499,199 @@ def direct_ksum(h, kmax, split: Basis, r_c, pos, q):
     Pt = np.einsum("k,ka,kb->ab", (dterm - 2.0 * fhat / kmag ** 2) * w, k, k)
     Pt += np.sum(fhat * w) * np.eye(3)
     return E, F, 0.5 * (Pt + Pt.T)
+
+
+# --------------------------------------------------------------------------
+# L3: near field — pair table, pair enumeration, fused pair sum
+# (realspace.py:29-157, kernel.py:41-97, system.py:75-222).  Pinned to the
+# reference by tests/golden/near_*.npz (tests/test_oracle_golden.py).
+
+
+def phi0(basis: Basis, r, r_c):
+    """eval_phi0 (pswf.py:277-292): (1/C0) int_0^{min(r/r_c,1)} psi_0; 1 at r >= r_c."""
+    r = np.asarray(r, dtype=float)
+    x = np.minimum(r / r_c, 1.0)
+    out = npleg.legval(x, npleg.legint(basis.coef, lbnd=0.0)) / basis.C0
+    return np.where(r >= r_c, 1.0, out)
+
+
+def near_value(basis: Basis, r_c, r):
+    """near_field (kernel.py:41-50) for r > 0."""
+    r = np.atleast_1d(np.asarray(r, dtype=float))
+    out = np.zeros_like(r)
+    inside = r < r_c
+    out[inside] = (1.0 - phi0(basis, r[inside], r_c)) / r[inside]
+    return out
+
+
+def far_value(basis: Basis, r_c, r):
+    """far_field (kernel.py:53-65)."""
+    r = np.atleast_1d(np.asarray(r, dtype=float))
+    out = np.empty_like(r)
+    z = r == 0.0
+    out[~z] = phi0(basis, r[~z], r_c) / r[~z]
+    out[z] = basis.psi0_at_zero / (basis.C0 * r_c)
+    return out
+
+
+def fn_value(basis: Basis, r_c, r):
+    """fn_weight (kernel.py:83-97)."""
+    r = np.asarray(r, dtype=float)
+    x = np.minimum(r / r_c, 1.0)
+    val = 1.0 - phi0(basis, r, r_c) + (r / (basis.C0 * r_c)) * basis.psi(x)
+    return np.where(r > r_c, 0.0, val)
+
+
+@dataclass(frozen=True)
+class PairTableO:
+    r_in: float
+    r_c: float
+    smooth: np.ndarray
+    fn: np.ndarray
+    smooth_spline: object
+    fn_spline: object
+
+
+def pair_table(basis: Basis, r_c, r_in=None, resolution=4096, order=8) -> PairTableO:
+    """build_pair_table (realspace.py:70-112)."""
+    from scipy.interpolate import CubicSpline
+    r_in = 0.1 * r_c if r_in is None else r_in
+    s = np.cos(np.pi * (2.0 * np.arange(order + 1) + 1.0) / (2.0 * (order + 1)))
+    for _ in range(12):
+        nodes = 0.5 * r_in * (s + 1.0)
+        smooth = np.polynomial.Polynomial.fit(nodes, far_value(basis, r_c, nodes), order,
+                                              domain=[0.0, r_in]).convert().coef
+        fnc = np.polynomial.Polynomial.fit(nodes, fn_value(basis, r_c, np.maximum(nodes, 1e-300)),
+                                           order, domain=[0.0, r_in]).convert().coef
+        probe = np.linspace(1e-6 * r_c, r_in, 512)
+        err = np.max(np.abs(np.polynomial.polynomial.polyval(probe, smooth)
+                            - far_value(basis, r_c, probe))) / far_value(basis, r_c, 0.0)[0]
+        if err <= 1e-11:
+            break
+        r_in *= 0.5
+    else:
+        raise ArithmeticError("inner-cutoff polynomial fit did not converge")
+    knots = np.linspace(r_in, r_c, resolution)
+    pad = np.zeros(order + 1)
+    pad[: smooth.size] = smooth
+    fpad = np.zeros(order + 1)
+    fpad[: fnc.size] = fnc
+    return PairTableO(r_in=float(r_in), r_c=float(r_c), smooth=pad, fn=fpad,
+                      smooth_spline=CubicSpline(knots, far_value(basis, r_c, knots)),
+                      fn_spline=CubicSpline(knots, fn_value(basis, r_c, knots)))
+
+
+def table_values(t: PairTableO, r):
+    """PairTable.near_field / fn_weight (realspace.py:42-67)."""
+    r = np.asarray(r, dtype=float)
+    nv = np.empty_like(r)
+    fv = np.empty_like(r)
+    lo = r <= t.r_in
+    hi = ~lo
+    pv = np.polynomial.polynomial.polyval
+    nv[lo] = 1.0 / r[lo] - pv(r[lo], t.smooth)
+    nv[hi] = 1.0 / r[hi] - t.smooth_spline(np.minimum(r[hi], t.r_c))
+    nv[r >= t.r_c] = 0.0
+    fv[lo] = pv(r[lo], t.fn)
+    fv[hi] = t.fn_spline(np.minimum(r[hi], t.r_c))
+    fv[r > t.r_c] = 0.0
+    return nv, fv
+
+
+def minimum_image(h, dr):
+    """system.py:75-79."""
+    h = np.asarray(h, dtype=float)
+    s = np.asarray(dr, dtype=float) @ np.linalg.inv(h).T
+    s -= np.floor(s + 0.5)
+    return s @ h.T
+
+
+def pairs_within(h, pos, reach, chunk=2048):
+    """All unordered pairs (i < j) with minimum-image distance <= reach, sorted
+    by (i, j) — the pair set of build_cell_list (system.py:144-222), by brute
+    force in row chunks (small N only)."""
+    pos = np.asarray(pos, dtype=float)
+    n = pos.shape[0]
+    I, J = [], []
+    for a in range(0, n, chunk):
+        rows = np.arange(a, min(n, a + chunk))
+        dr = minimum_image(h, pos[rows, None, :] - pos[None, :, :])
+        r2 = np.einsum("abk,abk->ab", dr, dr)
+        ii, jj = np.nonzero((r2 <= reach * reach) & (rows[:, None] < np.arange(n)[None, :]))
+        I.append(rows[ii])
+        J.append(jj)
+    i = np.concatenate(I) if I else np.zeros(0, dtype=np.int64)
+    j = np.concatenate(J) if J else np.zeros(0, dtype=np.int64)
+    o = np.lexsort((j, i))
+    return i[o].astype(np.int64), j[o].astype(np.int64)
+
+
+def pairs_within_kdtree(L, pos, reach):
+    """Orthorhombic pair set as the reference builds it (system.py:151-166,
+    periodic cKDTree)."""
+    from scipy.spatial import cKDTree
+    L = np.asarray(L, dtype=float)
+    p = np.maximum(np.minimum(np.asarray(pos, dtype=float), np.nextafter(L, 0.0)), 0.0)
+    pairs = cKDTree(p, boxsize=L).query_pairs(reach, output_type="ndarray")
+    if pairs.size == 0:
+        return np.zeros(0, dtype=np.int64), np.zeros(0, dtype=np.int64)
+    i = np.minimum(pairs[:, 0], pairs[:, 1])
+    j = np.maximum(pairs[:, 0], pairs[:, 1])
+    o = np.lexsort((j, i))
+    return i[o].astype(np.int64), j[o].astype(np.int64)
+
+
+def short_range(h, pos, q, i, j, basis: Basis, r_c, table: PairTableO | None = None,
+                chunk=4_000_000):
+    """realspace.short_range (realspace.py:115-157): returns (E, F, P, pairs)."""
+    h = np.asarray(h, dtype=float)
+    pos = np.asarray(pos, dtype=float)
+    q = np.asarray(q, dtype=float)
+    n = pos.shape[0]
+    F = np.zeros((n, 3))
+    E = 0.0
+    V = float(np.linalg.det(h))
+    W = np.zeros((3, 3))
+    count = 0
+    for a in range(0, len(i), chunk):
+        ii, jj = i[a:a + chunk], j[a:a + chunk]
+        dr = minimum_image(h, pos[ii] - pos[jj])
+        r = np.sqrt(np.einsum("ij,ij->i", dr, dr))
+        if np.any(r < 1e-12 * r_c):
+            raise ZeroDivisionError("coincident particles")
+        keep = r <= r_c
+        ii, jj, dr, r = ii[keep], jj[keep], dr[keep], r[keep]
+        qq = q[ii] * q[jj]
+        if table is not None:
+            nv, fv = table_values(table, r)
+        else:
+            nv, fv = near_value(basis, r_c, r), fn_value(basis, r_c, r)
+        E += float(np.sum(qq * nv))
+        fmag = qq * fv / r ** 3
+        pf = fmag[:, None] * dr
+        np.add.at(F, ii, pf)
+        np.add.at(F, jj, -pf)
+        W += (dr.T * fmag) @ dr
+        count += int(r.size)
+    P = W / V
+    return E, F, 0.5 * (P + P.T), count
+
+
+def short_range_rows(h, pos, q, rows, basis: Basis, r_c, table: PairTableO | None = None):
+    """Near-field forces on the particles ``rows`` only, against every other
+    particle by brute force (size-independent check at large N)."""
+    pos = np.asarray(pos, dtype=float)
+    q = np.asarray(q, dtype=float)
+    out = np.zeros((len(rows), 3))
+    for k, a in enumerate(rows):
+        dr = minimum_image(h, pos[a] - pos)
+        r = np.sqrt(np.einsum("ij,ij->i", dr, dr))
+        m = (r <= r_c) & (np.arange(pos.shape[0]) != a)
+        r, dr = r[m], dr[m]
+        nv, fv = table_values(table, r) if table is not None else (
+            near_value(basis, r_c, r), fn_value(basis, r_c, r))
+        out[k] = np.sum((q[a] * q[m] * fv / r ** 3)[:, None] * dr, axis=0)
+    return out
 
 
 # --------------------------------------------------------------------------

@@ -1,16 +1,19 @@
 """B200-native ESP long-range (k-space) path — drop-in for the mesh pipeline
 of ``prolate_ewald`` (arXiv 2601.00161).
 
-The hot path lives in ``libesp_b200.so`` (hand-written sm_100a CUDA + cuFFT,
+The k-space path and the near-field pair sum (realspace.py) live in
+``libesp_b200.so`` (hand-written sm_100a CUDA + cuFFT,
 C ABI in include/esp_b200.h); this package is the host-side mirror of the
 reference's Python API for that path.  There is no CPU fallback: device
 functions raise if the library or a GPU is missing.
 """
 
 from .cells import CellType, infer_cell_type
-from .errors import (CellError, DomainError, EspCudaError, MeshError, ParameterError,
-                     PlanningError, PswfError)
-from .kernel import SplitKernel, background_correction, far_field_hat, self_energy
+from .errors import (CellError, DomainError, EspCudaError, GeometryError, MeshError,
+                     ParameterError, PlanningError, PswfError, RealspaceError,
+                     SingularPairError)
+from .kernel import (SplitKernel, background_correction, far_field, far_field_hat, fn_weight,
+                     near_field, self_energy)
 from .mesh import (GridField, GridSpec, ModeWorkspace, TransformProvider, forward_density,
                    local_pressure, long_range_energy, long_range_forces,
                    long_range_pressure, plan_grid, spread_charges)
@@ -19,7 +22,9 @@ from .pswf import (PswfBasis, WindowTable, build_pswf, eval_psi0, solve_bandwidt
                    tabulate_window)
 from .solver import (CoulombSolver, EnergyBreakdown, EwaldParameters, KSpaceResult,
                      KSpaceSolver, evaluate_system)
-from .system import Cell, ParticleSystem, check_cutoff
+from .realspace import (NearFieldPlan, PairTable, ShortRangeResult, build_pair_table,
+                        short_range)
+from .system import Cell, NeighborList, ParticleSystem, check_cutoff, minimum_image
 
 __version__ = "0.1.0"
 
@@ -32,4 +37,7 @@ __all__ = [
     "eval_psi0", "evaluate_system", "far_field_hat", "forward_density", "infer_cell_type",
     "local_pressure", "long_range_energy", "long_range_forces", "long_range_pressure",
     "plan_grid", "self_energy", "solve_bandwidth", "spread_charges", "tabulate_window",
+    "GeometryError", "RealspaceError", "SingularPairError", "far_field", "fn_weight",
+    "near_field", "NearFieldPlan", "PairTable", "ShortRangeResult", "build_pair_table",
+    "short_range", "NeighborList", "minimum_image",
 ]

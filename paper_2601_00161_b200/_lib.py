@@ -32,6 +32,8 @@ ESP_WANT_ENERGY_PRESSURE = 1
 ESP_WANT_FORCES = 2
 ESP_FORCES_ANALYTIC = 4
 
+ESP_NEAR_ACCUMULATE = 1
+
 _dp = C.POINTER(C.c_double)
 
 
@@ -84,6 +86,30 @@ class CellDesc(C.Structure):
     ]
 
 
+class NearDesc(C.Structure):
+    """esp_near_desc (include/esp_b200.h)."""
+    _fields_ = [
+        ("r_c", C.c_double),
+        ("reach", C.c_double),
+        ("use_table", C.c_int32),
+        ("r_in", C.c_double),
+        ("poly_order", C.c_int32),
+        ("h_smooth_poly", _dp),
+        ("h_fn_poly", _dp),
+        ("n_knots", C.c_int32),
+        ("h_knots", _dp),
+        ("h_smooth_spline", _dp),
+        ("h_fn_spline", _dp),
+        ("n_legendre", C.c_int32),
+        ("h_legendre", _dp),
+        ("n_cumint", C.c_int32),
+        ("h_cumint", _dp),
+        ("C0", C.c_double),
+        ("max_particles", C.c_int64),
+        ("cell_div", C.c_int32),
+    ]
+
+
 _lib = None
 
 
@@ -130,6 +156,14 @@ def lib():
     L.esp_set_profiling.argtypes = [vp, C.c_int32]
     L.esp_profile_read.argtypes = [vp, C.c_char_p, C.c_int32, C.POINTER(C.c_double), C.c_int32]
     L.esp_probe_fp64.argtypes = [C.POINTER(C.c_double), vp]
+    L.esp_near_create.argtypes = [C.POINTER(NearDesc), C.POINTER(vp)]
+    L.esp_near_destroy.argtypes = [vp]
+    L.esp_near_reserve.argtypes = [vp, C.c_int64, C.c_int64]
+    L.esp_near_set_cell.argtypes = [vp, _dp, _dp, C.c_int32, C.c_double]
+    L.esp_near_evaluate.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp, vp]
+    L.esp_near_evaluate_pairs.argtypes = [vp, vp, vp, C.c_int64, vp, vp, C.c_int64,
+                                          C.c_int32, vp, vp, vp, vp]
+    L.esp_near_info.argtypes = [vp, C.POINTER(C.c_int64)]
     _lib = L
     return L
 
@@ -142,6 +176,8 @@ EXPORTED = [
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
     "esp_gather_fields", "esp_fields_ptr", "esp_fft_path",
     "esp_slab_layout", "esp_slab_forward", "esp_slab_reduce", "esp_slab_inverse",
+    "esp_near_create", "esp_near_destroy", "esp_near_reserve", "esp_near_set_cell",
+    "esp_near_evaluate", "esp_near_evaluate_pairs", "esp_near_info",
 ]
 
 

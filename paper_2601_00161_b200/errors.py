@@ -3,7 +3,8 @@
 PlanningError, MeshError   <- prolate_ewald/mesh.py:25-30
 ParameterError             <- prolate_ewald/evaluate.py:247
 PswfError, DomainError     <- prolate_ewald/pswf.py:33-38
-CellError                  <- prolate_ewald/system.py:12
+CellError, GeometryError   <- prolate_ewald/system.py:12-17
+RealspaceError, SingularPairError <- prolate_ewald/realspace.py:15-21
 """
 
 
@@ -29,6 +30,18 @@ class DomainError(PswfError):
 
 class CellError(Exception):
     """Invalid cell matrix or particle arrays."""
+
+
+class GeometryError(CellError):
+    """Cutoff too large for the cell, or other geometric safety violation."""
+
+
+class RealspaceError(Exception):
+    """Near-field (pair sum) failure."""
+
+
+class SingularPairError(RealspaceError):
+    """Coincident particles; physical configurations never need them."""
 
 
 class EspCudaError(RuntimeError):

@@ -1,11 +1,12 @@
 """Splitting-kernel constants used by the k-space path
 (reference: prolate_ewald/kernel.py).
 
-Only the quantities the far-field solver composes are provided: ``kmax =
-c / r_c`` (kernel.py:28-39), the far-field transform Fhat (kernel.py:68-80,
-host diagnostics — the device computes it per retained mode), the self
-energy (kernel.py:117-123) and the uniform-background correction
-(kernel.py:126-150).  The near field is out of scope.
+Host-side quantities: ``kmax = c / r_c`` (kernel.py:28-39), the far-field
+transform Fhat (kernel.py:68-80, host diagnostics — the device computes it
+per retained mode), the radial split functions near_field / far_field /
+fn_weight (kernel.py:41-97; used to tabulate the pair table, the device pair
+kernels evaluate them per pair), the self energy (kernel.py:117-123) and the
+uniform-background correction (kernel.py:126-150).
 """
 
 from __future__ import annotations
@@ -60,6 +61,50 @@ def phi0(basis: PswfBasis, r, r_c: float):
     x = np.minimum(ra / r_c, 1.0)
     out = L.legval(x, L.legint(basis.legendre_coeffs, lbnd=0.0)) / basis.C0
     return np.where(ra >= r_c, 1.0, out)
+
+
+def cumint_coeffs(basis: PswfBasis) -> np.ndarray:
+    """Legendre coefficients of int_0^x psi_0 (pswf.py:144-160, legint lbnd=0)."""
+    return L.legint(basis.legendre_coeffs, lbnd=0.0)
+
+
+def near_field(kern: SplitKernel, r):
+    """(1 - phi_0(r)) / r on (0, r_c]; zero beyond (kernel.py:41-50)."""
+    scalar = np.isscalar(r) or np.ndim(r) == 0
+    ra = np.atleast_1d(np.asarray(r, dtype=float))
+    if np.any(ra <= 0.0):
+        raise DomainError("near_field requires r > 0 (self-pairs are excluded)")
+    out = np.zeros_like(ra)
+    inside = ra < kern.r_c
+    out[inside] = (1.0 - phi0(kern.basis, ra[inside], kern.r_c)) / ra[inside]
+    return float(out[0]) if scalar else out
+
+
+def far_field(kern: SplitKernel, r):
+    """phi_0(r) / r, psi_0(0) / (C0 r_c) at r = 0 (kernel.py:53-65)."""
+    scalar = np.isscalar(r) or np.ndim(r) == 0
+    ra = np.atleast_1d(np.asarray(r, dtype=float))
+    if np.any(ra < 0.0):
+        raise DomainError("far_field requires r >= 0")
+    b = kern.basis
+    out = np.empty_like(ra)
+    zero = ra == 0.0
+    out[~zero] = phi0(b, ra[~zero], kern.r_c) / ra[~zero]
+    out[zero] = b.psi0_at_zero / (b.C0 * kern.r_c)
+    return float(out[0]) if scalar else out
+
+
+def fn_weight(kern: SplitKernel, r):
+    """F_N(r) = 1 - phi_0(r) + (r / (C0 r_c)) psi_0(r / r_c); 0 beyond r_c
+    (kernel.py:83-97)."""
+    ra = np.asarray(r, dtype=float)
+    if np.any(ra <= 0.0):
+        raise DomainError("fn_weight requires r > 0")
+    b = kern.basis
+    x = np.minimum(ra / kern.r_c, 1.0)
+    val = 1.0 - phi0(b, ra, kern.r_c) + (ra / (b.C0 * kern.r_c)) * b.psi_series(x)
+    out = np.where(ra > kern.r_c, 0.0, val)
+    return out if out.ndim else float(out)
 
 
 def self_energy(kern: SplitKernel, charges) -> float:

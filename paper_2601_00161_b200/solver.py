@@ -4,10 +4,9 @@
 (CUDA tensors, or host arrays that are copied in) -> far-field energy, the
 full 3x3 pressure tensor and ik forces in one device pipeline (bin, spread,
 1 forward FFT, fused scale/reduce, and for forces 3 inverse FFTs + gather).
-:class:`CoulombSolver` mirrors ``evaluate.CoulombSolver`` (evaluate.py:81-152)
-for the terms this build owns: far field + self energy + uniform background.
-The real-space near field is outside this build's scope (SURVEY §8(f) f3);
-pass its result in with ``near=`` to compose totals.
+:class:`CoulombSolver` mirrors ``evaluate.CoulombSolver`` (evaluate.py:81-152):
+near field (realspace.py, on the device), far field, self energy and the
+uniform background.
 """
 
 from __future__ import annotations
@@ -22,6 +21,7 @@ from .errors import ParameterError
 from .kernel import SplitKernel, background_correction, self_energy
 from .mesh import plan_grid
 from .plan import EspPlan, out7_to_tensor
+from .realspace import NearFieldPlan, build_pair_table, out7_to_pressure
 from .pswf import build_pswf, solve_bandwidth
 from .system import Cell, check_cutoff
 
@@ -72,7 +72,8 @@ class KSpaceResult:
 def _to_device(x, dtype=torch.float64):
     if isinstance(x, torch.Tensor):
         return x.to(device="cuda", dtype=dtype).contiguous()
-    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device="cuda").to(dtype)
+    npd = np.int64 if dtype == torch.int64 else np.float64
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=npd), device="cuda").to(dtype)
 
 
 class KSpaceSolver:
@@ -232,51 +233,77 @@ class EnergyBreakdown:
 
 
 class CoulombSolver:
-    """evaluate.CoulombSolver with the far field on the B200.
+    """evaluate.CoulombSolver (evaluate.py:81-152) on the B200.
 
-    ``near`` (optional) is any object with ``energy``, ``forces`` (N,3),
-    ``pressure`` (3,3) and ``pair_count`` — e.g. the reference's
-    ``short_range`` result — added to the totals exactly as evaluate.py:132-144.
-    """
+    Near field (device cell list or a caller NeighborList + pair table,
+    csrc/esp_near.cu), far field (the k-space pipeline), self energy and the
+    uniform-background terms compose exactly as evaluate.py:114-144.  Host
+    ``ParticleSystem`` inputs return numpy forces; CUDA-tensor systems keep
+    them on the device."""
 
     def __init__(self, cell, params: EwaldParameters):
         self.params = params
         self.kspace = KSpaceSolver(cell, params)
         self.kern = self.kspace.kern
         self.cell = self.kspace.cell
+        self.pair_table = build_pair_table(self.kern)
+        self.near = NearFieldPlan(self.kern, self.pair_table)
+        self.near.set_cell(self.cell)
 
     @property
     def spec(self):
         return self.kspace.spec
 
+    @property
+    def provider(self):
+        return self.kspace.plan
+
     def rebind_cell(self, cell, fixed_M=None):
+        """Bases and pair table persist (evaluate.py:99-112)."""
         self.kspace.rebind_cell(cell, fixed_M)
         self.cell = self.kspace.cell
+        self.near.set_cell(self.cell)
+
+    def evaluate_device(self, positions: torch.Tensor, charges: torch.Tensor,
+                        want_forces: bool = True, neighbors=None, stream=None):
+        """Device step without synchronising: (out7_far, out7_near, stats, F)
+        with F = far + near forces (prefactor 1) or None."""
+        out7_far, F = self.kspace.evaluate_device(positions, charges, want_forces,
+                                                  stream=stream)
+        if neighbors is None:
+            out7_near, Fn, stats = self.near.evaluate(positions, charges, forces=F,
+                                                      accumulate=want_forces, stream=stream)
+        else:
+            out7_near, Fn, stats = self.near.evaluate_pairs(
+                positions, charges, _to_device(neighbors.i, torch.int64),
+                _to_device(neighbors.j, torch.int64), forces=F, accumulate=want_forces,
+                stream=stream)
+        return out7_far, out7_near, stats, (F if want_forces else None)
 
     def evaluate(self, sys, want_forces: bool = True, want_pressure: bool = True,
-                 neighbors=None, near=None) -> EnergyBreakdown:
+                 neighbors=None) -> EnergyBreakdown:
         if not np.allclose(np.asarray(sys.cell.h), self.cell.h):
             raise ParameterError("system cell differs from the solver's cell; "
                                  "call rebind_cell first")
         pref = self.params.prefactor
-        far = self.kspace.evaluate(sys.positions, sys.charges, want_forces=want_forces)
-        q = np.asarray(sys.charges, dtype=float)
-        u_self = self_energy(self.kern, q)
-        u_cb, u_bb, p_corr = background_correction(self.kern, float(q.sum()), self.cell.volume)
-        e_near = getattr(near, "energy", 0.0) if near is not None else 0.0
-        out = EnergyBreakdown(u_near=pref * e_near, u_far=far.energy,
-                              u_self=pref * u_self, u_background=pref * (u_cb + u_bb),
-                              pair_count=getattr(near, "pair_count", 0) if near is not None else 0)
+        host = not isinstance(sys.positions, torch.Tensor)
+        pos = _to_device(sys.positions)
+        q = _to_device(sys.charges)
+        o_far, o_near, stats, F = self.evaluate_device(pos, q, want_forces, neighbors)
+        st = stats.cpu().numpy()
+        NearFieldPlan.check_stats(st)
+        e_far, p_far = out7_to_tensor(o_far)
+        e_near, p_near = out7_to_pressure(o_near)
+        qh = q.cpu().numpy()
+        u_self = self_energy(self.kern, qh)
+        u_cb, u_bb, p_corr = background_correction(self.kern, float(qh.sum()), self.cell.volume)
+        out = EnergyBreakdown(u_near=pref * e_near, u_far=pref * e_far, u_self=pref * u_self,
+                              u_background=pref * (u_cb + u_bb), pair_count=int(st[0]))
         if want_forces:
-            f = np.asarray(far.forces)
-            if near is not None:
-                f = f + pref * np.asarray(near.forces)
-            out.forces = f
+            F = F * pref
+            out.forces = F.cpu().numpy() if host else F
         if want_pressure:
-            p = far.pressure + pref * p_corr
-            if near is not None:
-                p = p + pref * np.asarray(near.pressure)
-            out.pressure = p
+            out.pressure = pref * (p_near + p_far + p_corr)
         return out
 
 

@@ -35,6 +35,9 @@ from prolate_ewald.mesh import (ModeWorkspace, TransformProvider,  # noqa: E402
                                 long_range_pressure, plan_grid,
                                 spread_charges)
 from prolate_ewald.oracle import direct_ksum  # noqa: E402
+from prolate_ewald.evaluate import CoulombSolver, EwaldParameters  # noqa: E402
+from prolate_ewald.realspace import build_pair_table, short_range  # noqa: E402
+from prolate_ewald.system import build_cell_list  # noqa: E402
 
 from paper_2601_00161_b200 import workloads  # noqa: E402
 
@@ -168,8 +171,84 @@ def window_tables():
     save("window_tables", versions=VERSIONS, **rows)
 
 
+NEAR_SMALL = [
+    # (name, h (columns = cell vectors), n, seed, delta, r_c, skin)
+    ("near_brick", np.diag([5.0, 6.0, 7.0]), 64, 21, 1e-5, 1.4, 0.0),
+    ("near_cube_skin", np.diag([7.0, 7.0, 7.0]), 128, 22, 1e-6, 1.5, 0.3),
+    ("near_tri", np.array([[6.0, 1.2, -0.8], [0.0, 6.5, 0.9], [0.0, 0.0, 7.0]]),
+     96, 23, 1e-6, 1.5, 0.0),
+    ("near_tight", np.diag([5.0, 5.0, 5.0]), 64, 24, 1e-8, 1.0, 0.0),
+]
+
+
+def near_cases():
+    """Near field (realspace.py): pair tables, short_range with the table and
+    with exact values, over the reference's own cell lists; CoulombSolver
+    totals for config 0; the near field of configs 0-2."""
+    tabs = {}
+    for (tag, delta, r_c) in (("d1e-5_rc10", 1e-5, 10.0), ("d1e-7_rc10", 1e-7, 10.0),
+                              ("d1e-8_rc1", 1e-8, 1.0), ("d1e-7_rc12", 1e-7, 12.0)):
+        kern = SplitKernel(basis=build_pswf(solve_bandwidth(delta)), r_c=r_c)
+        t = build_pair_table(kern)
+        tabs[f"{tag}_rin"] = np.array(t.r_in)
+        tabs[f"{tag}_smooth"] = t.smooth_coeffs
+        tabs[f"{tag}_fn"] = t.fn_coeffs
+        tabs[f"{tag}_sc"] = t.smooth_spline.c
+        tabs[f"{tag}_fc"] = t.fn_spline.c
+        tabs[f"{tag}_x"] = t.smooth_spline.x
+        r = np.exp(np.linspace(np.log(1e-3 * r_c), np.log(1.2 * r_c), 2001))
+        tabs[f"{tag}_probe_r"] = r
+        tabs[f"{tag}_probe_nv"] = t.near_field(r)
+        tabs[f"{tag}_probe_fv"] = t.fn_weight(r)
+    save("near_tables", versions=VERSIONS, **tabs)
+    for (name, h, n, seed, delta, r_c, skin) in NEAR_SMALL:
+        rng = np.random.default_rng(seed)
+        raw = rng.uniform(0.0, 1.0, (n, 3)) @ h.T
+        q = rng.normal(size=n)
+        q -= q.mean()
+        kern = SplitKernel(basis=build_pswf(solve_bandwidth(delta)), r_c=r_c)
+        sys_ = ParticleSystem(cell=Cell(h), positions=raw, charges=q)
+        nb = build_cell_list(sys_, r_c, skin=skin)
+        t = build_pair_table(kern)
+        a = short_range(sys_, kern, nb, table=t)
+        b = short_range(sys_, kern, nb)
+        save(name, h=h, pos=sys_.positions, q=q, delta=delta, r_c=r_c, skin=skin,
+             pi=nb.i, pj=nb.j, E_tab=a.energy, F_tab=a.forces, P_tab=a.pressure,
+             count=a.pair_count, E_exact=b.energy, F_exact=b.forces, P_exact=b.pressure,
+             versions=VERSIONS)
+    for idx in (0, 1, 2):
+        w, raw, q = workloads.generate(idx, wrap=False)
+        kern = SplitKernel(basis=build_pswf(solve_bandwidth(w.delta)), r_c=w.r_c)
+        cell = Cell(np.asarray(w.h, dtype=float))
+        sys_ = ParticleSystem(cell=cell, positions=raw, charges=q)
+        nb = build_cell_list(sys_, w.r_c)
+        a = short_range(sys_, kern, nb, table=build_pair_table(kern))
+        F = a.forces
+        stride = 1 if idx == 0 else 97
+        sel = np.arange(0, w.n, stride)
+        extra = {}
+        if idx == 0:
+            params = EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P)
+            solver = CoulombSolver(cell, params)
+            solver.rebind_cell(cell, fixed_M=tuple(w.M))
+            tot = solver.evaluate(sys_)
+            extra = dict(tot_u=np.array([tot.u_near, tot.u_far, tot.u_self, tot.u_background]),
+                         tot_F=tot.forces, tot_P=tot.pressure, tot_count=tot.pair_count)
+        save(f"near_cfg{idx}", E=a.energy, P=a.pressure, count=a.pair_count, F_idx=sel,
+             F_sel=F[sel], F_sum=F.sum(axis=0),
+             F_rms=np.sqrt(np.mean(np.sum(F * F, axis=1))), versions=VERSIONS, **extra)
+        del nb, a, F
+
+
 if __name__ == "__main__":
-    window_tables()
-    small_cases()
-    triclinic_cases()
-    configs()
+    parts = sys.argv[1:] or ["window", "small", "triclinic", "configs", "near"]
+    if "window" in parts:
+        window_tables()
+    if "small" in parts:
+        small_cases()
+    if "triclinic" in parts:
+        triclinic_cases()
+    if "configs" in parts:
+        configs()
+    if "near" in parts:
+        near_cases()

@@ -1,0 +1,294 @@
+"""Near field: realspace.short_range / build_cell_list on
+the B200 (csrc/esp_near.cu) against the reference goldens
+(tests/golden/near_*.npz, made by running the reference) and the CPU oracle.
+
+CPU tests pin the oracle restatement and the host pair-table construction
+to the reference.  GPU tests (``-m gpu``) run the CUDA pair sum through the
+C ABI.  Tolerances: fp64 energy and pressure (Frobenius) within 1e-10
+relative, forces within 1e-10 rms-relative, pair counts exact.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import esp_oracle as O
+from paper_2601_00161_b200 import workloads
+
+TOL = 1e-10
+TABLES = [("d1e-5_rc10", 1e-5, 10.0), ("d1e-7_rc10", 1e-7, 10.0),
+          ("d1e-8_rc1", 1e-8, 1.0), ("d1e-7_rc12", 1e-7, 12.0)]
+SMALL = ["near_brick", "near_cube_skin", "near_tri", "near_tight"]
+
+
+def _basis(delta):
+    return O.build_basis(O.solve_bandwidth(delta))
+
+
+# ---------------------------------------------------------------- CPU: pins
+
+
+@pytest.mark.parametrize("tag,delta,r_c", TABLES)
+def test_oracle_pair_table_matches_reference(tag, delta, r_c):
+    g = golden("near_tables")
+    t = O.pair_table(_basis(delta), r_c)
+    assert t.r_in == float(g[f"{tag}_rin"])
+    np.testing.assert_array_equal(t.smooth, g[f"{tag}_smooth"])
+    np.testing.assert_array_equal(t.fn, g[f"{tag}_fn"])
+    np.testing.assert_array_equal(t.smooth_spline.c, g[f"{tag}_sc"])
+    np.testing.assert_array_equal(t.fn_spline.c, g[f"{tag}_fc"])
+    nv, fv = O.table_values(t, g[f"{tag}_probe_r"])
+    np.testing.assert_array_equal(nv, g[f"{tag}_probe_nv"])
+    np.testing.assert_array_equal(fv, g[f"{tag}_probe_fv"])
+
+
+@pytest.mark.parametrize("tag,delta,r_c", TABLES)
+def test_package_pair_table_bit_identical(tag, delta, r_c):
+    """The host setup of the product (realspace.build_pair_table) builds the
+    reference's table bit for bit."""
+    from paper_2601_00161_b200 import SplitKernel, build_pswf, solve_bandwidth
+    from paper_2601_00161_b200.realspace import build_pair_table
+    g = golden("near_tables")
+    t = build_pair_table(SplitKernel(basis=build_pswf(solve_bandwidth(delta)), r_c=r_c))
+    assert t.r_in == float(g[f"{tag}_rin"])
+    np.testing.assert_array_equal(t.smooth_coeffs, g[f"{tag}_smooth"])
+    np.testing.assert_array_equal(t.fn_coeffs, g[f"{tag}_fn"])
+    np.testing.assert_array_equal(t.smooth_spline.c, g[f"{tag}_sc"])
+    np.testing.assert_array_equal(t.fn_spline.c, g[f"{tag}_fc"])
+    np.testing.assert_array_equal(t.smooth_spline.x, g[f"{tag}_x"])
+    np.testing.assert_array_equal(t.near_field(g[f"{tag}_probe_r"]), g[f"{tag}_probe_nv"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_oracle_short_range_matches_reference(name):
+    g = golden(name)
+    b = _basis(float(g["delta"]))
+    r_c = float(g["r_c"])
+    i, j = O.pairs_within(g["h"], g["pos"], r_c + float(g["skin"]))
+    np.testing.assert_array_equal(i, g["pi"])
+    np.testing.assert_array_equal(j, g["pj"])
+    t = O.pair_table(b, r_c)
+    E, F, P, cnt = O.short_range(g["h"], g["pos"], g["q"], i, j, b, r_c, t)
+    assert cnt == int(g["count"])
+    assert O.rel_scalar(E, g["E_tab"]) <= 1e-13
+    assert O.rel_frobenius(P, g["P_tab"]) <= 1e-13
+    assert O.rms_rel_forces(F, g["F_tab"]) <= 1e-13
+    E, F, P, _ = O.short_range(g["h"], g["pos"], g["q"], i, j, b, r_c, None)
+    assert O.rel_scalar(E, g["E_exact"]) <= 1e-13
+    assert O.rel_frobenius(P, g["P_exact"]) <= 1e-13
+    assert O.rms_rel_forces(F, g["F_exact"]) <= 1e-13
+
+
+def test_oracle_config0_near_matches_reference():
+    g = golden("near_cfg0")
+    w, pos, q = workloads.generate(0)
+    b = _basis(w.delta)
+    i, j = O.pairs_within_kdtree(np.diag(w.h), pos, w.r_c)
+    E, F, P, cnt = O.short_range(w.h, pos, q, i, j, b, w.r_c, O.pair_table(b, w.r_c))
+    assert cnt == int(g["count"])
+    assert O.rel_scalar(E, g["E"]) <= 1e-13
+    assert O.rel_frobenius(P, g["P"]) <= 1e-13
+    assert O.rms_rel_forces(F, g["F_sel"]) <= 1e-13
+
+
+def test_geometry_error_and_neighbor_list_host():
+    from paper_2601_00161_b200 import Cell
+    from paper_2601_00161_b200.errors import CellError, GeometryError
+    from paper_2601_00161_b200.system import NeighborList, check_cutoff, minimum_image
+    with pytest.raises(GeometryError):
+        check_cutoff(Cell.orthorhombic([10.0, 10.0, 10.0]), 5.0)
+    assert issubclass(GeometryError, CellError)
+    nb = NeighborList(i=np.array([0, 1]), j=np.array([1, 2]), r_c=1.0, skin=0.0)
+    assert nb.n_pairs == 2
+    c = Cell.orthorhombic([4.0, 5.0, 6.0])
+    np.testing.assert_allclose(minimum_image(c, np.array([[3.5, -4.0, 2.9]])),
+                               [[-0.5, 1.0, 2.9]])
+
+
+# ------------------------------------------------------------- GPU: parity
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _kern(delta, r_c):
+    from paper_2601_00161_b200 import SplitKernel, build_pswf, solve_bandwidth
+    return SplitKernel(basis=build_pswf(solve_bandwidth(delta)), r_c=r_c)
+
+
+def _sys(h, pos, q):
+    from paper_2601_00161_b200 import Cell, ParticleSystem
+    return ParticleSystem(cell=Cell(np.asarray(h, dtype=float)), positions=pos, charges=q)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("use_table", [True, False])
+@pytest.mark.parametrize("listed", [False, True])
+def test_short_range_small_against_reference(name, use_table, listed):
+    _torch()
+    from paper_2601_00161_b200.realspace import build_pair_table, short_range
+    from paper_2601_00161_b200.system import NeighborList
+    g = golden(name)
+    r_c = float(g["r_c"])
+    if not listed and float(g["skin"]) > 0.0:
+        pytest.skip("cell-list path enumerates pairs within r_c (no skin)")
+    kern = _kern(float(g["delta"]), r_c)
+    table = build_pair_table(kern) if use_table else None
+    sys_ = _sys(g["h"], g["pos"], g["q"])
+    nb = NeighborList(i=g["pi"], j=g["pj"], r_c=r_c, skin=float(g["skin"])) if listed else None
+    res = short_range(sys_, kern, nb, table=table)
+    sfx = "tab" if use_table else "exact"
+    assert res.pair_count == int(g["count"])
+    assert O.rel_scalar(res.energy, g[f"E_{sfx}"]) <= TOL
+    assert O.rel_frobenius(res.pressure, g[f"P_{sfx}"]) <= TOL
+    assert O.rms_rel_forces(res.forces, g[f"F_{sfx}"]) <= TOL
+    np.testing.assert_array_equal(res.pressure, res.pressure.T)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx", [0, 1, 2])
+@pytest.mark.parametrize("div", [1, 2, 3])
+def test_short_range_configs_against_reference(idx, div):
+    torch = _torch()
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table, out7_to_pressure
+    g = golden(f"near_cfg{idx}")
+    w, pos, q = workloads.generate(idx)
+    kern = _kern(w.delta, w.r_c)
+    plan = NearFieldPlan(kern, build_pair_table(kern), capacity=w.n, cell_div=div)
+    plan.set_cell(w.h)
+    out7, F, st = plan.evaluate(torch.as_tensor(pos, device="cuda"),
+                                torch.as_tensor(q, device="cuda"))
+    st = st.cpu().numpy()
+    assert int(st[0]) == int(g["count"]) and int(st[1]) == -1
+    E, P = out7_to_pressure(out7)
+    F = F.cpu().numpy()
+    assert O.rel_scalar(E, g["E"]) <= TOL
+    assert O.rel_frobenius(P, g["P"]) <= TOL
+    assert O.rms_rel_forces(F[g["F_idx"]], g["F_sel"]) <= TOL
+    assert np.abs(F.sum(axis=0)).max() <= 1e-9 * float(g["F_rms"]) * w.n ** 0.5
+
+
+@pytest.mark.gpu
+def test_coulomb_solver_totals_config0_against_reference():
+    """CoulombSolver.evaluate (evaluate.py:114-144): near + far + self +
+    background on the device, against the reference's totals."""
+    _torch()
+    from paper_2601_00161_b200 import CoulombSolver, EwaldParameters
+    g = golden("near_cfg0")
+    w, pos, q = workloads.generate(0)
+    solver = CoulombSolver(_sys(w.h, pos, q).cell,
+                           EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                           fixed_M=w.M))
+    out = solver.evaluate(_sys(w.h, pos, q))
+    u = g["tot_u"]
+    for got, want in zip((out.u_near, out.u_far, out.u_self, out.u_background), u):
+        assert abs(got - want) <= TOL * max(abs(want), 1.0)
+    assert O.rel_scalar(out.energy, float(np.sum(u))) <= TOL
+    assert out.pair_count == int(g["tot_count"])
+    assert O.rel_frobenius(out.pressure, g["tot_P"]) <= TOL
+    assert O.rms_rel_forces(out.forces, g["tot_F"]) <= TOL
+
+
+@pytest.mark.gpu
+def test_near_config3_triclinic_rows_against_oracle():
+    """Config 3 (1M charges, triclinic): forces on 64 particles against the
+    oracle's brute-force rows; momentum and pressure symmetry globally."""
+    torch = _torch()
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table, out7_to_pressure
+    w, pos, q = workloads.generate(3)
+    kern = _kern(w.delta, w.r_c)
+    table = build_pair_table(kern)
+    plan = NearFieldPlan(kern, table, capacity=w.n)
+    plan.set_cell(w.h)
+    out7, F, st = plan.evaluate(torch.as_tensor(pos, device="cuda"),
+                                torch.as_tensor(q, device="cuda"))
+    F = F.cpu().numpy()
+    rows = np.random.default_rng(5).choice(w.n, 64, replace=False)
+    b = _basis(w.delta)
+    ref = O.short_range_rows(w.h, pos, q, rows, b, w.r_c, O.pair_table(b, w.r_c))
+    assert O.rms_rel_forces(F[rows], ref) <= TOL
+    assert np.abs(F.sum(axis=0)).max() <= 1e-8 * np.sqrt(np.mean(np.sum(F * F, 1))) * w.n ** 0.5
+    E, P = out7_to_pressure(out7)
+    assert np.isfinite(E) and int(st.cpu()[0]) > 0
+
+
+@pytest.mark.gpu
+def test_near_deterministic_and_permutation_invariant():
+    torch = _torch()
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table
+    w, pos, q = workloads.generate(1)
+    kern = _kern(w.delta, w.r_c)
+    plan = NearFieldPlan(kern, build_pair_table(kern), capacity=w.n)
+    plan.set_cell(w.h)
+    P = torch.as_tensor(pos, device="cuda")
+    Q = torch.as_tensor(q, device="cuda")
+    a7, aF, _ = plan.evaluate(P, Q)
+    a7, aF = a7.clone(), aF.clone()
+    b7, bF, _ = plan.evaluate(P, Q)
+    assert torch.equal(a7, b7) and torch.equal(aF, bF)
+    perm = np.random.default_rng(0).permutation(w.n)
+    c7, cF, _ = plan.evaluate(P[perm].contiguous(), Q[perm].contiguous())
+    assert O.rel_scalar(c7[0].item(), a7[0].item()) <= 1e-13
+    assert O.rms_rel_forces(cF.cpu().numpy(), aF.cpu().numpy()[perm]) <= 1e-13
+
+
+@pytest.mark.gpu
+def test_near_edge_cases():
+    torch = _torch()
+    from paper_2601_00161_b200 import Cell, ParticleSystem
+    from paper_2601_00161_b200.errors import GeometryError, SingularPairError
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table, short_range
+    from paper_2601_00161_b200.system import NeighborList
+    kern = _kern(1e-5, 1.5)
+    table = build_pair_table(kern)
+    cell = Cell.orthorhombic([10.0, 10.0, 10.0])
+    # coincident particles raise, through both paths
+    s = ParticleSystem(cell=cell, positions=np.array([[1.0, 1.0, 1.0], [1.0, 1.0, 1.0]]),
+                       charges=np.array([1.0, -1.0]))
+    with pytest.raises(SingularPairError):
+        short_range(s, kern, None, table)
+    with pytest.raises(SingularPairError):
+        short_range(s, kern, NeighborList(i=np.array([0]), j=np.array([1]), r_c=1.5, skin=0.0),
+                    table)
+    # beyond the cutoff: exact zeros; single pair across the periodic face
+    s = ParticleSystem(cell=cell, positions=np.array([[0.2, 5.0, 5.0], [9.6, 5.0, 5.0]]),
+                       charges=np.array([1.0, -1.0]))
+    r = short_range(s, kern, None, table)
+    d = 0.6
+    assert r.pair_count == 1
+    assert r.energy == pytest.approx(-float(table.near_field(np.array([d]))[0]), rel=1e-12)
+    assert r.forces[0, 0] == pytest.approx(-float(table.fn_weight(np.array([d]))[0]) / d ** 2,
+                                           rel=1e-12)
+    s = ParticleSystem(cell=cell, positions=np.array([[1.0, 1.0, 1.0], [5.0, 1.0, 1.0]]),
+                       charges=np.array([1.0, -1.0]))
+    r = short_range(s, kern, None, table)
+    assert r.energy == 0.0 and r.pair_count == 0 and not np.any(r.forces)
+    assert not np.any(r.pressure)
+    # one particle, and a cutoff too large for the cell
+    s = ParticleSystem(cell=cell, positions=np.array([[1.0, 2.0, 3.0]]), charges=np.array([1.0]))
+    r = short_range(s, kern, None, table)
+    assert r.energy == 0.0 and r.pair_count == 0
+    plan = NearFieldPlan(_kern(1e-5, 6.0), None)
+    with pytest.raises(GeometryError):
+        plan.set_cell(cell)
+    # empty device system
+    plan = NearFieldPlan(kern, table)
+    plan.set_cell(cell)
+    out7, F, st = plan.evaluate(torch.zeros((0, 3), dtype=torch.float64, device="cuda"),
+                                torch.zeros(0, dtype=torch.float64, device="cuda"))
+    assert not torch.any(out7) and int(st[0]) == 0
+    # unwrapped positions (outside the cell) give the wrapped result
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0, 10, (200, 3))
+    qq = rng.normal(size=200)
+    base = plan.evaluate(torch.as_tensor(pos, device="cuda"), torch.as_tensor(qq, device="cuda"))
+    shifted = pos + np.array([10.0, -20.0, 30.0]) * (rng.integers(0, 2, (200, 1)))
+    moved = plan.evaluate(torch.as_tensor(shifted, device="cuda"),
+                          torch.as_tensor(qq, device="cuda"))
+    assert O.rel_scalar(moved[0][0].item(), base[0][0].item()) <= 1e-12
+    assert O.rms_rel_forces(moved[1].cpu().numpy(), base[1].cpu().numpy()) <= 1e-12
