@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--config", type=int, default=CONFIG)
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-near", dest="near", action="store_false",
+                    help="skip the near-field / whole-Coulomb-step leg")
     ap.add_argument("--profile-only", action="store_true",
                     help="run a few steps for ncu (no JSON contract line)")
     ap.add_argument("--slab", action="store_true",
@@ -311,6 +313,7 @@ def run_ours(args):
         ms_po = timed(g_po.replay, K, W)
         ms_e2e = timed(hs.launch, K, W)
         ms_eager = timed(lambda: step(True), K, W)
+        near = near_field_leg(w, pos, q, solver, timed, K, W) if args.near else None
     clocks = clk.summary()
     torch.cuda.synchronize()
     assert np.isfinite(hs.forces.numpy()).all() and np.isfinite(hs.out7.numpy()).all()
@@ -393,6 +396,9 @@ def run_ours(args):
         "kernel_ms": {k: round(v, 5) for k, v in prof.items()},
         "fp64_peak_tflops_measured": round(fp64_tflops, 2),
     }
+    if near is not None:
+        near["fp64_frac_est"] = round(near["fp64_tflops_est"] / fp64_tflops, 4)
+        line["near_field"] = near
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(args.config)
     if rank == 0:
@@ -400,6 +406,54 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+NEAR_FLOPS_PER_DIRECTED_PAIR = 55   # table path, DESIGN.md §9
+NEAR_FLOPS_PER_CANDIDATE = 8
+
+
+def near_field_leg(w, pos, q, kspace, timed, K, W):
+    """Near field on the same particles: the device cell
+    list + fused pair pass alone, and the whole Coulomb step (near + far +
+    forces summed) as CoulombSolver.evaluate_device runs it (eager launches).
+    Reported beside the headline, which stays the k-space metric."""
+    import torch
+
+    from paper_2601_00161_b200 import SplitKernel
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table
+
+    kern = SplitKernel(basis=kspace.kern.basis, r_c=w.r_c)
+    table = build_pair_table(kern)
+    plan = NearFieldPlan(kern, table, capacity=w.n)
+    plan.set_cell(w.h)
+    o7 = torch.empty(7, dtype=torch.float64, device=pos.device)
+    st = torch.empty(3, dtype=torch.int64, device=pos.device)
+    Fn = torch.empty((w.n, 3), dtype=torch.float64, device=pos.device)
+    o7f = torch.empty(7, dtype=torch.float64, device=pos.device)
+
+    def near():
+        plan.evaluate(pos, q, forces=Fn, out7=o7, stats=st)
+
+    def coulomb():
+        kspace.evaluate_device(pos, q, True, o7f, Fn)
+        plan.evaluate(pos, q, forces=Fn, accumulate=True, out7=o7, stats=st)
+
+    kn, wn = max(3, min(K, 20)), max(W, 3)
+    ms_near = timed(near, kn, wn)
+    ms_all = timed(coulomb, kn, wn)
+    pairs = int(st[0].item())
+    directed = 2.0 * pairs
+    tfl = directed * NEAR_FLOPS_PER_DIRECTED_PAIR / (ms_near * 1e-3) / 1e12
+    info = plan.info()
+    return {"ms_per_step": ms_near, "pairs_within_rc": pairs,
+            "directed_pair_evals_per_s": directed / (ms_near * 1e-3),
+            "fp64_tflops_est": round(tfl, 3),
+            "flops_model": f"{NEAR_FLOPS_PER_DIRECTED_PAIR} flop per directed pair (table path)",
+            "cells": list(info["cells"]), "launches_per_step": info["launches"],
+            "coulomb_step": {"ms_per_step": ms_all, "value": w.n / (ms_all * 1e-3),
+                             "unit": UNIT,
+                             "what": "far (k-space, eager) + near (cell list) + summed forces"},
+            "steps": kn}
 
 
 # --------------------------------------------------------------------------

@@ -14,7 +14,8 @@ import os
 from .errors import EspCudaError, MeshError, ParameterError, PlanningError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libesp_b200.so")
+# ESP_LIB overrides the library path (experiments with variant builds)
+LIB_PATH = os.environ.get("ESP_LIB") or os.path.join(_HERE, "libesp_b200.so")
 
 ESP_OK = 0
 ESP_ERR_PLANNING = 1

@@ -42,7 +42,13 @@ using esp::set_error;
 
 namespace {
 
-constexpr int kNearThreads = 128;  // 4 warps per cell CTA
+#ifndef ESP_NEAR_THREADS
+#define ESP_NEAR_THREADS 256
+#endif
+#ifndef ESP_NEAR_MINB
+#define ESP_NEAR_MINB 1
+#endif
+constexpr int kNearThreads = ESP_NEAR_THREADS;  // warps per cell CTA x 32
 constexpr int kQueue = 64;         // per-warp compaction queue (2 x 32)
 constexpr int kPolyMax = 16;
 constexpr int kLegMax = 64;
@@ -280,7 +286,7 @@ __device__ __forceinline__ void drain(const NearConst& C, Acc& a, double qi, con
 // intersect the sphere of radius reach around x_i, and split at the periodic
 // face into at most three contiguous runs of the cell-sorted records, each
 // with one image shift.  Hits are compacted through the warp's queue.
-__global__ void __launch_bounds__(kNearThreads)
+__global__ void __launch_bounds__(kNearThreads, ESP_NEAR_MINB)
     k_near_pairs(const __grid_constant__ NearConst C, const double4* __restrict__ rec,
                  const int* __restrict__ cell_start, const int* __restrict__ perm, CellGeom g,
                  const double* __restrict__ tab, int accumulate, double* __restrict__ forces,
@@ -300,7 +306,8 @@ __global__ void __launch_bounds__(kNearThreads)
   double* qz = s_q[warp][2];
   double* qj = s_q[warp][3];
   const unsigned lt = (1u << lane) - 1u;
-  const double wx = g.h[0] / nc0, wy = g.h[4] / nc1, wz = g.h[8] / nc2;
+  const double wy = g.h[4] / nc1, wz = g.h[8] / nc2;
+  const double iwx = nc0 / g.h[0];
   const double reach2 = C.reach2;
   for (int i = i0 + warp; i < i1; i += kNearThreads / 32) {
     const double4 ri = rec[i];
@@ -309,8 +316,7 @@ __global__ void __launch_bounds__(kNearThreads)
     int qn = 0;
     for (int oz = -div; oz <= div; ++oz) {
       int nz = cz + oz, sz = 0;
-      while (nz < 0) { nz += nc2; --sz; }
-      while (nz >= nc2) { nz -= nc2; ++sz; }
+      if (nz < 0) { nz += nc2; sz = -1; } else if (nz >= nc2) { nz -= nc2; sz = 1; }
       double gz2 = 0.0;
       if (g.ortho) {
         const double lo = (cz + oz) * wz;
@@ -320,8 +326,7 @@ __global__ void __launch_bounds__(kNearThreads)
       }
       for (int oy = -div; oy <= div; ++oy) {
         int ny = cy + oy, sy = 0;
-        while (ny < 0) { ny += nc1; --sy; }
-        while (ny >= nc1) { ny -= nc1; ++sy; }
+        if (ny < 0) { ny += nc1; sy = -1; } else if (ny >= nc1) { ny -= nc1; sy = 1; }
         int xlo = cx - div, xhi = cx + div;
         if (g.ortho) {
           const double lo = (cy + oy) * wy;
@@ -329,38 +334,44 @@ __global__ void __launch_bounds__(kNearThreads)
           const double rest = reach2 - gz2 - gap * gap;
           if (rest < 0.0) continue;
           const double chord = sqrt(rest) + g.eps;
-          xlo = max(xlo, (int)floor((ri.x - chord) / wx));
-          xhi = min(xhi, (int)floor((ri.x + chord) / wx));
+          xlo = max(xlo, (int)floor((ri.x - chord) * iwx));
+          xhi = min(xhi, (int)floor((ri.x + chord) * iwx));
         }
         const int row = (nz * nc1 + ny) * nc0;
+        // x_i minus the (y, z) part of the image shift h (sx, sy, sz)
+        const double bx = ri.x - (g.h[1] * sy + g.h[2] * sz);
+        const double by = ri.y - (g.h[4] * sy + g.h[5] * sz);
+        const double bz = ri.z - (g.h[7] * sy + g.h[8] * sz);
         for (int sx = -1; sx <= 1; ++sx) {
           const int ra = sx < 0 ? xlo : (sx == 0 ? max(xlo, 0) : max(xlo, nc0));
           const int rb = sx < 0 ? min(xhi, -1) : (sx == 0 ? min(xhi, nc0 - 1) : xhi);
           if (ra > rb) continue;
           const int j0 = cell_start[row + ra - sx * nc0];
           const int j1 = cell_start[row + rb - sx * nc0 + 1];
-          const bool noshift = (sx | sy | sz) == 0;
-          // image of the run next to this cell: x_j + h (sx, sy, sz)
-          const double shx = g.h[0] * sx + g.h[1] * sy + g.h[2] * sz;
-          const double shy = g.h[3] * sx + g.h[4] * sy + g.h[5] * sz;
-          const double shz = g.h[6] * sx + g.h[7] * sy + g.h[8] * sz;
+          const int self = (sx | sy | sz) == 0 ? i : -1;
+          const double xs = bx - g.h[0] * sx, ys = by - g.h[3] * sx, zs = bz - g.h[6] * sx;
+          // software pipeline: the next batch's record is in flight while
+          // this one is tested
+          double2 nxy = make_double2(0.0, 0.0), nzq = nxy;
+          if (j0 + lane < j1) {
+            const double2* rp = reinterpret_cast<const double2*>(rec + j0 + lane);
+            nxy = __ldg(rp);
+            nzq = __ldg(rp + 1);
+          }
           for (int jb = j0; jb < j1; jb += 32) {
             const int j = jb + lane;
-            bool hit = false;
-            double dx = 0, dy = 0, dz = 0, qjv = 0;
-            if (j < j1) {
-              const double2* rp = reinterpret_cast<const double2*>(rec + j);
-              const double2 xy = __ldg(rp), zq = __ldg(rp + 1);
-              dx = (ri.x - xy.x) - shx;
-              dy = (ri.y - xy.y) - shy;
-              dz = (ri.z - zq.x) - shz;
-              qjv = zq.y;
-              const double r2 = dx * dx + dy * dy + dz * dz;
-              hit = r2 <= reach2 && !(noshift && j == i);
-              if (hit && r2 < C.sing2) {
-                const unsigned long long a_ = (unsigned)perm[i], b_ = (unsigned)perm[j];
-                atomicMin(singular, (min(a_, b_) << 32) | max(a_, b_));
-              }
+            const double2 xy = nxy, zq = nzq;
+            if (j + 32 < j1) {
+              const double2* rp = reinterpret_cast<const double2*>(rec + j + 32);
+              nxy = __ldg(rp);
+              nzq = __ldg(rp + 1);
+            }
+            const double dx = xs - xy.x, dy = ys - xy.y, dz = zs - zq.x;
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            const bool hit = j < j1 && r2 <= reach2 && j != self;
+            if (hit && r2 < C.sing2) {
+              const unsigned long long a_ = (unsigned)perm[i], b_ = (unsigned)perm[j];
+              atomicMin(singular, (min(a_, b_) << 32) | max(a_, b_));
             }
             const unsigned m = __ballot_sync(0xffffffffu, hit);
             if (hit) {
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(kNearThreads)
               qx[slot] = dx;
               qy[slot] = dy;
               qz[slot] = dz;
-              qj[slot] = qjv;
+              qj[slot] = zq.y;
             }
             qn += __popc(m);
             if (qn >= 32) {
