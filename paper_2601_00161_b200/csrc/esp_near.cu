@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,6 +82,7 @@ struct esp_near {
   double volume = 1.0;
   long long cap = 0;
   int div = 2;
+  int kernel = 0;             // 0: staged tile kernel, 1: per-particle rows (ESP_NEAR_KERNEL=rows)
   int have_cell = 0;
   CellGeom g{};
   // tables
@@ -430,6 +432,257 @@ __global__ void __launch_bounds__(kNearThreads, ESP_NEAR_MINB)
   }
 }
 
+// Tile kernel (default).  One CTA per cell, passes of kTileI consecutive
+// particles of the cell (one per warp).  Per pass the candidate rows are
+// trimmed against the bounding box of the pass's particles (orthorhombic
+// cells), split into contiguous runs of cell-sorted records with one image
+// shift each, and the runs' records are staged in shared memory in chunks
+// of kTileCH (image shift applied, structure of arrays), so every warp tests
+// its particle against the same staged records with conflict-free loads.
+// Hits go through the warp's compaction queue as in k_near_pairs; the queue
+// and the accumulators persist across chunks.
+#ifndef ESP_TILE_W
+#define ESP_TILE_W 4
+#endif
+constexpr int kTileW = ESP_TILE_W;    // warps per CTA = particles per pass
+constexpr int kTileI = kTileW;
+constexpr int kTileCH = 1024;         // staged records per chunk
+constexpr int kTileMaxRuns = 3 * 81;  // 3 runs per row, (2 div + 1)^2 rows, div <= 4
+
+struct TileSmem {
+  double jx[kTileCH], jy[kTileCH], jz[kTileCH], jq[kTileCH];
+  int jid[kTileCH];                   // j index, bit 31 set for a shifted image
+  double q[kTileW][4][kQueue];
+  double sh[kTileMaxRuns][3];
+  int j0[kTileMaxRuns];
+  int pref[kTileMaxRuns + 1];
+  int flag[kTileMaxRuns];             // 0x80000000 for shifted runs
+  double box[6];
+  int nruns;
+};
+
+__global__ void __launch_bounds__(kTileW * 32)
+    k_near_tile(const __grid_constant__ NearConst C, const double4* __restrict__ rec,
+                const int* __restrict__ cell_start, const int* __restrict__ perm, CellGeom g,
+                const double* __restrict__ tab, int accumulate, double* __restrict__ forces,
+                double* __restrict__ part, unsigned long long* __restrict__ singular) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int cell = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = cell_start[cell], i1 = cell_start[cell + 1];
+  if (i0 == i1) return;
+  const int nc0 = g.nc[0], nc1 = g.nc[1], nc2 = g.nc[2];
+  const int cx = cell % nc0;
+  const int cy = (cell / nc0) % nc1;
+  const int cz = cell / (nc0 * nc1);
+  const int div = g.div, side = 2 * div + 1, nrows = side * side;
+  const double wy = g.h[4] / nc1, wz = g.h[8] / nc2, iwx = nc0 / g.h[0];
+  const double reach2 = C.reach2;
+  double* qx = S.q[warp][0];
+  double* qy = S.q[warp][1];
+  double* qz = S.q[warp][2];
+  double* qj = S.q[warp][3];
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = i0; base < i1; base += kTileI) {
+    const int ni = min(kTileI, i1 - base);
+    // bounding box of the pass's particles (home-image coordinates)
+    if (tid == 0) {
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (int k = 0; k < ni; ++k) {
+        const double4 r = rec[base + k];
+        lo[0] = fmin(lo[0], r.x); hi[0] = fmax(hi[0], r.x);
+        lo[1] = fmin(lo[1], r.y); hi[1] = fmax(hi[1], r.y);
+        lo[2] = fmin(lo[2], r.z); hi[2] = fmax(hi[2], r.z);
+      }
+      for (int d = 0; d < 3; ++d) {
+        S.box[d] = lo[d];
+        S.box[3 + d] = hi[d];
+      }
+    }
+    __syncthreads();
+    // candidate runs: thread t handles row t (3 run slots each)
+    for (int t = tid; t < nrows; t += kTileW * 32) {
+      const int oy = t % side - div, oz = t / side - div;
+      int ny = cy + oy, sy = 0, nz = cz + oz, sz = 0;
+      if (ny < 0) { ny += nc1; sy = -1; } else if (ny >= nc1) { ny -= nc1; sy = 1; }
+      if (nz < 0) { nz += nc2; sz = -1; } else if (nz >= nc2) { nz -= nc2; sz = 1; }
+      int xlo = cx - div, xhi = cx + div;
+      bool keep = true;
+      if (g.ortho) {
+        const double ylo = (cy + oy) * wy, zlo = (cz + oz) * wz;
+        const double gy = fmax(0.0, fmax(ylo - S.box[4], S.box[1] - (ylo + wy)) - g.eps);
+        const double gz = fmax(0.0, fmax(zlo - S.box[5], S.box[2] - (zlo + wz)) - g.eps);
+        const double rest = reach2 - gy * gy - gz * gz;
+        if (rest < 0.0) {
+          keep = false;
+        } else {
+          const double chord = sqrt(rest) + g.eps;
+          xlo = max(xlo, (int)floor((S.box[0] - chord) * iwx));
+          xhi = min(xhi, (int)floor((S.box[3] + chord) * iwx));
+        }
+      }
+      const int row = (nz * nc1 + ny) * nc0;
+      for (int sx = -1; sx <= 1; ++sx) {
+        const int slot = 3 * t + sx + 1;
+        const int ra = sx < 0 ? xlo : (sx == 0 ? max(xlo, 0) : max(xlo, nc0));
+        const int rb = sx < 0 ? min(xhi, -1) : (sx == 0 ? min(xhi, nc0 - 1) : xhi);
+        int len = 0, j0 = 0;
+        if (keep && ra <= rb) {
+          j0 = cell_start[row + ra - sx * nc0];
+          len = cell_start[row + rb - sx * nc0 + 1] - j0;
+        }
+        S.j0[slot] = j0;
+        S.pref[slot + 1] = len;  // lengths; prefix below
+        S.flag[slot] = (sx | sy | sz) != 0 ? (int)0x80000000 : 0;
+        S.sh[slot][0] = g.h[0] * sx + g.h[1] * sy + g.h[2] * sz;
+        S.sh[slot][1] = g.h[3] * sx + g.h[4] * sy + g.h[5] * sz;
+        S.sh[slot][2] = g.h[6] * sx + g.h[7] * sy + g.h[8] * sz;
+      }
+    }
+    __syncthreads();
+    const int nr = 3 * nrows;
+    if (warp == 0) {
+      // exclusive prefix of the run lengths: lane-contiguous blocks + warp scan
+      const int per = (nr + 31) / 32;  // <= 8 (nr <= 243)
+      const int a0 = lane * per, a1 = min(nr, a0 + per);
+      int lens[8];
+      int sum = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        lens[u] = a0 + u < a1 ? S.pref[a0 + u + 1] : 0;
+        sum += lens[u];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      __syncwarp();
+      int run = incl - sum;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (a0 + u < a1) {
+          S.pref[a0 + u] = run;
+          run += lens[u];
+        }
+      }
+      if (lane == 31) S.pref[nr] = incl;
+    }
+    __syncthreads();
+    const int total = S.pref[nr];
+    const bool active = warp < ni;
+    const int i = base + warp;
+    double4 ri = make_double4(0, 0, 0, 0);
+    if (active) ri = rec[i];
+    Acc a;
+    a.zero();
+    int qn = 0;
+    for (int c0 = 0; c0 < total; c0 += kTileCH) {
+      const int cnt = min(kTileCH, total - c0);
+      // warp-per-run staging: warp w copies the parts of runs w, w + W, ...
+      // that overlap this chunk (destination = run prefix - c0)
+      for (int r = warp; r < nr; r += kTileW) {
+        const int p0 = S.pref[r], p1 = S.pref[r + 1];
+        const int a = max(p0, c0), b = min(p1, c0 + cnt);
+        if (a >= b) continue;
+        const int jb = S.j0[r] - p0;
+        const double shx = S.sh[r][0], shy = S.sh[r][1], shz = S.sh[r][2];
+        const int fl = S.flag[r];
+        for (int c = a + lane; c < b; c += 32) {
+          const int j = jb + c;
+          const double2* rp = reinterpret_cast<const double2*>(rec + j);
+          const double2 xy = __ldg(rp), zq = __ldg(rp + 1);
+          const int k = c - c0;
+          S.jx[k] = xy.x + shx;
+          S.jy[k] = xy.y + shy;
+          S.jz[k] = zq.x + shz;
+          S.jq[k] = zq.y;
+          S.jid[k] = j | fl;
+        }
+      }
+      __syncthreads();
+      if (active) {
+        for (int kb = 0; kb < cnt; kb += 32) {
+          const int k = kb + lane;
+          bool hit = false;
+          double dx = 0.0, dy = 0.0, dz = 0.0, qv = 0.0;
+          int jid = -1;
+          if (k < cnt) {
+            dx = ri.x - S.jx[k];
+            dy = ri.y - S.jy[k];
+            dz = ri.z - S.jz[k];
+            qv = S.jq[k];
+            jid = S.jid[k];
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            hit = r2 <= reach2 && jid != i;
+            if (hit && r2 < C.sing2) {
+              const unsigned long long a_ = (unsigned)perm[i],
+                                       b_ = (unsigned)perm[jid & 0x7fffffff];
+              atomicMin(singular, (min(a_, b_) << 32) | max(a_, b_));
+            }
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (hit) {
+            const int slot = qn + __popc(m & lt);
+            qx[slot] = dx;
+            qy[slot] = dy;
+            qz[slot] = dz;
+            qj[slot] = qv;
+          }
+          qn += __popc(m);
+          if (qn >= 32) {
+            __syncwarp();
+            drain(C, a, ri.w, qx, qy, qz, qj, lane, 32, tab);
+            __syncwarp();
+            if (lane < qn - 32) {
+              qx[lane] = qx[lane + 32];
+              qy[lane] = qy[lane + 32];
+              qz[lane] = qz[lane + 32];
+              qj[lane] = qj[lane + 32];
+            }
+            qn -= 32;
+            __syncwarp();
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (active) {
+      __syncwarp();
+      drain(C, a, ri.w, qx, qy, qz, qj, lane, qn, tab);
+      __syncwarp();
+      const double fx = warp_sum(a.fx), fy = warp_sum(a.fy), fz = warp_sum(a.fz);
+      const double e = warp_sum(a.e), vxx = warp_sum(a.vxx), vxy = warp_sum(a.vxy),
+                   vxz = warp_sum(a.vxz), vyy = warp_sum(a.vyy), vyz = warp_sum(a.vyz),
+                   vzz = warp_sum(a.vzz), cn = warp_sum(a.n);
+      if (lane == 0) {
+        const long long oi = perm[i];
+        if (accumulate) {
+          forces[3 * oi] += fx;
+          forces[3 * oi + 1] += fy;
+          forces[3 * oi + 2] += fz;
+        } else {
+          forces[3 * oi] = fx;
+          forces[3 * oi + 1] = fy;
+          forces[3 * oi + 2] = fz;
+        }
+        double* pp = part + 8 * (size_t)i;
+        pp[0] = 0.5 * e;
+        pp[1] = 0.5 * vxx;
+        pp[2] = 0.5 * vxy;
+        pp[3] = 0.5 * vxz;
+        pp[4] = 0.5 * vyy;
+        pp[5] = 0.5 * vyz;
+        pp[6] = 0.5 * vzz;
+        pp[7] = cn;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Explicit pair list (realspace.short_range with a caller NeighborList):
 // directed entries sorted by endpoint; one warp per particle sums its entries
 // in list order.  Entry e = 2 * pair + side; side 0 is particle i (+f), side 1
@@ -731,7 +984,17 @@ int esp_near_create(const esp_near_desc* d, esp_near** out) {
     return ESP_ERR_PARAM;
   }
   esp_near* p = new esp_near();
-  p->div = d->cell_div > 0 ? std::min(d->cell_div, 4) : 2;
+  p->div = d->cell_div > 0 ? std::min(d->cell_div, 4) : 3;
+  {
+    const char* k = std::getenv("ESP_NEAR_KERNEL");
+    p->kernel = (k && std::strcmp(k, "rows") == 0) ? 1 : 0;
+    if (cudaFuncSetAttribute(k_near_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(TileSmem)) != cudaSuccess) {
+      set_error("near-field tile kernel: shared-memory opt-in failed");
+      delete p;
+      return ESP_ERR_CUDA;
+    }
+  }
   p->reach = d->reach;
   int st = near_reserve(p, std::max<long long>(d->max_particles, 1));
   if (st != ESP_OK) {
@@ -910,9 +1173,17 @@ int esp_near_evaluate(esp_near* p, const double* d_pos, const double* d_q, int64
   k_near_sorted<<<grid, B, 0, s>>>(p->d_key_sorted, p->d_perm, p->d_rec_u, n, p->g.ncells,
                                    p->d_rec, p->d_cell_start);
   p->launches++;
-  k_near_pairs<<<(unsigned)p->g.ncells, kNearThreads, 0, s>>>(
-      p->c, p->d_rec, p->d_cell_start, p->d_perm, p->g, p->d_tab, (flags & ESP_NEAR_ACCUMULATE) ? 1 : 0, d_forces, p->d_part,
-      (unsigned long long*)(d_stats + 1));
+  if (p->kernel == 1) {
+    k_near_pairs<<<(unsigned)p->g.ncells, kNearThreads, 0, s>>>(
+        p->c, p->d_rec, p->d_cell_start, p->d_perm, p->g, p->d_tab,
+        (flags & ESP_NEAR_ACCUMULATE) ? 1 : 0, d_forces, p->d_part,
+        (unsigned long long*)(d_stats + 1));
+  } else {
+    k_near_tile<<<(unsigned)p->g.ncells, kTileW * 32, sizeof(TileSmem), s>>>(
+        p->c, p->d_rec, p->d_cell_start, p->d_perm, p->g, p->d_tab,
+        (flags & ESP_NEAR_ACCUMULATE) ? 1 : 0, d_forces, p->d_part,
+        (unsigned long long*)(d_stats + 1));
+  }
   p->launches++;
   NEAR_CUDA(cudaGetLastError());
   return near_reduce(p, n, d_out7, (long long*)d_stats, s);
