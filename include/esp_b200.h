@@ -276,7 +276,15 @@ int esp_near_evaluate_pairs(esp_near* plan, const double* d_pos, const double* d
                             int64_t n, const int64_t* d_i, const int64_t* d_j,
                             int64_t n_pairs, int32_t flags, double* d_out7,
                             double* d_forces, int64_t* d_stats, void* stream);
-/* info8 = {nc_x, nc_y, nc_z, stencil cells, capacity, launches last call,
+/* Pair enumeration (system.build_cell_list, system.py:144-222): every
+ * unordered pair within reach under the minimum image, as i < j (original
+ * indices) sorted by (i, j), into plan-owned buffers; *n_pairs = the count
+ * (host).  Synchronises `stream`.  esp_near_copy_pairs then copies the list
+ * into caller int64 device arrays of n_pairs entries each.                 */
+int esp_near_build_pairs(esp_near* plan, const double* d_pos, int64_t n, int64_t* n_pairs,
+                         void* stream);
+int esp_near_copy_pairs(esp_near* plan, int64_t* d_i, int64_t* d_j, void* stream);
+/* info8 = {nc_x, nc_y, nc_z, candidate rows, capacity, launches last call,
  *          cells per reach, use_table}                                      */
 int esp_near_info(const esp_near* plan, int64_t* info8);
 

@@ -22,8 +22,8 @@ from .pswf import (PswfBasis, WindowTable, build_pswf, eval_psi0, solve_bandwidt
                    tabulate_window)
 from .solver import (CoulombSolver, EnergyBreakdown, EwaldParameters, KSpaceResult,
                      KSpaceSolver, evaluate_system)
-from .realspace import (NearFieldPlan, PairTable, ShortRangeResult, build_pair_table,
-                        short_range)
+from .realspace import (NearFieldPlan, PairTable, ShortRangeResult, build_cell_list,
+                        build_pair_table, short_range)
 from .system import Cell, NeighborList, ParticleSystem, check_cutoff, minimum_image
 
 __version__ = "0.1.0"
@@ -39,5 +39,5 @@ __all__ = [
     "plan_grid", "self_energy", "solve_bandwidth", "spread_charges", "tabulate_window",
     "GeometryError", "RealspaceError", "SingularPairError", "far_field", "fn_weight",
     "near_field", "NearFieldPlan", "PairTable", "ShortRangeResult", "build_pair_table",
-    "short_range", "NeighborList", "minimum_image",
+    "short_range", "NeighborList", "minimum_image", "build_cell_list",
 ]

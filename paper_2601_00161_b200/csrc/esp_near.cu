@@ -29,6 +29,7 @@
 // scipy PPoly (power sum, interval search as find_interval), 1/r is an IEEE
 // division; exact mode is the Legendre series (numpy legval, Clenshaw).
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -109,6 +110,15 @@ struct esp_near {
   long long* d_pent_sorted = nullptr;
   void* d_psort_tmp = nullptr;
   size_t psort_bytes = 0;
+  // enumerated pair list (esp_near_build_pairs)
+  long long list_cap = 0;
+  long long list_n = 0;
+  unsigned long long* d_list_keys = nullptr;
+  unsigned long long* d_list_keys2 = nullptr;
+  long long* d_list_i = nullptr;
+  long long* d_list_j = nullptr;
+  void* d_list_tmp = nullptr;
+  size_t list_tmp_bytes = 0;
   int launches = 0;
 };
 
@@ -252,7 +262,7 @@ __global__ void k_near_cells(const double* __restrict__ pos, const double* __res
   }
   key[i] = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
   idx[i] = (int)i;
-  rec[i] = make_double4(hx, hy, hz, q[i]);
+  rec[i] = make_double4(hx, hy, hz, q ? q[i] : 0.0);
 }
 
 // Sorted records and cell start offsets (lower bound of each cell id).
@@ -787,6 +797,98 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Pair enumeration (system.build_cell_list, system.py:144-222): one warp per
+// particle i (cell-sorted order) walks the same trimmed candidate rows as
+// k_near_pairs and keeps the partners j with original index above i's and
+// r^2 <= reach^2.  EMIT = false counts them; EMIT = true writes the keys
+// (orig_i << 32 | orig_j) at the particle's offset.  The caller sorts the
+// keys, which gives the reference's lexicographic (i, j) order.
+template <bool EMIT>
+__global__ void __launch_bounds__(128)
+    k_pair_enum(const double4* __restrict__ rec, const int* __restrict__ cell_start,
+                const int* __restrict__ key_sorted, const int* __restrict__ perm, long long n,
+                CellGeom g, double reach2,
+                const long long* __restrict__ offset, unsigned long long* __restrict__ out,
+                long long* __restrict__ count64) {
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int nc0 = g.nc[0], nc1 = g.nc[1], nc2 = g.nc[2];
+  const int cell = key_sorted[i];
+  const int cx = cell % nc0, cy = (cell / nc0) % nc1, cz = cell / (nc0 * nc1);
+  const int div = g.div;
+  const double wy = g.h[4] / nc1, wz = g.h[8] / nc2, iwx = nc0 / g.h[0];
+  const double4 ri = rec[i];
+  const unsigned oi = (unsigned)perm[i];
+  const unsigned lt = (1u << lane) - 1u;
+  long long pos = EMIT ? offset[i] : 0;
+  int found = 0;
+  for (int oz = -div; oz <= div; ++oz) {
+    int nz = cz + oz, sz = 0;
+    if (nz < 0) { nz += nc2; sz = -1; } else if (nz >= nc2) { nz -= nc2; sz = 1; }
+    double gz2 = 0.0;
+    if (g.ortho) {
+      const double lo = (cz + oz) * wz;
+      const double gap = fmax(0.0, fmax(lo - ri.z, ri.z - (lo + wz)) - g.eps);
+      gz2 = gap * gap;
+      if (gz2 > reach2) continue;
+    }
+    for (int oy = -div; oy <= div; ++oy) {
+      int ny = cy + oy, sy = 0;
+      if (ny < 0) { ny += nc1; sy = -1; } else if (ny >= nc1) { ny -= nc1; sy = 1; }
+      int xlo = cx - div, xhi = cx + div;
+      if (g.ortho) {
+        const double lo = (cy + oy) * wy;
+        const double gap = fmax(0.0, fmax(lo - ri.y, ri.y - (lo + wy)) - g.eps);
+        const double rest = reach2 - gz2 - gap * gap;
+        if (rest < 0.0) continue;
+        const double chord = sqrt(rest) + g.eps;
+        xlo = max(xlo, (int)floor((ri.x - chord) * iwx));
+        xhi = min(xhi, (int)floor((ri.x + chord) * iwx));
+      }
+      const int row = (nz * nc1 + ny) * nc0;
+      const double bx = ri.x - (g.h[1] * sy + g.h[2] * sz);
+      const double by = ri.y - (g.h[4] * sy + g.h[5] * sz);
+      const double bz = ri.z - (g.h[7] * sy + g.h[8] * sz);
+      for (int sx = -1; sx <= 1; ++sx) {
+        const int ra = sx < 0 ? xlo : (sx == 0 ? max(xlo, 0) : max(xlo, nc0));
+        const int rb = sx < 0 ? min(xhi, -1) : (sx == 0 ? min(xhi, nc0 - 1) : xhi);
+        if (ra > rb) continue;
+        const int j0 = cell_start[row + ra - sx * nc0];
+        const int j1 = cell_start[row + rb - sx * nc0 + 1];
+        const double xs = bx - g.h[0] * sx, ys = by - g.h[3] * sx, zs = bz - g.h[6] * sx;
+        for (int jb = j0; jb < j1; jb += 32) {
+          const int j = jb + lane;
+          bool hit = false;
+          unsigned oj = 0;
+          if (j < j1) {
+            const double2* rp = reinterpret_cast<const double2*>(rec + j);
+            const double2 xy = __ldg(rp), zq = __ldg(rp + 1);
+            const double dx = xs - xy.x, dy = ys - xy.y, dz = zs - zq.x;
+            oj = (unsigned)perm[j];
+            hit = oj > oi && dx * dx + dy * dy + dz * dz <= reach2;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (EMIT && hit)
+            out[pos + __popc(m & lt)] = ((unsigned long long)oi << 32) | oj;
+          pos += __popc(m);
+          found += __popc(m);
+        }
+      }
+    }
+  }
+  if (!EMIT && lane == 0) count64[i] = found;
+}
+
+__global__ void k_pair_split(const unsigned long long* __restrict__ keys, long long m,
+                             long long* __restrict__ pi, long long* __restrict__ pj) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const unsigned long long v = keys[k];
+  pi[k] = (long long)(v >> 32);
+  pj[k] = (long long)(v & 0xffffffffull);
+}
+
 constexpr int kRedBlocks = 148;
 constexpr int kRedT = 256;
 
@@ -1070,6 +1172,11 @@ int esp_near_destroy(esp_near* p) {
   cudaFree(p->d_pent);
   cudaFree(p->d_pent_sorted);
   cudaFree(p->d_psort_tmp);
+  cudaFree(p->d_list_keys);
+  cudaFree(p->d_list_keys2);
+  cudaFree(p->d_list_i);
+  cudaFree(p->d_list_j);
+  cudaFree(p->d_list_tmp);
   delete p;
   return ESP_OK;
 }
@@ -1233,6 +1340,107 @@ int esp_near_evaluate_pairs(esp_near* p, const double* d_pos, const double* d_q,
   p->launches++;
   NEAR_CUDA(cudaGetLastError());
   return near_reduce(p, n, d_out7, (long long*)d_stats, s);
+}
+
+int esp_near_build_pairs(esp_near* p, const double* d_pos, int64_t n, int64_t* n_pairs,
+                         void* stream) {
+  int st = check_plan(p, n);
+  if (st != ESP_OK) return st;
+  if (!n_pairs || (n > 0 && !d_pos)) {
+    set_error("null argument");
+    return ESP_ERR_PARAM;
+  }
+  if ((st = near_reserve(p, n)) != ESP_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  *n_pairs = 0;
+  p->list_n = 0;
+  if (n < 2) return ESP_OK;
+  const int B = 256;
+  const unsigned grid = (unsigned)((n + B - 1) / B);
+  k_near_cells<<<grid, B, 0, s>>>(d_pos, nullptr, n, p->g, p->d_key, p->d_idx, p->d_rec_u);
+  size_t bytes = p->sort_bytes;
+  NEAR_CUDA(cub::DeviceRadixSort::SortPairs(p->d_sort_tmp, bytes, p->d_key, p->d_key_sorted,
+                                            p->d_idx, p->d_perm, (int)n, 0,
+                                            bits_for(p->g.ncells), s));
+  k_near_sorted<<<grid, B, 0, s>>>(p->d_key_sorted, p->d_perm, p->d_rec_u, n, p->g.ncells,
+                                   p->d_rec, p->d_cell_start);
+  // per-particle counts and their exclusive prefix (n + 1 entries)
+  long long *d_cnt = nullptr, *d_off = nullptr;
+  NEAR_CUDA(cudaMallocAsync(&d_cnt, sizeof(long long) * (n + 1), s));
+  NEAR_CUDA(cudaMallocAsync(&d_off, sizeof(long long) * (n + 1), s));
+  NEAR_CUDA(cudaMemsetAsync(d_cnt + n, 0, sizeof(long long), s));
+  const unsigned wgrid = (unsigned)((n * 32 + 127) / 128);
+  k_pair_enum<false><<<wgrid, 128, 0, s>>>(p->d_rec, p->d_cell_start, p->d_key_sorted,
+                                            p->d_perm, n, p->g, p->reach * p->reach, nullptr,
+                                            nullptr, d_cnt);
+  NEAR_CUDA(cudaGetLastError());
+  size_t sb = 0;
+  NEAR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, d_cnt, d_off, (int)(n + 1), s));
+  void* tmp = nullptr;
+  NEAR_CUDA(cudaMallocAsync(&tmp, sb, s));
+  NEAR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, sb, d_cnt, d_off, (int)(n + 1), s));
+  long long m = 0;
+  NEAR_CUDA(cudaMemcpyAsync(&m, d_off + n, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  NEAR_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(d_cnt, s);
+  if (m >= (1ll << 31)) {
+    cudaFreeAsync(d_off, s);
+    set_error("pair list above 2^31 pairs");
+    return ESP_ERR_CAPACITY;
+  }
+  if (m > 0) {
+    if (m > p->list_cap) {
+      cudaFree(p->d_list_keys);
+      cudaFree(p->d_list_keys2);
+      cudaFree(p->d_list_i);
+      cudaFree(p->d_list_j);
+      cudaFree(p->d_list_tmp);
+      p->d_list_keys = p->d_list_keys2 = nullptr;
+      p->d_list_i = p->d_list_j = nullptr;
+      p->d_list_tmp = nullptr;
+      p->list_cap = 0;
+      NEAR_CUDA(cudaMalloc(&p->d_list_keys, sizeof(unsigned long long) * m));
+      NEAR_CUDA(cudaMalloc(&p->d_list_keys2, sizeof(unsigned long long) * m));
+      NEAR_CUDA(cudaMalloc(&p->d_list_i, sizeof(long long) * m));
+      NEAR_CUDA(cudaMalloc(&p->d_list_j, sizeof(long long) * m));
+      size_t tb = 0;
+      NEAR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, (const unsigned long long*)nullptr,
+                                               (unsigned long long*)nullptr, (int)m, 0, 64));
+      NEAR_CUDA(cudaMalloc(&p->d_list_tmp, tb));
+      p->list_tmp_bytes = tb;
+      p->list_cap = m;
+    }
+    k_pair_enum<true><<<wgrid, 128, 0, s>>>(p->d_rec, p->d_cell_start, p->d_key_sorted,
+                                             p->d_perm, n, p->g, p->reach * p->reach, d_off,
+                                             p->d_list_keys, nullptr);
+    const int hb = bits_for(n);
+    size_t tb = p->list_tmp_bytes;
+    NEAR_CUDA(cub::DeviceRadixSort::SortKeys(p->d_list_tmp, tb, p->d_list_keys,
+                                             p->d_list_keys2, (int)m, 0, 32 + hb, s));
+    k_pair_split<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(p->d_list_keys2, m, p->d_list_i,
+                                                             p->d_list_j);
+    NEAR_CUDA(cudaGetLastError());
+  }
+  cudaFreeAsync(d_off, s);
+  NEAR_CUDA(cudaStreamSynchronize(s));
+  *n_pairs = m;
+  p->list_n = m;
+  return ESP_OK;
+}
+
+int esp_near_copy_pairs(esp_near* p, int64_t* d_i, int64_t* d_j, void* stream) {
+  if (!p || (p->list_n > 0 && (!d_i || !d_j))) {
+    set_error("null argument");
+    return ESP_ERR_PARAM;
+  }
+  if (p->list_n == 0) return ESP_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  NEAR_CUDA(cudaMemcpyAsync(d_i, p->d_list_i, sizeof(int64_t) * p->list_n,
+                            cudaMemcpyDeviceToDevice, s));
+  NEAR_CUDA(cudaMemcpyAsync(d_j, p->d_list_j, sizeof(int64_t) * p->list_n,
+                            cudaMemcpyDeviceToDevice, s));
+  return ESP_OK;
 }
 
 int esp_near_info(const esp_near* p, int64_t* info8) {

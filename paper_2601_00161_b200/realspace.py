@@ -135,17 +135,22 @@ class NearFieldPlan:
     input order, stats = [pair count, first coincident pair or -1, first
     out-of-range pair or -1]."""
 
-    def __init__(self, kern: SplitKernel, table: PairTable | None = None,
-                 skin: float = 0.0, capacity: int = 1 << 16, cell_div: int = 0):
+    def __init__(self, kern: SplitKernel | None, table: PairTable | None = None,
+                 skin: float = 0.0, capacity: int = 1 << 16, cell_div: int = 0,
+                 r_c: float | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("the near-field pair sum needs a CUDA device (no CPU fallback)")
         self.kern, self.table = kern, table
-        self.r_c = float(kern.r_c)
+        self.r_c = float(kern.r_c if kern is not None else r_c)
         self.reach = self.r_c + float(skin)
         L = _lib.lib()
-        b = kern.basis
-        leg = np.ascontiguousarray(b.legendre_coeffs, dtype=np.float64)
-        cum = np.ascontiguousarray(cumint_coeffs(b), dtype=np.float64)
+        if kern is not None:
+            b = kern.basis
+            leg = np.ascontiguousarray(b.legendre_coeffs, dtype=np.float64)
+            cum = np.ascontiguousarray(cumint_coeffs(b), dtype=np.float64)
+            C0 = float(b.C0)
+        else:  # pair enumeration only (build_cell_list): no pair values
+            leg, cum, C0 = np.ones(1), np.array([0.0, 1.0]), 1.0
         d = _lib.NearDesc()
         d.r_c = self.r_c
         d.reach = self.reach
@@ -167,7 +172,7 @@ class NearFieldPlan:
             d.h_knots, d.h_smooth_spline, d.h_fn_spline = _dp(arrs[2]), _dp(arrs[3]), _dp(arrs[4])
         d.n_legendre, d.h_legendre = int(leg.size), _dp(leg)
         d.n_cumint, d.h_cumint = int(cum.size), _dp(cum)
-        d.C0 = float(b.C0)
+        d.C0 = C0
         d.max_particles = int(max(capacity, 1))
         d.cell_div = int(cell_div)
         h = C.c_void_p()
@@ -265,6 +270,24 @@ class NearFieldPlan:
         _lib.check(rc, "esp_near_evaluate_pairs")
         return out7, forces, stats
 
+    def build_pairs(self, pos: torch.Tensor, stream=None):
+        """All unordered pairs within reach (i < j, sorted by (i, j)) as two
+        int64 device tensors (system.build_cell_list semantics).  Synchronises."""
+        if self.cell is None:
+            raise RealspaceError("set_cell first")
+        if pos.dtype != torch.float64 or not pos.is_cuda or pos.dim() != 2 or pos.shape[1] != 3:
+            raise RealspaceError("positions must be an (N,3) float64 CUDA tensor")
+        pos = pos.contiguous()
+        m = C.c_int64()
+        _lib.check(self._L.esp_near_build_pairs(self._h, C.c_void_p(pos.data_ptr()),
+                                                pos.shape[0], C.byref(m), _stream(stream)),
+                   "esp_near_build_pairs")
+        out = torch.empty((2, int(m.value)), dtype=torch.int64, device=pos.device)
+        _lib.check(self._L.esp_near_copy_pairs(self._h, C.c_void_p(out[0].data_ptr()),
+                                               C.c_void_p(out[1].data_ptr()), _stream(stream)),
+                   "esp_near_copy_pairs")
+        return out[0], out[1]
+
     @staticmethod
     def check_stats(stats_host) -> None:
         """Raise the reference's errors from a host copy of ``stats``."""
@@ -303,6 +326,31 @@ def _as_device(x, dtype):
     if isinstance(x, torch.Tensor):
         return x.to(device="cuda", dtype=dtype).contiguous()
     return torch.as_tensor(np.ascontiguousarray(x), device="cuda").to(dtype).contiguous()
+
+
+_ENUM: dict = {}
+
+
+def build_cell_list(sys, r_c: float, skin: float = 0.0) -> NeighborList:
+    """Cell-list pair enumeration under the minimum-image convention
+    (system.py:144-222): each unordered pair within r_c + skin exactly once,
+    as i < j sorted by (i, j).  Runs on the device; host systems get numpy
+    index arrays, CUDA-tensor systems device tensors."""
+    check_cutoff(sys.cell, r_c)
+    host = not isinstance(sys.positions, torch.Tensor)
+    pos = _as_device(sys.positions, torch.float64)
+    key = (float(r_c), float(skin))
+    plan = _ENUM.get(key)
+    if plan is None:
+        if len(_ENUM) > 8:
+            _ENUM.clear()
+        plan = _ENUM[key] = NearFieldPlan(None, None, skin=skin, r_c=r_c)
+    if plan.cell is None or not np.array_equal(plan.cell.h, sys.cell.h):
+        plan.set_cell(sys.cell)
+    i, j = plan.build_pairs(pos)
+    if host:
+        i, j = i.cpu().numpy(), j.cpu().numpy()
+    return NeighborList(i=i, j=j, r_c=float(r_c), skin=float(skin))
 
 
 def short_range(sys, kern: SplitKernel, neighbors: NeighborList | None = None,

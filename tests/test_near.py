@@ -292,3 +292,33 @@ def test_near_edge_cases():
                           torch.as_tensor(qq, device="cuda"))
     assert O.rel_scalar(moved[0][0].item(), base[0][0].item()) <= 1e-12
     assert O.rms_rel_forces(moved[1].cpu().numpy(), base[1].cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SMALL)
+def test_build_cell_list_small_against_reference(name):
+    """Device pair enumeration = the reference's build_cell_list output
+    (same pairs, same (i, j) order), including skin and a triclinic cell."""
+    _torch()
+    from paper_2601_00161_b200.realspace import build_cell_list
+    g = golden(name)
+    nb = build_cell_list(_sys(g["h"], g["pos"], g["q"]), float(g["r_c"]), skin=float(g["skin"]))
+    np.testing.assert_array_equal(nb.i, g["pi"])
+    np.testing.assert_array_equal(nb.j, g["pj"])
+
+
+@pytest.mark.gpu
+def test_build_cell_list_config0_and_short_range_through_list():
+    _torch()
+    from paper_2601_00161_b200.realspace import build_cell_list, build_pair_table, short_range
+    g = golden("near_cfg0")
+    w, pos, q = workloads.generate(0)
+    nb = build_cell_list(_sys(w.h, pos, q), w.r_c)
+    i, j = O.pairs_within_kdtree(np.diag(w.h), pos, w.r_c)
+    np.testing.assert_array_equal(nb.i, i)
+    np.testing.assert_array_equal(nb.j, j)
+    kern = _kern(w.delta, w.r_c)
+    res = short_range(_sys(w.h, pos, q), kern, nb, build_pair_table(kern))
+    assert res.pair_count == int(g["count"])
+    assert O.rel_scalar(res.energy, g["E"]) <= TOL
+    assert O.rms_rel_forces(res.forces, g["F_sel"]) <= TOL
