@@ -51,7 +51,8 @@ enum esp_status {
   ESP_ERR_CUDA = 4,
   ESP_ERR_CUFFT = 5,
   ESP_ERR_OOM = 6,
-  ESP_ERR_CAPACITY = 7    /* N above the plan's particle capacity */
+  ESP_ERR_CAPACITY = 7,   /* N above the plan's particle capacity */
+  ESP_ERR_INPUT = 8       /* malformed particle file (cli.InputError) */
 };
 
 enum esp_precision { ESP_FP64 = 0, ESP_FP32 = 1 };
@@ -170,6 +171,20 @@ int esp_set_spectrum(esp_plan* plan, const void* d_spectrum, void* stream);
  * (grid lengths in {32,48,64,96,128,192,256,384}, full-grid plans),
  * 0 = cuFFT.  ESP_FFT=cufft in the environment forces 0 at set_cell. */
 int esp_fft_path(const esp_plan* plan);
+
+/* --- particle files (cli.py:57-112) -----------------------
+ * Native reader / writer of the reference's text format: header 'cell Lx Ly
+ * Lz' or 'cell3' + h in column order, then 'x y z q m' lines; '#' comments.
+ * Errors (ESP_ERR_INPUT) carry path:line[:column] as cli.InputError does.
+ * h9 is row-major (columns = cell vectors).  Positions are returned as read
+ * (the Python ParticleSystem wraps them, as the reference does).            */
+typedef struct esp_particles esp_particles;
+int esp_particles_read(const char* path, esp_particles** out);
+int esp_particles_info(const esp_particles* p, int64_t* n, int32_t* triclinic, double* h9);
+int esp_particles_copy(const esp_particles* p, double* h_pos, double* h_q, double* h_m);
+int esp_particles_free(esp_particles* p);
+int esp_particles_write(const char* path, int64_t n, const double* h9, int32_t triclinic,
+                        const double* h_pos, const double* h_q, const double* h_m);
 
 /* --- distributed z-slab transforms --------------------------- */
 /* Rank `rank` of `nranks` (<= 8) slabs of a full-grid plan whose

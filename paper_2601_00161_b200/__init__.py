@@ -9,7 +9,7 @@ functions raise if the library or a GPU is missing.
 """
 
 from .cells import CellType, infer_cell_type
-from .errors import (CellError, DomainError, EspCudaError, GeometryError, MeshError,
+from .errors import (CellError, DomainError, EspCudaError, GeometryError, InputError, MeshError,
                      ParameterError, PlanningError, PswfError, RealspaceError,
                      SingularPairError)
 from .kernel import (SplitKernel, background_correction, far_field, far_field_hat, fn_weight,
@@ -22,6 +22,7 @@ from .pswf import (PswfBasis, WindowTable, build_pswf, eval_psi0, solve_bandwidt
                    tabulate_window)
 from .solver import (CoulombSolver, EnergyBreakdown, EwaldParameters, KSpaceResult,
                      KSpaceSolver, evaluate_system)
+from .particles import read_particles, write_particles
 from .realspace import (NearFieldPlan, PairTable, ShortRangeResult, build_cell_list,
                         build_pair_table, short_range)
 from .system import Cell, NeighborList, ParticleSystem, check_cutoff, minimum_image
@@ -39,5 +40,6 @@ __all__ = [
     "plan_grid", "self_energy", "solve_bandwidth", "spread_charges", "tabulate_window",
     "GeometryError", "RealspaceError", "SingularPairError", "far_field", "fn_weight",
     "near_field", "NearFieldPlan", "PairTable", "ShortRangeResult", "build_pair_table",
-    "short_range", "NeighborList", "minimum_image", "build_cell_list",
+    "short_range", "NeighborList", "minimum_image", "build_cell_list", "read_particles",
+    "write_particles", "InputError",
 ]

@@ -11,7 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .errors import EspCudaError, MeshError, ParameterError, PlanningError
+from .errors import EspCudaError, InputError, MeshError, ParameterError, PlanningError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # ESP_LIB overrides the library path (experiments with variant builds)
@@ -25,6 +25,7 @@ ESP_ERR_CUDA = 4
 ESP_ERR_CUFFT = 5
 ESP_ERR_OOM = 6
 ESP_ERR_CAPACITY = 7
+ESP_ERR_INPUT = 8
 
 ESP_FP64 = 0
 ESP_FP32 = 1
@@ -167,6 +168,11 @@ def lib():
     L.esp_near_info.argtypes = [vp, C.POINTER(C.c_int64)]
     L.esp_near_build_pairs.argtypes = [vp, vp, C.c_int64, C.POINTER(C.c_int64), vp]
     L.esp_near_copy_pairs.argtypes = [vp, vp, vp, vp]
+    L.esp_particles_read.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.esp_particles_info.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), _dp]
+    L.esp_particles_copy.argtypes = [vp, _dp, _dp, _dp]
+    L.esp_particles_free.argtypes = [vp]
+    L.esp_particles_write.argtypes = [C.c_char_p, C.c_int64, _dp, C.c_int32, _dp, _dp, _dp]
     _lib = L
     return L
 
@@ -181,7 +187,8 @@ EXPORTED = [
     "esp_slab_layout", "esp_slab_forward", "esp_slab_reduce", "esp_slab_inverse",
     "esp_near_create", "esp_near_destroy", "esp_near_reserve", "esp_near_set_cell",
     "esp_near_evaluate", "esp_near_evaluate_pairs", "esp_near_info", "esp_near_build_pairs",
-    "esp_near_copy_pairs",
+    "esp_near_copy_pairs", "esp_particles_read", "esp_particles_info", "esp_particles_copy",
+    "esp_particles_free", "esp_particles_write",
 ]
 
 
@@ -196,4 +203,6 @@ def check(rc: int, what: str = "") -> None:
         raise MeshError(text)
     if rc in (ESP_ERR_PARAM, ESP_ERR_CAPACITY):
         raise ParameterError(text)
+    if rc == ESP_ERR_INPUT:
+        raise InputError(msg)
     raise EspCudaError(f"[{rc}] {text}")

@@ -5,6 +5,7 @@ ParameterError             <- prolate_ewald/evaluate.py:247
 PswfError, DomainError     <- prolate_ewald/pswf.py:33-38
 CellError, GeometryError   <- prolate_ewald/system.py:12-17
 RealspaceError, SingularPairError <- prolate_ewald/realspace.py:15-21
+InputError                 <- prolate_ewald/cli.py:46-47
 """
 
 
@@ -42,6 +43,10 @@ class RealspaceError(Exception):
 
 class SingularPairError(RealspaceError):
     """Coincident particles; physical configurations never need them."""
+
+
+class InputError(Exception):
+    """Malformed input file; the message carries path:line[:column] (cli.py:46-47)."""
 
 
 class EspCudaError(RuntimeError):

@@ -240,8 +240,34 @@ def near_cases():
         del nb, a, F
 
 
+def particle_files():
+    """Reference-written particle files (cli.write_particles) and what the
+    reference reads back from them (cli.read_particles)."""
+    from prolate_ewald.cli import read_particles, write_particles
+    rng = np.random.default_rng(31)
+    cases = {
+        "particles_ortho": ParticleSystem(cell=Cell.orthorhombic([5.0, 6.0, 7.0]),
+                                          positions=rng.uniform(-2, 9, (12, 3)),
+                                          charges=rng.standard_normal(12),
+                                          masses=rng.uniform(0.5, 2.0, 12)),
+        "particles_tri": ParticleSystem(
+            cell=Cell(np.array([[5.0, 0.4, 0.1], [0.0, 6.0, -0.3], [0.0, 0.0, 7.0]])),
+            positions=rng.uniform(-2, 9, (7, 3)), charges=rng.standard_normal(7),
+            masses=rng.uniform(0.5, 2.0, 7)),
+    }
+    for name, s_ in cases.items():
+        path = os.path.join(HERE, name + ".txt")
+        write_particles(path, s_)
+        back = read_particles(path)
+        write_particles(os.path.join(HERE, name + "_2.txt"), back)
+        save(name, h=back.cell.h, pos=back.positions, q=back.charges, m=back.masses,
+             versions=VERSIONS)
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["window", "small", "triclinic", "configs", "near"]
+    parts = sys.argv[1:] or ["window", "small", "triclinic", "configs", "near", "particles"]
+    if "particles" in parts:
+        particle_files()
     if "window" in parts:
         window_tables()
     if "small" in parts:
