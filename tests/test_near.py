@@ -322,3 +322,35 @@ def test_build_cell_list_config0_and_short_range_through_list():
     assert res.pair_count == int(g["count"])
     assert O.rel_scalar(res.energy, g["E"]) <= TOL
     assert O.rms_rel_forces(res.forces, g["F_sel"]) <= TOL
+
+
+@pytest.mark.gpu
+def test_coulomb_solver_explicit_list_and_rebind():
+    """CoulombSolver.evaluate with a caller NeighborList equals the cell-list
+    path; after an NPT-style rebind (M pinned) the near plan follows the new
+    cell (evaluate.py:99-112)."""
+    _torch()
+    from paper_2601_00161_b200 import Cell, CoulombSolver, EwaldParameters, ParticleSystem
+    from paper_2601_00161_b200.realspace import build_cell_list
+    w, pos, q = workloads.generate(0)
+    cell = Cell(np.asarray(w.h, dtype=float))
+    s = ParticleSystem(cell=cell, positions=pos, charges=q)
+    solver = CoulombSolver(cell, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                                 fixed_M=w.M))
+    a = solver.evaluate(s)
+    b = solver.evaluate(s, neighbors=build_cell_list(s, w.r_c))
+    assert a.pair_count == b.pair_count
+    assert O.rel_scalar(b.u_near, a.u_near) <= 1e-13
+    assert O.rms_rel_forces(b.forces, a.forces) <= 1e-13
+    cell2 = Cell(np.asarray(w.h, dtype=float) * 1.01)
+    solver.rebind_cell(cell2, fixed_M=w.M)
+    s2 = ParticleSystem(cell=cell2, positions=pos * 1.01, charges=q)
+    c = solver.evaluate(s2)
+    fresh = CoulombSolver(cell2, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                                 fixed_M=w.M)).evaluate(s2)
+    assert c.pair_count == fresh.pair_count
+    assert O.rel_scalar(c.energy, fresh.energy) <= 1e-12
+    assert O.rms_rel_forces(c.forces, fresh.forces) <= 1e-12
+    from paper_2601_00161_b200.errors import ParameterError
+    with pytest.raises(ParameterError):
+        solver.evaluate(s)
