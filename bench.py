@@ -244,6 +244,21 @@ def measured_peaks():
 # our arm
 
 
+def quiet_host_pools():
+    """Host thread pools (OpenBLAS / OpenMP / torch intra-op) busy-wait after
+    parallel CPU work; on the B200 box that slows pinned H2D DMA ~3x
+    (tools/tools_copy_probe3.py).  The timed path does no CPU math, so pin
+    the pools to one thread and let spinning threads park before timing."""
+    import torch
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    torch.set_num_threads(1)
+    time.sleep(0.3)
+
+
 def run_ours(args):
     import torch
 
@@ -308,6 +323,7 @@ def run_ours(args):
     hs = solver.host_stepper(n, True)            # public host-buffer API
     hs.positions.copy_(torch.as_tensor(pos_np))
     hs.charges.copy_(torch.as_tensor(q_np))
+    quiet_host_pools()
     with ClockSampler(local) as clk:
         ms_fp = timed(g_fp.replay, K, W)
         ms_po = timed(g_po.replay, K, W)

@@ -129,6 +129,9 @@ def lib():
     vp = C.c_void_p
     L.esp_last_error.restype = C.c_char_p
     L.esp_version.restype = C.c_int
+    L.esp_copy_async.argtypes = [vp, vp, C.c_int64, vp]
+    L.esp_host_alloc.argtypes = [C.c_int64, C.POINTER(vp)]
+    L.esp_host_free.argtypes = [vp]
     L.esp_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(vp)]
     L.esp_plan_destroy.argtypes = [vp]
     L.esp_plan_set_cell.argtypes = [vp, C.POINTER(CellDesc), vp]
@@ -179,7 +182,7 @@ def lib():
 
 EXPORTED = [
     "esp_plan_create", "esp_plan_destroy", "esp_plan_set_cell", "esp_last_error",
-    "esp_version", "esp_spread", "esp_forward", "esp_scale_reduce", "esp_forces_ik",
+    "esp_version", "esp_copy_async", "esp_host_alloc", "esp_host_free", "esp_spread", "esp_forward", "esp_scale_reduce", "esp_forces_ik",
     "esp_forces_analytic", "esp_local_pressure", "esp_evaluate", "esp_counters",
     "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
@@ -206,3 +209,32 @@ def check(rc: int, what: str = "") -> None:
     if rc == ESP_ERR_INPUT:
         raise InputError(msg)
     raise EspCudaError(f"[{rc}] {text}")
+
+
+class HostBuffer:
+    """Page-locked host memory from ``esp_host_alloc`` viewed as a CPU torch
+    tensor (freed with the object)."""
+
+    def __init__(self, shape, dtype=None):
+        import numpy as np
+        import torch
+        dtype = dtype or torch.float64
+        n = 1
+        for d in shape:
+            n *= int(d)
+        item = torch.empty(0, dtype=dtype).element_size()
+        self._p = C.c_void_p()
+        check(lib().esp_host_alloc(n * item, C.byref(self._p)), "esp_host_alloc")
+        npd = {torch.float64: np.float64, torch.float32: np.float32,
+               torch.int64: np.int64}[dtype]
+        buf = (C.c_char * max(n * item, 1)).from_address(self._p.value)
+        arr = np.frombuffer(buf, dtype=npd, count=n).reshape(shape)
+        self.tensor = torch.from_numpy(arr)
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            if self._p and self._p.value:
+                lib().esp_host_free(self._p)
+                self._p = None
+        except Exception:
+            pass

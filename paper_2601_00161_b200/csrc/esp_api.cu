@@ -110,6 +110,31 @@ const char* esp_last_error(void) { return esp::g_last_error.c_str(); }
 
 int esp_version(void) { return 100; }
 
+int esp_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) {
+    set_error("bad host allocation arguments");
+    return ESP_ERR_PARAM;
+  }
+  *out = nullptr;
+  ESP_CUDA(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault));
+  return ESP_OK;
+}
+
+int esp_host_free(void* p) {
+  if (p) ESP_CUDA(cudaFreeHost(p));
+  return ESP_OK;
+}
+
+int esp_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) {
+    set_error("bad copy arguments");
+    return ESP_ERR_PARAM;
+  }
+  if (bytes == 0) return ESP_OK;
+  ESP_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return ESP_OK;
+}
+
 int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   if (!d || !out) {
     set_error("null argument");
