@@ -44,6 +44,9 @@ using esp::set_error;
 
 namespace {
 
+#ifndef ESP_NEAR_HERMITE
+#define ESP_NEAR_HERMITE 1
+#endif
 #ifndef ESP_NEAR_THREADS
 #define ESP_NEAR_THREADS 256
 #endif
@@ -56,7 +59,7 @@ constexpr int kPolyMax = 16;
 constexpr int kLegMax = 64;
 
 struct NearConst {
-  double r_c, rc2_hi, reach2, sing2, r_in, inv_dk, C0, c0rc;
+  double r_c, rc2_hi, reach2, sing2, r_in, inv_dk, C0, c0rc, dk, h26;
   int use_table, n_poly, n_knots, n_leg, n_cum;
   double smooth_poly[kPolyMax];
   double fn_poly[kPolyMax];
@@ -156,9 +159,12 @@ __device__ __forceinline__ double legval_np(double x, const double* c, int n) {
 
 // Near-field value N(r) and force weight F_N(r) for 0 < r <= r_c
 // (realspace.py:42-67 with a table, kernel.py:41-97 without); rinv = 1/r.
-// Table records (80 B): {knot, -}, {s0, s1}, {s2, s3}, {f0, f1}, {f2, f3}
-// with the scipy PPoly coefficients (highest power first) of the far-field
-// and force-weight splines on the interval starting at the knot.
+// Default table (ESP_NEAR_HERMITE): per knot the value and second derivative
+// of the far-field and force-weight splines (32 B; a pair reads two adjacent
+// knots), which fix the same cubic pieces as the reference's PPoly
+// coefficients (values agree to rounding) in 40% of the bytes.  Otherwise
+// 80 B records {knot, -}, {s0, s1}, {s2, s3}, {f0, f1}, {f2, f3} with the
+// scipy PPoly coefficients (highest power first).
 __device__ __forceinline__ void pair_values(const NearConst& C, double r, double rinv,
                                             const double* __restrict__ tab, double& nv,
                                             double& fv) {
@@ -166,6 +172,17 @@ __device__ __forceinline__ void pair_values(const NearConst& C, double r, double
     if (r <= C.r_in) {
       nv = rinv - poly_horner(r, C.smooth_poly, C.n_poly);
       fv = poly_horner(r, C.fn_poly, C.n_poly);
+    } else if (ESP_NEAR_HERMITE) {
+      // the same cubic pieces from knot values and second derivatives
+      // (32 B per knot: y_s, M_s, y_f, M_f)
+      const double u = (r - C.r_in) * C.inv_dk;
+      const int k = min(max((int)u, 0), C.n_knots - 2);
+      const double2* t = reinterpret_cast<const double2*>(tab + 4 * (size_t)k);
+      const double2 s0 = __ldg(t), f0 = __ldg(t + 1), s1 = __ldg(t + 2), f1 = __ldg(t + 3);
+      const double B = u - k, A = 1.0 - B;
+      const double ca = (A * A - 1.0) * A * C.h26, cb = (B * B - 1.0) * B * C.h26;
+      nv = rinv - fma(ca, s0.y, fma(cb, s1.y, fma(A, s0.x, B * s1.x)));
+      fv = fma(ca, f0.y, fma(cb, f1.y, fma(A, f0.x, B * f1.x)));
     } else {
       int k = (int)((r - C.r_in) * C.inv_dk);
       k = min(max(k, 0), C.n_knots - 2);
@@ -1133,12 +1150,43 @@ int esp_near_create(const esp_near_desc* d, esp_near** out) {
     c.n_knots = d->n_knots;
     c.inv_dk = (double)(d->n_knots - 1) / (d->h_knots[d->n_knots - 1] - d->h_knots[0]);
     const int nk = d->n_knots - 1;
-    std::vector<double> tab(10 * (size_t)nk, 0.0);
-    for (int k = 0; k < nk; ++k) {
-      tab[10 * (size_t)k] = d->h_knots[k];
-      for (int m = 0; m < 4; ++m) {
-        tab[10 * (size_t)k + 2 + m] = d->h_smooth_spline[(size_t)m * nk + k];
-        tab[10 * (size_t)k + 6 + m] = d->h_fn_spline[(size_t)m * nk + k];
+    c.dk = (d->h_knots[nk] - d->h_knots[0]) / nk;
+    c.h26 = c.dk * c.dk / 6.0;
+    std::vector<double> tab;
+    if (ESP_NEAR_HERMITE) {
+      // per knot: value and second derivative of both splines (the cubic on
+      // [x_k, x_k+1] is fixed by them; last knot from the last piece at s = h)
+      tab.assign(4 * (size_t)(nk + 1), 0.0);
+      const double* S = d->h_smooth_spline;
+      const double* F = d->h_fn_spline;
+      auto c_ = [&](const double* P, int m, int k) { return P[(size_t)m * nk + k]; };
+      for (int k = 0; k <= nk; ++k) {
+        for (int w = 0; w < 2; ++w) {
+          const double* P = w == 0 ? S : F;
+          double y, M;
+          if (k < nk) {
+            y = c_(P, 3, k);
+            M = 2.0 * c_(P, 1, k);
+          } else {
+            const double h = d->h_knots[nk] - d->h_knots[nk - 1];
+            y = ((c_(P, 0, nk - 1) * h + c_(P, 1, nk - 1)) * h + c_(P, 2, nk - 1)) * h +
+                c_(P, 3, nk - 1);
+            M = 6.0 * c_(P, 0, nk - 1) * h + 2.0 * c_(P, 1, nk - 1);
+          }
+          // layout per knot: y_s, M_s, y_f, M_f -> double2 {y, M} per spline;
+          // loads read (s0, f0, s1, f1) as consecutive double2
+          tab[4 * (size_t)k + 2 * w] = y;
+          tab[4 * (size_t)k + 2 * w + 1] = M;
+        }
+      }
+    } else {
+      tab.assign(10 * (size_t)nk, 0.0);
+      for (int k = 0; k < nk; ++k) {
+        tab[10 * (size_t)k] = d->h_knots[k];
+        for (int m = 0; m < 4; ++m) {
+          tab[10 * (size_t)k + 2 + m] = d->h_smooth_spline[(size_t)m * nk + k];
+          tab[10 * (size_t)k + 6 + m] = d->h_fn_spline[(size_t)m * nk + k];
+        }
       }
     }
     if (cudaMalloc(&p->d_tab, sizeof(double) * tab.size()) != cudaSuccess ||
