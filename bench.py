@@ -454,9 +454,14 @@ def near_field_leg(w, pos, q, kspace, timed, K, W):
         kspace.evaluate_device(pos, q, True, o7f, Fn)
         plan.evaluate(pos, q, forces=Fn, accumulate=True, out7=o7, stats=st)
 
+    from paper_2601_00161_b200 import CoulombSolver, EwaldParameters
+    cs = CoulombSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                            fixed_M=w.M, cell_type=w.cell_type))
+    g_all, _ = cs.graphed(pos, q, True)
     kn, wn = max(3, min(K, 20)), max(W, 3)
     ms_near = timed(near, kn, wn)
     ms_all = timed(coulomb, kn, wn)
+    ms_graph = timed(g_all.replay, kn, wn)
     pairs = int(st[0].item())
     directed = 2.0 * pairs
     tfl = directed * NEAR_FLOPS_PER_DIRECTED_PAIR / (ms_near * 1e-3) / 1e12
@@ -469,6 +474,9 @@ def near_field_leg(w, pos, q, kspace, timed, K, W):
             "coulomb_step": {"ms_per_step": ms_all, "value": w.n / (ms_all * 1e-3),
                              "unit": UNIT,
                              "what": "far (k-space, eager) + near (cell list) + summed forces"},
+            "coulomb_step_graphed": {
+                "ms_per_step": ms_graph, "value": w.n / (ms_graph * 1e-3), "unit": UNIT,
+                "what": "CoulombSolver.graphed: near and far on two streams of one CUDA graph"},
             "steps": kn}
 
 

@@ -294,6 +294,51 @@ class CoulombSolver:
                 stream=stream)
         return out7_far, out7_near, stats, (F if want_forces else None)
 
+    def graphed(self, positions: torch.Tensor, charges: torch.Tensor,
+                want_forces: bool = True):
+        """Capture the whole device step (near and far field) into one CUDA
+        graph on fixed buffers.  The near-field pair sum and the k-space
+        pipeline run on two streams of the graph and their forces are summed
+        at the end.  Returns (graph, outputs) with outputs = dict(out7_far,
+        out7_near, stats, forces); ``graph.replay()`` recomputes them after
+        the caller updates ``positions`` / ``charges`` in place.  Energies and
+        forces are prefactor 1 (evaluate() applies the prefactor)."""
+        n = positions.shape[0]
+        dev = positions.device
+        f64 = torch.float64
+        out = {"out7_far": torch.empty(7, dtype=f64, device=dev),
+               "out7_near": torch.empty(7, dtype=f64, device=dev),
+               "stats": torch.empty(3, dtype=torch.int64, device=dev),
+               "forces": torch.empty((n, 3), dtype=f64, device=dev) if want_forces else None}
+        f_far = torch.empty((n, 3), dtype=f64, device=dev) if want_forces else None
+        f_near = torch.empty((n, 3), dtype=f64, device=dev)
+        self.near.reserve(n)
+        self.kspace.plan.ensure_capacity(n)
+        side = torch.cuda.Stream()
+
+        def body():
+            main = torch.cuda.current_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self.near.evaluate(positions, charges, forces=f_near, out7=out["out7_near"],
+                                   stats=out["stats"])
+            self.kspace.evaluate_device(positions, charges, want_forces, out["out7_far"], f_far)
+            main.wait_stream(side)
+            if want_forces:
+                torch.add(f_far, f_near, out=out["forces"])
+
+        warm = torch.cuda.Stream()
+        warm.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(warm):
+            body()
+        torch.cuda.current_stream().wait_stream(warm)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        torch.cuda.synchronize()
+        return g, out
+
     def evaluate(self, sys, want_forces: bool = True, want_pressure: bool = True,
                  neighbors=None) -> EnergyBreakdown:
         if not np.allclose(np.asarray(sys.cell.h), self.cell.h):
