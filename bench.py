@@ -443,7 +443,7 @@ def near_field_leg(w, pos, q, kspace, timed, K, W):
     plan = NearFieldPlan(kern, table, capacity=w.n)
     plan.set_cell(w.h)
     o7 = torch.empty(7, dtype=torch.float64, device=pos.device)
-    st = torch.empty(3, dtype=torch.int64, device=pos.device)
+    st = torch.empty(4, dtype=torch.int64, device=pos.device)
     Fn = torch.empty((w.n, 3), dtype=torch.float64, device=pos.device)
     o7f = torch.empty(7, dtype=torch.float64, device=pos.device)
 

@@ -248,9 +248,9 @@ int esp_probe_fp64(double* tflops, void* stream);
  *
  * out7 = [E_near, P_xx, P_xy, P_xz, P_yy, P_yz, P_zz] (pressure = virial / V,
  * realspace.py:155-156); forces (N,3) in the caller's order (overwritten, or
- * added to with ESP_NEAR_ACCUMULATE); stats (device int64[3]) = {pair count
+ * added to with ESP_NEAR_ACCUMULATE); stats (device int64[4]) = {pair count
  * within r_c, first coincident pair (i << 32 | j) or -1, first pair with an
- * index outside [0, N) or -1}.  A coincident pair (r < 1e-12 r_c) is the
+ * index outside [0, N) or -1, directed pair count}.  A coincident pair (r < 1e-12 r_c) is the
  * reference's SingularPairError (realspace.py:20-21, 134-137).            */
 enum esp_near_flags { ESP_NEAR_ACCUMULATE = 1 };
 
@@ -294,6 +294,13 @@ int esp_near_set_cell(esp_near* plan, const double* h_h, const double* h_hinv,
 int esp_near_evaluate(esp_near* plan, const double* d_pos, const double* d_q, int64_t n,
                       int32_t flags, double* d_out7, double* d_forces, int64_t* d_stats,
                       void* stream);
+/* Slab-local variant (multi-GPU near field): particles [0, n_owned) of the
+ * input are this rank's, [n_owned, n) ghosts within reach of its slab from
+ * other ranks.  Sums (out7, forces, directed count) cover the owned
+ * particles' directed pairs only; forces has n_owned rows.                  */
+int esp_near_evaluate_local(esp_near* plan, const double* d_pos, const double* d_q, int64_t n,
+                            int64_t n_owned, int32_t flags, double* d_out7, double* d_forces,
+                            int64_t* d_stats, void* stream);
 /* Pairs (d_i[k], d_j[k]) as given (int64 device arrays), separation by
  * minimum_image.                                                           */
 int esp_near_evaluate_pairs(esp_near* plan, const double* d_pos, const double* d_q,

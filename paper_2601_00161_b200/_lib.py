@@ -166,6 +166,8 @@ def lib():
     L.esp_near_reserve.argtypes = [vp, C.c_int64, C.c_int64]
     L.esp_near_set_cell.argtypes = [vp, _dp, _dp, C.c_int32, C.c_double]
     L.esp_near_evaluate.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp, vp]
+    L.esp_near_evaluate_local.argtypes = [vp, vp, vp, C.c_int64, C.c_int64, C.c_int32, vp, vp,
+                                          vp, vp]
     L.esp_near_evaluate_pairs.argtypes = [vp, vp, vp, C.c_int64, vp, vp, C.c_int64,
                                           C.c_int32, vp, vp, vp, vp]
     L.esp_near_info.argtypes = [vp, C.POINTER(C.c_int64)]
@@ -189,7 +191,7 @@ EXPORTED = [
     "esp_gather_fields", "esp_fields_ptr", "esp_fft_path",
     "esp_slab_layout", "esp_slab_forward", "esp_slab_reduce", "esp_slab_inverse",
     "esp_near_create", "esp_near_destroy", "esp_near_reserve", "esp_near_set_cell",
-    "esp_near_evaluate", "esp_near_evaluate_pairs", "esp_near_info", "esp_near_build_pairs",
+    "esp_near_evaluate", "esp_near_evaluate_local", "esp_near_evaluate_pairs", "esp_near_info", "esp_near_build_pairs",
     "esp_near_copy_pairs", "esp_particles_read", "esp_particles_info", "esp_particles_copy",
     "esp_particles_free", "esp_particles_write",
 ]

@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(kNearThreads, ESP_NEAR_MINB)
     k_near_pairs(const __grid_constant__ NearConst C, const double4* __restrict__ rec,
                  const int* __restrict__ cell_start, const int* __restrict__ perm, CellGeom g,
                  const double* __restrict__ tab, int accumulate, double* __restrict__ forces,
-                 double* __restrict__ part, unsigned long long* __restrict__ singular) {
+                 double* __restrict__ part, unsigned long long* __restrict__ singular,
+                 int n_owned) {
   __shared__ double s_q[kNearThreads / 32][4][kQueue];
   const int cell = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -339,6 +340,11 @@ __global__ void __launch_bounds__(kNearThreads, ESP_NEAR_MINB)
   const double iwx = nc0 / g.h[0];
   const double reach2 = C.reach2;
   for (int i = i0 + warp; i < i1; i += kNearThreads / 32) {
+    if (perm[i] >= n_owned) {  // ghost (slab halo): partner only
+      if (lane == 0)
+        for (int c = 0; c < 8; ++c) part[8 * (size_t)i + c] = 0.0;
+      continue;
+    }
     const double4 ri = rec[i];
     Acc a;
     a.zero();
@@ -492,7 +498,8 @@ __global__ void __launch_bounds__(kTileW * 32)
     k_near_tile(const __grid_constant__ NearConst C, const double4* __restrict__ rec,
                 const int* __restrict__ cell_start, const int* __restrict__ perm, CellGeom g,
                 const double* __restrict__ tab, int accumulate, double* __restrict__ forces,
-                double* __restrict__ part, unsigned long long* __restrict__ singular) {
+                double* __restrict__ part, unsigned long long* __restrict__ singular,
+                int n_owned) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
   const int cell = blockIdx.x;
@@ -599,8 +606,13 @@ __global__ void __launch_bounds__(kTileW * 32)
     }
     __syncthreads();
     const int total = S.pref[nr];
-    const bool active = warp < ni;
     const int i = base + warp;
+    // particles with input index >= n_owned are ghosts (slab halos): partners
+    // only, no sums of their own
+    const bool ghost = warp < ni && perm[i] >= n_owned;
+    const bool active = warp < ni && !ghost;
+    if (ghost && lane == 0)
+      for (int c = 0; c < 8; ++c) part[8 * (size_t)i + c] = 0.0;
     double4 ri = make_double4(0, 0, 0, 0);
     if (active) ri = rec[i];
     Acc a;
@@ -947,7 +959,10 @@ __global__ void __launch_bounds__(kRedT)
     for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double*)red)[8 * b + threadIdx.x];
     if (threadIdx.x == 0) out7[0] = s;
     else if (threadIdx.x < 7) out7[threadIdx.x] = __ddiv_rn(s, volume);
-    else stats[0] = (long long)(0.5 * s + 0.25);
+    else {
+      stats[0] = (long long)(0.5 * s + 0.25);
+      stats[3] = (long long)(s + 0.5);  // directed count (slab ranks sum it)
+    }
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }
@@ -1045,6 +1060,7 @@ int near_reduce(esp_near* p, long long n, double* d_out7, long long* d_stats, cu
   if (n == 0) {
     NEAR_CUDA(cudaMemsetAsync(d_out7, 0, sizeof(double) * 7, s));
     NEAR_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(long long), s));
+    NEAR_CUDA(cudaMemsetAsync(d_stats + 3, 0, sizeof(long long), s));
     return ESP_OK;
   }
   const int blocks = (int)std::min<long long>(kRedBlocks, (n + kRedT - 1) / kRedT);
@@ -1301,13 +1317,23 @@ int esp_near_set_cell(esp_near* p, const double* h, const double* hinv, int32_t 
 int esp_near_evaluate(esp_near* p, const double* d_pos, const double* d_q, int64_t n,
                       int32_t flags, double* d_out7, double* d_forces, int64_t* d_stats,
                       void* stream) {
+  return esp_near_evaluate_local(p, d_pos, d_q, n, n, flags, d_out7, d_forces, d_stats, stream);
+}
+
+int esp_near_evaluate_local(esp_near* p, const double* d_pos, const double* d_q, int64_t n,
+                            int64_t n_owned, int32_t flags, double* d_out7, double* d_forces,
+                            int64_t* d_stats, void* stream) {
+  if (n_owned < 0 || n_owned > n) {
+    set_error("n_owned must lie in [0, n]");
+    return ESP_ERR_PARAM;
+  }
   int st = check_plan(p, n);
   if (st != ESP_OK) return st;
   if (n > p->cap) {
     set_error("particle count exceeds the near-field plan capacity (esp_near_reserve)");
     return ESP_ERR_CAPACITY;
   }
-  if (!d_out7 || !d_stats || (n > 0 && (!d_pos || !d_q || !d_forces))) {
+  if (!d_out7 || !d_stats || (n > 0 && (!d_pos || !d_q)) || (n_owned > 0 && !d_forces)) {
     set_error("null argument");
     return ESP_ERR_PARAM;
   }
@@ -1332,12 +1358,12 @@ int esp_near_evaluate(esp_near* p, const double* d_pos, const double* d_q, int64
     k_near_pairs<<<(unsigned)p->g.ncells, kNearThreads, 0, s>>>(
         p->c, p->d_rec, p->d_cell_start, p->d_perm, p->g, p->d_tab,
         (flags & ESP_NEAR_ACCUMULATE) ? 1 : 0, d_forces, p->d_part,
-        (unsigned long long*)(d_stats + 1));
+        (unsigned long long*)(d_stats + 1), (int)n_owned);
   } else {
     k_near_tile<<<(unsigned)p->g.ncells, kTileW * 32, sizeof(TileSmem), s>>>(
         p->c, p->d_rec, p->d_cell_start, p->d_perm, p->g, p->d_tab,
         (flags & ESP_NEAR_ACCUMULATE) ? 1 : 0, d_forces, p->d_part,
-        (unsigned long long*)(d_stats + 1));
+        (unsigned long long*)(d_stats + 1), (int)n_owned);
   }
   p->launches++;
   NEAR_CUDA(cudaGetLastError());

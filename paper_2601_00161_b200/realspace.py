@@ -133,7 +133,7 @@ class NearFieldPlan:
     asynchronously on the current stream and return device tensors:
     out7 = [E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz] (prefactor 1), forces (N,3) in
     input order, stats = [pair count, first coincident pair or -1, first
-    out-of-range pair or -1]."""
+    out-of-range pair or -1, directed pair count]."""
 
     def __init__(self, kern: SplitKernel | None, table: PairTable | None = None,
                  skin: float = 0.0, capacity: int = 1 << 16, cell_div: int = 0,
@@ -221,7 +221,7 @@ class NearFieldPlan:
         if out7 is None:
             out7 = torch.empty(7, dtype=torch.float64, device=dev)
         if stats is None:
-            stats = torch.empty(3, dtype=torch.int64, device=dev)
+            stats = torch.empty(4, dtype=torch.int64, device=dev)
         return forces, out7, stats
 
     @staticmethod
@@ -247,6 +247,23 @@ class NearFieldPlan:
             _lib.ESP_NEAR_ACCUMULATE if accumulate else 0, C.c_void_p(out7.data_ptr()),
             C.c_void_p(forces.data_ptr()), C.c_void_p(stats.data_ptr()), _stream(stream))
         _lib.check(rc, "esp_near_evaluate")
+        return out7, forces, stats
+
+    def evaluate_local(self, pos: torch.Tensor, q: torch.Tensor, n_owned: int, forces=None,
+                       out7=None, stats=None, stream=None):
+        """Slab-local pair sum: rows [0, n_owned) are this rank's particles,
+        the rest ghosts (partners only).  forces has n_owned rows."""
+        if self.cell is None:
+            raise RealspaceError("set_cell first")
+        self._check_particles(pos, q)
+        n = pos.shape[0]
+        self.reserve(n)
+        forces, out7, stats = self._outputs(n_owned, pos.device, forces, out7, stats)
+        rc = self._L.esp_near_evaluate_local(
+            self._h, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()), n, int(n_owned), 0,
+            C.c_void_p(out7.data_ptr()), C.c_void_p(forces.data_ptr()),
+            C.c_void_p(stats.data_ptr()), _stream(stream))
+        _lib.check(rc, "esp_near_evaluate_local")
         return out7, forces, stats
 
     def evaluate_pairs(self, pos: torch.Tensor, q: torch.Tensor, i: torch.Tensor,

@@ -308,7 +308,7 @@ class CoulombSolver:
         f64 = torch.float64
         out = {"out7_far": torch.empty(7, dtype=f64, device=dev),
                "out7_near": torch.empty(7, dtype=f64, device=dev),
-               "stats": torch.empty(3, dtype=torch.int64, device=dev),
+               "stats": torch.empty(4, dtype=torch.int64, device=dev),
                "forces": torch.empty((n, 3), dtype=f64, device=dev) if want_forces else None}
         f_far = torch.empty((n, 3), dtype=f64, device=dev) if want_forces else None
         f_near = torch.empty((n, 3), dtype=f64, device=dev)

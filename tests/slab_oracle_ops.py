@@ -53,3 +53,44 @@ class OracleSlabOps:
         f = fields.detach().cpu().numpy().reshape(3, -1)
         F = np.stack([-q * np.einsum("np,np->n", f[d][flat], wt) for d in range(3)], axis=1)
         return torch.as_tensor(F)
+
+
+class OracleNearOps:
+    """Test-only local pair sum for the distributed near field: the oracle's
+    pair values (realspace.py restatement) over the rank's owned + ghost
+    particles, sums for the owned particles' directed pairs only."""
+
+    def __init__(self, h, basis, r_c, table=None):
+        self.h = np.asarray(h, dtype=float)
+        self.basis, self.r_c, self.table = basis, float(r_c), table
+
+    def evaluate(self, pos, q, n_owned):
+        P = pos.detach().cpu().numpy()
+        Q = q.detach().cpu().numpy()
+        F = np.zeros((n_owned, 3))
+        out = np.zeros(8)
+        npairs = 0
+        if len(P) >= 2:
+            i, j = O.pairs_within(self.h, P, self.r_c)
+            oi, oj = i < n_owned, j < n_owned
+            keep = oi | oj
+            i, j, oi, oj = i[keep], j[keep], oi[keep], oj[keep]
+            dr = O.minimum_image(self.h, P[i] - P[j])
+            r = np.sqrt(np.einsum("ij,ij->i", dr, dr))
+            m = r <= self.r_c
+            i, j, oi, oj, dr, r = i[m], j[m], oi[m], oj[m], dr[m], r[m]
+            qq = Q[i] * Q[j]
+            nv, fv = (O.table_values(self.table, r) if self.table is not None else
+                      (O.near_value(self.basis, self.r_c, r), O.fn_value(self.basis, self.r_c, r)))
+            fmag = qq * fv / r ** 3
+            w = 0.5 * (oi.astype(float) + oj.astype(float))
+            out[0] = np.sum(w * qq * nv)
+            W = (dr.T * (w * fmag)) @ dr / float(np.linalg.det(self.h))
+            out[1:7] = [W[0, 0], W[0, 1], W[0, 2], W[1, 1], W[1, 2], W[2, 2]]
+            out[7] = float(np.sum(oi) + np.sum(oj))
+            pf = fmag[:, None] * dr
+            np.add.at(F, i[oi], pf[oi])
+            np.add.at(F, j[oj], -pf[oj])
+            npairs = int(np.sum(oi & oj))
+        stats = torch.tensor([npairs, -1, -1, int(out[7])], dtype=torch.int64)
+        return torch.as_tensor(out), torch.as_tensor(F), stats

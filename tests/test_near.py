@@ -384,3 +384,51 @@ def test_coulomb_graphed_step_matches_evaluate():
         assert O.rel_scalar(Ef, ref.u_far) <= 1e-13
         assert int(out["stats"][0]) == ref.pair_count
         assert O.rms_rel_forces(out["forces"].cpu().numpy(), ref.forces) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx,R", [(1, 1), (1, 2), (1, 4), (3, 3)])
+def test_slab_local_near_field_emulated_on_one_gpu(idx, R):
+    """esp_near_evaluate_local for R slab ranks run one after another on one
+    device (owned particles + ghosts within reach of the slab, chosen as
+    SlabNearField chooses them): the summed energy / pressure / pair count
+    and every rank's forces equal the single-plan pair sum."""
+    torch = _torch()
+    from paper_2601_00161_b200 import Cell
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table, out7_to_pressure
+    from paper_2601_00161_b200.slab_near import CudaNearOps, SlabNearField
+    w, pos, q = workloads.generate(idx)
+    kern = _kern(w.delta, w.r_c)
+    table = build_pair_table(kern)
+    full = NearFieldPlan(kern, table, capacity=w.n)
+    full.set_cell(w.h)
+    o7, F0, st0 = full.evaluate(torch.as_tensor(pos, device="cuda"),
+                                torch.as_tensor(q, device="cuda"))
+    E0, P0 = out7_to_pressure(o7)
+    F0 = F0.cpu().numpy()
+    ops = CudaNearOps(kern, table, Cell(np.asarray(w.h, dtype=float)))
+    bounds = np.linspace(0.0, 1.0, R + 1) + 0.01
+    sl = SlabNearField.__new__(SlabNearField)   # geometry only, no process group
+    sl.R, sl.rank, sl.group = R, 0, None
+    sl.cell = Cell(np.asarray(w.h, dtype=float))
+    sl.reach = w.r_c
+    sl.bounds = bounds
+    sl.hinv = np.linalg.inv(sl.cell.h)
+    sl.dz = w.r_c / sl.cell.perpendicular_widths()[2] * (1 + 1e-9) + 1e-12
+    owner = sl.owner(pos)
+    s = sl.frac_z(pos)
+    tot = np.zeros(8)
+    F = np.zeros_like(F0)
+    for r in range(R):
+        own = np.nonzero(owner == r)[0]
+        gh = np.nonzero((owner != r) & sl._ghost_mask(s, r))[0]
+        idx_all = np.concatenate([own, gh])
+        out8, Fr, st = ops.evaluate(torch.as_tensor(pos[idx_all], device="cuda"),
+                                    torch.as_tensor(q[idx_all], device="cuda"), len(own))
+        tot += out8.cpu().numpy()
+        F[own] = Fr.cpu().numpy()
+    assert abs(tot[0] - E0) <= 1e-12 * abs(E0)
+    P = np.array([[tot[1], tot[2], tot[3]], [tot[2], tot[4], tot[5]], [tot[3], tot[5], tot[6]]])
+    assert O.rel_frobenius(P, P0) <= 1e-12
+    assert int(round(0.5 * tot[7])) == int(st0[0])
+    assert O.rms_rel_forces(F, F0) <= 1e-12
