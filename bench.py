@@ -632,9 +632,42 @@ def run_slab(args):
             dist.barrier()
         return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / K, dist, dev)
 
+    near = None
+    if args.near:
+        from paper_2601_00161_b200 import Cell, SplitKernel
+        from paper_2601_00161_b200.realspace import build_pair_table
+        from paper_2601_00161_b200.slab_near import CudaNearOps, SlabNearField
+        kern = SplitKernel(basis=basis, r_c=w.r_c)
+        sn = SlabNearField.from_kspace(s, w.r_c, CudaNearOps(kern, build_pair_table(kern),
+                                                             Cell(np.asarray(w.h, float))))
+        sn.ops.plan.reserve(pos.shape[0] + pos.shape[0] // 2)
+
+    def timed_near(K, W):
+        for _ in range(W):
+            sn.evaluate(pos, q)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(K)]
+        for i in range(K):
+            flush.zero_()
+            ev[i][0].record(stream)
+            sn.evaluate(pos, q)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / K, dist, dev)
+
     with ClockSampler(local) as clk:
         ms_fp = timed(True, args.steps, args.warmup)
         ms_po = timed(False, args.steps, args.warmup)
+        if args.near:
+            ms_near = timed_near(max(3, min(args.steps, 5)), 2)
+            near = {"ms_per_step": ms_near, "value": w.n / (ms_near * 1e-3), "unit": UNIT,
+                    "what": "slab near field (ghost all-to-all, slab-local pair sums, "
+                            "rank-ordered reduction), slab_near.SlabNearField"}
     line = {"metric": METRIC, "value": w.n / (ms_fp * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_fp,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -646,6 +679,8 @@ def run_slab(args):
             "pressure_only": {"value": w.n / (ms_po * 1e-3), "unit": UNIT,
                               "ms_per_step": ms_po},
             "clocks": clk.summary()}
+    if near is not None:
+        line["near_field"] = near
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

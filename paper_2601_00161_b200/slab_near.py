@@ -95,13 +95,16 @@ class SlabNearField:
         s = np.where(s >= self.bounds[-1], s - 1.0, s)
         return np.clip(np.searchsorted(self.bounds, s, side="right") - 1, 0, self.R - 1)
 
-    def _ghost_mask(self, s: np.ndarray, d: int) -> np.ndarray:
-        lo, hi = self.bounds[d], self.bounds[d + 1]
-        best = np.full(s.shape, np.inf)
+    def _ghost_mask(self, s, d: int):
+        """Positions (fractional z ``s``, numpy or torch) within reach of rank
+        d's slab, periodically."""
+        lo, hi = float(self.bounds[d]), float(self.bounds[d + 1])
+        mod = torch if isinstance(s, torch.Tensor) else np
+        best = None
         for k in (-1.0, 0.0, 1.0):
             t = s + k
-            gap = np.maximum(np.maximum(lo - t, t - hi), 0.0)
-            best = np.minimum(best, gap)
+            gap = mod.maximum(mod.maximum(lo - t, t - hi), mod.zeros_like(t))
+            best = gap if best is None else mod.minimum(best, gap)
         return best <= self.dz
 
     def evaluate(self, pos: torch.Tensor, q: torch.Tensor):
@@ -128,16 +131,21 @@ class SlabNearField:
 
     # -- communication -------------------------------------------------------
     def _exchange(self, pos: torch.Tensor, q: torch.Tensor):
-        s = self.frac_z(pos.detach().cpu().numpy())
-        sel = [np.nonzero(self._ghost_mask(s, d))[0] if d != self.rank else
-               np.zeros(0, dtype=np.int64) for d in range(self.R)]
+        """Ghost selection on the particles' device (torch ops), then counts
+        and [x, y, z, q] rows by all-to-all."""
         if self.R == 1:
             z3 = torch.zeros((0, 3), dtype=pos.dtype, device=pos.device)
             return z3, torch.zeros(0, dtype=q.dtype, device=q.device)
-        idx = torch.as_tensor(np.concatenate(sel).astype(np.int64), device=pos.device)
+        hz = torch.as_tensor(self.hinv[2], dtype=pos.dtype, device=pos.device)
+        s = pos @ hz
+        s = s - torch.floor(s)
+        sel = [torch.nonzero(self._ghost_mask(s, d)).reshape(-1) if d != self.rank else
+               torch.zeros(0, dtype=torch.int64, device=pos.device) for d in range(self.R)]
+        idx = torch.cat(sel)
         send = torch.cat([pos[idx], q[idx].reshape(-1, 1)], dim=1).contiguous()
-        in_splits = [int(len(x)) for x in sel]
-        cnt_in = torch.tensor(in_splits, dtype=torch.int64, device=pos.device)
+        cnt_in = torch.stack([torch.tensor(x.numel(), dtype=torch.int64) for x in sel]).to(
+            pos.device)
+        in_splits = [int(x.numel()) for x in sel]
         cnt_out = torch.empty_like(cnt_in)
         dist.all_to_all_single(cnt_out, cnt_in, group=self.group)
         out_splits = [int(v) for v in cnt_out.cpu().tolist()]
