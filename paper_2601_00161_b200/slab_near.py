@@ -159,3 +159,79 @@ class SlabNearField:
         bufs = [torch.empty_like(x) for _ in range(self.R)]
         dist.all_gather(bufs, x.contiguous(), group=self.group)
         return [b.detach().cpu().numpy() for b in bufs]
+
+
+class SlabCoulombSolver:
+    """Multi-GPU ``CoulombSolver.evaluate`` (evaluate.py:114-144): the k-space
+    slab solver and the slab near field on the same particle ownership
+    (z anchor plane of the k-space layout), plus self and background terms.
+
+    ``evaluate(pos, q)`` takes this rank's particles (``owned(pos_all)``) and
+    returns an EnergyBreakdown with global energies / pressure / pair count
+    and the forces of this rank's particles (prefactor applied).  ``kspace``
+    / ``near_ops`` are pluggable for the CPU decomposition tests only."""
+
+    def __init__(self, h, params, group=None, kspace=None, near_ops=None):
+        from .kernel import SplitKernel
+        from .mesh import plan_grid
+        from .pswf import build_pswf, solve_bandwidth
+        from .realspace import build_pair_table
+        from .slab import SlabKSpaceSolver
+        d_split, d_spread, P = params.resolved()
+        self.params = params
+        self.cell = Cell(np.asarray(h, dtype=float))
+        check_cutoff(self.cell, params.r_c)
+        basis = build_pswf(solve_bandwidth(d_split))
+        spread = basis if abs(d_spread - d_split) <= 1e-300 else build_pswf(
+            solve_bandwidth(d_spread))
+        self.kern = SplitKernel(basis=basis, r_c=params.r_c)
+        if kspace is None:
+            ortho = self.cell.is_orthorhombic
+            spec = plan_grid(self.cell, self.kern, delta_spread=d_spread, P=P,
+                             oversampling=params.oversampling, spread_basis=spread,
+                             fixed_M=params.fixed_M, allow_triclinic=not ortho)
+            kspace = SlabKSpaceSolver(self.cell.h, spec.M, P, basis, spec.window, params.r_c,
+                                      spread_basis=spread, group=group,
+                                      precision=params.precision)
+        self.kspace = kspace
+        if near_ops is None:
+            near_ops = CudaNearOps(self.kern, build_pair_table(self.kern), self.cell)
+        self.near = SlabNearField.from_kspace(kspace, params.r_c, near_ops, group)
+        self.group = group
+
+    def owned(self, pos_all: np.ndarray) -> np.ndarray:
+        return self.kspace.owned(pos_all)
+
+    def _sum_ranks(self, x: float) -> float:
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        if self.near.R == 1:
+            return float(x)
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        t = t.to(dev)
+        bufs = [torch.empty_like(t) for _ in range(self.near.R)]
+        dist.all_gather(bufs, t, group=self.group)
+        tot = 0.0
+        for b in bufs:                      # rank order
+            tot += float(b.item())
+        return tot
+
+    def evaluate(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool = True,
+                 want_pressure: bool = True):
+        from .kernel import background_correction
+        from .solver import EnergyBreakdown
+        pref = self.params.prefactor
+        e_far, p_far, f_far = self.kspace.evaluate(pos, q, want_forces)
+        e_near, p_near, f_near, npairs = self.near.evaluate(pos, q)
+        qh = q.detach().cpu().numpy()
+        q2 = self._sum_ranks(float(np.sum(qh * qh)))
+        qt = self._sum_ranks(float(np.sum(qh)))
+        b = self.kern.basis
+        u_self = float(-(b.psi0_at_zero / (2.0 * b.C0 * self.kern.r_c)) * q2)
+        u_cb, u_bb, p_corr = background_correction(self.kern, qt, self.cell.volume)
+        out = EnergyBreakdown(u_near=pref * e_near, u_far=pref * e_far, u_self=pref * u_self,
+                              u_background=pref * (u_cb + u_bb), pair_count=npairs)
+        if want_forces:
+            out.forces = pref * (f_far.to(f_near.dtype) + f_near.to(f_far.device))
+        if want_pressure:
+            out.pressure = pref * (np.asarray(p_near) + np.asarray(p_far) + p_corr)
+        return out

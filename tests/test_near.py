@@ -432,3 +432,27 @@ def test_slab_local_near_field_emulated_on_one_gpu(idx, R):
     assert O.rel_frobenius(P, P0) <= 1e-12
     assert int(round(0.5 * tot[7])) == int(st0[0])
     assert O.rms_rel_forces(F, F0) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_slab_coulomb_solver_single_rank_equals_coulomb_solver():
+    """SlabCoulombSolver at R = 1 on the GPU (slab k-space plan + slab near
+    field) equals CoulombSolver.evaluate."""
+    torch = _torch()
+    from paper_2601_00161_b200 import Cell, CoulombSolver, EwaldParameters, ParticleSystem
+    from paper_2601_00161_b200.slab_near import SlabCoulombSolver
+    w, pos, q = workloads.generate(1)
+    params = EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M,
+                             prefactor=0.5)
+    cell = Cell(np.asarray(w.h, dtype=float))
+    ref = CoulombSolver(cell, params).evaluate(ParticleSystem(cell=cell, positions=pos, charges=q))
+    sc = SlabCoulombSolver(w.h, params)
+    mine = sc.owned(pos)
+    assert mine.all()
+    r = sc.evaluate(torch.as_tensor(pos, device="cuda"), torch.as_tensor(q, device="cuda"))
+    assert O.rel_scalar(r.u_near, ref.u_near) <= 1e-12
+    assert O.rel_scalar(r.u_far, ref.u_far) <= 1e-10
+    assert O.rel_scalar(r.energy, ref.energy) <= 1e-10
+    assert O.rel_frobenius(r.pressure, ref.pressure) <= 1e-10
+    assert O.rms_rel_forces(r.forces.cpu().numpy(), ref.forces) <= 1e-10
+    assert r.pair_count == ref.pair_count

@@ -116,3 +116,75 @@ def test_single_rank_slab_equals_whole_grid():
     assert O.rel_scalar(E, oE) <= 1e-12
     assert O.rel_frobenius(Pt, oP) <= 1e-12
     assert O.rms_rel_forces(F.numpy(), oF) <= 1e-12
+
+
+def _coulomb_worker(rank, world, port, case, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from slab_oracle_ops import OracleNearOps, OracleSlabOps
+        from paper_2601_00161_b200 import EwaldParameters
+        from paper_2601_00161_b200.slab import SlabKSpaceSolver, SlabLayout
+        from paper_2601_00161_b200.slab_near import SlabCoulombSolver
+        c = CASES[case]
+        pos, q = _system(c)
+        basis = build_pswf(solve_bandwidth(c["delta"]))
+        oplan = O.make_plan(c["h"], c["M"], c["P"], c["delta"], c["r_c"])
+        lay = SlabLayout(c["M"][2], c["M"][1], world, c["P"])
+        ks = SlabKSpaceSolver(c["h"], c["M"], c["P"], basis, tabulate_window(basis, c["P"]),
+                              c["r_c"], ops=OracleSlabOps(oplan, lay.zstart[rank],
+                                                          lay.zcount[rank]),
+                              device=torch.device("cpu"))
+        ob = O.build_basis(O.solve_bandwidth(c["delta"]))
+        near_ops = OracleNearOps(c["h"], ob, c["r_c"], O.pair_table(ob, c["r_c"]))
+        params = EwaldParameters(r_c=c["r_c"], delta_split=c["delta"], P=c["P"],
+                                 fixed_M=c["M"], prefactor=1.5)
+        sc = SlabCoulombSolver(c["h"], params, kspace=ks, near_ops=near_ops)
+        mine = sc.owned(pos)
+        r = sc.evaluate(torch.as_tensor(pos[mine]), torch.as_tensor(q[mine]))
+        Fg = np.zeros((len(q), 3))
+        Fg[mine] = np.asarray(r.forces)
+        t = torch.as_tensor(Fg)
+        dist.all_reduce(t)
+        out.put((rank, r.u_near, r.u_far, r.u_self, r.u_background, r.pressure, t.numpy(),
+                 r.pair_count))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world", [("ortho", 2), ("tri", 3)])
+def test_slab_coulomb_solver_matches_single_process(case, world):
+    """SlabCoulombSolver (k-space slabs + slab near field + self/background)
+    on gloo ranks equals the single-process oracle composition of
+    evaluate.py:114-144 (prefactor 1.5)."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_coulomb_worker, args=(r, world, port, case, out))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([out.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    c = CASES[case]
+    pos, q = _system(c)
+    pref = 1.5
+    oplan = O.make_plan(c["h"], c["M"], c["P"], c["delta"], c["r_c"])
+    oE, oP, oF = O.kspace(oplan, pos, q)
+    b = O.build_basis(O.solve_bandwidth(c["delta"]))
+    i, j = O.pairs_within(c["h"], pos, c["r_c"])
+    nE, nF, nP, npairs = O.short_range(c["h"], pos, q, i, j, b, c["r_c"], O.pair_table(b, c["r_c"]))
+    u_self = -(b.psi0_at_zero / (2.0 * b.C0 * c["r_c"])) * float(np.sum(q * q))
+    for (_, u_near, u_far, us, ub, P, F, cnt) in res:
+        assert O.rel_scalar(u_near, pref * nE) <= 1e-12
+        assert O.rel_scalar(u_far, pref * oE) <= 1e-12
+        assert O.rel_scalar(us, pref * u_self) <= 1e-12
+        assert abs(ub) <= 1e-12                      # neutral system
+        assert O.rel_frobenius(P, pref * (nP + oP)) <= 1e-12
+        assert O.rms_rel_forces(F, pref * (nF + oF)) <= 1e-12
+        assert cnt == npairs
