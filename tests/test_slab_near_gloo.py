@@ -56,7 +56,7 @@ def _worker(rank, world, port, case, out):
         sl = SlabNearField(c["h"], c["r_c"], bounds, OracleNearOps(c["h"], b, c["r_c"], table))
         own = np.nonzero(sl.owner(pos) == rank)[0]
         E, P, F, cnt = sl.evaluate(torch.as_tensor(pos[own]), torch.as_tensor(q[own]))
-        out[rank] = (own, E, P, np.asarray(F), cnt)
+        out.put((rank, own, E, P, np.asarray(F), cnt))
     finally:
         dist.destroy_process_group()
 
@@ -70,13 +70,19 @@ def test_slab_near_field_matches_single_process(case, world):
     table = O.pair_table(b, c["r_c"])
     i, j = O.pairs_within(c["h"], pos, c["r_c"])
     E0, F0, P0, n0 = O.short_range(c["h"], pos, q, i, j, b, c["r_c"], table)
-    mgr = mp.Manager()
-    out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [out.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
     F = np.zeros_like(F0)
     seen = np.zeros(len(pos), dtype=int)
-    for r in range(world):
-        own, E, P, Fr, cnt = out[r]
+    for (_, own, E, P, Fr, cnt) in res:
         F[own] = Fr
         seen[own] += 1
         assert abs(E - E0) <= 1e-12 * abs(E0)
