@@ -456,3 +456,77 @@ def test_slab_coulomb_solver_single_rank_equals_coulomb_solver():
     assert O.rel_frobenius(r.pressure, ref.pressure) <= 1e-10
     assert O.rms_rel_forces(r.forces.cpu().numpy(), ref.forces) <= 1e-10
     assert r.pair_count == ref.pair_count
+
+
+def test_pair_table_argument_errors_and_cutoff_zero():
+    """realspace.py:81-82 (bad r_in) and :60-61/:66-67 (zero beyond r_c)."""
+    from paper_2601_00161_b200.errors import RealspaceError
+    from paper_2601_00161_b200.realspace import build_pair_table
+    kern = _kern(1e-5, 0.9)
+    with pytest.raises(RealspaceError):
+        build_pair_table(kern, r_in=kern.r_c)
+    with pytest.raises(RealspaceError):
+        build_pair_table(kern, r_in=-0.1)
+    t = build_pair_table(kern)
+    r = np.array([kern.r_c, 1.1 * kern.r_c, 5.0 * kern.r_c])
+    assert np.all(t.near_field(r) == 0.0)
+    assert np.all(t.fn_weight(r)[1:] == 0.0)
+    assert build_pair_table(_kern(1e-8, 1.0)).r_in <= 0.1
+
+
+@pytest.mark.gpu
+def test_near_forces_are_energy_gradient_and_pressure_is_box_derivative():
+    """test_realspace.py:235-282 analogues on the device: forces against a
+    4-point finite difference of the pair-sum energy, diagonal pressure
+    against -(L_a/V) dE/dL_a at fixed fractional coordinates."""
+    _torch()
+    from paper_2601_00161_b200 import Cell, ParticleSystem
+    from paper_2601_00161_b200.realspace import short_range
+    kern = _kern(1e-6, 1.3)
+    rng = np.random.default_rng(15)
+    L = np.array([5.0, 5.5, 6.0])
+    pos = rng.uniform(0, 1, (24, 3)) * L
+    q = rng.normal(size=24)
+    q -= q.mean()
+    cell = Cell.orthorhombic(L)
+    base = short_range(ParticleSystem(cell=cell, positions=pos, charges=q), kern)
+    step = 1e-5
+    for idx in (0, 7, 13):
+        for axis in range(3):
+            num = 0.0
+            for sgn, coef in ((1, 8.0), (-1, -8.0), (2, -1.0), (-2, 1.0)):
+                p2 = pos.copy()
+                p2[idx, axis] += sgn * step
+                num += coef * short_range(ParticleSystem(cell=cell, positions=p2, charges=q),
+                                          kern).energy
+            num /= 12.0 * step
+            assert base.forces[idx, axis] == pytest.approx(-num, abs=2e-6)
+    frac = pos / L
+    for axis in range(3):
+        num = 0.0
+        for sgn, coef in ((1, 8.0), (-1, -8.0), (2, -1.0), (-2, 1.0)):
+            L2 = L.copy()
+            L2[axis] += sgn * step
+            c2 = Cell.orthorhombic(L2)
+            num += coef * short_range(ParticleSystem(cell=c2, positions=frac * L2, charges=q),
+                                      kern).energy
+        num /= 12.0 * step
+        assert base.pressure[axis, axis] == pytest.approx(-L[axis] / cell.volume * num, abs=2e-6)
+
+
+@pytest.mark.gpu
+def test_near_translation_invariance():
+    torch = _torch()
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table
+    w, pos, q = workloads.generate(2)
+    kern = _kern(w.delta, w.r_c)
+    plan = NearFieldPlan(kern, build_pair_table(kern), capacity=w.n)
+    plan.set_cell(w.h)
+    a7, aF, _ = plan.evaluate(torch.as_tensor(pos, device="cuda"), torch.as_tensor(q, device="cuda"))
+    a7, aF = a7.clone(), aF.clone()
+    shifted = (pos + np.array([1.7, -2.3, 0.9])) % np.diag(w.h)
+    b7, bF, _ = plan.evaluate(torch.as_tensor(shifted, device="cuda"),
+                              torch.as_tensor(q, device="cuda"))
+    assert O.rel_scalar(b7[0].item(), a7[0].item()) <= 1e-11
+    assert O.rms_rel_forces(bF.cpu().numpy(), aF.cpu().numpy()) <= 1e-11
+    assert O.rel_frobenius(b7[1:].cpu().numpy(), a7[1:].cpu().numpy()) <= 1e-11
