@@ -12,8 +12,9 @@ from .cells import CellType, infer_cell_type
 from .errors import (CellError, DomainError, EspCudaError, GeometryError, InputError, MeshError,
                      ParameterError, PlanningError, PswfError, RealspaceError,
                      SingularPairError)
-from .kernel import (SplitKernel, background_correction, far_field, far_field_hat, fn_weight,
-                     near_field, self_energy)
+from .kernel import (SplitKernel, background_correction, background_integral, eval_phi0,
+                     far_field, far_field_hat, fn_weight, near_field, pressure_kernel_hat,
+                     self_energy)
 from .mesh import (GridField, GridSpec, ModeWorkspace, TransformProvider, forward_density,
                    local_pressure, long_range_energy, long_range_forces,
                    long_range_pressure, plan_grid, spread_charges)
@@ -21,7 +22,7 @@ from .plan import EspPlan, cell_tables
 from .pswf import (PswfBasis, WindowTable, build_pswf, eval_psi0, solve_bandwidth,
                    tabulate_window)
 from .solver import (CoulombSolver, EnergyBreakdown, EwaldParameters, KSpaceResult,
-                     KSpaceSolver, evaluate_system)
+                     KSpaceSolver, evaluate_system, kinetic_pressure)
 from .particles import read_particles, write_particles
 from .realspace import (NearFieldPlan, PairTable, ShortRangeResult, build_cell_list,
                         build_pair_table, short_range)
@@ -41,5 +42,6 @@ __all__ = [
     "GeometryError", "RealspaceError", "SingularPairError", "far_field", "fn_weight",
     "near_field", "NearFieldPlan", "PairTable", "ShortRangeResult", "build_pair_table",
     "short_range", "NeighborList", "minimum_image", "build_cell_list", "read_particles",
-    "write_particles", "InputError",
+    "write_particles", "InputError", "eval_phi0", "pressure_kernel_hat", "background_integral",
+    "kinetic_pressure",
 ]

@@ -63,6 +63,46 @@ def phi0(basis: PswfBasis, r, r_c: float):
     return np.where(ra >= r_c, 1.0, out)
 
 
+def eval_phi0(basis: PswfBasis, r, r_c: float):
+    """Normalized cumulative integral phi_0(r) (pswf.py:277-292): DomainError
+    for r < 0 or r_c <= 0; 1 for r >= r_c."""
+    if r_c <= 0.0:
+        raise DomainError("cutoff r_c must be positive")
+    ra = np.asarray(r, dtype=float)
+    if np.any(ra < 0.0):
+        raise DomainError("radius must be nonnegative")
+    out = phi0(basis, ra, r_c)
+    return out if out.ndim else float(out)
+
+
+def pressure_kernel_hat(kern: SplitKernel, kvec) -> np.ndarray:
+    """Mode-by-mode 3x3 pressure kernel of one wavevector (kernel.py:99-114;
+    host reference for the per-mode table the device builds)."""
+    kv = np.asarray(kvec, dtype=float)
+    k2 = float(kv @ kv)
+    if k2 == 0.0:
+        raise ZeroModeError("k = 0 is excluded from the pressure kernel")
+    k = np.sqrt(k2)
+    if k > kern.kmax:
+        return np.zeros((3, 3))
+    b = kern.basis
+    x = min(k * kern.r_c / b.c, 1.0)
+    fhat = far_field_hat(kern, k)
+    kk = np.outer(kv, kv)
+    pref = 2.0 * np.pi * b.lambda0 / b.C0
+    dterm = pref * x * b.psi_series(x, derivative=1) / k2 ** 2
+    return fhat * (np.eye(3) - 2.0 * kk / k2) + dterm * kk
+
+
+def background_integral(kern: SplitKernel, n_nodes: int = 128) -> float:
+    """J = r_c^2/2 - int_0^{r_c} r phi_0(r) dr by fixed Gauss-Legendre
+    (kernel.py:126-134)."""
+    nodes, weights = np.polynomial.legendre.leggauss(n_nodes)
+    r = 0.5 * kern.r_c * (nodes + 1.0)
+    w = 0.5 * kern.r_c * weights
+    return 0.5 * kern.r_c ** 2 - float(np.sum(w * r * phi0(kern.basis, r, kern.r_c)))
+
+
 def cumint_coeffs(basis: PswfBasis) -> np.ndarray:
     """Legendre coefficients of int_0^x psi_0 (pswf.py:144-160, legint lbnd=0)."""
     return L.legint(basis.legendre_coeffs, lbnd=0.0)

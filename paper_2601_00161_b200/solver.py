@@ -375,3 +375,10 @@ CoulombSolver.local_pressure = _coulomb_local_pressure
 
 def evaluate_system(sys, params: EwaldParameters, want_forces=True, want_pressure=True):
     return CoulombSolver(sys.cell, params).evaluate(sys, want_forces, want_pressure)
+
+
+def kinetic_pressure(sys) -> np.ndarray:
+    """(1/V) sum_i p_i p_i^T / m_i (evaluate.py:163-166)."""
+    p = np.asarray(sys.momenta, dtype=float)
+    m = np.asarray(sys.masses, dtype=float)
+    return np.einsum("ia,ib->ab", p / m[:, None], p) / sys.cell.volume

@@ -240,6 +240,44 @@ def near_cases():
         del nb, a, F
 
 
+def host_helpers():
+    """Host-side kernel / solver helpers of the reference (kernel.py,
+    pswf.eval_phi0, evaluate.kinetic_pressure) at fixed arguments."""
+    from prolate_ewald.evaluate import kinetic_pressure
+    from prolate_ewald.kernel import (background_correction, background_integral, far_field,
+                                      far_field_hat, fn_weight, near_field,
+                                      pressure_kernel_hat, self_energy)
+    from prolate_ewald.pswf import eval_phi0
+    out = {}
+    for tag, delta, r_c in (("a", 1e-5, 10.0), ("b", 1e-7, 1.3)):
+        kern = SplitKernel(basis=build_pswf(solve_bandwidth(delta)), r_c=r_c)
+        r = np.linspace(0.01, 1.2, 97) * r_c
+        out[f"{tag}_r"] = r
+        out[f"{tag}_phi0"] = eval_phi0(kern.basis, r, r_c)
+        out[f"{tag}_near"] = near_field(kern, r)
+        out[f"{tag}_far"] = far_field(kern, np.concatenate([[0.0], r]))
+        out[f"{tag}_fn"] = fn_weight(kern, r)
+        ks = np.array([[0.1, 0.2, 0.3], [0.5, -0.4, 0.2], [1.2, 0.0, 0.0]]) * kern.kmax
+        out[f"{tag}_k"] = ks
+        out[f"{tag}_pk"] = np.stack([pressure_kernel_hat(kern, k) for k in ks])
+        out[f"{tag}_fhat"] = far_field_hat(kern, np.linalg.norm(ks, axis=1))
+        out[f"{tag}_J"] = np.array(background_integral(kern))
+        q = np.array([0.5, -0.2, 0.9, 0.1])
+        out[f"{tag}_self"] = np.array(self_energy(kern, q))
+        u_cb, u_bb, pc = background_correction(kern, float(q.sum()), 1234.5)
+        out[f"{tag}_bg"] = np.array([u_cb, u_bb])
+        out[f"{tag}_pcorr"] = pc
+    rng = np.random.default_rng(5)
+    sys_ = ParticleSystem(cell=Cell(np.array([[5.0, 0.4, 0.1], [0.0, 6.0, -0.3], [0.0, 0.0, 7.0]])),
+                          positions=rng.uniform(0, 5, (9, 3)), charges=rng.normal(size=9),
+                          masses=rng.uniform(0.5, 2.0, 9), momenta=rng.normal(size=(9, 3)))
+    out["kin_h"] = sys_.cell.h
+    out["kin_p"] = sys_.momenta
+    out["kin_m"] = sys_.masses
+    out["kin_P"] = kinetic_pressure(sys_)
+    save("host_helpers", versions=VERSIONS, **out)
+
+
 def particle_files():
     """Reference-written particle files (cli.write_particles) and what the
     reference reads back from them (cli.read_particles)."""
@@ -265,9 +303,12 @@ def particle_files():
 
 
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["window", "small", "triclinic", "configs", "near", "particles"]
+    parts = sys.argv[1:] or ["window", "small", "triclinic", "configs", "near", "particles",
+                                 "helpers"]
     if "particles" in parts:
         particle_files()
+    if "helpers" in parts:
+        host_helpers()
     if "window" in parts:
         window_tables()
     if "small" in parts:

@@ -141,3 +141,41 @@ def test_membrane_recipe_small():
     s = workloads.wrap_positions(h, pos) @ np.linalg.inv(h).T
     in_slab = (s[:, 2] > 0.41) & (s[:, 2] < 0.59)
     assert np.all(np.isin(q[in_slab & (np.abs(q) == 0.5)], [0.5, -0.5]))
+
+
+@pytest.mark.parametrize("tag,delta,r_c", [("a", 1e-5, 10.0), ("b", 1e-7, 1.3)])
+def test_host_kernel_helpers_match_reference(tag, delta, r_c):
+    """kernel.py / pswf.eval_phi0 host helpers against the reference's values
+    (tests/golden/host_helpers.npz)."""
+    from conftest import golden
+    from paper_2601_00161_b200 import (SplitKernel, background_correction, background_integral,
+                                       build_pswf, eval_phi0, far_field, far_field_hat,
+                                       fn_weight, near_field, pressure_kernel_hat, self_energy,
+                                       solve_bandwidth)
+    g = golden("host_helpers")
+    kern = SplitKernel(basis=build_pswf(solve_bandwidth(delta)), r_c=r_c)
+    r = g[f"{tag}_r"]
+    np.testing.assert_allclose(eval_phi0(kern.basis, r, r_c), g[f"{tag}_phi0"], rtol=1e-14, atol=0)
+    np.testing.assert_allclose(near_field(kern, r), g[f"{tag}_near"], rtol=1e-13, atol=1e-300)
+    np.testing.assert_allclose(far_field(kern, np.concatenate([[0.0], r])), g[f"{tag}_far"],
+                               rtol=1e-14)
+    np.testing.assert_allclose(fn_weight(kern, r), g[f"{tag}_fn"], rtol=1e-13, atol=1e-300)
+    pk = np.stack([pressure_kernel_hat(kern, k) for k in g[f"{tag}_k"]])
+    np.testing.assert_allclose(pk, g[f"{tag}_pk"], rtol=1e-13, atol=1e-300)
+    np.testing.assert_allclose(far_field_hat(kern, np.linalg.norm(g[f"{tag}_k"], axis=1)),
+                               g[f"{tag}_fhat"], rtol=1e-14)
+    assert background_integral(kern) == pytest.approx(float(g[f"{tag}_J"]), rel=1e-14)
+    q = np.array([0.5, -0.2, 0.9, 0.1])
+    assert self_energy(kern, q) == pytest.approx(float(g[f"{tag}_self"]), rel=1e-14)
+    u_cb, u_bb, pc = background_correction(kern, float(q.sum()), 1234.5)
+    np.testing.assert_allclose([u_cb, u_bb], g[f"{tag}_bg"], rtol=1e-14)
+    np.testing.assert_allclose(pc, g[f"{tag}_pcorr"], rtol=1e-14)
+
+
+def test_kinetic_pressure_matches_reference():
+    from conftest import golden
+    from paper_2601_00161_b200 import Cell, ParticleSystem, kinetic_pressure
+    g = golden("host_helpers")
+    s = ParticleSystem(cell=Cell(g["kin_h"]), positions=np.zeros((len(g["kin_m"]), 3)),
+                       charges=np.zeros(len(g["kin_m"])), masses=g["kin_m"], momenta=g["kin_p"])
+    np.testing.assert_allclose(kinetic_pressure(s), g["kin_P"], rtol=1e-14)
