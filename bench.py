@@ -106,8 +106,8 @@ class ClockSampler:
         self._th = None
 
     def _run(self):
-        # NVML polls every 2 ms (the timed regions are tens of ms); nvidia-smi
-        # every 200 ms when NVML is unavailable
+        # NVML polls every ESP_BENCH_CLOCK_MS ms (default 2; the timed regions
+        # are tens of ms); nvidia-smi every 200 ms when NVML is unavailable
         try:
             import pynvml as nv
             nv.nvmlInit()
@@ -122,7 +122,7 @@ class ClockSampler:
                        (bits["hw_slowdown"], bits["hw_thermal_slowdown"],
                         bits["sw_thermal_slowdown"], bits["sw_power_cap"])]
                 self.samples.append([str(sm), str(mx), hex(r)] + act)
-                self._stop.wait(0.002)
+                self._stop.wait(float(os.environ.get("ESP_BENCH_CLOCK_MS", "2")) * 1e-3)
             return
         except Exception:
             pass

@@ -133,6 +133,10 @@ int esp_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * measured B200 box, H2D copies from these run at ~52 GB/s against ~12 GB/s
  * from torch's pinned allocator (tools/tools_copy_probe.py).               */
 int esp_host_alloc(int64_t bytes, void** out);
+/* The next esp_evaluate / esp_spread waits on `event` (a cudaEvent_t) before
+ * its first kernel that reads the charges, so a charge copy on another
+ * stream overlaps the position binning (host-buffer step).  One-shot.      */
+int esp_set_charges_event(esp_plan* plan, void* event);
 int esp_host_free(void* p);
 
 /* --- stages (reference-function granularity) ----------------------------- */

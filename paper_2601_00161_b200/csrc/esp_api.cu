@@ -110,6 +110,15 @@ const char* esp_last_error(void) { return esp::g_last_error.c_str(); }
 
 int esp_version(void) { return 100; }
 
+int esp_set_charges_event(esp_plan* p, void* event) {
+  if (!p) {
+    set_error("null plan");
+    return ESP_ERR_PARAM;
+  }
+  p->q_ready = (cudaEvent_t)event;
+  return ESP_OK;
+}
+
 int esp_host_alloc(int64_t bytes, void** out) {
   if (!out || bytes < 0) {
     set_error("bad host allocation arguments");

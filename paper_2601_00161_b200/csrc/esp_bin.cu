@@ -358,6 +358,11 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
     if (e != cudaSuccess) return e;
     p->launches += 3;
     prof_mark(p, s, "bin_sort");
+    if (p->q_ready) {  // charges copied on another stream (host-buffer step)
+      e = cudaStreamWaitEvent(s, p->q_ready, 0);
+      p->q_ready = nullptr;
+      if (e != cudaSuccess) return e;
+    }
     e = p->precision == ESP_FP64 ? launch_sorted_r<double>(p, g, d_pos, d_q, n, grid, B, s)
                                  : launch_sorted_r<float>(p, g, d_pos, d_q, n, grid, B, s);
     if (e != cudaSuccess) return e;
@@ -377,6 +382,11 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
   p->launches++;
   prof_mark(p, s, "bin_scan");
   if (n == 0) return cudaGetLastError();
+  if (p->q_ready) {  // charges copied on another stream (host-buffer step)
+    e = cudaStreamWaitEvent(s, p->q_ready, 0);
+    p->q_ready = nullptr;
+    if (e != cudaSuccess) return e;
+  }
   if (p->deterministic) {
     k_bin_scatter<<<grid, B, 0, s>>>(d_pos, d_q, n, g, p->d_key, p->d_slot,
                                      p->d_offsets, p->cap, p->d_u_tmp, p->d_q_tmp,

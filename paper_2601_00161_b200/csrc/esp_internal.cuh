@@ -363,6 +363,7 @@ struct esp_plan {
   // profiling: events recorded after each stage kernel when enabled
   int profiling;
   int n_ev;
+  cudaEvent_t q_ready = nullptr;   // esp_set_charges_event: wait before reading q
   cudaEvent_t ev[48];
   const char* ev_name[48];
 };

@@ -207,9 +207,21 @@ class _HostStepper:
             _lib.check(L.esp_copy_async(C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()),
                                         src.numel() * src.element_size(), s), "esp_copy_async")
 
+        # the charge copy runs on a forked stream and overlaps the binning of
+        # the positions (the step waits on it before its first charge read)
+        qside = torch.cuda.Stream()
+        qev = torch.cuda.Event()
+        self._qside, self._qev = qside, qev
+
         def pre():
+            main = torch.cuda.current_stream()
+            qside.wait_stream(main)
+            with torch.cuda.stream(qside):
+                copy(self._d_q, self.charges)
+                qev.record(qside)
             copy(self._d_pos, self.positions)
-            copy(self._d_q, self.charges)
+            _lib.check(L.esp_set_charges_event(solver.plan._handle, C.c_void_p(qev.cuda_event)),
+                       "esp_set_charges_event")
 
         def post():
             if want_forces:

@@ -288,6 +288,15 @@ def test_cuda_graph_replay_matches_eager():
     hs.charges.copy_(torch.as_tensor(q))
     h7, hF = hs.step()
     assert torch.equal(h7, e7.cpu()) and torch.equal(hF, eF.cpu())
+    # new charges through the host buffers (copied on the forked stream):
+    # the step must use them
+    q2 = q * np.linspace(0.5, 1.5, len(q))
+    hs.charges.copy_(torch.as_tensor(q2))
+    h7, hF = hs.step()
+    r7, rF = s.evaluate_device(torch.as_tensor(pos, device="cuda"),
+                               torch.as_tensor(q2, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.equal(h7, r7.cpu()) and torch.equal(hF, rF.cpu())
 
 
 @pytest.mark.slow
