@@ -675,18 +675,21 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
   cudaStream_t s0 = (cudaStream_t)stream;
   esp::prof_mark(p, s0, "start");
   const int ikmode = want_f ? (analytic ? 2 : 1) : 0;
-  if (p->fused && !analytic) {
-    // spread -> fused band-pruned transforms (+ scale/reduce, ik spectra and
-    // inverse transforms) -> gather
+  if (p->fused && (!analytic || p->P <= 8)) {
+    // spread -> fused band-pruned transforms (+ scale/reduce, the ik spectra
+    // or, for analytic forces, the potential spectrum, and the inverse
+    // transforms) -> gather
     rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
     if (rc) return rc;
-    ESP_CUDA(esp::launch_fused_fft(p, want_f, d_out7, s0));
+    ESP_CUDA(esp::launch_fused_fft(p, want_f ? (analytic ? 2 : 1) : 0, d_out7, s0));
     p->fwd_count++;
     p->have_spec = 1;   // in-band box of d_spec is current
     p->have_ik = 0;
     if (want_f) {
-      p->inv_count += 3;
-      if (p->last_n > 0) ESP_CUDA(esp::launch_gather_ik(p, d_forces, s0));
+      p->inv_count += analytic ? 1 : 3;
+      if (p->last_n > 0)
+        ESP_CUDA(analytic ? esp::launch_gather_grad(p, d_forces, s0)
+                          : esp::launch_gather_ik(p, d_forces, s0));
     }
     return ESP_OK;
   }

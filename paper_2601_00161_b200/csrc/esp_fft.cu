@@ -388,6 +388,7 @@ struct FusedArgs {
   double ik_scale;
   double escale, pscale;
   int by0, npy;        // pencil rows by0 .. by0+npy-1 of the in-band box (one GPU: 0, nby)
+  int potential;       // 1: one potential spectrum A X h3/G (analytic forces) instead of ik x3
 };
 
 // Deterministic two-level completion of a per-block reduction: block b has
@@ -644,9 +645,15 @@ k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __re
       if (live && bz >= 0) {
         const double A = __ldg(fa.modeA + ((long long)bz * nby + by) * nbx + mx);
         const C Xv = __ldg(spec + ((long long)mz * fa.M[1] + my) * fa.Hx + mx);
-        const double cf = A * fa.ik_scale * __dadd_rn(kxy, __ldg(K + fa.koff[2] + mz));
-        v[it].x = (real)(-cf * (double)Xv.y);
-        v[it].y = (real)(cf * (double)Xv.x);
+        if (fa.potential) {   // analytic forces: A X h3/G (mesh.py:344-346)
+          const double cf = A * fa.ik_scale;
+          v[it].x = (real)(cf * (double)Xv.x);
+          v[it].y = (real)(cf * (double)Xv.y);
+        } else {              // ik forces: i k_d A X h3/G
+          const double cf = A * fa.ik_scale * __dadd_rn(kxy, __ldg(K + fa.koff[2] + mz));
+          v[it].x = (real)(-cf * (double)Xv.y);
+          v[it].y = (real)(cf * (double)Xv.x);
+        }
       }
     }
 #pragma unroll
@@ -969,7 +976,7 @@ static cudaError_t launch_z_ik(const esp_plan* p, void* ik, const void* tw, cons
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long nlines = (long long)fa.npy * fa.ldx;
-  const dim3 grid((unsigned)((nlines + L - 1) / L), 3);
+  const dim3 grid((unsigned)((nlines + L - 1) / L), fa.potential ? 1 : 3);
   k_z_ik<real, N><<<grid, threads_yz<real>(N), smem, s>>>(
       reinterpret_cast<const C*>(p->d_spec), reinterpret_cast<C*>(ik),
       reinterpret_cast<const C*>(tw), fa, nlines, smap);
@@ -978,10 +985,10 @@ static cudaError_t launch_z_ik(const esp_plan* p, void* ik, const void* tw, cons
 
 template <typename real, int N>
 static cudaError_t launch_y_inv(const esp_plan* p, const void* in, void* out, const void* tw,
-                                int ldx, int nz, cudaStream_t s) {
+                                int ldx, int nz, cudaStream_t s, int ncomp = 3) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N);
-  const long long nlines = 3LL * nz * ldx;
+  const long long nlines = (long long)ncomp * nz * ldx;
   const size_t smem = sizeof(C) * L * pitch(N);
   cudaError_t e = cudaFuncSetAttribute(k_y_inv<real, N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -994,10 +1001,10 @@ static cudaError_t launch_y_inv(const esp_plan* p, const void* in, void* out, co
 
 template <typename real, int N>
 static cudaError_t launch_x_c2r(const esp_plan* p, const void* in, void* fld, const void* tw,
-                                int ldx, int nz, cudaStream_t s) {
+                                int ldx, int nz, cudaStream_t s, int ncomp = 3) {
   using C = typename Cx<real>::t;
   constexpr int PP = pairs_x(N);
-  const long long nrows = 3LL * p->M[1] * nz;
+  const long long nrows = (long long)ncomp * p->M[1] * nz;
   const long long nblk = (nrows + 2 * PP - 1) / (2 * PP);
   k_x_c2r<real, N><<<(unsigned)nblk, kThreadsX, 0, s>>>(
       reinterpret_cast<const C*>(in), reinterpret_cast<real*>(fld),
@@ -1027,13 +1034,13 @@ static cudaError_t launch_xy_fwd(const esp_plan* p, void* out, const void* tw, i
 
 template <typename real, int N>
 static cudaError_t launch_yx_inv(const esp_plan* p, const void* in, const void* tw, int ldx,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, int ncomp = 3) {
   using C = typename Cx<real>::t;
   const size_t smem = plane_smem<real, N>();
   cudaError_t e = cudaFuncSetAttribute(k_yx_inv<real, N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_yx_inv<real, N><<<(unsigned)(3 * p->M[2]), 256, smem, s>>>(
+  k_yx_inv<real, N><<<(unsigned)(ncomp * p->M[2]), 256, smem, s>>>(
       reinterpret_cast<const C*>(in), reinterpret_cast<real*>(p->d_fields),
       reinterpret_cast<const C*>(tw), ldx, p->nbx, p->nby);
   return cudaGetLastError();
@@ -1176,7 +1183,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
     prof_mark(p, s, "fft_y");
     if ((e = debug_check(s, "fft_y")) != cudaSuccess) return e;
   }
-  FusedArgs fa;
+  FusedArgs fa{};
   for (int d = 0; d < 3; ++d) {
     fa.M[d] = p->M[d];
     fa.koff[d] = p->koff[d];
@@ -1196,6 +1203,8 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   fa.pscale = h3sq / (2.0 * p->volume * p->volume);
   fa.by0 = 0;
   fa.npy = p->nby;
+  fa.potential = want_ik == 2 ? 1 : 0;
+  const int ncomp = want_ik == 2 ? 1 : 3;
   e = cudaErrorInvalidValue;
   switch (p->M[2]) {
 #define ESP_CASE(v)                                                                       \
@@ -1225,9 +1234,9 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   if (plane) {
     e = cudaErrorInvalidValue;
     switch (p->M[0]) {
-      case 32: e = launch_yx_inv<real, 32>(p, f->bufC, f->tw[0], ldx, s); break;
-      case 48: e = launch_yx_inv<real, 48>(p, f->bufC, f->tw[0], ldx, s); break;
-      case 64: e = launch_yx_inv<real, 64>(p, f->bufC, f->tw[0], ldx, s); break;
+      case 32: e = launch_yx_inv<real, 32>(p, f->bufC, f->tw[0], ldx, s, ncomp); break;
+      case 48: e = launch_yx_inv<real, 48>(p, f->bufC, f->tw[0], ldx, s, ncomp); break;
+      case 64: e = launch_yx_inv<real, 64>(p, f->bufC, f->tw[0], ldx, s, ncomp); break;
     }
     if (e != cudaSuccess) return e;
     p->launches++;
@@ -1237,7 +1246,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   e = cudaErrorInvalidValue;
   switch (p->M[1]) {
 #define ESP_CASE(v) \
-  case v: e = launch_y_inv<real, v>(p, f->bufC, f->bufD, f->tw[1], ldx, p->M[2], s); break;
+  case v: e = launch_y_inv<real, v>(p, f->bufC, f->bufD, f->tw[1], ldx, p->M[2], s, ncomp); break;
     ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
   }
@@ -1248,7 +1257,8 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   e = cudaErrorInvalidValue;
   switch (p->M[0]) {
 #define ESP_CASE(v) \
-  case v: e = launch_x_c2r<real, v>(p, f->bufD, p->d_fields, f->tw[0], ldx, p->M[2], s); break;
+  case v: e = launch_x_c2r<real, v>(p, f->bufD, p->d_fields, f->tw[0], ldx, p->M[2], s, ncomp); \
+    break;
     ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
   }
@@ -1315,7 +1325,7 @@ static cudaError_t slab_reduce_t(esp_plan* p, const esp_slab_desc* d, const void
   auto* f = reinterpret_cast<FusedFft*>(p->fused);
   int by_start[kMaxRanks + 1];
   slab_by_split(p->nby, d->nranks, by_start);
-  FusedArgs fa;
+  FusedArgs fa{};
   for (int k = 0; k < 3; ++k) {
     fa.M[k] = p->M[k];
     fa.koff[k] = p->koff[k];

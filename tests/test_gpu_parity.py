@@ -623,3 +623,25 @@ def test_fused_slab_transforms_emulated_on_one_gpu(R, precision):
         refp = ref_fields[:, z_start[r]:z_start[r + 1]]
         err = (f - refp).abs().max().item()
         assert err <= tol * refp.abs().max().item()
+
+
+def test_fused_analytic_forces_config1_against_oracle():
+    """Analytic-differentiation forces on the band-pruned fused transforms
+    (one potential spectrum, one inverse transform, window-gradient gather)
+    at config 1, against the oracle's analytic forces (mesh.py:343-349)."""
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    w, pos, q = workloads.generate(1)
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M,
+                                          force_mode="analytic"), capacity=w.n)
+    assert s.plan.fft_path == "fused"
+    s.plan.reset_counters()
+    r = s.evaluate(pos, q)
+    assert s.plan.counters() == (1, 1)
+    plan = O.make_plan(w.h, w.M, w.P, w.delta, w.r_c)
+    modes = O.Modes(plan)
+    rh = O.forward_density(plan, pos, q)
+    Fa = O.forces_analytic(plan, modes, rh, pos, q)
+    assert O.rel_scalar(r.energy, O.energy(modes, rh)) <= F64_TOL
+    assert O.rel_frobenius(r.pressure, O.pressure(modes, rh)) <= F64_TOL
+    assert O.rms_rel_forces(r.forces, Fa) <= F64_TOL
