@@ -102,6 +102,8 @@ static void free_all(esp_plan* p) {
   }
   delete p->h_fast;
   p->h_fast = nullptr;
+  delete p->h_fast_d;
+  p->h_fast_d = nullptr;
 }
 
 extern "C" {
@@ -316,6 +318,16 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
       p->h_fast->cf[i] = (float)d->h_window_coef[i];
     }
     for (int i = 0; i <= p->n_pieces; ++i) p->h_fast->brk[i] = d->h_window_breaks[i];
+  }
+  p->h_fast_d = new esp::FastTab;
+  std::memset(p->h_fast_d, 0, sizeof(esp::FastTab));
+  if (p->h_fast->enabled && d->h_window_deriv_coef) {
+    p->h_fast_d->enabled = 1;
+    for (size_t i = 0; i < nt; ++i) {
+      p->h_fast_d->c[i] = d->h_window_deriv_coef[i];
+      p->h_fast_d->cf[i] = (float)d->h_window_deriv_coef[i];
+    }
+    for (int i = 0; i <= p->n_pieces; ++i) p->h_fast_d->brk[i] = d->h_window_breaks[i];
   }
   {
     std::vector<int> ent_all, cnt_all;

@@ -315,22 +315,57 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = lane >> 4, h = (lane >> 3) & 1, k = lane & 7;
-  for (long long pb = p0 + warp * 2; pb < p1; pb += (kTileThreads / 32) * 2) {
+  constexpr int kStep = (kTileThreads / 32) * 2;
+  constexpr int kRec = 3 * RS;                                  // reals per record
+  constexpr int kChunks = (2 * kRec * (int)sizeof(real)) / 16;  // 16 B pieces per pair
+  // per warp: 2 buffers x (W records of the pair | D records of the pair)
+  real* ring = reinterpret_cast<real*>(
+                   smem_raw + ((sizeof(real) * (size_t)g.PZ * kPlaneZ + 15) & ~size_t(15))) +
+               (size_t)warp * 2 * 4 * kRec;
+  auto fetch = [&](long long pb, int b) {
+    const int avail = (int)min((long long)2, p1 - pb);
+    const int bytes_needed = avail * kRec * (int)sizeof(real);
+    for (int c = lane; c < 2 * kChunks; c += 32) {
+      const int which = c >= kChunks;          // 0: W records, 1: D records
+      const int piece = which ? c - kChunks : c;
+      if (piece * 16 < bytes_needed) {
+        const real* srcb = which ? drec : wrec;
+        const char* src = reinterpret_cast<const char*>(srcb + pb * kRec) + piece * 16;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(
+            reinterpret_cast<char*>(ring + ((size_t)b * 4 + 2 * which) * kRec) + piece * 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  long long pb = p0 + warp * 2;
+  int buf = 0;
+  if (pb < p1) fetch(pb, 0);
+  for (; pb < p1; pb += kStep, buf ^= 1) {
     const long long pl = pb + slot;
     const bool live = pl < p1 && k < P;
+    const long long nx = pb + kStep;
+    int pk = 0;
+    if (pl < p1) pk = PK[pl];
+    if (nx < p1) {
+      fetch(nx, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;");
+    } else {
+      asm volatile("cp.async.wait_group 0;");
+    }
+    __syncwarp();
     real gx = 0, gy = 0, gz = 0;
     if (live) {
-      const int pk = PK[pl];
       const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = (pk >> 16) - tz * g.TZ;
-      const real* W = wrec + pl * (3 * RS);
-      const real* D = drec + pl * (3 * RS);
+      const real* W = ring + ((size_t)buf * 4 + slot) * kRec;
+      const real* D = ring + ((size_t)buf * 4 + 2 + slot) * kRec;
       real wx[P], dx[P], wy[P], dy[P];
 #pragma unroll
-      for (int s = 0; s < P; ++s) {
-        wx[s] = W[s];
-        dx[s] = D[s];
-        wy[s] = W[RS + s];
-        dy[s] = D[RS + s];
+      for (int s2 = 0; s2 < P; ++s2) {
+        wx[s2] = W[s2];
+        dx[s2] = D[s2];
+        wy[s2] = W[RS + s2];
+        dy[s2] = D[RS + s2];
       }
       const real wzk = W[2 * RS + k], dzk = D[2 * RS + k];
       const real* row = s_f + (zl + k) * kPlaneZ + (yl + h) * kRowZ + xl;
@@ -364,38 +399,39 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
       gy += __shfl_xor_sync(0xffffffffu, gy, o);
       gz += __shfl_xor_sync(0xffffffffu, gz, o);
     }
+    __syncwarp();   // the ring slot is refilled next iteration
     if ((lane & 15) == 0 && pl < p1) {
       const double q = Q[pl];
       const double G3[3] = {(double)gx, (double)gy, (double)gz};
       double* f = forces + (long long)IDX[pl] * 3;
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-        f[a] = -q * ((G3[0] * J.j[0 * 3 + a] + G3[1] * J.j[1 * 3 + a]) + G3[2] * J.j[2 * 3 + a]);
+      for (int a2 = 0; a2 < 3; ++a2)
+        f[a2] = -q * ((G3[0] * J.j[0 * 3 + a2] + G3[1] * J.j[1 * 3 + a2]) + G3[2] * J.j[2 * 3 + a2]);
     }
   }
 }
 
 // Window-derivative records dW/dt of every binned particle (analytic mode).
+// Window-derivative weights for the analytic gather: one thread per
+// (particle, axis), unrolled Horner on the derivative table (FastTab) like the
+// binning pass's weight records.
 template <typename real, int P>
-__global__ void k_dweights(Geom g, const real* __restrict__ dtab,
+__global__ void k_dweights(Geom g, FastTab ft, const real* __restrict__ dtab,
                            const double* __restrict__ brk, int n_pieces, int ncoef,
                            long long n, long long cap, const double* __restrict__ U,
                            real* __restrict__ drec) {
-  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (j >= n) return;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= 3 * n) return;
+  const long long j = t / 3;
+  const int d = (int)(t - 3 * j);
   constexpr int RS = rec_stride(P);
-  real* out = drec + j * (3 * RS);
+  const double u = U[d * cap + j];
+  const double base = anchor_base(g, u);
+  real w[P];
+  stencil_weights<real, P>(ft, dtab, brk, n_pieces, ncoef, u, base, g.lo, real(1), w);
+  real* out = drec + j * (3 * RS) + d * RS;
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double u = U[d * cap + j];
-    const double base = anchor_base(g, u);
-#pragma unroll
-    for (int s = 0; s < RS; ++s) {
-      real v = real(0);
-      if (s < P) v = window_eval<real>(dtab, brk, n_pieces, ncoef, u - (base + (double)(g.lo + s)));
-      out[d * RS + s] = v;
-    }
-  }
+  for (int s = 0; s < RS; ++s) out[s] = s < P ? w[s] : real(0);
 }
 
 template <typename real, int P>
@@ -609,8 +645,8 @@ static cudaError_t grad_p(esp_plan* p, double* d_forces, cudaStream_t s) {
                            : reinterpret_cast<const real*>(p->d_dtabf);
     const int B = 256;
     const long long n = p->last_n;
-    k_dweights<real, P><<<(unsigned)((n + B - 1) / B), B, 0, s>>>(
-        g, dtab, p->d_breaks, p->n_pieces, p->ncoef, n, p->cap, p->d_u,
+    k_dweights<real, P><<<(unsigned)((3 * n + B - 1) / B), B, 0, s>>>(
+        g, *p->h_fast_d, dtab, p->d_breaks, p->n_pieces, p->ncoef, n, p->cap, p->d_u,
         reinterpret_cast<real*>(p->d_drec));
     p->launches++;
     prof_mark(p, s, "dweights");
@@ -619,7 +655,10 @@ static cudaError_t grad_p(esp_plan* p, double* d_forces, cudaStream_t s) {
       for (int a = 0; a < 3; ++a)
         J.j[d * 3 + a] = p->ortho ? (d == a ? 1.0 / p->spacing[d] : 0.0)
                                   : (double)p->Mu[d] * p->hinv[d * 3 + a];
-    const size_t smem = sizeof(real) * (size_t)p->PZ * GatherLayout<real, P>::kPlaneZ;
+    constexpr int RS = rec_stride(P);
+    const size_t smem = ((sizeof(real) * (size_t)p->PZ * GatherLayout<real, P>::kPlaneZ + 15) &
+                         ~size_t(15)) +
+                        sizeof(real) * (size_t)(kTileThreads / 32) * 2 * 4 * 3 * RS;
     static size_t attr_set = 0;
     if (smem > attr_set) {
       cudaError_t e = cudaFuncSetAttribute(k_gather_grad<real, P>,

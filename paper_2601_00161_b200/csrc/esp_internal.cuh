@@ -350,6 +350,7 @@ struct esp_plan {
   int* d_comb_cnt;
   long long comb_off[3];
   esp::FastTab* h_fast;   // host copy of the fast window table (kernel param)
+  esp::FastTab* h_fast_d = nullptr;   // derivative window table (analytic gather)
   cufftHandle fwd, inv3, inv1;
   int have_fwd, have_inv3, have_inv1;
   long long fwd_count, inv_count;

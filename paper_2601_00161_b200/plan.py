@@ -466,7 +466,8 @@ class EspPlan:
 
     # -- CUDA graphs ---------------------------------------------------------
     def graph(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool,
-              out7: torch.Tensor, forces: torch.Tensor | None, pre=None, post=None):
+              out7: torch.Tensor, forces: torch.Tensor | None, pre=None, post=None,
+              analytic: bool = False):
         """Capture one whole step (optionally with caller copies before/after)
         into a CUDA graph and return it; ``g.replay()`` re-runs the step on the
         same buffers with a single launch from the host."""
@@ -476,7 +477,7 @@ class EspPlan:
         def body():
             if pre is not None:
                 pre()
-            self.evaluate(pos, q, want_forces, out7, forces)
+            self.evaluate(pos, q, want_forces, out7, forces, analytic=analytic)
             if post is not None:
                 post()
 

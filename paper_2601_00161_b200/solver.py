@@ -139,7 +139,8 @@ class KSpaceSolver:
                                                          device=positions.device)
         if want_forces and forces is None:
             forces = torch.empty((n, 3), dtype=torch.float64, device=positions.device)
-        g = self.plan.graph(positions, charges, want_forces, out7, forces)
+        g = self.plan.graph(positions, charges, want_forces, out7, forces,
+                            analytic=self.params.force_mode == "analytic")
         return g, out7, forces
 
     def host_stepper(self, n: int, want_forces: bool = True):
@@ -229,7 +230,8 @@ class _HostStepper:
             copy(self.out7, self._d_out7)
 
         self.graph = solver.plan.graph(self._d_pos, self._d_q, want_forces, self._d_out7,
-                                       self._d_F, pre=pre, post=post)
+                                       self._d_F, pre=pre, post=post,
+                                       analytic=solver.params.force_mode == "analytic")
 
     def launch(self):
         """Enqueue one step (no host synchronisation)."""

@@ -645,3 +645,15 @@ def test_fused_analytic_forces_config1_against_oracle():
     assert O.rel_scalar(r.energy, O.energy(modes, rh)) <= F64_TOL
     assert O.rel_frobenius(r.pressure, O.pressure(modes, rh)) <= F64_TOL
     assert O.rms_rel_forces(r.forces, Fa) <= F64_TOL
+    # the CUDA-graph and host-buffer paths run the same analytic step
+    P_ = torch.as_tensor(pos, device="cuda")
+    Q_ = torch.as_tensor(q, device="cuda")
+    g, o7, oF = s.graphed(P_, Q_)
+    g.replay()
+    torch.cuda.synchronize()
+    assert O.rms_rel_forces(oF.cpu().numpy(), Fa) <= F64_TOL
+    hs = s.host_stepper(w.n)
+    hs.positions.copy_(torch.as_tensor(pos))
+    hs.charges.copy_(torch.as_tensor(q))
+    _, hF = hs.step()
+    assert torch.equal(hF, oF.cpu())
