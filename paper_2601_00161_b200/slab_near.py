@@ -178,6 +178,8 @@ class SlabCoulombSolver:
         from .realspace import build_pair_table
         from .slab import SlabKSpaceSolver
         d_split, d_spread, P = params.resolved()
+        if params.force_mode != "ik":
+            raise ParameterError("the z-slab k-space solver computes ik forces only")
         self.params = params
         self.cell = Cell(np.asarray(h, dtype=float))
         check_cutoff(self.cell, params.r_c)
