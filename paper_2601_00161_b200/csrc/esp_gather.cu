@@ -21,6 +21,17 @@
 
 namespace esp {
 
+// Asynchronous global -> shared copy of one real (cp.async, 4 or 8 bytes):
+// the field-tile staging issues every plane's loads without waiting on any.
+template <typename real>
+__device__ __forceinline__ void cp_async_real(real* dst_smem, const real* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  if (sizeof(real) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src));
+}
+
 template <typename real, int P>
 __device__ __forceinline__ void stage_weights_g(
     const Geom& g, const real* s_tab, const double* s_brk, int n_pieces, int ncoef,
@@ -147,13 +158,14 @@ k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
     int gz = wrap_near(tz * g.TZ + g.lo, g.M[2]);
     for (int pz = 0; pz < g.PZ; ++pz) {
       const long long o = gz * Mxy + col;
-      R2 v;
-      v.x = f0[o];
-      v.y = f1[o];
-      s_f01[pz * kPlane + r] = v;
-      s_f2[pz * kPlaneZ + (r >> 4) * kRowZ + (r & 15)] = f2[o];
+      real* d01 = reinterpret_cast<real*>(s_f01 + pz * kPlane + r);
+      cp_async_real(d01, f0 + o);
+      cp_async_real(d01 + 1, f1 + o);
+      cp_async_real(s_f2 + pz * kPlaneZ + (r >> 4) * kRowZ + (r & 15), f2 + o);
       gz = gz + 1 == g.M[2] ? 0 : gz + 1;
     }
+    asm volatile("cp.async.commit_group;");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   __syncthreads();
 
@@ -308,9 +320,11 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
     const long long col = (long long)gy * g.M[0] + gx;
     int gz = wrap_near(tz * g.TZ + g.lo, g.M[2]);
     for (int pz = 0; pz < g.PZ; ++pz) {
-      s_f[pz * kPlaneZ + (r >> 4) * kRowZ + (r & 15)] = fld[gz * Mxy + col];
+      cp_async_real(s_f + pz * kPlaneZ + (r >> 4) * kRowZ + (r & 15), fld + gz * Mxy + col);
       gz = gz + 1 == g.M[2] ? 0 : gz + 1;
     }
+    asm volatile("cp.async.commit_group;");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -341,14 +355,27 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
   long long pb = p0 + warp * 2;
   int buf = 0;
   if (pb < p1) fetch(pb, 0);
+  // the pair's scalars (anchor, charge, index) one iteration ahead
+  int pk_n = 0, id_n = 0;
+  double q_n = 0.0;
+  if (pb + slot < p1) {
+    pk_n = PK[pb + slot];
+    q_n = Q[pb + slot];
+    id_n = IDX[pb + slot];
+  }
   for (; pb < p1; pb += kStep, buf ^= 1) {
     const long long pl = pb + slot;
     const bool live = pl < p1 && k < P;
     const long long nx = pb + kStep;
-    int pk = 0;
-    if (pl < p1) pk = PK[pl];
+    const int pk = pk_n, id_c = id_n;
+    const double q_c = q_n;
     if (nx < p1) {
       fetch(nx, buf ^ 1);
+      if (nx + slot < p1) {
+        pk_n = PK[nx + slot];
+        q_n = Q[nx + slot];
+        id_n = IDX[nx + slot];
+      }
       asm volatile("cp.async.wait_group 1;");
     } else {
       asm volatile("cp.async.wait_group 0;");
@@ -359,13 +386,16 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
       const int xl = pk & 0xff, yl = (pk >> 8) & 0xff, zl = (pk >> 16) - tz * g.TZ;
       const real* W = ring + ((size_t)buf * 4 + slot) * kRec;
       const real* D = ring + ((size_t)buf * 4 + 2 + slot) * kRec;
-      real wx[P], dx[P], wy[P], dy[P];
+      real wx[RS], dx[RS], wy[RS], dy[RS];
+      // 16-byte loads of the weight rows (records are 16 B aligned)
+      using V = typename Vec16<real>::type;
+      constexpr int kPer = 16 / (int)sizeof(real);
 #pragma unroll
-      for (int s2 = 0; s2 < P; ++s2) {
-        wx[s2] = W[s2];
-        dx[s2] = D[s2];
-        wy[s2] = W[RS + s2];
-        dy[s2] = D[RS + s2];
+      for (int c = 0; c < RS / kPer; ++c) {
+        Vec16<real>::split(reinterpret_cast<const V*>(W)[c], wx + c * kPer);
+        Vec16<real>::split(reinterpret_cast<const V*>(D)[c], dx + c * kPer);
+        Vec16<real>::split(reinterpret_cast<const V*>(W + RS)[c], wy + c * kPer);
+        Vec16<real>::split(reinterpret_cast<const V*>(D + RS)[c], dy + c * kPer);
       }
       const real wzk = W[2 * RS + k], dzk = D[2 * RS + k];
       const real* row = s_f + (zl + k) * kPlaneZ + (yl + h) * kRowZ + xl;
@@ -401,9 +431,9 @@ k_gather_grad(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
     }
     __syncwarp();   // the ring slot is refilled next iteration
     if ((lane & 15) == 0 && pl < p1) {
-      const double q = Q[pl];
+      const double q = q_c;
       const double G3[3] = {(double)gx, (double)gy, (double)gz};
-      double* f = forces + (long long)IDX[pl] * 3;
+      double* f = forces + (long long)id_c * 3;
 #pragma unroll
       for (int a2 = 0; a2 < 3; ++a2)
         f[a2] = -q * ((G3[0] * J.j[0 * 3 + a2] + G3[1] * J.j[1 * 3 + a2]) + G3[2] * J.j[2 * 3 + a2]);
