@@ -331,6 +331,16 @@ def run_ours(args):
         F_an = torch.empty((n, 3), dtype=torch.float64, device=dev)
         o7_an = torch.empty(7, dtype=torch.float64, device=dev)
         g_an, _, _ = solver_an.graphed(pos, q, True, o7_an, F_an)
+    # fp32 mode (BASELINE config 1 lists fp64 and fp32; fp64 positions/anchors,
+    # fp32 grid / transforms / fields, fp64 reductions; tolerance 1e-5)
+    f32 = None
+    if args.precision == "fp64":
+        solver32 = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
+                                                     fixed_M=w.M, precision="fp32",
+                                                     cell_type=w.cell_type), capacity=n)
+        F32 = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        o7_32 = torch.empty(7, dtype=torch.float64, device=dev)
+        g_32, _, _ = solver32.graphed(pos, q, True, o7_32, F32)
     hs = solver.host_stepper(n, True)            # public host-buffer API
     hs.positions.copy_(torch.as_tensor(pos_np))
     hs.charges.copy_(torch.as_tensor(q_np))
@@ -340,6 +350,11 @@ def run_ours(args):
         ms_po = timed(g_po.replay, K, W)
         ms_e2e = timed(hs.launch, K, W)
         ms_eager = timed(lambda: step(True), K, W)
+        if args.precision == "fp64":
+            ms_32 = timed(g_32.replay, K, W)
+            f32 = {"ms_per_step": ms_32, "value": world * n / (ms_32 * 1e-3), "unit": UNIT,
+                   "what": "force+pressure, precision='fp32' (fp32 grid, transforms and "
+                           "fields; fp64 coordinates and reductions)"}
         if w.cell_type != "triclinic":
             ms_an = timed(g_an.replay, K, W)
             an = {"ms_per_step": ms_an, "value": world * n / (ms_an * 1e-3), "unit": UNIT,
@@ -430,6 +445,8 @@ def run_ours(args):
     }
     if an is not None:
         line["analytic_forces"] = an
+    if f32 is not None:
+        line["fp32_mode"] = f32
     if near is not None:
         near["fp64_frac_est"] = round(near["fp64_tflops_est"] / fp64_tflops, 4)
         line["near_field"] = near
