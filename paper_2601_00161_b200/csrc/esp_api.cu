@@ -691,7 +691,9 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
     // spread -> fused band-pruned transforms (+ scale/reduce, the ik spectra
     // or, for analytic forces, the potential spectrum, and the inverse
     // transforms) -> gather
+    p->want_drec = want_f && analytic;
     rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
+    p->want_drec = 0;
     if (rc) return rc;
     ESP_CUDA(esp::launch_fused_fft(p, want_f ? (analytic ? 2 : 1) : 0, d_out7, s0));
     p->fwd_count++;

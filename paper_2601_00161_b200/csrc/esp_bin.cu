@@ -52,6 +52,24 @@ __device__ __forceinline__ void record_dim_store(const Geom& g, int key, int d,
   }
 }
 
+// Derivative-weight row of one dimension (analytic forces): computed in the
+// binning pass when the step needs it, so the gradient gather needs no
+// separate pass over the particles.
+template <typename real, int P>
+__device__ __forceinline__ void drec_dim_store(const Geom& g, const FastTab& ftd,
+                                               const real* __restrict__ dtab,
+                                               const double* __restrict__ brk, int n_pieces,
+                                               int ncoef, int d, double u, long long dst,
+                                               real* __restrict__ drec) {
+  constexpr int RS = rec_stride(P);
+  const double base = anchor_base(g, u);
+  real w[P];
+  stencil_weights<real, P>(ftd, dtab, brk, n_pieces, ncoef, u, base, g.lo, real(1), w);
+  real* out = drec + dst * (3 * RS) + d * RS;
+#pragma unroll
+  for (int s = 0; s < RS; ++s) out[s] = s < P ? w[s < P ? s : 0] : real(0);
+}
+
 template <typename real, int P>
 __device__ __forceinline__ void write_record_dim(const Geom& g, const FastTab& ft,
                                                  const real* __restrict__ tab,
@@ -115,11 +133,13 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
              const int* __restrict__ skey, const int* __restrict__ sval,
              const double* __restrict__ pos, const double* __restrict__ q,
              double* __restrict__ u_out, double* __restrict__ q_out,
-             int* __restrict__ idx_out, real* __restrict__ wrec, int* __restrict__ pk) {
+             int* __restrict__ idx_out, real* __restrict__ wrec, int* __restrict__ pk,
+             FastTab ftd, const real* __restrict__ dtab, real* __restrict__ drec) {
   // The block's 32 records (and packed anchors) are assembled in shared
   // memory and written out as one contiguous run.
   constexpr int RS = rec_stride(P);
   __shared__ __align__(16) real s_rec[kBinPerBlock * 3 * RS];
+  __shared__ __align__(16) real s_drec[kBinPerBlock * 3 * RS];
   __shared__ int s_pk[kBinPerBlock];
   const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
   const long long j0 = (long long)blockIdx.x * kBinPerBlock;
@@ -139,6 +159,14 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
     record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
 #pragma unroll
     for (int t = 0; t < RS; ++t) s_rec[(l * 3 + d) * RS + t] = t < P ? w[t < P ? t : 0] : real(0);
+    if (drec) {   // derivative row staged like the weights, written contiguously below
+      real dw[P];
+      stencil_weights<real, P>(ftd, dtab, brk, n_pieces, ncoef, u, anchor_base(g, u), g.lo,
+                               real(1), dw);
+#pragma unroll
+      for (int t = 0; t < RS; ++t)
+        s_drec[(l * 3 + d) * RS + t] = t < P ? dw[t < P ? t : 0] : real(0);
+    }
     unsigned char* pb = reinterpret_cast<unsigned char*>(s_pk + l);
     if (d == 2) {
       *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
@@ -152,6 +180,10 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
   real* dst = wrec + j0 * (3 * RS);
   for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) dst[t] = s_rec[t];
   for (int t = threadIdx.x; t < nb; t += 3 * kBinPerBlock) pk[j0 + t] = s_pk[t];
+  if (drec) {
+    real* ddst = drec + j0 * (3 * RS);
+    for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) ddst[t] = s_drec[t];
+  }
 }
 
 // Scatter to key segments.  Writes grid coordinates u (SoA), charge and the
@@ -188,7 +220,8 @@ k_bin_canon(Geom g, FastTab ft, const real* __restrict__ tab, const double* __re
             const double* __restrict__ u_tmp, const double* __restrict__ q_tmp,
             const int* __restrict__ idx_tmp, double* __restrict__ u_out,
             double* __restrict__ q_out, int* __restrict__ idx_out, real* __restrict__ wrec,
-            int* __restrict__ pk) {
+            int* __restrict__ pk, FastTab ftd, const real* __restrict__ dtab,
+            real* __restrict__ drec) {
   __shared__ long long s_dst[kBinPerBlock];
   const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
   const long long j = (long long)blockIdx.x * kBinPerBlock + l;
@@ -228,6 +261,7 @@ k_bin_canon(Geom g, FastTab ft, const real* __restrict__ tab, const double* __re
   const long long dst = s_dst[l];
   u_out[d * cap + dst] = u;
   record_dim_store<real, P>(g, key, d, w, a, dst, wrec, pk);
+  if (drec) drec_dim_store<real, P>(g, ftd, dtab, brk, n_pieces, ncoef, d, u, dst, drec);
 }
 
 // Non-deterministic mode: records straight after the atomic-slot scatter.
@@ -254,12 +288,21 @@ static void launch_tail(esp_plan* p, const Geom& g, long long n, unsigned grid, 
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
   real* wrec = reinterpret_cast<real*>(p->d_wrec);
+  const real* dtab = std::is_same<real, double>::value
+                         ? reinterpret_cast<const real*>(p->d_dtab)
+                         : reinterpret_cast<const real*>(p->d_dtabf);
+  // derivative records in the same pass when the step's forces are analytic
+  real* drec = p->want_drec && p->deterministic && P <= 8 && p->h_fast_d->enabled
+                   ? reinterpret_cast<real*>(p->d_drec)
+                   : nullptr;
+  p->drec_ready = drec != nullptr;
   const unsigned g3 = (unsigned)((n + kBinPerBlock - 1) / kBinPerBlock);
   if (p->deterministic) {
     k_bin_canon<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
                                            p->ncoef, n, p->cap, p->d_bkey, p->d_offsets,
                                            p->d_u_tmp, p->d_q_tmp, p->d_idx_tmp, p->d_u,
-                                           p->d_q, p->d_idx, wrec, p->d_pk);
+                                           p->d_q, p->d_idx, wrec, p->d_pk, *p->h_fast_d, dtab,
+                                           drec);
   } else {
     k_bin_records<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
                                              p->ncoef, n, p->cap, p->d_key, p->d_slot,
@@ -293,11 +336,19 @@ static void launch_sorted(esp_plan* p, const Geom& g, const double* d_pos, const
   const real* tab = std::is_same<real, double>::value
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
+  const real* dtab = std::is_same<real, double>::value
+                         ? reinterpret_cast<const real*>(p->d_dtab)
+                         : reinterpret_cast<const real*>(p->d_dtabf);
+  real* drec = p->want_drec && P <= 8 && p->h_fast_d->enabled
+                   ? reinterpret_cast<real*>(p->d_drec)
+                   : nullptr;
+  p->drec_ready = drec != nullptr;
   const unsigned g3 = (unsigned)((n + kBinPerBlock - 1) / kBinPerBlock);
   k_bin_sorted<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
                                           p->ncoef, n, p->cap, p->d_bkey, p->d_idx_tmp, d_pos,
                                           d_q, p->d_u, p->d_q, p->d_idx,
-                                          reinterpret_cast<real*>(p->d_wrec), p->d_pk);
+                                          reinterpret_cast<real*>(p->d_wrec), p->d_pk,
+                                          *p->h_fast_d, dtab, drec);
 }
 
 template <typename real>

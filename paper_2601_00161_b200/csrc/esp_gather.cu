@@ -675,11 +675,13 @@ static cudaError_t grad_p(esp_plan* p, double* d_forces, cudaStream_t s) {
                            : reinterpret_cast<const real*>(p->d_dtabf);
     const int B = 256;
     const long long n = p->last_n;
-    k_dweights<real, P><<<(unsigned)((3 * n + B - 1) / B), B, 0, s>>>(
-        g, *p->h_fast_d, dtab, p->d_breaks, p->n_pieces, p->ncoef, n, p->cap, p->d_u,
-        reinterpret_cast<real*>(p->d_drec));
-    p->launches++;
-    prof_mark(p, s, "dweights");
+    if (!p->drec_ready) {   // not produced by the binning pass of this step
+      k_dweights<real, P><<<(unsigned)((3 * n + B - 1) / B), B, 0, s>>>(
+          g, *p->h_fast_d, dtab, p->d_breaks, p->n_pieces, p->ncoef, n, p->cap, p->d_u,
+          reinterpret_cast<real*>(p->d_drec));
+      p->launches++;
+      prof_mark(p, s, "dweights");
+    }
     Jac J;
     for (int d = 0; d < 3; ++d)
       for (int a = 0; a < 3; ++a)

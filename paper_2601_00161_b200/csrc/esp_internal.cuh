@@ -351,6 +351,8 @@ struct esp_plan {
   long long comb_off[3];
   esp::FastTab* h_fast;   // host copy of the fast window table (kernel param)
   esp::FastTab* h_fast_d = nullptr;   // derivative window table (analytic gather)
+  int want_drec = 0;    // next binning also writes derivative records (analytic step)
+  int drec_ready = 0;   // d_drec holds the last binning's derivative records
   cufftHandle fwd, inv3, inv1;
   int have_fwd, have_inv3, have_inv1;
   long long fwd_count, inv_count;
