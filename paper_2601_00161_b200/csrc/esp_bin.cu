@@ -126,7 +126,7 @@ __global__ void k_bin_keys(const double* __restrict__ pos, long long n, Geom g,
 
 // After the stable radix sort: gather each particle into its binned slot and
 // write its weight record.  Reads are random, writes contiguous per block.
-template <typename real, int P>
+template <typename real, int P, bool DREC>
 __global__ void __launch_bounds__(3 * kBinPerBlock)
 k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __restrict__ brk,
              int n_pieces, int ncoef, long long n, long long cap,
@@ -139,7 +139,7 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
   // memory and written out as one contiguous run.
   constexpr int RS = rec_stride(P);
   __shared__ __align__(16) real s_rec[kBinPerBlock * 3 * RS];
-  __shared__ __align__(16) real s_drec[kBinPerBlock * 3 * RS];
+  __shared__ __align__(16) real s_drec[DREC ? kBinPerBlock * 3 * RS : 2];
   __shared__ int s_pk[kBinPerBlock];
   const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
   const long long j0 = (long long)blockIdx.x * kBinPerBlock;
@@ -159,7 +159,7 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
     record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
 #pragma unroll
     for (int t = 0; t < RS; ++t) s_rec[(l * 3 + d) * RS + t] = t < P ? w[t < P ? t : 0] : real(0);
-    if (drec) {   // derivative row staged like the weights, written contiguously below
+    if (DREC) {   // derivative row staged like the weights, written contiguously below
       real dw[P];
       stencil_weights<real, P>(ftd, dtab, brk, n_pieces, ncoef, u, anchor_base(g, u), g.lo,
                                real(1), dw);
@@ -180,7 +180,7 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
   real* dst = wrec + j0 * (3 * RS);
   for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) dst[t] = s_rec[t];
   for (int t = threadIdx.x; t < nb; t += 3 * kBinPerBlock) pk[j0 + t] = s_pk[t];
-  if (drec) {
+  if (DREC) {
     real* ddst = drec + j0 * (3 * RS);
     for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) ddst[t] = s_drec[t];
   }
@@ -344,11 +344,16 @@ static void launch_sorted(esp_plan* p, const Geom& g, const double* d_pos, const
                    : nullptr;
   p->drec_ready = drec != nullptr;
   const unsigned g3 = (unsigned)((n + kBinPerBlock - 1) / kBinPerBlock);
-  k_bin_sorted<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(g, *p->h_fast, tab, p->d_breaks, p->n_pieces,
-                                          p->ncoef, n, p->cap, p->d_bkey, p->d_idx_tmp, d_pos,
-                                          d_q, p->d_u, p->d_q, p->d_idx,
-                                          reinterpret_cast<real*>(p->d_wrec), p->d_pk,
-                                          *p->h_fast_d, dtab, drec);
+  if (drec)
+    k_bin_sorted<real, P, true><<<g3, 3 * kBinPerBlock, 0, s>>>(
+        g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, n, p->cap, p->d_bkey,
+        p->d_idx_tmp, d_pos, d_q, p->d_u, p->d_q, p->d_idx, reinterpret_cast<real*>(p->d_wrec),
+        p->d_pk, *p->h_fast_d, dtab, drec);
+  else
+    k_bin_sorted<real, P, false><<<g3, 3 * kBinPerBlock, 0, s>>>(
+        g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, n, p->cap, p->d_bkey,
+        p->d_idx_tmp, d_pos, d_q, p->d_u, p->d_q, p->d_idx, reinterpret_cast<real*>(p->d_wrec),
+        p->d_pk, *p->h_fast_d, dtab, nullptr);
 }
 
 template <typename real>
