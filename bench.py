@@ -417,6 +417,17 @@ def run_ours(args):
         else:
             line_smem = None
 
+    # stage-wise roofline of the whole step: per stage
+    # max(compulsory bytes / HBM, flops / FP peak), binning excluded
+    stages = ["spread", "fft_forward", "scale_reduce", "fft_inverse_x3", "gather"]
+    fp_peak = fp64_tflops if real_b == 8 else 2 * fp64_tflops
+    t_roof = sum(max(alg[k]["bytes"] / (hbm_peak * 1e9), alg[k]["flops"] / (fp_peak * 1e12))
+                 for k in stages) * 1e3
+    step_roof = {"model": "SURVEY §8(d) stage-wise: spread, forward FFT, scale/reduce, "
+                          "3 inverse FFTs, gather; max(bytes/HBM, flops/FP peak) per stage, "
+                          "binning not counted",
+                 "t_roof_ms": round(t_roof, 5), "frac": round(t_roof / ms_fp, 4),
+                 "hbm_gbs": hbm_peak, "fp_peak_tflops": round(fp_peak, 2)}
     value = world * n / (ms_fp * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -440,6 +451,7 @@ def run_ours(args):
         "roofline": roof,
         "roofline_fp": roof_fp,
         "roofline_smem": line_smem,
+        "step_roofline": step_roof,
         "kernel_ms": {k: round(v, 5) for k, v in prof.items()},
         "fp64_peak_tflops_measured": round(fp64_tflops, 2),
     }
