@@ -1,5 +1,6 @@
 /*
- * esp_b200.h — C ABI of the B200-native ESP k-space (long-range) path.
+ * esp_b200.h — C ABI of the B200-native ESP k-space (long-range) path, plus
+ * the near-field pair sum and the particle-file reader that complete a step.
  *
  * Drop-in replacement for the k-space pipeline of the reference package
  * `prolate_ewald` (arXiv 2601.00161), /root/reference/pkg/src/prolate_ewald:
@@ -17,6 +18,10 @@
  *                     <- plan_grid + ModeWorkspace      (mesh.py:81-142, 229-282)
  *   esp_counters      <- TransformProvider.forward_count / inverse_count
  *                                                     (mesh.py:33-55)
+ *   esp_near_*        <- realspace.short_range / build_pair_table,
+ *                        system.build_cell_list        (realspace.py:29-157,
+ *                                                     system.py:144-222)
+ *   esp_particles_*   <- cli.read_particles / write_particles (cli.py:57-112)
  *
  * Conventions
  *  - All pointers named d_* are DEVICE pointers; h_* are host pointers.
