@@ -87,6 +87,7 @@ struct esp_near {
   long long cap = 0;
   int div = 2;
   int kernel = 0;             // 0: staged tile kernel, 1: per-particle rows (ESP_NEAR_KERNEL=rows)
+  int octants = 1;            // cell-octant sub-order for the tile kernel (ESP_NEAR_OCT=0 off)
   int have_cell = 0;
   CellGeom g{};
   // tables
@@ -253,13 +254,17 @@ __device__ __forceinline__ double frac_coord(const CellGeom& g, int d, double x,
 
 // Cell of each particle and its record moved into the home image (positions
 // already inside the cell, as ParticleSystem wraps them, are unchanged).
+// sub = 1: the key also carries the particle's octant within its cell
+// (key = cell * 8 + octant), so the tile kernel's passes of consecutive
+// particles are spatially compact (tighter pass bounding boxes, fewer
+// candidates); the order stays deterministic (stable sort by index).
 __global__ void k_near_cells(const double* __restrict__ pos, const double* __restrict__ q,
                              long long n, CellGeom g, int* __restrict__ key,
-                             int* __restrict__ idx, double4* __restrict__ rec) {
+                             int* __restrict__ idx, double4* __restrict__ rec, int sub) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
-  int c[3];
+  int c[3], oct = 0;
   double img[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
@@ -270,6 +275,7 @@ __global__ void k_near_cells(const double* __restrict__ pos, const double* __res
     const double t = (s - fl) * g.nc[d];
     int cd = (int)fmin(fmax(t, 0.0), (double)(g.nc[d] - 1));
     c[d] = cd;
+    oct |= (t - cd >= 0.5 ? 1 : 0) << d;
   }
   double hx = x, hy = y, hz = z;
   if (img[0] != 0.0 || img[1] != 0.0 || img[2] != 0.0) {
@@ -277,7 +283,8 @@ __global__ void k_near_cells(const double* __restrict__ pos, const double* __res
     hy = y - (g.h[3] * img[0] + g.h[4] * img[1] + g.h[5] * img[2]);
     hz = z - (g.h[6] * img[0] + g.h[7] * img[1] + g.h[8] * img[2]);
   }
-  key[i] = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
+  const int cell = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
+  key[i] = sub ? cell * 8 + oct : cell;
   idx[i] = (int)i;
   rec[i] = make_double4(hx, hy, hz, q ? q[i] : 0.0);
 }
@@ -286,12 +293,13 @@ __global__ void k_near_cells(const double* __restrict__ pos, const double* __res
 __global__ void k_near_sorted(const int* __restrict__ key_sorted, const int* __restrict__ perm,
                               const double4* __restrict__ rec_u, long long n,
                               long long ncells, double4* __restrict__ rec,
-                              int* __restrict__ cell_start) {
+                              int* __restrict__ cell_start, int sub) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= n) return;
   rec[k] = rec_u[perm[k]];
-  const int c = key_sorted[k];
-  const int cp = k > 0 ? key_sorted[k - 1] : -1;
+  const int sh = sub ? 3 : 0;   // octant bits below the cell id
+  const int c = key_sorted[k] >> sh;
+  const int cp = k > 0 ? (key_sorted[k - 1] >> sh) : -1;
   for (int cc = cp + 1; cc <= c; ++cc) cell_start[cc] = (int)k;
   if (k == n - 1)
     for (long long cc = c + 1; cc <= ncells; ++cc) cell_start[cc] = (int)n;
@@ -1123,6 +1131,8 @@ int esp_near_create(const esp_near_desc* d, esp_near** out) {
   {
     const char* k = std::getenv("ESP_NEAR_KERNEL");
     p->kernel = (k && std::strcmp(k, "rows") == 0) ? 1 : 0;
+    const char* oc = std::getenv("ESP_NEAR_OCT");
+    p->octants = !(oc && oc[0] == '0');
     if (cudaFuncSetAttribute(k_near_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(TileSmem)) != cudaSuccess) {
       set_error("near-field tile kernel: shared-memory opt-in failed");
@@ -1344,15 +1354,16 @@ int esp_near_evaluate_local(esp_near* p, const double* d_pos, const double* d_q,
   if (n == 0) return near_reduce(p, 0, d_out7, (long long*)d_stats, s);
   const int B = 256;
   const unsigned grid = (unsigned)((n + B - 1) / B);
-  k_near_cells<<<grid, B, 0, s>>>(d_pos, d_q, n, p->g, p->d_key, p->d_idx, p->d_rec_u);
+  const int sub = p->kernel == 0 ? p->octants : 0;
+  k_near_cells<<<grid, B, 0, s>>>(d_pos, d_q, n, p->g, p->d_key, p->d_idx, p->d_rec_u, sub);
   p->launches++;
   size_t bytes = p->sort_bytes;
   NEAR_CUDA(cub::DeviceRadixSort::SortPairs(p->d_sort_tmp, bytes, p->d_key, p->d_key_sorted,
                                             p->d_idx, p->d_perm, (int)n, 0,
-                                            bits_for(p->g.ncells), s));
+                                            bits_for(p->g.ncells * (sub ? 8 : 1)), s));
   p->launches += 3;
   k_near_sorted<<<grid, B, 0, s>>>(p->d_key_sorted, p->d_perm, p->d_rec_u, n, p->g.ncells,
-                                   p->d_rec, p->d_cell_start);
+                                   p->d_rec, p->d_cell_start, sub);
   p->launches++;
   if (p->kernel == 1) {
     k_near_pairs<<<(unsigned)p->g.ncells, kNearThreads, 0, s>>>(
@@ -1431,13 +1442,13 @@ int esp_near_build_pairs(esp_near* p, const double* d_pos, int64_t n, int64_t* n
   if (n < 2) return ESP_OK;
   const int B = 256;
   const unsigned grid = (unsigned)((n + B - 1) / B);
-  k_near_cells<<<grid, B, 0, s>>>(d_pos, nullptr, n, p->g, p->d_key, p->d_idx, p->d_rec_u);
+  k_near_cells<<<grid, B, 0, s>>>(d_pos, nullptr, n, p->g, p->d_key, p->d_idx, p->d_rec_u, 0);
   size_t bytes = p->sort_bytes;
   NEAR_CUDA(cub::DeviceRadixSort::SortPairs(p->d_sort_tmp, bytes, p->d_key, p->d_key_sorted,
                                             p->d_idx, p->d_perm, (int)n, 0,
                                             bits_for(p->g.ncells), s));
   k_near_sorted<<<grid, B, 0, s>>>(p->d_key_sorted, p->d_perm, p->d_rec_u, n, p->g.ncells,
-                                   p->d_rec, p->d_cell_start);
+                                   p->d_rec, p->d_cell_start, 0);
   // per-particle counts and their exclusive prefix (n + 1 entries)
   long long *d_cnt = nullptr, *d_off = nullptr;
   NEAR_CUDA(cudaMallocAsync(&d_cnt, sizeof(long long) * (n + 1), s));
