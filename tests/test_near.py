@@ -530,3 +530,37 @@ def test_near_translation_invariance():
     assert O.rel_scalar(b7[0].item(), a7[0].item()) <= 1e-11
     assert O.rms_rel_forces(bF.cpu().numpy(), aF.cpu().numpy()) <= 1e-11
     assert O.rel_frobenius(b7[1:].cpu().numpy(), a7[1:].cpu().numpy()) <= 1e-11
+
+
+@pytest.mark.gpu
+def test_near_orderings_agree():
+    """Cell-octant sub-order (default), plain cell order (ESP_NEAR_OCT=0) and
+    the per-particle row kernel (ESP_NEAR_KERNEL=rows) sum the same pairs:
+    equal pair counts, energies / forces to round-off."""
+    import os
+    torch = _torch()
+    from paper_2601_00161_b200.realspace import NearFieldPlan, build_pair_table
+    w, pos, q = workloads.generate(1)
+    kern = _kern(w.delta, w.r_c)
+    table = build_pair_table(kern)
+    P = torch.as_tensor(pos, device="cuda")
+    Q = torch.as_tensor(q, device="cuda")
+    res = []
+    for env in ({}, {"ESP_NEAR_OCT": "0"}, {"ESP_NEAR_KERNEL": "rows"}):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            plan = NearFieldPlan(kern, table, capacity=w.n)
+            plan.set_cell(w.h)
+            o7, F, st = plan.evaluate(P, Q)
+            res.append((o7.cpu().numpy(), F.cpu().numpy(), int(st[0])))
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+    for o7, F, cnt in res[1:]:
+        assert cnt == res[0][2]
+        assert O.rel_scalar(o7[0], res[0][0][0]) <= 1e-12
+        assert O.rms_rel_forces(F, res[0][1]) <= 1e-12
