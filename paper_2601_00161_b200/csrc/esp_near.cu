@@ -84,6 +84,7 @@ struct esp_near {
   NearConst c{};
   double reach = 0.0;
   double volume = 1.0;
+  double width[3] = {0, 0, 0};   // perpendicular widths of the bound cell
   long long cap = 0;
   int div = 2;
   int kernel = 0;             // 0: staged tile kernel, 1: per-particle rows (ESP_NEAR_KERNEL=rows)
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kNearThreads, ESP_NEAR_MINB)
 // Hits go through the warp's compaction queue as in k_near_pairs; the queue
 // and the accumulators persist across chunks.
 #ifndef ESP_TILE_W
-#define ESP_TILE_W 4
+#define ESP_TILE_W 8
 #endif
 constexpr int kTileW = ESP_TILE_W;    // warps per CTA = particles per pass
 constexpr int kTileI = kTileW;
@@ -1095,6 +1096,48 @@ int check_plan(const esp_near* p, long long n) {
   return ESP_OK;
 }
 
+// Cell lattice with `div` cells per reach along each axis (fewer if the box
+// would need more than 2^23 cells; thicker cells stay valid).
+int near_layout(esp_near* p, int div) {
+  CellGeom& g = p->g;
+  long long nc[3], total;
+  for (;;) {
+    total = 1;
+    for (int d = 0; d < 3; ++d) {
+      nc[d] = (long long)std::floor(p->width[d] * div / p->reach);
+      nc[d] = std::max<long long>(1, std::min<long long>(nc[d], 1024));
+      total *= nc[d];
+    }
+    if (total <= (1ll << 23) || div == 1) break;
+    --div;
+  }
+  while (total > (1ll << 23)) {
+    total = 1;
+    for (int d = 0; d < 3; ++d) {
+      nc[d] = std::max<long long>(1, nc[d] / 2);
+      total *= nc[d];
+    }
+  }
+  const int st = near_reserve_cells(p, std::max<long long>(total + 1, p->cap + 1));
+  if (st != ESP_OK) return st;
+  for (int d = 0; d < 3; ++d) g.nc[d] = (int)nc[d];
+  g.ncells = total;
+  g.div = div;
+  g.n_rows = (2 * div + 1) * (2 * div + 1);
+  return ESP_OK;
+}
+
+// Automatic cells-per-reach (measured): 3 for small, dense
+// orthorhombic systems (>= 24 particles per 2-per-reach cell and fewer than
+// 8192 such cells: the finer trimming pays), otherwise 2.
+int near_auto_div(const esp_near* p, long long n) {
+  if (!p->g.ortho) return 2;
+  long long c2 = 1;
+  for (int d = 0; d < 3; ++d)
+    c2 *= std::max<long long>(1, (long long)std::floor(p->width[d] * 2 / p->reach));
+  return (c2 < 8192 && n >= 24 * c2) ? 3 : 2;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1127,7 +1170,7 @@ int esp_near_create(const esp_near_desc* d, esp_near** out) {
     return ESP_ERR_PARAM;
   }
   esp_near* p = new esp_near();
-  p->div = d->cell_div > 0 ? std::min(d->cell_div, 4) : 3;
+  p->div = d->cell_div > 0 ? std::min(d->cell_div, 4) : 0;   // 0: automatic
   {
     const char* k = std::getenv("ESP_NEAR_KERNEL");
     p->kernel = (k && std::strcmp(k, "rows") == 0) ? 1 : 0;
@@ -1282,44 +1325,22 @@ int esp_near_set_cell(esp_near* p, const double* h, const double* hinv, int32_t 
     g.hinv[k] = hinv[k];
   }
   g.ortho = orthorhombic ? 1 : 0;
+  g.eps = 1e-9 * std::max(std::max(h[0], h[4]), h[8]);
   // perpendicular width along lattice axis d: 1 / |row d of h^-1|
-  double width[3];
   for (int d = 0; d < 3; ++d) {
     const double a = hinv[3 * d], b = hinv[3 * d + 1], c = hinv[3 * d + 2];
-    width[d] = 1.0 / std::sqrt(a * a + b * b + c * c);
-    if (!(p->reach < 0.5 * width[d])) {
+    p->width[d] = 1.0 / std::sqrt(a * a + b * b + c * c);
+    if (!(p->reach < 0.5 * p->width[d])) {
       set_error("cutoff not below half the minimum perpendicular width");
       return ESP_ERR_PARAM;
     }
   }
-  int div = p->div;
-  long long nc[3], total;
-  for (;;) {
-    total = 1;
-    for (int d = 0; d < 3; ++d) {
-      nc[d] = (long long)std::floor(width[d] * div / p->reach);
-      nc[d] = std::max<long long>(1, std::min<long long>(nc[d], 1024));
-      total *= nc[d];
-    }
-    if (total <= (1ll << 23) || div == 1) break;
-    --div;
-  }
-  while (total > (1ll << 23)) {  // huge boxes: coarser cells (thicker cells stay valid)
-    total = 1;
-    for (int d = 0; d < 3; ++d) {
-      nc[d] = std::max<long long>(1, nc[d] / 2);
-      total *= nc[d];
-    }
-  }
-  for (int d = 0; d < 3; ++d) g.nc[d] = (int)nc[d];
-  g.ncells = total;
-  g.div = div;
-  g.n_rows = (2 * div + 1) * (2 * div + 1);
-  g.eps = 1e-9 * std::max(std::max(h[0], h[4]), h[8]);
-  const int st = near_reserve_cells(p, std::max<long long>(total + 1, p->cap + 1));
-  if (st != ESP_OK) return st;
   p->g = g;
   p->volume = volume;
+  // cell-start storage for the finest lattice the plan may pick
+  int st = near_layout(p, p->div > 0 ? p->div : 3);
+  if (st != ESP_OK) return st;
+  if (p->div == 0 && (st = near_layout(p, 2)) != ESP_OK) return st;
   p->have_cell = 1;
   return ESP_OK;
 }
@@ -1349,6 +1370,10 @@ int esp_near_evaluate_local(esp_near* p, const double* d_pos, const double* d_q,
   }
   cudaStream_t s = (cudaStream_t)stream;
   p->launches = 0;
+  if (p->div == 0) {   // automatic lattice for this particle count (storage preallocated)
+    const int want = near_auto_div(p, n);
+    if (want != p->g.div && (st = near_layout(p, want)) != ESP_OK) return st;
+  }
   // stats[1]: first coincident pair, stats[2]: first bad pair (all ones = none)
   NEAR_CUDA(cudaMemsetAsync(d_stats + 1, 0xff, 2 * sizeof(int64_t), s));
   if (n == 0) return near_reduce(p, 0, d_out7, (long long*)d_stats, s);
