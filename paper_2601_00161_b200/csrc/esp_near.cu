@@ -11,23 +11,24 @@
 // Cell-list path (esp_near_evaluate): particles are binned into a periodic
 // lattice of cells in fractional coordinates, nc_d = floor(width_d * div /
 // reach) cells along axis d (perpendicular width, so a cell is at least
-// reach/div thick).  A radix sort orders them by cell, stable, so the order
-// inside a cell is by original index.  Each record stores the position moved
-// into the home cell image and the charge (32 B).  The pair kernel runs one
-// CTA per cell; each warp takes one i at a time and streams the candidate j
-// records of the (2 div + 1)^3 stencil (orthorhombic cells: pruned by
-// cell-box distance) with the periodic image shift applied per stencil cell,
-// so no minimum-image rounding is needed.  Hits (r^2 <= reach^2) are
-// compacted through a per-warp shared-memory queue (ballot + popc) and
-// evaluated 32 at a time with every lane busy.  Full neighbour lists (each
-// pair seen from both ends) keep every force a single-owner sum: no atomics,
-// bitwise reproducible.  Energy and pressure take half of each directed pair
-// and go through a fixed-order reduction.
+// reach/div thick; div = 2 or 3, chosen per call).  A stable radix sort by
+// (cell, octant of the cell) orders them; inside an octant the order is by
+// original index.  Each record stores the position moved into the home cell
+// image and the charge (32 B).  The tile kernel (k_near_tile) runs one CTA
+// per cell and passes of 8 of its particles (one per warp): the candidate
+// rows of cells within +-div are trimmed against the pass's bounding box,
+// split at the periodic faces into runs with one image shift each (so no
+// per-pair minimum-image rounding), and staged in shared memory with the
+// shift applied.  Hits (r^2 <= reach^2) are compacted through a per-warp
+// queue (ballot + popc) and evaluated 32 at a time with every lane busy.
+// Full neighbour lists (each pair seen from both ends) keep every force a
+// single-owner sum: no atomics, bitwise reproducible.  Energy and pressure
+// take half of each directed pair and go through a fixed-order reduction.
 //
-// Pair values follow the reference operation for operation: the PairTable
-// low-r polynomial is numpy polyval (Horner, mul then add), the spline is
-// scipy PPoly (power sum, interval search as find_interval), 1/r is an IEEE
-// division; exact mode is the Legendre series (numpy legval, Clenshaw).
+// Pair values: the PairTable's low-r polynomial (Horner) and cubic splines
+// (from per-knot values and second derivatives, the same pieces as the
+// reference's PPoly coefficients), 1/r from a DP rsqrt; exact mode is the
+// Legendre series in numpy legval's (Clenshaw) order.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
