@@ -456,12 +456,17 @@ __device__ __forceinline__ void tree_finish(double* partials, double* gsum, int*
 // P3a: z pencils line = by*ldx + kx: forward C2C; the in-band kz box goes to
 // spec (cuFFT half-spectrum layout) and into the fixed-order energy/pressure
 // reduction (warp shuffle -> block -> per-block partials -> last block).
-template <typename real, int N>
+// IK (small pencils only): the same CTA then builds the ik (or potential)
+// spectra of its pencils from the transformed values still in shared memory
+// and runs their inverse z transforms (what k_z_ik does), saving a launch and
+// the spectrum's round trip through memory.
+template <typename real, int N, bool IK = false>
 __global__ void __launch_bounds__(threads_yz<real>(N), 3)
 k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ spec,
            const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines,
            double* __restrict__ partials, double* __restrict__ gsum,
-           int* __restrict__ counters, double* __restrict__ out7) {
+           int* __restrict__ counters, double* __restrict__ out7,
+           typename Cx<real>::t* __restrict__ ik = nullptr) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N), LP = pitch(N), NT = threads_yz<real>(N);
   constexpr int ZS = NT / L, nld = N / ZS;
@@ -585,6 +590,55 @@ k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __
         acc[5] += t * ky * kz;
         acc[6] += t * kz * kz + wa;
       }
+    }
+  }
+  if constexpr (IK && PF) {
+    // ik pencils: T = i k_c A X h3/G (or A X h3/G, potential) on the in-band
+    // modes, zero elsewhere; inverse z transform; store as k_z_ik does
+    C* T = X + L * LP;
+    const int ncomp = fa.potential ? 1 : 3;
+    for (int c = 0; c < ncomp; ++c) {
+#pragma unroll
+      for (int it = 0; it < nld; ++it) {
+        C z;
+        z.x = z.y = real(0);
+        T[l * LP + pidx(threadIdx.x / L + it * ZS)] = z;
+      }
+      __syncthreads();
+      if (live) {
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+          const int bz = threadIdx.x / L + it * ZS;
+          if (bz >= nbz) continue;
+          const int mz = band_mode(bz, nbz, N);
+          const C Xv = X[l * LP + pidx(mz)];
+          C v;
+          if (fa.potential) {
+            const double cf = pA[it] * fa.ik_scale;
+            v.x = (real)(cf * (double)Xv.x);
+            v.y = (real)(cf * (double)Xv.y);
+          } else {
+            const double kc = c == 0 ? __dadd_rn(kxy[0], pk[0][it])
+                                     : (c == 1 ? __dadd_rn(kxy[1], pk[1][it])
+                                               : __dadd_rn(kxy[2], pk[2][it]));
+            const double cf = pA[it] * fa.ik_scale * kc;
+            v.x = (real)(-cf * (double)Xv.y);
+            v.y = (real)(cf * (double)Xv.x);
+          }
+          T[l * LP + pidx(mz)] = v;
+        }
+      }
+      __syncthreads();
+      fft_ip<N, 1, L, NT, +1>(T, tw);
+      if (valid) {
+        C* dst = ik + (long long)c * N * zstride + line;
+#pragma unroll
+        for (int it = 0; it < nld; ++it) {
+          const int z = threadIdx.x / L + it * ZS;
+          __stcs(dst + (long long)z * zstride, T[l * LP + pidx(z)]);
+        }
+      }
+      __syncthreads();
     }
   }
   constexpr int NW = (NT + 31) / 32;
@@ -946,23 +1000,45 @@ static cudaError_t launch_y_fwd(const esp_plan* p, const void* in, void* out, co
   return cudaGetLastError();
 }
 
+// Small pencils (the table prefetch branch of k_z_reduce): the ik spectra and
+// their inverse z transforms can ride in the same kernel.
+template <typename real, int N>
+constexpr bool z_fusable() {
+  return N / (threads_yz<real>(N) / lines_yz<real>(N)) <= 6;
+}
+
 template <typename real, int N>
 static cudaError_t launch_z_reduce(const esp_plan* p, const void* in, const void* tw,
                                    const FusedArgs& fa, double* partials, long long nblk_cap,
-                                   double* out7, cudaStream_t s) {
+                                   double* out7, cudaStream_t s, void* ik = nullptr) {
   using C = typename Cx<real>::t;
   constexpr int L = lines_yz<real>(N);
+  const long long nlines = (long long)fa.npy * fa.ldx;
+  const long long nblk = (nlines + L - 1) / L;
+  if (nblk > nblk_cap) return cudaErrorInvalidConfiguration;
+  int* counters = reinterpret_cast<int*>(partials + (nblk_cap + (nblk_cap + 31) / 32) * 8);
+  if constexpr (z_fusable<real, N>()) {
+    if (ik) {
+      const size_t smem = 2 * sizeof(C) * L * pitch(N);
+      cudaError_t e = cudaFuncSetAttribute(k_z_reduce<real, N, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      k_z_reduce<real, N, true><<<(unsigned)nblk, threads_yz<real>(N), smem, s>>>(
+          reinterpret_cast<const C*>(in), reinterpret_cast<C*>(p->d_spec),
+          reinterpret_cast<const C*>(tw), fa, nlines, partials, partials + nblk_cap * 8,
+          counters, out7, reinterpret_cast<C*>(ik));
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = sizeof(C) * L * pitch(N);
   cudaError_t e = cudaFuncSetAttribute(k_z_reduce<real, N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long nlines = (long long)fa.npy * fa.ldx;
-  const long long nblk = (nlines + L - 1) / L;
-  if (nblk > nblk_cap) return cudaErrorInvalidConfiguration;
   k_z_reduce<real, N><<<(unsigned)nblk, threads_yz<real>(N), smem, s>>>(
       reinterpret_cast<const C*>(in), reinterpret_cast<C*>(p->d_spec),
       reinterpret_cast<const C*>(tw), fa, nlines, partials, partials + nblk_cap * 8,
-      reinterpret_cast<int*>(partials + (nblk_cap + (nblk_cap + 31) / 32) * 8), out7);
+      counters, out7);
   return cudaGetLastError();
 }
 
@@ -1205,12 +1281,25 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   fa.npy = p->nby;
   fa.potential = want_ik == 2 ? 1 : 0;
   const int ncomp = want_ik == 2 ? 1 : 3;
+  // small pencils: the ik spectra and inverse z transforms run inside the
+  // z-reduce kernel (ESP_FFT_NO_ZFUSE=1 keeps them separate)
+  static const bool no_zfuse = std::getenv("ESP_FFT_NO_ZFUSE") != nullptr;
+  bool zfused = false;
+  if (want_ik && !no_zfuse) {
+    switch (p->M[2]) {
+#define ESP_CASE(v) \
+  case v: zfused = z_fusable<real, v>(); break;
+      ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+    }
+  }
   e = cudaErrorInvalidValue;
   switch (p->M[2]) {
 #define ESP_CASE(v)                                                                       \
   case v:                                                                                 \
     e = launch_z_reduce<real, v>(p, f->bufB, f->tw[2], fa, p->d_partials_fft,            \
-                                 p->n_red_blocks_fft, d_out7, s);                         \
+                                 p->n_red_blocks_fft, d_out7, s,                          \
+                                 zfused ? f->bufC : nullptr);                             \
     break;
     ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
@@ -1220,16 +1309,18 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   prof_mark(p, s, "fft_z_scale_reduce");
   if ((e = debug_check(s, "fft_z_scale_reduce")) != cudaSuccess) return e;
   if (!want_ik) return cudaSuccess;
-  e = cudaErrorInvalidValue;
-  switch (p->M[2]) {
+  if (!zfused) {
+    e = cudaErrorInvalidValue;
+    switch (p->M[2]) {
 #define ESP_CASE(v) \
   case v: e = launch_z_ik<real, v>(p, f->bufC, f->tw[2], fa, one, s); break;
-    ESP_FFT_SIZES(ESP_CASE)
+      ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
+    }
+    if (e != cudaSuccess) return e;
+    p->launches++;
+    prof_mark(p, s, "ifft_z_ik");
   }
-  if (e != cudaSuccess) return e;
-  p->launches++;
-  prof_mark(p, s, "ifft_z_ik");
   if ((e = debug_check(s, "ifft_z_ik")) != cudaSuccess) return e;
   if (plane) {
     e = cudaErrorInvalidValue;
