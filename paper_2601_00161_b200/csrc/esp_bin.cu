@@ -14,6 +14,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "esp_internal.cuh"
 
 namespace esp {
@@ -184,6 +186,65 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
     real* ddst = drec + j0 * (3 * RS);
     for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) ddst[t] = s_drec[t];
   }
+}
+
+// Small key spaces (<= kScanMax keys, e.g. config 1's 4096): every scatter
+// CTA scans the key counts in shared memory itself (CTA 0 also publishes the
+// offsets), so the separate device-wide scan launch disappears from the step.
+constexpr int kScanT = 256;
+constexpr int kScanMax = 8192;
+
+__global__ void __launch_bounds__(kScanT)
+    k_bin_scatter_scan(const double* __restrict__ pos, const double* __restrict__ q,
+                       long long n, Geom g, const int* __restrict__ key,
+                       const int* __restrict__ slot, const int* __restrict__ counts, int nk1,
+                       int* __restrict__ offsets_out, long long cap,
+                       double* __restrict__ u_out, double* __restrict__ q_out,
+                       int* __restrict__ idx_out, int* __restrict__ key_out) {
+  __shared__ int s_off[kScanMax];
+  __shared__ int s_wsum[kScanT / 32];
+  const int per = (nk1 + kScanT - 1) / kScanT;
+  const int a0 = threadIdx.x * per;
+  for (int k = threadIdx.x; k < nk1; k += kScanT) s_off[k] = counts[k];
+  __syncthreads();
+  int sum = 0;
+  for (int k = 0; k < per; ++k)
+    if (a0 + k < nk1) sum += s_off[a0 + k];
+  // exclusive block scan of the per-thread sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += s_wsum[w];
+  int run = wbase + incl - sum;
+  for (int k = 0; k < per; ++k) {
+    if (a0 + k < nk1) {
+      const int c = s_off[a0 + k];
+      s_off[a0 + k] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < nk1; k += kScanT) offsets_out[k] = s_off[k];
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double u[3];
+  grid_coords(g, pos[3 * i + 0], pos[3 * i + 1], pos[3 * i + 2], u);
+  const int k = key[i];
+  const long long dst = (long long)s_off[k] + slot[i];
+  u_out[dst] = u[0];
+  u_out[cap + dst] = u[1];
+  u_out[2 * cap + dst] = u[2];
+  q_out[dst] = q[i];
+  idx_out[dst] = (int)i;
+  if (key_out) key_out[dst] = k;
 }
 
 // Scatter to key segments.  Writes grid coordinates u (SoA), charge and the
@@ -431,19 +492,31 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
     p->launches++;
     prof_mark(p, s, "bin_count");
   }
-  size_t bytes = p->cub_bytes;
-  e = cub::DeviceScan::ExclusiveSum(p->d_cub, bytes, p->d_counts, p->d_offsets,
-                                    (int)(p->n_keys + 1), s);
-  if (e != cudaSuccess) return e;
-  p->launches++;
-  prof_mark(p, s, "bin_scan");
+  static const bool no_fuse_scan = std::getenv("ESP_BIN_NO_FUSED_SCAN") != nullptr;
+  const bool fused_scan = n > 0 && p->deterministic && !no_fuse_scan &&
+                          p->n_keys + 1 <= kScanMax && B == kScanT;
+  if (!fused_scan) {
+    size_t bytes = p->cub_bytes;
+    e = cub::DeviceScan::ExclusiveSum(p->d_cub, bytes, p->d_counts, p->d_offsets,
+                                      (int)(p->n_keys + 1), s);
+    if (e != cudaSuccess) return e;
+    p->launches++;
+    prof_mark(p, s, "bin_scan");
+  }
   if (n == 0) return cudaGetLastError();
   if (p->q_ready) {  // charges copied on another stream (host-buffer step)
     e = cudaStreamWaitEvent(s, p->q_ready, 0);
     p->q_ready = nullptr;
     if (e != cudaSuccess) return e;
   }
-  if (p->deterministic) {
+  if (fused_scan) {
+    k_bin_scatter_scan<<<grid, kScanT, 0, s>>>(d_pos, d_q, n, g, p->d_key, p->d_slot,
+                                               p->d_counts, (int)(p->n_keys + 1),
+                                               p->d_offsets, p->cap, p->d_u_tmp, p->d_q_tmp,
+                                               p->d_idx_tmp, p->d_bkey);
+    prof_mark(p, s, "bin_scatter");
+    p->launches += 1;
+  } else if (p->deterministic) {
     k_bin_scatter<<<grid, B, 0, s>>>(d_pos, d_q, n, g, p->d_key, p->d_slot,
                                      p->d_offsets, p->cap, p->d_u_tmp, p->d_q_tmp,
                                      p->d_idx_tmp, p->d_bkey);
