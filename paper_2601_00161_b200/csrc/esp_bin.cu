@@ -284,25 +284,36 @@ k_bin_canon(Geom g, FastTab ft, const real* __restrict__ tab, const double* __re
             int* __restrict__ pk, FastTab ftd, const real* __restrict__ dtab,
             real* __restrict__ drec) {
   __shared__ long long s_dst[kBinPerBlock];
+  __shared__ int s_rank[3][kBinPerBlock];
   const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
   const long long j = (long long)blockIdx.x * kBinPerBlock + l;
   const bool live = j < n;
-  // rank by original index (warp 0); its loads are issued in batches of 8
-  if (d == 0 && live) {
+  // rank by original index: the particle's three threads each count a third
+  // of its key segment (loads issued in batches of 8), then warp 0 combines
+  int s0 = 0;
+  int me = 0;
+  if (live) {
     const int k = key_tmp[j];
-    const int s0 = offsets[k], s1 = offsets[k + 1];
-    const int me = idx_tmp[j];
+    s0 = offsets[k];
+    const int s1 = offsets[k + 1];
+    me = idx_tmp[j];
+    const int len = s1 - s0, part = (len + 2) / 3;
+    const int b0 = s0 + d * part, b1 = min(s1, b0 + part);
     int rank = 0;
-    int t = s0;
-    for (; t + 8 <= s1; t += 8) {
+    int t = b0;
+    for (; t + 8 <= b1; t += 8) {
       int v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = idx_tmp[t + i];
 #pragma unroll
       for (int i = 0; i < 8; ++i) rank += (v[i] < me);
     }
-    for (; t < s1; ++t) rank += (idx_tmp[t] < me);
-    const long long dst = (long long)s0 + rank;
+    for (; t < b1; ++t) rank += (idx_tmp[t] < me);
+    s_rank[d][l] = rank;
+  }
+  __syncthreads();
+  if (d == 0 && live) {
+    const long long dst = (long long)s0 + s_rank[0][l] + s_rank[1][l] + s_rank[2][l];
     s_dst[l] = dst;
     q_out[dst] = q_tmp[j];
     idx_out[dst] = me;
