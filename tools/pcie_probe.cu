@@ -1,3 +1,4 @@
+// Build: nvcc -O2 -std=c++17 -gencode arch=compute_100a,code=sm_100a tools/pcie_probe.cu -o tools/bin/pcie_probe
 // PCIe probe: H2D / D2H bandwidth for pinned, write-combined and zero-copy
 // (kernel reads mapped host memory) transfers of a few MB.
 #include <cstdio>
