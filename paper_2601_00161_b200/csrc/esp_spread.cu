@@ -287,7 +287,14 @@ k_spread_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
           reinterpret_cast<char*>(&s_raw[b][0]) + 16 * i);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 16 * i));
     }
-    if (tid < n) {
+    if (NT < 64) {   // one warp: both small arrays from every lane
+      if (tid < n) {
+        const unsigned dpk = (unsigned)__cvta_generic_to_shared(&s_pk[b][tid]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dpk), "l"(PK + c0 + tid));
+        const unsigned dq = (unsigned)__cvta_generic_to_shared(&s_q[b][tid]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dq), "l"(Q + c0 + tid));
+      }
+    } else if (tid < n) {
       const unsigned dpk = (unsigned)__cvta_generic_to_shared(&s_pk[b][tid]);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dpk), "l"(PK + c0 + tid));
     } else if (tid >= 32 && tid < 64 && tid - 32 < n) {
@@ -390,7 +397,16 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s, bool with_combine) {
   // 4-warp column-block kernel
   if (P <= 8 && !legacy && p->n_tiles_s * 2 >= 148 * 4) {
     constexpr int PW = P <= 8 ? P : 8;
-    if (p->n_tiles_s * 2 >= 148 * 12) {
+    static const int rows_env = std::getenv("ESP_SPREAD_ROWS") ? std::atoi(std::getenv("ESP_SPREAD_ROWS")) : 0;
+    if (rows_env == 1) {
+      k_spread_warp<real, PW, 1><<<(unsigned)p->n_tiles_s, spread_warp_threads(1), 0, s>>>(
+          g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
+          reinterpret_cast<real*>(p->d_scratch));
+    } else if (rows_env == 8) {
+      k_spread_warp<real, PW, 8><<<(unsigned)p->n_tiles_s, spread_warp_threads(8), 0, s>>>(
+          g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
+          reinterpret_cast<real*>(p->d_scratch));
+    } else if (rows_env == 4 || (rows_env == 0 && p->n_tiles_s * 2 >= 148 * 12)) {
       k_spread_warp<real, PW, 4><<<(unsigned)p->n_tiles_s, spread_warp_threads(4), 0, s>>>(
           g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
           reinterpret_cast<real*>(p->d_scratch));
