@@ -160,6 +160,23 @@ __device__ __forceinline__ double legval_np(double x, const double* c, int n) {
   return __dadd_rn(c0, __dmul_rn(c1, x));
 }
 
+// Hermite-form table piece: u = (r - r_in)/dk, knot k, and the cubic from the
+// knot records s0, f0 (knot k) and s1, f1 (knot k + 1).
+__device__ __forceinline__ double hermite_u(const NearConst& C, double r) {
+  return (r - C.r_in) * C.inv_dk;
+}
+__device__ __forceinline__ int hermite_knot(const NearConst& C, double u) {
+  return min(max((int)u, 0), C.n_knots - 2);
+}
+__device__ __forceinline__ void hermite_eval(const NearConst& C, double u, int k, double rinv,
+                                             double2 s0, double2 f0, double2 s1, double2 f1,
+                                             double& nv, double& fv) {
+  const double B = u - k, A = 1.0 - B;
+  const double ca = (A * A - 1.0) * A * C.h26, cb = (B * B - 1.0) * B * C.h26;
+  nv = rinv - fma(ca, s0.y, fma(cb, s1.y, fma(A, s0.x, B * s1.x)));
+  fv = fma(ca, f0.y, fma(cb, f1.y, fma(A, f0.x, B * f1.x)));
+}
+
 // Near-field value N(r) and force weight F_N(r) for 0 < r <= r_c
 // (realspace.py:42-67 with a table, kernel.py:41-97 without); rinv = 1/r.
 // Default table (ESP_NEAR_HERMITE): per knot the value and second derivative
@@ -178,14 +195,10 @@ __device__ __forceinline__ void pair_values(const NearConst& C, double r, double
     } else if (ESP_NEAR_HERMITE) {
       // the same cubic pieces from knot values and second derivatives
       // (32 B per knot: y_s, M_s, y_f, M_f)
-      const double u = (r - C.r_in) * C.inv_dk;
-      const int k = min(max((int)u, 0), C.n_knots - 2);
+      const double u = hermite_u(C, r);
+      const int k = hermite_knot(C, u);
       const double2* t = reinterpret_cast<const double2*>(tab + 4 * (size_t)k);
-      const double2 s0 = __ldg(t), f0 = __ldg(t + 1), s1 = __ldg(t + 2), f1 = __ldg(t + 3);
-      const double B = u - k, A = 1.0 - B;
-      const double ca = (A * A - 1.0) * A * C.h26, cb = (B * B - 1.0) * B * C.h26;
-      nv = rinv - fma(ca, s0.y, fma(cb, s1.y, fma(A, s0.x, B * s1.x)));
-      fv = fma(ca, f0.y, fma(cb, f1.y, fma(A, f0.x, B * f1.x)));
+      hermite_eval(C, u, k, rinv, __ldg(t), __ldg(t + 1), __ldg(t + 2), __ldg(t + 3), nv, fv);
     } else {
       int k = (int)((r - C.r_in) * C.inv_dk);
       k = min(max(k, 0), C.n_knots - 2);
@@ -213,19 +226,8 @@ struct Acc {
   __device__ void zero() { e = fx = fy = fz = vxx = vxy = vxz = vyy = vyz = vzz = n = 0.0; }
 };
 
-// One directed pair (i <- j) with separation d = x_i - x_j (image applied);
-// pairs with r > r_c (or r = 0) contribute nothing (realspace.py:141).
-__device__ __forceinline__ void pair_accumulate(const NearConst& C, Acc& a, double qi,
-                                                double qj, double dx, double dy, double dz,
-                                                const double* __restrict__ tab) {
-  const double r2 = dx * dx + dy * dy + dz * dz;
-  if (!(r2 <= C.rc2_hi) || r2 == 0.0) return;
-  const double rinv = rsqrt(r2);
-  const double r = r2 * rinv;
-  if (!(r <= C.r_c)) return;
-  double nv, fv;
-  pair_values(C, r, rinv, tab, nv, fv);
-  const double qq = qi * qj;
+__device__ __forceinline__ void pair_add(Acc& a, double qq, double nv, double fv, double rinv,
+                                         double dx, double dy, double dz) {
   const double fmag = qq * fv * (rinv * rinv * rinv);
   a.e = fma(qq, nv, a.e);
   const double gx = fmag * dx, gy = fmag * dy, gz = fmag * dz;
@@ -239,6 +241,63 @@ __device__ __forceinline__ void pair_accumulate(const NearConst& C, Acc& a, doub
   a.vyz = fma(gy, dz, a.vyz);
   a.vzz = fma(gz, dz, a.vzz);
   a.n += 1.0;
+}
+
+// One directed pair (i <- j) with separation d = x_i - x_j (image applied);
+// pairs with r > r_c (or r = 0) contribute nothing (realspace.py:141).
+__device__ __forceinline__ void pair_accumulate(const NearConst& C, Acc& a, double qi,
+                                                double qj, double dx, double dy, double dz,
+                                                const double* __restrict__ tab) {
+  const double r2 = dx * dx + dy * dy + dz * dz;
+  if (!(r2 <= C.rc2_hi) || r2 == 0.0) return;
+  const double rinv = rsqrt(r2);
+  const double r = r2 * rinv;
+  if (!(r <= C.r_c)) return;
+  double nv, fv;
+  pair_values(C, r, rinv, tab, nv, fv);
+  pair_add(a, qi * qj, nv, fv, rinv, dx, dy, dz);
+}
+
+// Two directed pairs per lane (queue slots lane and lane + 32), accumulated
+// in that order -- the same sums, in the same order, as two single drains.
+// When both pairs take the Hermite table pieces (the common case), their
+// table loads are issued together so their L2 latencies overlap.
+__device__ __forceinline__ void pair_accumulate2(const NearConst& C, Acc& a, double qi,
+                                                 bool ua, double qa, double xa, double ya,
+                                                 double za, bool ub, double qb, double xb,
+                                                 double yb, double zb,
+                                                 const double* __restrict__ tab) {
+  const double r2a = xa * xa + ya * ya + za * za;
+  const double r2b = xb * xb + yb * yb + zb * zb;
+  ua = ua && r2a <= C.rc2_hi && r2a != 0.0;
+  ub = ub && r2b <= C.rc2_hi && r2b != 0.0;
+  const double ria = rsqrt(ua ? r2a : 1.0), rib = rsqrt(ub ? r2b : 1.0);
+  const double ra = r2a * ria, rb = r2b * rib;
+  ua = ua && ra <= C.r_c;
+  ub = ub && rb <= C.r_c;
+  if (!(ESP_NEAR_HERMITE && C.use_table && (!ua || ra > C.r_in) && (!ub || rb > C.r_in))) {
+    if (ua) pair_accumulate(C, a, qi, qa, xa, ya, za, tab);
+    if (ub) pair_accumulate(C, a, qi, qb, xb, yb, zb, tab);
+    return;
+  }
+  const double uA = hermite_u(C, ra), uB = hermite_u(C, rb);
+  const int kA = ua ? hermite_knot(C, uA) : 0, kB = ub ? hermite_knot(C, uB) : 0;
+  const double2* tA = reinterpret_cast<const double2*>(tab + 4 * (size_t)kA);
+  const double2* tB = reinterpret_cast<const double2*>(tab + 4 * (size_t)kB);
+  const double2 sA0 = __ldg(tA), fA0 = __ldg(tA + 1), sA1 = __ldg(tA + 2), fA1 = __ldg(tA + 3);
+  const double2 sB0 = __ldg(tB), fB0 = __ldg(tB + 1), sB1 = __ldg(tB + 2), fB1 = __ldg(tB + 3);
+  if (ua) {
+    double nv, fv;
+    hermite_eval(C, uA, kA, ria, sA0, fA0, sA1, fA1, nv, fv);
+    if (ra >= C.r_c) nv = 0.0;
+    pair_add(a, qi * qa, nv, fv, ria, xa, ya, za);
+  }
+  if (ub) {
+    double nv, fv;
+    hermite_eval(C, uB, kB, rib, sB0, fB0, sB1, fB1, nv, fv);
+    if (rb >= C.r_c) nv = 0.0;
+    pair_add(a, qi * qb, nv, fv, rib, xb, yb, zb);
+  }
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -310,6 +369,19 @@ __global__ void k_near_sorted(const int* __restrict__ key_sorted, const int* __r
 __global__ void k_fill_int(int* p, long long n, int v) {
   const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k < n) p[k] = v;
+}
+
+// Warp-wide evaluation of up to 64 queued pairs: lane l takes slots l and
+// l + 32 (in that order, as two 32-pair drains would).
+__device__ __forceinline__ void drain2(const NearConst& C, Acc& a, double qi, const double* qx,
+                                       const double* qy, const double* qz, const double* qqj,
+                                       int lane, int cnt, const double* __restrict__ tab) {
+  const int l2 = lane + 32;
+  const bool ua = lane < cnt, ub = l2 < cnt;
+  if (!ua) return;
+  pair_accumulate2(C, a, qi, true, qqj[lane], qx[lane], qy[lane], qz[lane], ub,
+                   ub ? qqj[l2] : 0.0, ub ? qx[l2] : 0.0, ub ? qy[l2] : 0.0,
+                   ub ? qz[l2] : 0.0, tab);
 }
 
 // Warp-wide evaluation of the queued pairs; lanes >= cnt idle.
@@ -490,12 +562,17 @@ __global__ void __launch_bounds__(kNearThreads, ESP_NEAR_MINB)
 constexpr int kTileW = ESP_TILE_W;    // warps per CTA = particles per pass
 constexpr int kTileI = kTileW;
 constexpr int kTileCH = 1024;         // staged records per chunk
+#ifndef ESP_NEAR_DRAIN2
+#define ESP_NEAR_DRAIN2 1             // drain 64 queued pairs (2 per lane) at a time
+#endif
+constexpr int kTileDrain = ESP_NEAR_DRAIN2 ? 64 : 32;
+constexpr int kTileQueue = kTileDrain + 32;
 constexpr int kTileMaxRuns = 3 * 81;  // 3 runs per row, (2 div + 1)^2 rows, div <= 4
 
 struct TileSmem {
   double jx[kTileCH], jy[kTileCH], jz[kTileCH], jq[kTileCH];
   int jid[kTileCH];                   // j index, bit 31 set for a shifted image
-  double q[kTileW][4][kQueue];
+  double q[kTileW][4][kTileQueue];
   double sh[kTileMaxRuns][3];
   int j0[kTileMaxRuns];
   int pref[kTileMaxRuns + 1];
@@ -681,17 +758,20 @@ __global__ void __launch_bounds__(kTileW * 32)
             qj[slot] = qv;
           }
           qn += __popc(m);
-          if (qn >= 32) {
+          if (qn >= kTileDrain) {
             __syncwarp();
-            drain(C, a, ri.w, qx, qy, qz, qj, lane, 32, tab);
+            if (kTileDrain == 64)
+              drain2(C, a, ri.w, qx, qy, qz, qj, lane, 64, tab);
+            else
+              drain(C, a, ri.w, qx, qy, qz, qj, lane, 32, tab);
             __syncwarp();
-            if (lane < qn - 32) {
-              qx[lane] = qx[lane + 32];
-              qy[lane] = qy[lane + 32];
-              qz[lane] = qz[lane + 32];
-              qj[lane] = qj[lane + 32];
+            if (lane < qn - kTileDrain) {
+              qx[lane] = qx[lane + kTileDrain];
+              qy[lane] = qy[lane + kTileDrain];
+              qz[lane] = qz[lane + kTileDrain];
+              qj[lane] = qj[lane + kTileDrain];
             }
-            qn -= 32;
+            qn -= kTileDrain;
             __syncwarp();
           }
         }
@@ -700,7 +780,10 @@ __global__ void __launch_bounds__(kTileW * 32)
     }
     if (active) {
       __syncwarp();
-      drain(C, a, ri.w, qx, qy, qz, qj, lane, qn, tab);
+      if (kTileDrain == 64)
+        drain2(C, a, ri.w, qx, qy, qz, qj, lane, qn, tab);
+      else
+        drain(C, a, ri.w, qx, qy, qz, qj, lane, qn, tab);
       __syncwarp();
       const double fx = warp_sum(a.fx), fy = warp_sum(a.fy), fz = warp_sum(a.fz);
       const double e = warp_sum(a.e), vxx = warp_sum(a.vxx), vxy = warp_sum(a.vxy),
