@@ -565,8 +565,13 @@ constexpr int kTileCH = 1024;         // staged records per chunk
 #ifndef ESP_NEAR_DRAIN2
 #define ESP_NEAR_DRAIN2 1             // drain 64 queued pairs (2 per lane) at a time
 #endif
+#ifndef ESP_NEAR_TEST2
+#define ESP_NEAR_TEST2 2              // candidate batches of 32 tested per step (1 or 2)
+#endif
 constexpr int kTileDrain = ESP_NEAR_DRAIN2 ? 64 : 32;
-constexpr int kTileQueue = kTileDrain + 32;
+constexpr int kTileTest = ESP_NEAR_TEST2;
+static_assert(kTileTest >= 1 && 32 * kTileTest <= kTileDrain, "one drain per step must keep the queue below its drain threshold");
+constexpr int kTileQueue = kTileDrain + 32 * kTileTest;
 constexpr int kTileMaxRuns = 3 * 81;  // 3 runs per row, (2 div + 1)^2 rows, div <= 4
 
 struct TileSmem {
@@ -730,34 +735,43 @@ __global__ void __launch_bounds__(kTileW * 32)
       }
       __syncthreads();
       if (active) {
-        for (int kb = 0; kb < cnt; kb += 32) {
-          const int k = kb + lane;
-          bool hit = false;
-          double dx = 0.0, dy = 0.0, dz = 0.0, qv = 0.0;
-          int jid = -1;
-          if (k < cnt) {
-            dx = ri.x - S.jx[k];
-            dy = ri.y - S.jy[k];
-            dz = ri.z - S.jz[k];
-            qv = S.jq[k];
-            jid = S.jid[k];
-            const double r2 = dx * dx + dy * dy + dz * dz;
-            hit = r2 <= reach2 && jid != i;
-            if (hit && r2 < C.sing2) {
-              const unsigned long long a_ = (unsigned)perm[i],
-                                       b_ = (unsigned)perm[jid & 0x7fffffff];
-              atomicMin(singular, (min(a_, b_) << 32) | max(a_, b_));
+        // candidates in pairs of 32-wide batches (both batches' loads and
+        // tests in flight together), appended to the queue in batch order
+        for (int kb = 0; kb < cnt; kb += 32 * kTileTest) {
+          unsigned m[kTileTest];
+          double dx[kTileTest], dy[kTileTest], dz[kTileTest], qv[kTileTest];
+#pragma unroll
+          for (int u = 0; u < kTileTest; ++u) {
+            const int k = kb + 32 * u + lane;
+            bool hit = false;
+            dx[u] = dy[u] = dz[u] = qv[u] = 0.0;
+            if (k < cnt) {
+              dx[u] = ri.x - S.jx[k];
+              dy[u] = ri.y - S.jy[k];
+              dz[u] = ri.z - S.jz[k];
+              qv[u] = S.jq[k];
+              const int jid = S.jid[k];
+              const double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
+              hit = r2 <= reach2 && jid != i;
+              if (hit && r2 < C.sing2) {
+                const unsigned long long a_ = (unsigned)perm[i],
+                                         b_ = (unsigned)perm[jid & 0x7fffffff];
+                atomicMin(singular, (min(a_, b_) << 32) | max(a_, b_));
+              }
             }
+            m[u] = __ballot_sync(0xffffffffu, hit);
           }
-          const unsigned m = __ballot_sync(0xffffffffu, hit);
-          if (hit) {
-            const int slot = qn + __popc(m & lt);
-            qx[slot] = dx;
-            qy[slot] = dy;
-            qz[slot] = dz;
-            qj[slot] = qv;
+#pragma unroll
+          for (int u = 0; u < kTileTest; ++u) {
+            if (m[u] & (1u << lane)) {
+              const int slot = qn + __popc(m[u] & lt);
+              qx[slot] = dx[u];
+              qy[slot] = dy[u];
+              qz[slot] = dz[u];
+              qj[slot] = qv[u];
+            }
+            qn += __popc(m[u]);
           }
-          qn += __popc(m);
           if (qn >= kTileDrain) {
             __syncwarp();
             if (kTileDrain == 64)
@@ -765,11 +779,11 @@ __global__ void __launch_bounds__(kTileW * 32)
             else
               drain(C, a, ri.w, qx, qy, qz, qj, lane, 32, tab);
             __syncwarp();
-            if (lane < qn - kTileDrain) {
-              qx[lane] = qx[lane + kTileDrain];
-              qy[lane] = qy[lane + kTileDrain];
-              qz[lane] = qz[lane + kTileDrain];
-              qj[lane] = qj[lane + kTileDrain];
+            for (int l = lane; l < qn - kTileDrain; l += 32) {
+              qx[l] = qx[l + kTileDrain];
+              qy[l] = qy[l + kTileDrain];
+              qz[l] = qz[l + kTileDrain];
+              qj[l] = qj[l + kTileDrain];
             }
             qn -= kTileDrain;
             __syncwarp();
