@@ -561,7 +561,10 @@ __global__ void __launch_bounds__(kNearThreads, ESP_NEAR_MINB)
 #endif
 constexpr int kTileW = ESP_TILE_W;    // warps per CTA = particles per pass
 constexpr int kTileI = kTileW;
-constexpr int kTileCH = 1024;         // staged records per chunk
+#ifndef ESP_TILE_CH
+#define ESP_TILE_CH 1024
+#endif
+constexpr int kTileCH = ESP_TILE_CH;  // staged records per chunk
 #ifndef ESP_NEAR_DRAIN2
 #define ESP_NEAR_DRAIN2 1             // drain 64 queued pairs (2 per lane) at a time
 #endif
