@@ -657,3 +657,33 @@ def test_fused_analytic_forces_config1_against_oracle():
     hs.charges.copy_(torch.as_tensor(q))
     _, hF = hs.step()
     assert torch.equal(hF, oF.cpu())
+
+
+def test_spread_row_layouts_bitwise_identical():
+    """Every rows-per-thread layout of the tile spread (ESP_SPREAD_ROWS, read
+    once per process) owns each grid column with one thread that adds the
+    charges in the same order, so the step's results are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+    _torch()
+    code = (
+        "import sys, hashlib, numpy as np, torch\n"
+        "sys.path.insert(0, '.')\n"
+        "from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver, workloads\n"
+        "w, pos, q = workloads.generate(1)\n"
+        "s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,"
+        " fixed_M=w.M, cell_type=w.cell_type), capacity=w.n)\n"
+        "r = s.evaluate(pos, q)\n"
+        "h = hashlib.sha1(np.float64(r.energy).tobytes() + np.asarray(r.pressure).tobytes()"
+        " + np.asarray(r.forces).tobytes()).hexdigest()\n"
+        "print('HASH', h)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hashes = {}
+    for rows in ("1", "2", "4", "8"):
+        env = dict(os.environ, ESP_SPREAD_ROWS=rows)
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env,
+                             capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        hashes[rows] = [ln for ln in out.stdout.splitlines() if ln.startswith("HASH")][0]
+    assert len(set(hashes.values())) == 1, hashes
