@@ -438,7 +438,11 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s, bool with_combine) {
   if (!with_combine) return cudaGetLastError();
   const CombineTabs ct = combine_tabs(p);
   // 128-thread blocks: config 4 combine 0.88 -> 0.82 ms against 256 (ESP_COMBINE_B sweeps)
-  static const int B = std::getenv("ESP_COMBINE_B") ? std::atoi(std::getenv("ESP_COMBINE_B")) : 128;
+  static const int B = [] {
+    const char* e = std::getenv("ESP_COMBINE_B");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 32 && v <= 1024 && v % 32 == 0 ? v : 128;
+  }();
   k_combine<real><<<(unsigned)((p->G + B - 1) / B), B, 0, s>>>(
       g, ct, reinterpret_cast<const real*>(p->d_scratch), reinterpret_cast<real*>(p->d_grid));
   p->launches++;
