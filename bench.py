@@ -1,24 +1,33 @@
 #!/usr/bin/env python
 """Benchmark: ESP long-range (k-space) atom-steps/s on B200.
 
-Workload (BASELINE.json metric config): config 1 — 90,000
-charges (30,000 rigid 3-site waters), 67x67x67.5 A semi-isotropic cell,
-grid 64^3, P=8, Delta=1e-7, r_c=10, fp64, seeded synthetic inputs.  One step
-= bin -> spread -> 1 forward FFT -> fused scale/reduce (E + 6 pressure
-components) -> 3 ik inverse FFTs -> force gather.  ``value`` is whole-job
-force+pressure atom-steps/s with inputs resident in HBM; ``pressure_only``
-is the same for the pressure-only path; ``e2e`` goes through the public API
-with pinned host buffers and the H2D/D2H copies inside the timed region.
-L2 (126 MB) is flushed between timed steps by writing a 256 MB buffer.
+Workload: config 4 (BASELINE.json ``configs[4]``), the largest configuration
+and the one the metric is quoted on at N=1 — 8,100,000 charges (2.7M rigid
+3-site waters), cubic 300 A cell, grid 384^3, P=8, Delta=1e-7, r_c=10, fp64,
+seeded synthetic inputs.  One step = bin -> spread -> 1
+forward FFT -> fused scale/reduce (E + 6 pressure components) -> 3 ik
+inverse FFTs -> force gather, replayed as one CUDA graph.  ``value`` is
+whole-job force+pressure atom-steps/s with inputs resident in HBM, from the
+MEDIAN of the K CUDA-event-timed steps; ``pressure_only`` is
+the same for the pressure-only path; ``e2e`` goes through the public API
+(``KSpaceSolver.host_stepper``) with pinned host buffers and the H2D/D2H
+copies inside the timed region.  L2 (126 MB) is flushed between timed steps
+by writing a 256 MB buffer (the config-4 grids are 0.45 GB each anyway).
+``--config i`` selects another BASELINE config (0-3 are parity cases).
 
---impl reference times the CPU oracle port of the reference algorithm
+--impl reference times the CPU port of the reference algorithm
 (oracle/esp_oracle.py; the reference is pure numpy, nothing to compile) on
-all host cores: particle chunks of spread/gather in a process pool (exact by
-linearity), numpy pocketfft transforms.
+all host cores: particle chunks of spread/gather in a fork process pool over
+shared-memory buffers (exact by linearity), numpy pocketfft transforms as the
+reference calls them.  Each step is a full config-4 step; the run is bounded
+by a time budget (``--ref-budget`` seconds of timed steps, at least one).
 
-Multi-GPU (torchrun, N>1): config 1 does not shard (G = 2.6e5 is
-latency-bound on one GPU), so N ranks run N independent
-replicas ("scaling": "weak"); timings are max over ranks.
+Multi-GPU (torchrun, N>1): config 4 is decomposed into z-slabs over the N
+ranks (``slab.SlabKSpaceSolver``: NCCL halo send/recv, band-pruned transforms
+whose transposes are stored into the peer ranks' buffers, rank-ordered
+7-double reduction) — strong scaling, ``"scaling": "strong"``; timings are
+the max over ranks.  ``--replicas`` runs N independent single-GPU copies
+instead (weak scaling, the small configs).
 """
 
 from __future__ import annotations
@@ -37,7 +46,7 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-CONFIG = 1
+CONFIG = 4
 METRIC = "ESP long-range atom-steps/s (force+pressure)"
 UNIT = "atom-steps/s"
 
@@ -45,7 +54,7 @@ UNIT = "atom-steps/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=CONFIG)
@@ -56,8 +65,12 @@ def parse():
     ap.add_argument("--profile-only", action="store_true",
                     help="run a few steps for ncu (no JSON contract line)")
     ap.add_argument("--slab", action="store_true",
-                    help="multi-GPU z-slab decomposition of one system (strong "
-                         "scaling; default workload config 4)")
+                    help="z-slab decomposition of one system even at N=1 (strong "
+                         "scaling; the default whenever WORLD_SIZE > 1)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="with N>1: N independent single-GPU replicas (weak scaling)")
+    ap.add_argument("--ref-budget", type=float, default=300.0,
+                    help="--impl reference: seconds of timed CPU steps (at least one)")
     return ap.parse_args()
 
 
@@ -241,6 +254,42 @@ def measured_peaks():
 
 
 # --------------------------------------------------------------------------
+# timing
+
+
+def timed_steps(fn, K, W, flush, stream, dist, dev, stats=None, tag=None):
+    """W untimed warm-up steps, then K steps each bracketed by CUDA events on
+    the launching stream, L2 flushed (256 MB write) before each; a barrier +
+    synchronize on both sides.  Returns the MEDIAN step time in ms (SURVEY
+    §8(d)), max over ranks; mean / min / max go into ``stats[tag]``."""
+    import torch
+    for _ in range(W):
+        fn()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    for i in range(K):
+        flush.zero_()                      # evict L2 between timed steps
+        ev[i][0].record(stream)
+        fn()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ts = [a.elapsed_time(b) for a, b in ev]
+    med = max_over_ranks(statistics.median(ts), dist, dev)
+    if stats is not None and tag:
+        stats[tag] = {"median_ms": round(med, 5),
+                      "mean_ms": round(max_over_ranks(sum(ts) / K, dist, dev), 5),
+                      "min_ms": round(min(ts), 5), "max_ms": round(max(ts), 5), "steps": K}
+    return med
+
+
+# --------------------------------------------------------------------------
 # our arm
 
 
@@ -290,27 +339,10 @@ def run_ours(args):
         torch.cuda.synchronize()
         return None
 
-    def timed(fn, K, W):
-        for _ in range(W):
-            fn()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        total = 0.0
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(K)]
-        for i in range(K):
-            flush.zero_()                      # evict L2 between timed steps
-            ev[i][0].record(stream)
-            fn()
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        total = sum(a.elapsed_time(b) for a, b in ev)
-        return max_over_ranks(total / K, dist, dev)
+    stats = {}
+
+    def timed(fn, K, W, tag=None):
+        return timed_steps(fn, K, W, flush, stream, dist, dev, stats, tag)
 
     K, W = args.steps, args.warmup
     # The whole step is captured once as a CUDA graph (bin, spread, combine,
@@ -346,17 +378,17 @@ def run_ours(args):
     hs.charges.copy_(torch.as_tensor(q_np))
     quiet_host_pools()
     with ClockSampler(local) as clk:
-        ms_fp = timed(g_fp.replay, K, W)
-        ms_po = timed(g_po.replay, K, W)
-        ms_e2e = timed(hs.launch, K, W)
-        ms_eager = timed(lambda: step(True), K, W)
+        ms_fp = timed(g_fp.replay, K, W, "force_pressure")
+        ms_po = timed(g_po.replay, K, W, "pressure_only")
+        ms_e2e = timed(hs.launch, K, W, "e2e")
+        ms_eager = timed(lambda: step(True), K, W, "eager")
         if args.precision == "fp64":
-            ms_32 = timed(g_32.replay, K, W)
+            ms_32 = timed(g_32.replay, K, W, "fp32")
             f32 = {"ms_per_step": ms_32, "value": world * n / (ms_32 * 1e-3), "unit": UNIT,
                    "what": "force+pressure, precision='fp32' (fp32 grid, transforms and "
                            "fields; fp64 coordinates and reductions)"}
         if w.cell_type != "triclinic":
-            ms_an = timed(g_an.replay, K, W)
+            ms_an = timed(g_an.replay, K, W, "analytic")
             an = {"ms_per_step": ms_an, "value": world * n / (ms_an * 1e-3), "unit": UNIT,
                   "what": "force+pressure with analytic-differentiation forces "
                           "(force_mode='analytic'; the headline uses ik, the reference default)"}
@@ -432,19 +464,23 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": ms_fp, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if real_b == 8 else "f32",
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+        "dtype": "f64" if real_b == 8 else "f32",
         "data": "synthetic (seeded config recipe, SURVEY §8(d.1))",
         "config": {"workload": w.name, "n_charges": n, "grid": list(w.M), "P": w.P,
                    "delta": w.delta, "r_c": w.r_c, "cell_type": w.cell_type,
                    "precision": args.precision,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "flushed between timed steps (256 MB write)"},
+                   "l2": "flushed between timed steps (256 MB write)",
+                   "statistic": "median step time"},
         "pressure_only": {"value": world * n / (ms_po * 1e-3), "unit": UNIT,
                           "ms_per_step": ms_po, "gpu_launches_per_step": launches_po},
         "e2e": {"value": world * n / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": int(hs.h2d_bytes), "d2h_bytes_per_step": int(hs.d2h_bytes),
                 "api": "KSpaceSolver.host_stepper (pinned host in/out, one CUDA graph)"},
         "eager_ms_per_step": ms_eager,
+        "timing": dict(stats, statistic="median over the K timed steps (CUDA events, "
+                                         "L2 flushed before each)"),
         "gpu_launches": int(launches * K),
         "gpu_launches_per_step": launches,
         "clocks": clocks,
@@ -505,7 +541,7 @@ def near_field_leg(w, pos, q, kspace, timed, K, W):
     cs = CoulombSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
                                             fixed_M=w.M, cell_type=w.cell_type))
     g_all, _ = cs.graphed(pos, q, True)
-    kn, wn = max(3, min(K, 20)), max(W, 3)
+    kn, wn = max(3, min(K, 20 if w.n < 2_000_000 else 5)), max(min(W, 5), 3)
     ms_near = timed(near, kn, wn)
     ms_all = timed(coulomb, kn, wn)
     ms_graph = timed(g_all.replay, kn, wn)
@@ -531,51 +567,100 @@ def near_field_leg(w, pos, q, kspace, timed, K, W):
 # CPU legs
 
 
+CPU_SAMPLE_CHARGES = 100_000
+
+
 def cpu_baseline_port(config):
-    """Oracle port, 1 thread, one full step of the workload (bounded sample)."""
+    """Oracle port (the reference's numpy algorithm), 1 thread, bounded
+    sample of one step.  Small configs: one full step.  Large configs (config
+    4 would take ~11 min on one core): every mesh stage once at full size
+    (spread grid -> fftn -> energy + pressure; one ik spectrum + ifftn, x3),
+    plus spread and the 3-field gather of the first CPU_SAMPLE_CHARGES
+    charges, scaled to N (both are per-charge linear, mesh.py:204-218)."""
     from oracle import esp_oracle as O
     from paper_2601_00161_b200 import workloads
     w, pos, q = workloads.generate(config)
     plan = O.make_plan(w.h, w.M, w.P, w.delta, w.r_c)
     modes = O.Modes(plan)
+    ns = min(w.n, CPU_SAMPLE_CHARGES) if w.n > 3 * CPU_SAMPLE_CHARGES else w.n
+    h3 = plan.volume_element
     t0 = time.perf_counter()
-    rh = O.forward_density(plan, pos, q)
+    grid = O.spread(plan, pos[:ns], q[:ns])
+    t1 = time.perf_counter()
+    rh = np.fft.fftn(grid) * h3
     O.energy(modes, rh)
     O.pressure(modes, rh)
-    t1 = time.perf_counter()
-    O.forces_ik(plan, modes, rh, pos, q)
     t2 = time.perf_counter()
-    return {"value": w.n / (t2 - t0), "unit": UNIT, "cores": 1, "kind": "port",
-            "pressure_only_value": w.n / (t1 - t0),
-            "sample": f"1 full {w.name} force+pressure step ({w.n} charges, grid "
-                      f"{'x'.join(map(str, w.M))}, P={w.P}), numpy oracle port "
-                      f"(oracle/esp_oracle.py), single thread; ModeWorkspace setup excluded",
-            "seconds": round(t2 - t0, 3)}
+    scale = modes.fhat * modes.w_inv2 * rh[modes.mask]
+    n_inv = 3 if ns == w.n else 1
+    fields = []
+    for d in range(n_inv):
+        spec = np.zeros(plan.M, dtype=complex)
+        spec[modes.mask] = 1j * modes.kvec[d] * scale
+        fields.append(np.fft.ifftn(spec).real / h3)
+    t3 = time.perf_counter()
+    for d in range(3):
+        O.gather(plan, fields[d % n_inv], pos[:ns])
+    t4 = time.perf_counter()
+    per_charge = ((t1 - t0) + (t4 - t3)) / ns
+    mesh_fwd = t2 - t1
+    mesh_inv = (t3 - t2) * (3 / n_inv)
+    step = mesh_fwd + mesh_inv + per_charge * w.n
+    step_po = mesh_fwd + (t1 - t0) / ns * w.n
+    if ns == w.n:
+        sample = (f"1 full {w.name} force+pressure step ({w.n} charges, grid "
+                  f"{'x'.join(map(str, w.M))}, P={w.P}), numpy oracle port "
+                  f"(oracle/esp_oracle.py), single thread; ModeWorkspace setup excluded")
+    else:
+        sample = (f"{w.name}: full-size mesh stages timed once (fftn + energy/pressure "
+                  f"{mesh_fwd:.1f} s; one ik spectrum + ifftn {mesh_inv / 3:.1f} s, x3) plus "
+                  f"spread and 3-field gather of {ns} of {w.n} charges "
+                  f"({((t1 - t0) + (t4 - t3)):.1f} s), scaled linearly to N; numpy oracle "
+                  f"port, single thread; ModeWorkspace setup excluded")
+    return {"value": w.n / step, "unit": UNIT, "cores": 1, "kind": "port",
+            "pressure_only_value": w.n / step_po, "sample": sample,
+            "seconds": round(t4 - t0, 3), "step_seconds_est": round(step, 3)}
 
 
 _POOL_STATE = {}
 
 
+def _shared_array(shape):
+    """Zero-filled float64 array in an anonymous MAP_SHARED mapping: fork
+    children inherit it, so pool workers read and write it without pickling."""
+    import mmap
+    n = int(np.prod(shape))
+    buf = mmap.mmap(-1, max(8 * n, 8))
+    return np.frombuffer(buf, dtype=np.float64, count=n).reshape(shape)
+
+
 def _spread_chunk(args):
-    lo, hi = args
+    i, lo, hi = args
     st = _POOL_STATE
     from oracle import esp_oracle as O
-    return O.spread(st["plan"], st["pos"][lo:hi], st["q"][lo:hi])
+    st["parts"][i] = O.spread(st["plan"], st["pos"][lo:hi], st["q"][lo:hi],
+                              chunk=st["chunk"]).reshape(-1)
+    return i
 
 
 def _gather_chunk(args):
-    lo, hi, fields = args
+    lo, hi = args
     st = _POOL_STATE
     from oracle import esp_oracle as O
-    out = np.empty((hi - lo, 3))
+    M = st["plan"].M
     for d in range(3):
-        out[:, d] = O.gather(st["plan"], fields[d], st["pos"][lo:hi])
-    return out
+        st["F"][lo:hi, d] = O.gather(st["plan"], st["fields"][d].reshape(M),
+                                     st["pos"][lo:hi], chunk=st["chunk"])
+    return lo
 
 
 def run_reference(args):
-    """Reference arm: the oracle port of the reference CPU path on all host
-    cores, same config/metric as our arm.  Rank 0 only."""
+    """Reference arm: the oracle port of the reference CPU path (the same
+    numpy operations as mesh.py:204-342) on all host cores, same config and
+    metric as our arm.  Spread and gather run over particle chunks in a fork
+    process pool writing into shared-memory buffers (exact by linearity; the
+    per-chunk grids are summed in chunk order); the FFTs are numpy's, called
+    as the reference calls them.  Rank 0 only; other ranks exit 0."""
     rank, world, local = dist_env()
     if rank != 0:
         return
@@ -587,49 +672,65 @@ def run_reference(args):
     plan = O.make_plan(w.h, w.M, w.P, w.delta, w.r_c)
     modes = O.Modes(plan)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    _POOL_STATE.update(plan=plan, pos=pos, q=q)
-    ctx = mp.get_context("fork")
+    G = int(np.prod(w.M))
     chunks = np.linspace(0, w.n, cores + 1).astype(int)
     spans = [(int(a), int(b)) for a, b in zip(chunks[:-1], chunks[1:]) if b > a]
+    parts = _shared_array((len(spans), G))
+    fields = _shared_array((3, G))
+    F = _shared_array((w.n, 3))
+    _POOL_STATE.update(plan=plan, pos=pos, q=q, parts=parts, fields=fields, F=F,
+                       chunk=50_000)
     h3 = plan.volume_element
-    with ctx.Pool(cores) as pool:
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(spans)) as pool:
         def one_step():
-            grid = sum(pool.map(_spread_chunk, spans))
-            rh = np.fft.fftn(grid) * h3
+            pool.map(_spread_chunk, [(i, a, b) for i, (a, b) in enumerate(spans)])
+            grid = parts[0].copy()
+            for i in range(1, len(spans)):
+                grid += parts[i]
+            rh = np.fft.fftn(grid.reshape(w.M)) * h3
             O.energy(modes, rh)
             O.pressure(modes, rh)
             scale = modes.fhat * modes.w_inv2 * rh[modes.mask]
-            fields = []
             for d in range(3):
                 spec = np.zeros(plan.M, dtype=complex)
                 spec[modes.mask] = 1j * modes.kvec[d] * scale
-                fields.append(np.fft.ifftn(spec).real / h3)
-            parts = pool.map(_gather_chunk, [(a, b, fields) for a, b in spans])
-            return -q[:, None] * h3 * np.concatenate(parts)
+                fields[d] = (np.fft.ifftn(spec).real / h3).reshape(-1)
+            pool.map(_gather_chunk, spans)
+            return -q[:, None] * h3 * F
 
-        budget = 150.0
         t_start = time.perf_counter()
+        warm = 0
         for _ in range(args.warmup):
             one_step()
+            warm += 1
+            if time.perf_counter() - t_start > 0.25 * args.ref_budget:
+                break
         times = []
+        t_timed = time.perf_counter()
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            one_step()
+            Fr = one_step()
             times.append(time.perf_counter() - t0)
-            if time.perf_counter() - t_start > budget:
+            if time.perf_counter() - t_timed > args.ref_budget:
                 break
-    ms = 1e3 * float(np.mean(times))
+    assert np.isfinite(Fr).all()
+    ms = 1e3 * float(statistics.median(times))
     v = w.n / (ms * 1e-3)
     sample = (f"{len(times)} of {args.steps} requested full {w.name} force+pressure steps "
-              f"({w.n} charges); spread/gather in {cores} processes, numpy FFT")
+              f"({w.n} charges, grid {'x'.join(map(str, w.M))}) after {warm} warm-up; "
+              f"spread/gather in {len(spans)} processes over shared memory, numpy FFT "
+              f"(single-threaded, as the reference); median step; time budget "
+              f"{args.ref_budget:.0f} s of timed steps; ModeWorkspace setup excluded")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(times),
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded config recipe, SURVEY §8(d.1))",
             "config": {"workload": w.name, "n_charges": w.n, "grid": list(w.M), "P": w.P,
-                       "delta": w.delta, "r_c": w.r_c, "parallelism": "cpu"},
+                       "delta": w.delta, "r_c": w.r_c, "cell_type": w.cell_type,
+                       "precision": "fp64", "parallelism": "cpu"},
             "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": len(spans), "kind": "port",
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -649,7 +750,7 @@ def run_slab(args):
     dist = init_dist(world, local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg = args.config if args.config != CONFIG else 4
+    cfg = args.config
     w, pos_np, q_np = workloads.generate(cfg)
     basis = build_pswf(solve_bandwidth(w.delta))
     window = tabulate_window(basis, w.P)
@@ -661,23 +762,11 @@ def run_slab(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
+    stats = {}
+
     def timed(want_forces, K, W):
-        for _ in range(W):
-            s.evaluate(pos, q, want_forces)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(K)]
-        for i in range(K):
-            flush.zero_()
-            ev[i][0].record(stream)
-            s.evaluate(pos, q, want_forces)
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / K, dist, dev)
+        return timed_steps(lambda: s.evaluate(pos, q, want_forces), K, W, flush, stream,
+                           dist, dev, stats, "force_pressure" if want_forces else "pressure_only")
 
     near = None
     if args.near:
@@ -690,22 +779,8 @@ def run_slab(args):
         sn.ops.plan.reserve(pos.shape[0] + pos.shape[0] // 2)
 
     def timed_near(K, W):
-        for _ in range(W):
-            sn.evaluate(pos, q)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(K)]
-        for i in range(K):
-            flush.zero_()
-            ev[i][0].record(stream)
-            sn.evaluate(pos, q)
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / K, dist, dev)
+        return timed_steps(lambda: sn.evaluate(pos, q), K, W, flush, stream, dist, dev,
+                           stats, "near_field")
 
     with ClockSampler(local) as clk:
         ms_fp = timed(True, args.steps, args.warmup)
@@ -725,6 +800,7 @@ def run_slab(args):
                        "l2": "flushed between timed steps (256 MB write)"},
             "pressure_only": {"value": w.n / (ms_po * 1e-3), "unit": UNIT,
                               "ms_per_step": ms_po},
+            "timing": dict(stats, statistic="median over the K timed steps, max over ranks"),
             "clocks": clk.summary()}
     if near is not None:
         line["near_field"] = near
@@ -737,9 +813,10 @@ def run_slab(args):
 
 def main():
     args = parse()
+    _, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)
-    elif args.slab:
+    elif args.slab or (world > 1 and not args.replicas):
         run_slab(args)
     else:
         run_ours(args)

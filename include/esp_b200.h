@@ -182,6 +182,11 @@ void* esp_grid_ptr(esp_plan* plan);       /* real grid, [z][y][x]          */
 void* esp_spectrum_ptr(esp_plan* plan);   /* complex half spectrum          */
 void* esp_fields_ptr(esp_plan* plan);     /* 3 ik force fields, [3][z][y][x] */
 int esp_grid_info(const esp_plan* plan, int64_t* info8);
+/* 1 in *radix when a step over n charges bins with the device radix sort
+ * (n >= the plan's sort threshold; ESP_SORT_THRESHOLD at plan creation
+ * overrides the default 5e5), 0 for the counting sort.  Both binnings give
+ * bitwise-identical results (replaces nothing: introspection for tests). */
+int esp_binning_radix(const esp_plan* plan, int64_t n, int32_t* radix);
 /* info8 = {Mx, My, Mz, Hx(=Mx/2+1), n_modes_retained(full spectrum),
  *          kernel_launches_last_step, n_tiles, precision}                   */
 int esp_set_spectrum(esp_plan* plan, const void* d_spectrum, void* stream);

@@ -153,6 +153,7 @@ def lib():
     L.esp_fields_ptr.argtypes = [vp]
     L.esp_fields_ptr.restype = vp
     L.esp_grid_info.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.esp_binning_radix.argtypes = [vp, C.c_int64, C.POINTER(C.c_int32)]
     L.esp_fft_path.argtypes = [vp]
     L.esp_slab_layout.argtypes = [vp, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
     L.esp_slab_forward.argtypes = [vp, C.POINTER(SlabDesc), vp, vp]
@@ -189,6 +190,7 @@ EXPORTED = [
     "esp_set_charges_event", "esp_spread", "esp_forward", "esp_scale_reduce", "esp_forces_ik",
     "esp_forces_analytic", "esp_local_pressure", "esp_evaluate", "esp_counters",
     "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
+    "esp_binning_radix",
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
     "esp_gather_fields", "esp_fields_ptr", "esp_fft_path",
     "esp_slab_layout", "esp_slab_forward", "esp_slab_reduce", "esp_slab_inverse",

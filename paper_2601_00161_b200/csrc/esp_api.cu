@@ -870,4 +870,10 @@ int esp_grid_info(const esp_plan* p, int64_t* info) {
   return ESP_OK;
 }
 
+int esp_binning_radix(const esp_plan* p, int64_t n, int32_t* radix) {
+  if (!p || !radix) return ESP_ERR_PARAM;
+  *radix = (n >= p->sort_threshold && p->d_sort_tmp) ? 1 : 0;
+  return ESP_OK;
+}
+
 }  // extern "C"

@@ -260,6 +260,14 @@ class EspPlan:
         _lib.check(_lib.lib().esp_grid_info(self._handle, buf), "esp_grid_info")
         return list(buf)
 
+    def radix_binning(self, n: int) -> bool:
+        """True when a step over n charges bins with the device radix sort
+        (esp_binning_radix); False for the counting sort."""
+        r = C.c_int32()
+        _lib.check(_lib.lib().esp_binning_radix(self._handle, int(n), C.byref(r)),
+                   "esp_binning_radix")
+        return bool(r.value)
+
     # -- distributed z-slab transforms (esp_slab_*) -----------------------------
     def slab_layout(self, nranks: int):
         """(by_start, info): the in-band ky rows owned per rank and
