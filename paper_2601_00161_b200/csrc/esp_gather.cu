@@ -601,14 +601,11 @@ static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s, OutMa
   Geom g = make_geom(p);
   if constexpr (P <= 8) {
     const size_t smem = GatherLayout<real, P>::bytes(p->PZ);
-    static size_t attr_set = 0;  // set once per instantiation (capture-safe)
-    if (smem > attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(k_gather_warp<real, P>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      attr_set = smem;
-    }
+    // the opt-in is per device: set it on every call (host-only, capture-safe)
+    cudaError_t e = cudaFuncSetAttribute(k_gather_warp<real, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
     k_gather_warp<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
         g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q, p->d_idx,
         reinterpret_cast<const real*>(p->d_fields), p->G, d_forces, om);
@@ -620,14 +617,11 @@ static cudaError_t gather_p(esp_plan* p, double* d_forces, cudaStream_t s, OutMa
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
   const size_t smem = gather_smem<real>(P, p->n_pieces, p->ncoef);
-  static size_t attr_set = 0;  // set once per instantiation (capture-safe)
-  if (smem > attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gather_ik<real, P>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = smem;
-  }
+  // the opt-in is per device: set it on every call (host-only, capture-safe)
+  cudaError_t e = cudaFuncSetAttribute(k_gather_ik<real, P>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
   k_gather_ik<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
       g, tab, p->d_breaks, p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->d_q,
       p->d_idx, p->cap, reinterpret_cast<const real*>(p->d_fields), p->G, d_forces, om);
@@ -691,14 +685,11 @@ static cudaError_t grad_p(esp_plan* p, double* d_forces, cudaStream_t s) {
     const size_t smem = ((sizeof(real) * (size_t)p->PZ * GatherLayout<real, P>::kPlaneZ + 15) &
                          ~size_t(15)) +
                         sizeof(real) * (size_t)(kTileThreads / 32) * 2 * 4 * 3 * RS;
-    static size_t attr_set = 0;
-    if (smem > attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(k_gather_grad<real, P>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      attr_set = smem;
-    }
+    // the opt-in is per device: set it on every call (host-only, capture-safe)
+    cudaError_t e = cudaFuncSetAttribute(k_gather_grad<real, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
     k_gather_grad<real, P><<<(unsigned)p->n_tiles, kTileThreads, smem, s>>>(
         g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec),
         reinterpret_cast<const real*>(p->d_drec), p->d_pk, p->d_q, p->d_idx,

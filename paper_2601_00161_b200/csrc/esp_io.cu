@@ -27,16 +27,57 @@ struct esp_particles {
 
 namespace {
 
-bool is_space(char c) {
-  return c == ' ' || c == '\t' || c == '\r' || c == '\v' || c == '\f';
+// Python's str.splitlines() boundaries after read_text()'s universal-newline
+// translation: \n, \r, \r\n, \v, \f, \x1c-\x1e and the UTF-8 encodings of
+// U+0085, U+2028, U+2029.  Returns the byte length of the break at i (0: none).
+size_t line_break(const std::string& t, size_t i) {
+  const unsigned char c = (unsigned char)t[i];
+  if (c == '\r') return (i + 1 < t.size() && t[i + 1] == '\n') ? 2 : 1;
+  if (c == '\n' || c == '\v' || c == '\f' || (c >= 0x1c && c <= 0x1e)) return 1;
+  if (c == 0xC2 && i + 1 < t.size() && (unsigned char)t[i + 1] == 0x85) return 2;
+  if (c == 0xE2 && i + 2 < t.size() && (unsigned char)t[i + 1] == 0x80 &&
+      ((unsigned char)t[i + 2] == 0xA8 || (unsigned char)t[i + 2] == 0xA9))
+    return 3;
+  return 0;
 }
 
-// One token as a Python float(): the whole token must parse; hex forms,
-// which strtod accepts and float() does not, are rejected.
-bool parse_double(const std::string& tok, double* out) {
-  if (tok.empty()) return false;
-  for (char c : tok)
-    if (c == 'x' || c == 'X' || c == 'p' || c == 'P') return false;
+// Python's str.split() / strip() whitespace (str.isspace) inside a line:
+// ASCII \t \n \v \f \r space \x1c-\x1f, and the UTF-8 encodings of U+0085,
+// U+00A0, U+1680, U+2000-U+200A, U+2028, U+2029, U+202F, U+205F, U+3000.
+// Returns the byte length of the whitespace character at i (0: none).
+size_t space_len(const std::string& t, size_t i) {
+  const unsigned char c = (unsigned char)t[i];
+  if (c == ' ' || (c >= '\t' && c <= '\r') || (c >= 0x1c && c <= 0x1f)) return 1;
+  auto b = [&](size_t k) { return i + k < t.size() ? (unsigned char)t[i + k] : 0u; };
+  if (c == 0xC2 && (b(1) == 0x85 || b(1) == 0xA0)) return 2;
+  if (c == 0xE1 && b(1) == 0x9A && b(2) == 0x80) return 3;
+  if (c == 0xE2 && b(1) == 0x80 && ((b(2) >= 0x80 && b(2) <= 0x8A) || b(2) == 0xA8 ||
+                                    b(2) == 0xA9 || b(2) == 0xAF))
+    return 3;
+  if (c == 0xE2 && b(1) == 0x81 && b(2) == 0x9F) return 3;
+  if (c == 0xE3 && b(1) == 0x80 && b(2) == 0x80) return 3;
+  return 0;
+}
+
+bool is_digit(char c) { return c >= '0' && c <= '9'; }
+
+// One token as a Python float(): the whole token must parse.  Underscores
+// are accepted only between two digits (PEP 515) and removed; hex forms and
+// 'nan(...)', which strtod accepts and float() does not, are rejected.
+bool parse_double(const std::string& raw, double* out) {
+  if (raw.empty()) return false;
+  std::string tok;
+  tok.reserve(raw.size());
+  for (size_t i = 0; i < raw.size(); ++i) {
+    const char c = raw[i];
+    if (c == 'x' || c == 'X' || c == 'p' || c == 'P' || c == '(') return false;
+    if (c == '_') {
+      if (i == 0 || i + 1 >= raw.size() || !is_digit(raw[i - 1]) || !is_digit(raw[i + 1]))
+        return false;
+      continue;
+    }
+    tok.push_back(c);
+  }
   const char* s = tok.c_str();
   char* end = nullptr;
   errno = 0;
@@ -84,21 +125,22 @@ int esp_particles_read(const char* path, esp_particles** out) {
     return ESP_ERR_INPUT;
   };
   while (pos < text.size()) {
-    size_t eol = text.find('\n', pos);
-    if (eol == std::string::npos) eol = text.size();
+    size_t eol = pos, brk = 0;
+    while (eol < text.size() && (brk = line_break(text, eol)) == 0) ++eol;
     ++ln;
     size_t stop = text.find('#', pos);
     if (stop == std::string::npos || stop > eol) stop = eol;
     cols.clear();
     size_t a = pos;
     while (a < stop) {
-      while (a < stop && is_space(text[a])) ++a;
+      size_t w;
+      while (a < stop && (w = space_len(text, a)) > 0) a += w;
       size_t b = a;
-      while (b < stop && !is_space(text[b])) ++b;
+      while (b < stop && space_len(text, b) == 0) ++b;
       if (b > a) cols.emplace_back(text, a, b - a);
       a = b;
     }
-    pos = eol + 1;
+    pos = eol + (brk ? brk : 1);
     if (cols.empty()) continue;
     if (!have_cell) {
       const bool ortho = cols[0] == "cell", tri = cols[0] == "cell3";

@@ -421,14 +421,11 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s, bool with_combine) {
   } else {
     const int chunk = p->M[2] <= 128 ? 128 : 64;
     const size_t smem = SpreadLayout<real, P>::bytes(chunk);
-    static size_t attr_set = 0;  // set once per instantiation (capture-safe)
-    if (smem > attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(k_spread_tiles<real, P>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      attr_set = smem;
-    }
+    // the opt-in is per device: set it on every call (host-only, capture-safe)
+    cudaError_t e = cudaFuncSetAttribute(k_spread_tiles<real, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
     k_spread_tiles<real, P><<<(unsigned)p->n_tiles_s, kSpreadThreads, smem, s>>>(
         g, p->d_offsets, reinterpret_cast<const real*>(p->d_wrec), p->d_pk, p->d_q,
         reinterpret_cast<real*>(p->d_scratch), chunk);

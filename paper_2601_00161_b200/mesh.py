@@ -12,14 +12,18 @@ module (mesh.py:25-379); the work runs in ``libesp_b200.so``:
 
 Inputs may be the reference's own dataclasses (duck-typed: ``positions``,
 ``charges``, ``cell.h``; ``spec.M``, ``spec.P``, ``spec.window``) or this
-package's.  Fourier fields are kept on the device as the half spectrum;
-``GridField.full()`` materialises the reference's full (Mx, My, Mz) numpy
-spectrum for inspection.
+package's.  Systems given as numpy arrays get numpy results in the
+reference's layouts (``GridField.values`` is the [x][y][z] grid or the full
+[mx][my][mz] spectrum, forces are (N,3) ndarrays), so the reference's own
+tests apply unchanged; systems given as CUDA tensors keep every result on
+the device.  Plans and kernels are cached on the spec object; particles are
+re-binned on every call that gathers, so mutated or different systems never
+reuse stale bins.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -76,7 +80,6 @@ class GridSpec:
     delta_spread: float
     oversampling: float
     lengths: tuple
-    _plans: dict = field(default_factory=dict, compare=False, repr=False)
 
     @property
     def n_grid(self) -> int:
@@ -155,47 +158,96 @@ def _window_of(spec) -> WindowTable:
                        breaks=np.asarray(val.x, dtype=float), basis_c=float(w.basis_c))
 
 
-_SPEC_KERNELS = {}
+def _spec_cache(spec) -> dict:
+    """Per-spec cache living ON the spec object (frozen dataclasses still
+    carry a ``__dict__``), so its lifetime is the spec's and no id() can be
+    reused while an entry exists."""
+    c = spec.__dict__.get("_b200_cache")
+    if c is None:
+        c = {"plans": {}}
+        object.__setattr__(spec, "_b200_cache", c)
+    return c
 
 
 def _get_plan(spec, kern, cell, precision="fp64") -> EspPlan:
-    """Device plan cached per (spec, kernel, cell, precision)."""
+    """Device plan cached per (spec, kernel, cell, precision).  Entries hold
+    the kernel they were built for and are matched by identity."""
     h = np.asarray(cell.h, dtype=float)
+    cache = _spec_cache(spec)
     if kern is None:
         # Spread/transform only: a kernel whose band covers the whole grid.
-        kern = _SPEC_KERNELS.get(id(spec))
+        kern = cache.get("spread_kern")
         if kern is None:
             sb = spec.spread_basis
             kmax = np.pi / min(spec.spacing)
             kern = SplitKernel(basis=sb, r_c=sb.c / kmax)
-            _SPEC_KERNELS[id(spec)] = kern
-    plans = spec._plans if hasattr(spec, "_plans") else _SPEC_KERNELS.setdefault(("plans", id(spec)), {})
+            cache["spread_kern"] = kern
     key = (id(kern), h.tobytes(), precision)
-    plan = plans.get(key)
-    if plan is None:
-        plan = EspPlan(spec.M, spec.P, _window_of(spec), kern.basis, kern.r_c,
-                       spread=spec.spread_basis, precision=precision)
-        plan.set_cell(h)
-        plan._kern = kern
-        plans[key] = plan
+    hit = cache["plans"].get(key)
+    if hit is not None and hit[0] is kern:
+        return hit[1]
+    plan = EspPlan(spec.M, spec.P, _window_of(spec), kern.basis, kern.r_c,
+                   spread=spec.spread_basis, precision=precision)
+    plan.set_cell(h)
+    plan._kern = kern
+    cache["plans"][key] = (kern, plan)
     return plan
 
 
-@dataclass
 class GridField:
     """Scalar field on the periodic mesh, real or Fourier (mesh.py:145-151).
 
-    Real fields: ``values`` is a CUDA tensor indexed [x, y, z] like the
-    reference (a view of the device [z][y][x] layout).  Fourier fields:
-    ``values`` is the CUDA half spectrum [kz, ky, kx<=Mx/2] already scaled by
-    the volume element; ``full()`` gives the reference's full spectrum.
+    ``values`` follows the reference: for systems given as numpy arrays it is
+    a numpy array in the reference layout — the real grid indexed [x, y, z]
+    (C order, z contiguous), or the FULL complex spectrum [mx, my, mz] with
+    the continuum normalisation of ``forward_density`` (mesh.py:221-226).
+    For systems given as CUDA tensors ``values`` stays on the device: the
+    real grid as an [x, y, z] view of the device [z][y][x] layout, the
+    spectrum as the half spectrum [kz, ky, kx <= Mx/2].
+
+    ``device`` always holds the device copy (real: (Mz, My, Mx); Fourier:
+    half spectrum (Mz, My, Mx//2+1), volume-element scaled) that the
+    pipeline functions consume; the numpy ``values`` are materialised from it
+    on first access.  Assigning ``values`` makes the assigned array the
+    field's content (it is uploaded when a pipeline function reads it).
     """
 
-    values: object
-    spec: object
-    space: str = "real"
-    _plan: object = field(default=None, repr=False)
-    _version: int = field(default=-1, repr=False)
+    def __init__(self, values=None, spec=None, space: str = "real"):
+        self._values = values
+        self.spec = spec
+        self.space = space
+        self.device = None
+        self._host = True
+        self._plan = None
+        self._version = -1
+
+    @classmethod
+    def _from_device(cls, dev, spec, space, host, plan=None, version=-1):
+        f = cls(None, spec, space)
+        f.device = dev
+        f._host = host
+        f._plan = plan
+        f._version = version
+        return f
+
+    @property
+    def values(self):
+        if self._values is None and self.device is not None:
+            if not self._host:
+                return self.device.permute(2, 1, 0) if self.space == "real" else self.device
+            self._values = (np.ascontiguousarray(self.device.permute(2, 1, 0).cpu().numpy())
+                            if self.space == "real" else self.full())
+        return self._values
+
+    @values.setter
+    def values(self, v):
+        self._values = v
+        self.device = None
+        self._plan = None
+        self._version = -1
+
+    def __repr__(self):
+        return f"GridField(space={self.space!r}, M={getattr(self.spec, 'M', None)})"
 
     def numpy(self) -> np.ndarray:
         if self.space == "real":
@@ -204,19 +256,37 @@ class GridField:
         return self.full()
 
     def full(self) -> np.ndarray:
-        """Full complex spectrum in the reference layout [mx, my, mz]."""
+        """Full complex spectrum in the reference layout [mx, my, mz]
+        (Hermitian extension of the device half spectrum)."""
         if self.space != "fourier":
             raise MeshError("full() is defined for spectral fields only")
-        half = self.values.detach().cpu().numpy()      # [kz][ky][kx_h]
+        if self.device is None:
+            v = self._values
+            return v.detach().cpu().numpy() if isinstance(v, torch.Tensor) else np.asarray(v)
+        half = self.device                                  # [kz][ky][kx_h]
         Mx, My, Mz = self.spec.M
-        out = np.empty((Mz, My, Mx), dtype=complex)
-        out[:, :, : half.shape[2]] = half
-        kx = np.arange(half.shape[2], Mx)
-        mirror_x = (-kx) % Mx
-        zz = (-np.arange(Mz)) % Mz
-        yy = (-np.arange(My)) % My
-        out[:, :, half.shape[2]:] = np.conj(half[zz][:, yy][:, :, mirror_x])
-        return np.transpose(out, (2, 1, 0))
+        hx = half.shape[2]
+        dev = half.device
+        zz = (-torch.arange(Mz, device=dev)) % Mz
+        yy = (-torch.arange(My, device=dev)) % My
+        xx = (-torch.arange(hx, Mx, device=dev)) % Mx
+        upper = torch.conj(half.index_select(0, zz).index_select(1, yy).index_select(2, xx))
+        out = torch.cat([half, upper], dim=2)               # [kz][ky][kx]
+        return np.ascontiguousarray(out.permute(2, 1, 0).cpu().numpy())
+
+    def half_spectrum(self, plan: EspPlan) -> torch.Tensor:
+        """Device half spectrum [kz][ky][kx<=Mx/2], volume-element scaled."""
+        if self.device is not None:
+            return self.device
+        v = self._values
+        if isinstance(v, torch.Tensor) and v.is_cuda and tuple(v.shape) == (
+                plan.M[2], plan.M[1], plan.Hx):
+            return v
+        full = torch.as_tensor(np.asarray(v), device="cuda") if not isinstance(v, torch.Tensor) \
+            else v.cuda()
+        if tuple(full.shape) != tuple(plan.M):
+            raise MeshError("spectral field shape does not match the grid")
+        return full[: plan.Hx].permute(2, 1, 0).contiguous().to(torch.complex128)
 
 
 def _particles(sys):
@@ -229,13 +299,16 @@ def _particles(sys):
     return pos.to(torch.float64).contiguous(), q.to(torch.float64).contiguous()
 
 
+def _host_inputs(sys) -> bool:
+    return not isinstance(sys.positions, torch.Tensor)
+
+
 def spread_charges(sys, spec) -> GridField:
     """Deposit q_j W(r_g - r_j) on the mesh (mesh.py:204-210)."""
     plan = _get_plan(spec, getattr(spec, "_kern", None), sys.cell)
     pos, q = _particles(sys)
     grid = plan.spread(pos, q).clone()
-    plan._bins_for = id(sys)
-    return GridField(values=grid.permute(2, 1, 0), spec=spec, space="real")
+    return GridField._from_device(grid, spec, "real", _host_inputs(sys))
 
 
 def forward_density(sys, spec, provider: TransformProvider) -> GridField:
@@ -244,24 +317,23 @@ def forward_density(sys, spec, provider: TransformProvider) -> GridField:
     plan = _get_plan(spec, getattr(spec, "_kern", None), sys.cell)
     pos, q = _particles(sys)
     plan.spread(pos, q)
-    plan._bins_for = id(sys)
     plan.forward()
     provider.forward_count += 1
     vals = plan.spectrum_view() * plan.tables.volume_element
-    return GridField(values=vals, spec=spec, space="fourier", _plan=plan,
-                     _version=plan.version)
+    return GridField._from_device(vals, spec, "fourier", _host_inputs(sys), plan, plan.version)
 
 
-def _spectrum_plan(rho_hat: GridField, kern, spec, cell) -> EspPlan:
+def _spectrum_plan(rho_hat: GridField, kern, spec, cell, n_particles: int = 0) -> EspPlan:
+    """The plan holding ``rho_hat``: reused when the plan's spectrum is still
+    this field's (same plan and version), otherwise uploaded.  Capacity for
+    ``n_particles`` is reserved first (growing re-creates the plan)."""
     plan = _get_plan(spec, kern, cell)
+    plan.ensure_capacity(n_particles)
     if rho_hat._plan is plan and rho_hat._version == plan.version:
         return plan
-    vals = rho_hat.values
-    if not isinstance(vals, torch.Tensor):
-        raise MeshError("spectral field must come from forward_density")
-    scale = plan.tables.volume_element
-    plan.set_spectrum((vals / scale).to(torch.complex128 if plan.precision == "fp64"
-                                        else torch.complex64))
+    half = rho_hat.half_spectrum(plan)
+    plan.set_spectrum((half / plan.tables.volume_element).to(
+        torch.complex128 if plan.precision == "fp64" else torch.complex64))
     rho_hat._plan = plan
     rho_hat._version = plan.version
     return plan
@@ -348,47 +420,55 @@ def long_range_pressure(rho_hat: GridField, kern: SplitKernel, spec, cell,
     return _reduce(rho_hat, kern, spec, cell)[1].copy()
 
 
+def _bin(plan: EspPlan, sys):
+    """Bin (and spread) ``sys`` on the plan without touching its spectrum:
+    the gather must see these positions, not whatever was binned last."""
+    pos, q = _particles(sys)
+    version = plan.version
+    plan.spread(pos, q)
+    plan.version = version       # the spectrum is untouched
+    return pos
+
+
 def long_range_forces(rho_hat: GridField, sys, kern: SplitKernel, spec, cell,
                       mode: str = "ik", provider: TransformProvider | None = None,
-                      modes: ModeWorkspace | None = None) -> np.ndarray:
-    """Far-field forces by ik differentiation and window gathering
-    (mesh.py:315-342): three inverse transforms, counted on ``provider``."""
+                      modes: ModeWorkspace | None = None):
+    """Far-field forces by spectral differentiation and window gathering
+    (mesh.py:315-342): ik = three inverse transforms, analytic = one,
+    counted on ``provider``.  numpy (N,3) for numpy systems, a CUDA tensor
+    for CUDA-tensor systems."""
     if rho_hat.space != "fourier":
         raise MeshError("long_range_forces expects a spectral density")
     if mode not in ("ik", "analytic"):
         raise MeshError(f"unknown differentiation mode {mode!r}")
     provider = provider or TransformProvider()
-    plan = _spectrum_plan(rho_hat, kern, spec, cell)
-    pos, q = _particles(sys)
+    n = int(sys.positions.shape[0])
+    plan = _spectrum_plan(rho_hat, kern, spec, cell, n)
+    _bin(plan, sys)
     version = plan.version
-    if getattr(plan, "_bins_for", None) != id(sys):
-        plan.spread(pos, q)        # re-bin these particles; the spectrum is untouched
-        plan._bins_for = id(sys)
     if mode == "analytic":
-        F = plan.forces_analytic(pos.shape[0])
+        F = plan.forces_analytic(n)
         provider.inverse_count += 1
     else:
         plan.scale_reduce(write_ik=True)
-        F = plan.forces_ik(pos.shape[0])
+        F = plan.forces_ik(n)
         provider.inverse_count += 3
     plan.version = version
-    return F.cpu().numpy()
+    return F.cpu().numpy() if _host_inputs(sys) else F
 
 
 def local_pressure(rho_hat: GridField, sys, kern, spec, cell,
-                   provider: TransformProvider | None = None, modes=None) -> np.ndarray:
+                   provider: TransformProvider | None = None, modes=None):
     """Per-particle far-field pressure tensors (N,3,3) (mesh.py:353-379): six
     inverse transforms (two batched C2R x3) and window gathers."""
     if rho_hat.space != "fourier":
         raise MeshError("local_pressure expects a spectral density")
     provider = provider or TransformProvider()
-    plan = _spectrum_plan(rho_hat, kern, spec, cell)
-    pos, q = _particles(sys)
+    n = int(sys.positions.shape[0])
+    plan = _spectrum_plan(rho_hat, kern, spec, cell, n)
+    _bin(plan, sys)
     version = plan.version
-    if getattr(plan, "_bins_for", None) != id(sys):
-        plan.spread(pos, q)
-        plan._bins_for = id(sys)
-    out = plan.local_pressure(pos.shape[0])
+    out = plan.local_pressure(n)
     provider.inverse_count += 6
     plan.version = version
-    return out.cpu().numpy()
+    return out.cpu().numpy() if _host_inputs(sys) else out

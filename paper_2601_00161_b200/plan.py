@@ -156,7 +156,8 @@ class EspPlan:
         self.capacity = int(max(capacity, 1))
         self._handle = None
         self._cell = None
-        self.version = 0          # bumps on every forward transform
+        self.version = 0          # bumps on every forward transform / spectrum change
+        self.generation = 0       # bumps when device buffers or cell constants change
         self._create()
 
     # -- lifetime -----------------------------------------------------------
@@ -218,6 +219,8 @@ class EspPlan:
         self.close()
         self.capacity = max(int(n), 2 * self.capacity)
         self._create()
+        self.version += 1         # the recreated plan holds no spectrum
+        self.generation += 1
         if cell is not None:
             self._cell = None
             self.set_cell(cell)
@@ -252,6 +255,8 @@ class EspPlan:
                    "esp_plan_set_cell")
         self._cell = t.h.copy()
         self.tables = t
+        self.version += 1         # mode tables changed: cached reductions are stale
+        self.generation += 1
         return t
 
     # -- introspection --------------------------------------------------------
@@ -499,7 +504,7 @@ class EspPlan:
         with torch.cuda.graph(g):
             body()
         torch.cuda.synchronize()
-        return g
+        return PlanGraph(g, [self])
 
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.lib().esp_set_profiling(self._handle, int(bool(on))), "esp_set_profiling")
@@ -513,6 +518,32 @@ class EspPlan:
             _lib.check(-n, "esp_profile_read")
         labels = names.value.decode().split(",") if n else []
         return list(zip(labels, [float(ms[i]) for i in range(n)]))
+
+
+class PlanGraph:
+    """A captured CUDA graph bound to the plans it was captured on.
+
+    A graph bakes in device addresses (grids, scratch, mode tables) and
+    by-value cell constants (spacing, volume).  ``set_cell`` (an NPT rebind)
+    re-uploads the cell tables and ``ensure_capacity`` re-creates the plan, so
+    a graph captured before either must not replay: ``replay()`` checks each
+    plan's generation and raises instead of reading freed memory or the old
+    geometry.  Graphs are tied to a fixed N and cell; re-capture after a
+    rebind."""
+
+    def __init__(self, graph, plans):
+        self.graph = graph
+        self._deps = [(p, p.generation) for p in plans]
+
+    @property
+    def valid(self) -> bool:
+        return all(p.generation == g for p, g in self._deps)
+
+    def replay(self):
+        if not self.valid:
+            raise ParameterError("CUDA graph captured before a cell rebind or capacity growth "
+                                 "of its plan; capture it again")
+        self.graph.replay()
 
 
 def probe_fp64_tflops(stream=None) -> float:

@@ -181,6 +181,8 @@ class NearFieldPlan:
         self._L = L
         self.cell: Cell | None = None
         self._n_pairs_cap = 0
+        self._n_cap = int(max(capacity, 1))
+        self.generation = 0       # bumps on set_cell / reserve (captured graphs go stale)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -203,10 +205,14 @@ class NearFieldPlan:
                                              1 if cell.is_orthorhombic else 0,
                                              float(cell.volume)), "esp_near_set_cell")
         self.cell = cell
+        self.generation += 1
 
     def reserve(self, n: int, n_pairs: int = 0) -> None:
+        if int(n) > self._n_cap or int(n_pairs) > self._n_pairs_cap:
+            self.generation += 1  # buffers may be re-allocated
         _lib.check(self._L.esp_near_reserve(self._h, int(n), int(n_pairs)), "esp_near_reserve")
         self._n_pairs_cap = max(self._n_pairs_cap, int(n_pairs))
+        self._n_cap = max(self._n_cap, int(n))
 
     def info(self) -> dict:
         a = (C.c_int64 * 8)()

@@ -22,8 +22,8 @@ from . import _lib
 from .cells import CellType, infer_cell_type
 from .errors import ParameterError
 from .kernel import SplitKernel, background_correction, self_energy
-from .mesh import plan_grid
-from .plan import EspPlan, out7_to_tensor
+from .mesh import ModeWorkspace, TransformProvider, plan_grid
+from .plan import EspPlan, PlanGraph, out7_to_tensor
 from .realspace import NearFieldPlan, build_pair_table, out7_to_pressure
 from .pswf import build_pswf, solve_bandwidth
 from .system import Cell, check_cutoff
@@ -108,17 +108,36 @@ class KSpaceSolver:
         return self.spec.M
 
     def rebind_cell(self, cell, fixed_M=None):
-        """NPT rebind with the grid pinned (evaluate.py:99-112)."""
+        """Re-plan the mesh for a new cell (evaluate.py:99-112).
+
+        ``fixed_M`` pins the grid counts (the barostat's cheap rebind: the
+        per-cell tables are re-uploaded, no host re-plan).  Without it the
+        grid is re-planned like the reference: ``params.fixed_M`` if the
+        solver was built with one, else the automatic plan from the
+        oversampling factor.  When the counts change the device plan is
+        rebuilt.  The window table and bases persist.  CUDA graphs captured
+        before a rebind refuse to replay (``PlanGraph``)."""
         h = np.asarray(cell.h if hasattr(cell, "h") else cell, dtype=float)
-        if fixed_M is not None and tuple(fixed_M) != tuple(self.spec.M):
-            raise ParameterError("the B200 plan keeps M pinned; build a new solver to re-grid")
         new = Cell(h)
         self.cell_type.validate(new.h)
         check_cutoff(new, self.params.r_c)
-        self.spec = plan_grid(new, self.kern, delta_spread=self.spec.delta_spread,
-                              P=self.spec.P, spread_basis=self.spec.spread_basis,
-                              fixed_M=self.spec.M, window=self.spec.window,
-                              allow_triclinic=self.cell_type is CellType.TRICLINIC)
+        target = fixed_M if fixed_M is not None else self.params.fixed_M
+        spec = plan_grid(new, self.kern, delta_spread=self.spec.delta_spread,
+                         P=self.spec.P, oversampling=self.params.oversampling,
+                         spread_basis=self.spec.spread_basis,
+                         fixed_M=tuple(target) if target is not None else None,
+                         window=self.spec.window,
+                         allow_triclinic=self.cell_type is CellType.TRICLINIC)
+        if tuple(spec.M) != tuple(self.spec.M):
+            old = self.plan
+            self.plan = EspPlan(spec.M, spec.P, spec.window, self.kern.basis, self.params.r_c,
+                                spread=spec.spread_basis, precision=self.params.precision,
+                                deterministic=self.params.deterministic,
+                                capacity=old.capacity)
+            self.plan.generation = old.generation + 1
+            old.generation += 1          # graphs on the old plan are stale
+            old.close()
+        self.spec = spec
         self.cell = new
         self.plan.set_cell(new.h)
 
@@ -277,17 +296,25 @@ class CoulombSolver:
         self.pair_table = build_pair_table(self.kern)
         self.near = NearFieldPlan(self.kern, self.pair_table)
         self.near.set_cell(self.cell)
+        # transform counters (evaluate.py:92): evaluate() counts the forward
+        # transform and the force / local-pressure inverse transforms here
+        self.provider = TransformProvider()
+        self._modes = None
 
     @property
     def spec(self):
         return self.kspace.spec
 
     @property
-    def provider(self):
-        return self.kspace.plan
+    def modes(self):
+        """ModeWorkspace of the current spec and cell (evaluate.py:112)."""
+        if self._modes is None or self._modes._spec is not self.spec:
+            self._modes = ModeWorkspace(self.spec, self.kern, self.cell)
+        return self._modes
 
     def rebind_cell(self, cell, fixed_M=None):
-        """Bases and pair table persist (evaluate.py:99-112)."""
+        """Re-plan for a new cell; bases and pair table persist
+        (evaluate.py:99-112).  ``fixed_M=None`` re-plans the grid counts."""
         self.kspace.rebind_cell(cell, fixed_M)
         self.cell = self.kspace.cell
         self.near.set_cell(self.cell)
@@ -351,7 +378,7 @@ class CoulombSolver:
         with torch.cuda.graph(g):
             body()
         torch.cuda.synchronize()
-        return g, out
+        return PlanGraph(g, [self.kspace.plan, self.near]), out
 
     def evaluate(self, sys, want_forces: bool = True, want_pressure: bool = True,
                  neighbors=None) -> EnergyBreakdown:
@@ -363,6 +390,9 @@ class CoulombSolver:
         pos = _to_device(sys.positions)
         q = _to_device(sys.charges)
         o_far, o_near, stats, F = self.evaluate_device(pos, q, want_forces, neighbors)
+        self.provider.forward_count += 1
+        if want_forces:
+            self.provider.inverse_count += 1 if self.params.force_mode == "analytic" else 3
         st = stats.cpu().numpy()
         NearFieldPlan.check_stats(st)
         e_far, p_far = out7_to_tensor(o_far)
@@ -381,6 +411,10 @@ class CoulombSolver:
 
 
 def _coulomb_local_pressure(self, sys):
+    """Per-particle far-field pressure tensors, prefactored (evaluate.py:147-152):
+    one forward and six inverse transforms."""
+    self.provider.forward_count += 1
+    self.provider.inverse_count += 6
     return self.kspace.local_pressure(sys.positions, sys.charges)
 
 

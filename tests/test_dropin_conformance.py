@@ -1,0 +1,368 @@
+"""Drop-in conformance: the reference's own mesh-pipeline checks
+(``pkg/tests/test_mesh.py:97-307``) run against ``paper_2601_00161_b200``'s
+mirror of ``prolate_ewald.mesh``, through the reference's calling
+conventions — numpy systems in, numpy ``GridField.values`` out ([x][y][z]
+real grids, full [mx][my][mz] spectra), ``TransformProvider`` counters,
+``ModeWorkspace`` host arrays, the reference exception classes.
+
+``/root/reference`` does not exist on the GPU box, so the checks are
+restated here against this package's API; each cites the reference test it
+mirrors.  Mode-sum references come from the oracle's restatement of the
+reference's ``direct_ksum`` (oracle.py:60-106), pinned to the reference's
+own ``direct_ksum`` outputs by the triclinic goldens.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import esp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+_BASES = {}
+
+
+def _basis(delta):
+    from paper_2601_00161_b200 import build_pswf, solve_bandwidth
+    if delta not in _BASES:
+        _BASES[delta] = build_pswf(solve_bandwidth(delta))
+    return _BASES[delta]
+
+
+def _plan(delta, r_c, lengths, P=None, oversampling=2.0):
+    """The reference tests' make_plan (test_mesh.py:20-28) over this package."""
+    from paper_2601_00161_b200 import Cell, SplitKernel, plan_grid
+    _torch()
+    kern = SplitKernel(basis=_basis(delta), r_c=r_c)
+    P = int(np.ceil(-np.log10(delta))) + 1 if P is None else P
+    cell = Cell.orthorhombic(list(lengths))
+    spec = plan_grid(cell, kern, delta_spread=delta, P=P, oversampling=oversampling,
+                     spread_basis=_basis(delta))
+    return cell, kern, spec
+
+
+def _neutral(n, lengths, seed):
+    """conftest.random_neutral_system (alternating charges)."""
+    from paper_2601_00161_b200 import Cell, ParticleSystem
+    rng = np.random.default_rng(seed)
+    lengths = np.asarray(lengths, dtype=float)
+    pos = rng.uniform(0.0, 1.0, (n, 3)) * lengths
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    if n % 2:
+        q = q - q.sum() / n
+    return ParticleSystem(cell=Cell.orthorhombic(lengths), positions=pos, charges=q)
+
+
+def _single(pos, q=1.0, L=6.0):
+    from paper_2601_00161_b200 import Cell, ParticleSystem
+    return ParticleSystem(cell=Cell.orthorhombic([L, L, L]), positions=np.array([pos]),
+                          charges=np.array([q]))
+
+
+def _mode_sum(sys, kern, delta):
+    b = O.build_basis(O.solve_bandwidth(delta))
+    return O.direct_ksum(sys.cell.h, kern.kmax, b, kern.r_c, sys.positions, sys.charges)
+
+
+# -- spreading (test_mesh.py:97-149) -------------------------------------------
+
+
+def test_spread_values_are_numpy_with_p_cubed_support():
+    from paper_2601_00161_b200 import spread_charges
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0])
+    rho = spread_charges(_single([1.234, 2.345, 3.456]), spec)
+    assert isinstance(rho.values, np.ndarray) and rho.values.shape == spec.M
+    assert rho.space == "real"
+    assert np.count_nonzero(rho.values) == spec.P ** 3
+
+
+def test_spread_odd_order_symmetric_about_grid_point():
+    from paper_2601_00161_b200 import spread_charges
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0], P=5)
+    at = [4 * spec.spacing[0], 4 * spec.spacing[1], 4 * spec.spacing[2]]
+    rho = spread_charges(_single(at), spec).values
+    line = rho[2:7, 4, 4]
+    np.testing.assert_allclose(line, line[::-1], rtol=1e-13)
+    assert rho[4, 4, 4] == np.max(rho)
+
+
+def test_spread_linearity():
+    from paper_2601_00161_b200 import ParticleSystem, spread_charges
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0])
+    a = _single([1.1, 2.2, 3.3], q=0.7)
+    b = _single([4.4, 0.5, 5.1], q=-1.3)
+    ab = ParticleSystem(cell=a.cell, positions=np.vstack([a.positions, b.positions]),
+                        charges=np.concatenate([a.charges, b.charges]))
+    np.testing.assert_allclose(spread_charges(ab, spec).values,
+                               spread_charges(a, spec).values + spread_charges(b, spec).values,
+                               atol=1e-15)
+
+
+def test_spread_wraps_across_the_periodic_face():
+    from paper_2601_00161_b200 import spread_charges
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0])
+    rho = spread_charges(_single([0.01, 3.0, 3.0]), spec).values
+    assert np.any(rho[-2:, :, :] != 0.0) and np.any(rho[:2, :, :] != 0.0)
+
+
+def test_spread_total_weight_is_window_transform_at_zero():
+    from paper_2601_00161_b200 import spread_charges
+    cell, kern, spec = _plan(1e-8, 1.0, [6.0, 6.0, 6.0])
+    rho = spread_charges(_single([1.234, 2.345, 3.456]), spec)
+    sb = spec.spread_basis
+    w0 = np.prod([w * sb.lambda0 * sb.psi0_at_zero for w in spec.omega])
+    assert float(rho.values.sum()) * spec.cell_volume_element == pytest.approx(w0, rel=1e-8)
+
+
+# -- transforms (test_mesh.py:152-185) -------------------------------------------
+
+
+def test_forward_density_full_spectrum_zero_mode():
+    from paper_2601_00161_b200 import TransformProvider, forward_density, spread_charges
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0])
+    sys = _neutral(32, [6.0, 6.0, 6.0], 0)
+    rho = spread_charges(sys, spec)
+    rho_hat = forward_density(sys, spec, TransformProvider())
+    assert rho_hat.space == "fourier"
+    assert isinstance(rho_hat.values, np.ndarray) and rho_hat.values.shape == spec.M
+    assert rho_hat.values[0, 0, 0] == pytest.approx(
+        rho.values.sum() * spec.cell_volume_element, rel=1e-12)
+    # the whole spectrum is the reference's: h^3 * fftn of the real grid
+    ref = np.fft.fftn(rho.values) * spec.cell_volume_element
+    assert np.max(np.abs(rho_hat.values - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_energy_and_pressure_ride_on_one_forward_transform():
+    from paper_2601_00161_b200 import (TransformProvider, forward_density, long_range_energy,
+                                       long_range_pressure)
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0])
+    sys = _neutral(32, [6.0, 6.0, 6.0], 1)
+    prov = TransformProvider()
+    rho_hat = forward_density(sys, spec, prov)
+    long_range_energy(rho_hat, kern, spec, cell)
+    long_range_pressure(rho_hat, kern, spec, cell)
+    assert (prov.forward_count, prov.inverse_count) == (1, 0)
+
+
+def test_real_space_field_rejected_everywhere():
+    from paper_2601_00161_b200 import (MeshError, local_pressure, long_range_energy,
+                                       long_range_forces, long_range_pressure, spread_charges)
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0])
+    sys = _neutral(8, [6.0, 6.0, 6.0], 2)
+    rho = spread_charges(sys, spec)
+    for call in (lambda: long_range_energy(rho, kern, spec, cell),
+                 lambda: long_range_pressure(rho, kern, spec, cell),
+                 lambda: long_range_forces(rho, sys, kern, spec, cell),
+                 lambda: local_pressure(rho, sys, kern, spec, cell)):
+        with pytest.raises(MeshError):
+            call()
+
+
+# -- long range (test_mesh.py:188-265) -------------------------------------------
+
+
+def _setup(delta=1e-5, seed=0, lengths=(6.0, 6.0, 6.0), n=32):
+    from paper_2601_00161_b200 import TransformProvider, forward_density
+    cell, kern, spec = _plan(delta, 1.2, list(lengths))
+    sys = _neutral(n, list(lengths), seed)
+    prov = TransformProvider()
+    return cell, kern, spec, sys, prov, forward_density(sys, spec, prov)
+
+
+def test_energy_matches_mode_sum():
+    from paper_2601_00161_b200 import long_range_energy
+    cell, kern, spec, sys, prov, rho_hat = _setup()
+    e_ref, _, _ = _mode_sum(sys, kern, 1e-5)
+    assert long_range_energy(rho_hat, kern, spec, cell) == pytest.approx(e_ref, rel=1e-5)
+
+
+def test_forces_match_mode_sum_numpy_out():
+    from paper_2601_00161_b200 import long_range_forces
+    cell, kern, spec, sys, prov, rho_hat = _setup(seed=3)
+    _, f_ref, _ = _mode_sum(sys, kern, 1e-5)
+    f = long_range_forces(rho_hat, sys, kern, spec, cell, provider=prov)
+    assert isinstance(f, np.ndarray) and f.shape == (sys.n, 3)
+    assert np.linalg.norm(f - f_ref) / np.linalg.norm(f_ref) < 1e-5
+    assert (prov.forward_count, prov.inverse_count) == (1, 3)
+
+
+def test_pressure_matches_mode_sum():
+    from paper_2601_00161_b200 import long_range_pressure
+    cell, kern, spec, sys, prov, rho_hat = _setup(seed=4, lengths=(5.0, 6.0, 7.0))
+    _, _, p_ref = _mode_sum(sys, kern, 1e-5)
+    p = long_range_pressure(rho_hat, kern, spec, cell)
+    assert np.linalg.norm(p - p_ref) / np.linalg.norm(p_ref) < 1e-4
+
+
+def test_ik_forces_conserve_momentum():
+    from paper_2601_00161_b200 import long_range_forces
+    cell, kern, spec, sys, prov, rho_hat = _setup(seed=5)
+    f = long_range_forces(rho_hat, sys, kern, spec, cell, mode="ik", provider=prov)
+    assert np.linalg.norm(f.sum(axis=0)) < 1e-10 * np.linalg.norm(f, axis=1).max()
+
+
+def test_analytic_forces_are_the_mesh_energy_gradient():
+    from paper_2601_00161_b200 import (ModeWorkspace, ParticleSystem, forward_density,
+                                       long_range_energy, long_range_forces)
+    cell, kern, spec, sys, prov, rho_hat = _setup(delta=1e-6, seed=6, n=8)
+    f = long_range_forces(rho_hat, sys, kern, spec, cell, mode="analytic", provider=prov)
+    modes = ModeWorkspace(spec, kern, cell)
+
+    def energy(positions):
+        probe = ParticleSystem(cell=cell, positions=positions, charges=sys.charges)
+        return long_range_energy(forward_density(probe, spec, prov), kern, spec, cell,
+                                 modes=modes)
+
+    step = 1e-6
+    for idx in np.random.default_rng(1).choice(sys.n, size=3, replace=False):
+        for axis in range(3):
+            num = 0.0
+            for sign, coef in ((1, 8.0), (-1, -8.0), (2, -1.0), (-2, 1.0)):
+                pos = sys.positions.copy()
+                pos[idx, axis] += sign * step
+                num += coef * energy(pos)
+            assert f[idx, axis] == pytest.approx(-num / (12.0 * step), abs=1e-5)
+
+
+def test_unknown_force_mode_rejected():
+    from paper_2601_00161_b200 import MeshError, long_range_forces
+    cell, kern, spec, sys, prov, rho_hat = _setup(n=8)
+    with pytest.raises(MeshError):
+        long_range_forces(rho_hat, sys, kern, spec, cell, mode="spline")
+
+
+def test_virial_trace_identity_on_full_spectrum():
+    from paper_2601_00161_b200 import ModeWorkspace, long_range_pressure
+    cell, kern, spec, sys, prov, rho_hat = _setup(seed=7)
+    m = ModeWorkspace(spec, kern, cell)
+    p = long_range_pressure(rho_hat, kern, spec, cell, modes=m)
+    amp2 = np.abs(rho_hat.values[m.mask]) ** 2
+    scaled = m.w_inv2 * amp2 / (2.0 * m.volume ** 2)
+    assert np.trace(p) == pytest.approx(float(np.sum((m.fhat + m.dterm * m.k2) * scaled)),
+                                        rel=1e-12)
+
+
+# -- local pressure (test_mesh.py:268-307) ---------------------------------------
+
+
+def test_local_pressure_zero_charges():
+    from paper_2601_00161_b200 import (ParticleSystem, TransformProvider, forward_density,
+                                       local_pressure)
+    cell, kern, spec = _plan(1e-4, 1.0, [6.0, 6.0, 6.0])
+    sys = ParticleSystem(cell=cell, positions=np.random.default_rng(0).uniform(0, 6, (16, 3)),
+                         charges=np.zeros(16))
+    rho_hat = forward_density(sys, spec, TransformProvider())
+    assert np.all(local_pressure(rho_hat, sys, kern, spec, cell) == 0.0)
+
+
+def test_local_pressure_sums_to_global():
+    from paper_2601_00161_b200 import (TransformProvider, forward_density, local_pressure,
+                                       long_range_pressure)
+    cell, kern, spec = _plan(1e-5, 1.2, [6.0, 7.0, 8.0])
+    sys = _neutral(48, [6.0, 7.0, 8.0], 9)
+    rho_hat = forward_density(sys, spec, TransformProvider())
+    total = local_pressure(rho_hat, sys, kern, spec, cell).sum(axis=0)
+    glob = long_range_pressure(rho_hat, kern, spec, cell)
+    assert np.linalg.norm(total - glob) < 1e-8 * max(np.linalg.norm(glob), 1e-30)
+
+
+def test_local_pressure_mirror_pair_equal_and_symmetric():
+    from paper_2601_00161_b200 import (ParticleSystem, TransformProvider, forward_density,
+                                       local_pressure)
+    cell, kern, spec = _plan(1e-5, 1.2, [6.0, 6.0, 6.0])
+    sys = ParticleSystem(cell=cell, positions=np.array([[2.25, 3.0, 3.0], [3.75, 3.0, 3.0]]),
+                         charges=np.array([1.0, 1.0]))
+    t = local_pressure(forward_density(sys, spec, TransformProvider()), sys, kern, spec, cell)
+    np.testing.assert_allclose(t[0], t[1], rtol=1e-10, atol=1e-14)
+    cell, kern, spec = _plan(1e-4, 1.1, [6.0, 6.0, 6.0])
+    sys = _neutral(16, [6.0, 6.0, 6.0], 10)
+    t = local_pressure(forward_density(sys, spec, TransformProvider()), sys, kern, spec, cell)
+    np.testing.assert_array_equal(t, np.swapaxes(t, 1, 2))
+
+
+# -- drop-in semantics the reference relies on -------------------------------------
+
+
+def test_user_built_spectrum_and_mutated_positions():
+    """A GridField built from a numpy spectrum (the reference's dataclass
+    constructor) is uploaded; positions mutated in place are re-binned
+    before the gather (no stale bins)."""
+    from paper_2601_00161_b200 import (GridField, TransformProvider, forward_density,
+                                       long_range_energy, long_range_forces)
+    cell, kern, spec, sys, prov, rho_hat = _setup(seed=11)
+    e = long_range_energy(rho_hat, kern, spec, cell)
+    copy = GridField(values=np.array(rho_hat.values), spec=spec, space="fourier")
+    assert long_range_energy(copy, kern, spec, cell) == pytest.approx(e, rel=1e-13)
+    f0 = long_range_forces(rho_hat, sys, kern, spec, cell)
+    sys.positions[:] = sys.positions[::-1].copy()         # in place: same object
+    sys.charges[:] = sys.charges[::-1].copy()
+    f1 = long_range_forces(forward_density(sys, spec, TransformProvider()), sys, kern, spec,
+                           cell)
+    np.testing.assert_allclose(f1, f0[::-1], rtol=1e-9, atol=1e-12 * np.abs(f0).max())
+
+
+def test_device_inputs_keep_results_on_the_device():
+    torch = _torch()
+    from paper_2601_00161_b200 import (ParticleSystem, TransformProvider, forward_density,
+                                       long_range_forces)
+    cell, kern, spec, sys, prov, rho_hat = _setup(seed=12)
+    dsys = ParticleSystem.__new__(ParticleSystem)
+    object.__setattr__(dsys, "cell", sys.cell)
+    object.__setattr__(dsys, "positions", torch.as_tensor(sys.positions, device="cuda"))
+    object.__setattr__(dsys, "charges", torch.as_tensor(sys.charges, device="cuda"))
+    d_hat = forward_density(dsys, spec, TransformProvider())
+    assert isinstance(d_hat.values, torch.Tensor) and d_hat.values.is_cuda
+    fd = long_range_forces(d_hat, dsys, kern, spec, cell)
+    assert isinstance(fd, torch.Tensor) and fd.is_cuda
+    fh = long_range_forces(rho_hat, sys, kern, spec, cell)
+    np.testing.assert_array_equal(fd.cpu().numpy(), fh)
+
+
+def test_coulomb_solver_provider_and_replanning_rebind():
+    """CoulombSolver.provider is a TransformProvider counting the step's
+    transforms; rebind_cell(cell) re-plans M like evaluate.py:99-112, and
+    rebind_cell(cell, fixed_M) pins it."""
+    _torch()
+    from paper_2601_00161_b200 import Cell, CoulombSolver, EwaldParameters, TransformProvider
+    sys = _neutral(64, [12.0, 12.0, 12.0], 13)
+    s = CoulombSolver(sys.cell, EwaldParameters(r_c=4.0, delta_split=1e-5))
+    assert isinstance(s.provider, TransformProvider)
+    s.evaluate(sys)
+    assert (s.provider.forward_count, s.provider.inverse_count) == (1, 3)
+    s.evaluate(sys, want_forces=False)
+    assert (s.provider.forward_count, s.provider.inverse_count) == (2, 3)
+    M0 = s.spec.M
+    big = Cell.orthorhombic([15.0, 15.0, 15.0])
+    s.rebind_cell(big)
+    fresh = CoulombSolver(big, EwaldParameters(r_c=4.0, delta_split=1e-5))
+    assert s.spec.M == fresh.spec.M != M0
+    s.rebind_cell(Cell.orthorhombic([15.3, 15.3, 15.3]), fixed_M=s.spec.M)
+    assert s.spec.M == fresh.spec.M
+    assert s.modes.mask.shape == s.spec.M
+
+
+def test_graph_refuses_replay_after_rebind():
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver, ParameterError
+    sys = _neutral(64, [12.0, 12.0, 12.0], 14)
+    s = KSpaceSolver(sys.cell.h, EwaldParameters(r_c=4.0, delta_split=1e-5))
+    P_ = torch.as_tensor(sys.positions, device="cuda")
+    Q_ = torch.as_tensor(sys.charges, device="cuda")
+    g, o7, F = s.graphed(P_, Q_)
+    g.replay()
+    s.rebind_cell(np.diag([12.2, 12.2, 12.2]), fixed_M=s.spec.M)
+    with pytest.raises(ParameterError):
+        g.replay()
+    g2, o7b, Fb = s.graphed(P_, Q_)
+    g2.replay()
+    r = s.evaluate(P_, Q_)
+    torch.cuda.synchronize()
+    assert torch.equal(Fb, r.forces)

@@ -71,10 +71,15 @@ def test_config4_full_size_against_reference(cfg4, precision, tol):
     assert O.rel_scalar(E, float(g["E"])) <= tol
     assert O.rel_frobenius(Pt, g["Pt"]) <= tol
     assert O.rms_rel_forces(Fs, g["F_sel"]) <= tol
-    # momentum over all 8.1M charges (ik forces conserve it, test_mesh.py:218-222)
+    # momentum over all 8.1M charges (ik forces conserve it, test_mesh.py:218-222);
+    # fp32 fields: the residual is a random walk of fp32 roundings, so it is
+    # bounded against sqrt(N) x rms|F|
     Fn = F.cpu().numpy()
-    assert np.linalg.norm(Fn.sum(axis=0)) < 1e-9 * np.linalg.norm(Fn, axis=1).max() * (
-        1.0 if precision == "fp64" else 1e4)
+    net = np.linalg.norm(Fn.sum(axis=0))
+    if precision == "fp64":
+        assert net < 1e-9 * np.linalg.norm(Fn, axis=1).max()
+    else:
+        assert net < 1e-5 * np.sqrt(w.n) * np.sqrt(np.mean(np.sum(Fn * Fn, axis=1)))
     del s, F
 
 
