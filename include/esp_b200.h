@@ -180,7 +180,14 @@ int esp_reset_counters(esp_plan* plan);
 /* Device pointers into the plan (valid until destroy / next set_cell).     */
 void* esp_grid_ptr(esp_plan* plan);       /* real grid, [z][y][x]          */
 void* esp_spectrum_ptr(esp_plan* plan);   /* complex half spectrum          */
-void* esp_fields_ptr(esp_plan* plan);     /* 3 ik force fields, [3][z][y][x] */
+void* esp_fields_ptr(esp_plan* plan);     /* 3 ik force fields (layout below) */
+/* Layout of the fields behind esp_fields_ptr after the last force step:
+ * {origin offset, row pitch, rows per plane, planes, component stride} in
+ * elements; field c at (x, y, z) is ptr[origin + c*cstride + (z*rows + y)*pitch
+ * + x].  The band-pruned ik path of fp64 plans writes ghost-padded fields
+ * (periodic images around the grid, read by the TMA gather); other paths
+ * write the dense [3][z][y][x] grid (origin 0, pitch Mx). */
+int esp_fields_layout(const esp_plan* plan, int64_t* layout5);
 int esp_grid_info(const esp_plan* plan, int64_t* info8);
 /* 1 in *radix when a step over n charges bins with the device radix sort
  * (n >= the plan's sort threshold; ESP_SORT_THRESHOLD at plan creation

@@ -152,6 +152,7 @@ def lib():
     L.esp_spectrum_ptr.restype = vp
     L.esp_fields_ptr.argtypes = [vp]
     L.esp_fields_ptr.restype = vp
+    L.esp_fields_layout.argtypes = [vp, C.POINTER(C.c_int64)]
     L.esp_grid_info.argtypes = [vp, C.POINTER(C.c_int64)]
     L.esp_binning_radix.argtypes = [vp, C.c_int64, C.POINTER(C.c_int32)]
     L.esp_fft_path.argtypes = [vp]
@@ -192,7 +193,7 @@ EXPORTED = [
     "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
     "esp_binning_radix",
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
-    "esp_gather_fields", "esp_fields_ptr", "esp_fft_path",
+    "esp_gather_fields", "esp_fields_ptr", "esp_fields_layout", "esp_fft_path",
     "esp_slab_layout", "esp_slab_forward", "esp_slab_reduce", "esp_slab_inverse",
     "esp_near_create", "esp_near_destroy", "esp_near_reserve", "esp_near_set_cell",
     "esp_near_evaluate", "esp_near_evaluate_local", "esp_near_evaluate_pairs", "esp_near_info", "esp_near_build_pairs",

@@ -85,7 +85,7 @@ static void free_all(esp_plan* p) {
                   p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
                   p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt,
                   p->d_wrec,     p->d_pk,       p->d_drec,    p->d_err_out7,
-                  p->d_sort_tmp, p->d_partials_fft};
+                  p->d_sort_tmp, p->d_partials_fft, p->d_fpad};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   esp_fused_fft_destroy(p->fused);
@@ -470,6 +470,20 @@ int esp_plan_set_cell(esp_plan* p, const esp_cell_desc* c, void* stream) {
     }
     if (!keep && want && p->Mu[2] == p->M[2] && p->zshift == 0) {
       p->fused = esp_fused_fft_create(p);
+      // ghost-padded ik fields + tensor map for the TMA gather (grids whose
+      // inverse x pass is k_x_c2r: not the small square plane kernels)
+      const bool plane_grid = p->M[0] == p->M[1] &&
+                              (p->M[0] == 32 || p->M[0] == 48 || p->M[0] == 64);
+      if (p->fused && !p->d_fpad && !plane_grid && esp::tma_gather_eligible(p)) {
+        p->fpad = esp::make_field_pad(p);
+        const size_t fb = sizeof(double) * 3 * (size_t)p->fpad.cstride;
+        ESP_CUDA(cudaMalloc(&p->d_fpad, fb));
+        ESP_CUDA(cudaMemset(p->d_fpad, 0, fb));
+        if (esp::make_field_tmap(p) != cudaSuccess) {   // no TMA: the cp.async gather
+          cudaFree(p->d_fpad);
+          p->d_fpad = nullptr;
+        }
+      }
       if (p->fused) {
         p->n_red_blocks_fft = esp::fused_reduce_blocks(p);
         const long long nb = p->n_red_blocks_fft, ng = (nb + 31) / 32;
@@ -604,6 +618,7 @@ int esp_forces_ik(esp_plan* p, double* d_forces, void* stream) {
     ESP_CUFFT(cufftExecC2R(p->inv3, (cufftComplex*)p->d_ikspec, (cufftReal*)p->d_fields));
   }
   esp::prof_mark(p, s, "fft_inverse_x3");
+  p->fpad_written = 0;
   p->inv_count += 3;
   p->have_ik = 0;  // the C2R transform overwrites its input
   if (p->last_n > 0) ESP_CUDA(esp::launch_gather_ik(p, d_forces, s));
@@ -642,6 +657,7 @@ int esp_forces_analytic(esp_plan* p, double* d_forces, void* stream) {
   } else {
     ESP_CUFFT(cufftExecC2R(p->inv1, (cufftComplex*)p->d_ikspec, (cufftReal*)p->d_fields));
   }
+  p->fpad_written = 0;
   esp::prof_mark(p, s, "fft_inverse_x1");
   p->inv_count += 1;
   p->have_ik = 0;
@@ -669,6 +685,7 @@ int esp_local_pressure(esp_plan* p, double* d_tensors, void* stream) {
     } else {
       ESP_CUFFT(cufftExecC2R(p->inv3, (cufftComplex*)p->d_ikspec, (cufftReal*)p->d_fields));
     }
+    p->fpad_written = 0;
     p->inv_count += 3;
     if (p->last_n > 0) ESP_CUDA(esp::launch_gather_ik(p, d_tensors, s, nullptr, maps[half]));
   }
@@ -702,8 +719,9 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
     if (want_f) {
       p->inv_count += analytic ? 1 : 3;
       if (p->last_n > 0)
-        ESP_CUDA(analytic ? esp::launch_gather_grad(p, d_forces, s0)
-                          : esp::launch_gather_ik(p, d_forces, s0));
+        ESP_CUDA(analytic          ? esp::launch_gather_grad(p, d_forces, s0)
+                 : p->fpad_written ? esp::launch_gather_tma(p, d_forces, s0)
+                                   : esp::launch_gather_ik(p, d_forces, s0));
     }
     return ESP_OK;
   }
@@ -783,7 +801,29 @@ int esp_profile_read(esp_plan* p, char* names, int32_t names_len, double* ms, in
 
 void* esp_grid_ptr(esp_plan* p) { return p ? p->d_grid : nullptr; }
 void* esp_spectrum_ptr(esp_plan* p) { return p ? p->d_spec : nullptr; }
-void* esp_fields_ptr(esp_plan* p) { return p ? p->d_fields : nullptr; }
+void* esp_fields_ptr(esp_plan* p) {
+  if (!p) return nullptr;
+  return p->fpad_written ? p->d_fpad : p->d_fields;
+}
+
+int esp_fields_layout(const esp_plan* p, int64_t* layout5) {
+  if (!p || !layout5) return ESP_ERR_PARAM;
+  if (p->fpad_written) {
+    const esp::FieldPad& f = p->fpad;
+    layout5[0] = ((long long)f.S[2] * f.E[1] + f.S[1]) * f.E[0] + f.S[0];
+    layout5[1] = f.E[0];
+    layout5[2] = f.E[1];
+    layout5[3] = f.E[2];
+    layout5[4] = f.cstride;
+  } else {
+    layout5[0] = 0;
+    layout5[1] = p->M[0];
+    layout5[2] = p->M[1];
+    layout5[3] = p->M[2];
+    layout5[4] = p->G;
+  }
+  return ESP_OK;
+}
 
 int esp_fft_path(const esp_plan* p) { return p && p->fused ? 1 : 0; }
 

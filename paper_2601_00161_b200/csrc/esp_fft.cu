@@ -778,10 +778,58 @@ k_y_inv(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __res
 // (zero-padded to the half spectrum; kx = 0 and Nyquist taken as real, as a
 // C2R transform does).  Each in-band column is read once and placed at k and
 // N - k (conjugate-symmetric extension).
+// Ghost-padded field rows (esp_gather_tma.cu): row `ra` = (c*Mz + z)*My + y
+// of the fields lands at up to 4 padded rows (its y and z periodic images);
+// the CTA precomputes their base offsets once, so each element store is one
+// add (plus its x image near the row ends).
+__host__ __device__ constexpr int pad_rows_smem(int PP) { return 2 * PP; }
+
+struct PadRows {
+  long long base[4];
+  int n;
+};
+
+__device__ __forceinline__ PadRows pad_rows(const FieldPad& f, int ra) {
+  const int My = f.M[1], Mz = f.M[2];
+  const int c = ra / (My * Mz);
+  const int rem = ra - c * My * Mz;
+  const int z = rem / My, y = rem - z * My;
+  int ys[2], zs[2], ny = 0, nz = 0;
+  ys[ny++] = y + f.S[1];
+  if (y + f.S[1] + My < f.E[1]) ys[ny++] = y + f.S[1] + My;
+  else if (y + f.S[1] - My >= 0) ys[ny++] = y + f.S[1] - My;
+  zs[nz++] = z + f.S[2];
+  if (z + f.S[2] + Mz < f.E[2]) zs[nz++] = z + f.S[2] + Mz;
+  else if (z + f.S[2] - Mz >= 0) zs[nz++] = z + f.S[2] - Mz;
+  PadRows r;
+  r.n = 0;
+  for (int a = 0; a < nz; ++a)
+    for (int b = 0; b < ny; ++b)
+      r.base[r.n++] = (long long)c * f.cstride + ((long long)zs[a] * f.E[1] + ys[b]) * f.E[0] +
+                      f.S[0];
+  return r;
+}
+
+template <typename real>
+__device__ __forceinline__ void store_padded(const FieldPad& f, const PadRows& r,
+                                             real* __restrict__ fld, int x, real v) {
+  const int Mx = f.M[0];
+  const int xi = x + f.S[0] + Mx < f.E[0] ? Mx : (x + f.S[0] - Mx >= 0 ? -Mx : 0);
+  __stcs(fld + r.base[0] + x, v);
+  if (xi) __stcs(fld + r.base[0] + x + xi, v);
+  if (r.n > 1) {                          // y / z ghost rows (a few rows per plane)
+    for (int k = 1; k < r.n; ++k) {
+      __stcs(fld + r.base[k] + x, v);
+      if (xi) __stcs(fld + r.base[k] + x + xi, v);
+    }
+  }
+}
+
 template <typename real, int N>
 __global__ void __launch_bounds__(kThreadsX, 6)
 k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
-        const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx) {
+        const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx,
+        FieldPad pad) {
   using C = typename Cx<real>::t;
   constexpr int PP = pairs_x(N), LP = pitch(N), NT = kThreadsX;
   constexpr int half = N / 2, NH = half + 1;
@@ -821,6 +869,9 @@ k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
       }
     }
   }
+  __shared__ PadRows s_rows[pad_rows_smem(PP)];
+  if (pad.enabled && threadIdx.x < 2 * PP && r0 + threadIdx.x < nrows)
+    s_rows[threadIdx.x] = pad_rows(pad, (int)(r0 + threadIdx.x));
   __syncthreads();
   fft_ip<N, 1, PP, NT, +1>(buf, tw);
   constexpr int nld = (PP * N + NT - 1) / NT;
@@ -831,8 +882,13 @@ k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
       const int l = e / N, i = e - l * N;
       const long long ra = r0 + 2 * l;
       const C z = buf[l * LP + pidx(i)];
-      if (ra < nrows) __stcs(fld + ra * N + i, z.x);
-      if (ra + 1 < nrows) __stcs(fld + (ra + 1) * N + i, z.y);
+      if (pad.enabled) {
+        if (ra < nrows) store_padded(pad, s_rows[2 * l], fld, i, z.x);
+        if (ra + 1 < nrows) store_padded(pad, s_rows[2 * l + 1], fld, i, z.y);
+      } else {
+        if (ra < nrows) __stcs(fld + ra * N + i, z.x);
+        if (ra + 1 < nrows) __stcs(fld + (ra + 1) * N + i, z.y);
+      }
     }
   }
 }
@@ -1077,14 +1133,15 @@ static cudaError_t launch_y_inv(const esp_plan* p, const void* in, void* out, co
 
 template <typename real, int N>
 static cudaError_t launch_x_c2r(const esp_plan* p, const void* in, void* fld, const void* tw,
-                                int ldx, int nz, cudaStream_t s, int ncomp = 3) {
+                                int ldx, int nz, cudaStream_t s, int ncomp = 3,
+                                FieldPad pad = FieldPad{}) {
   using C = typename Cx<real>::t;
   constexpr int PP = pairs_x(N);
   const long long nrows = (long long)ncomp * p->M[1] * nz;
   const long long nblk = (nrows + 2 * PP - 1) / (2 * PP);
   k_x_c2r<real, N><<<(unsigned)nblk, kThreadsX, 0, s>>>(
       reinterpret_cast<const C*>(in), reinterpret_cast<real*>(fld),
-      reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx);
+      reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx, pad);
   return cudaGetLastError();
 }
 
@@ -1345,10 +1402,15 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   p->launches++;
   prof_mark(p, s, "ifft_y");
   if ((e = debug_check(s, "ifft_y")) != cudaSuccess) return e;
+  // ik fields of a TMA-gather plan go straight into the ghost-padded layout
+  const bool padded = ncomp == 3 && p->d_fpad != nullptr;
+  p->fpad_written = padded ? 1 : 0;
+  void* fdst = padded ? p->d_fpad : p->d_fields;
+  const FieldPad pad = padded ? p->fpad : FieldPad{};
   e = cudaErrorInvalidValue;
   switch (p->M[0]) {
 #define ESP_CASE(v) \
-  case v: e = launch_x_c2r<real, v>(p, f->bufD, p->d_fields, f->tw[0], ldx, p->M[2], s, ncomp); \
+  case v: e = launch_x_c2r<real, v>(p, f->bufD, fdst, f->tw[0], ldx, p->M[2], s, ncomp, pad); \
     break;
     ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE

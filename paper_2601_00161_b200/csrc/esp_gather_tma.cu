@@ -1,0 +1,374 @@
+// esp_gather_tma.cu — persistent, TMA-fed ik force gather (mesh.py:213-218
+// `_gather` for the three ik fields of long_range_forces, mesh.py:336-342).
+//
+// Production gather for fp64, P <= 8, on the band-pruned transform path.
+//
+// * Fields: the inverse x pass (k_x_c2r) writes the three ik fields into a
+//   ghost-padded array [3][E2][E1][E0] whose ghost planes/rows/columns hold
+//   the periodic images, so every anchor tile's stencil box is one dense,
+//   in-bounds box: one cp.async.bulk.tensor (TMA) per field, completing on
+//   an mbarrier.  TMA boxes must start on a 16-byte boundary along x, so the
+//   box is 18 columns wide from the even column at or below the tile's first
+//   column (tiles are 17 - P = 9 anchors wide: every other tile starts odd).
+// * Persistent CTAs (one per SM): a producer warp streams tile boxes into a
+//   2-stage ring (full/empty mbarriers); NW consumer warps gather while the
+//   next tile lands.  Tiles are visited z-slab-major so neighbouring tiles'
+//   halo boxes are served from L2.
+// * Weights are evaluated in the kernel from the binned grid coordinates u
+//   (the same unrolled Horner chains as the binning pass, coefficients from
+//   the constant bank; no 192 B/charge weight records): a warp takes its
+//   particles in batches of 10, lane (particle, axis) evaluates one axis's
+//   weights into a per-warp shared-memory slot, then the batch is gathered
+//   two particles at a time.
+// * Warp = 2 particles x 8 stencil rows x 2 x-parities.  Lane (p, j, e)
+//   sums row y = yl + j, columns x = xl + e + 2i (i < 4), over the 8 planes.
+//   Rows of 18 doubles (144 B) put row j at bank offset 2j, so the 16 lanes
+//   of a particle (2j + e) hit 16 distinct 8-byte bank pairs for every load:
+//   conflict-free without a swizzle.
+//   The 16 lanes reduce with 4 xor-shuffle levels; one lane writes the
+//   force.  No atomics, fixed order: bitwise reproducible.
+//
+// F_c = -q * sum (the h3 factors of mesh.py:341-342 cancel; the 1/G of the
+// inverse transform is folded into the spectrum).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "esp_internal.cuh"
+
+namespace esp {
+
+namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred done;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+      "@!done bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+
+constexpr int kTmaStages = 2;
+
+template <int NW>
+struct TmaGatherLayout {
+  static constexpr int kBatch = NW > 12 ? 6 : (NW > 8 ? 8 : 10);   // particles per warp batch
+  static constexpr int kWarpW = kBatch * 24 + kBatch + 2 * kBatch;   // weights, q, anchors+ids (8 B slots)
+  static constexpr int kRow = 18;         // box columns (16 needed + alignment slack)
+  __host__ __device__ static size_t box_elems(int PZ) { return (size_t)kRow * 16 * PZ; }
+  __host__ __device__ static size_t bytes(int PZ) {
+    size_t b = 1024;                                          // alignment slack
+    b += sizeof(double) * 3 * box_elems(PZ) * kTmaStages;     // field boxes
+    b += sizeof(double) * (size_t)NW * kWarpW;                // weight slots
+    b += sizeof(uint64_t) * 2 * kTmaStages;                   // full / empty barriers
+    return b;
+  }
+};
+
+template <int P, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
+             const double* __restrict__ tab, const double* __restrict__ brk, int n_pieces,
+             int ncoef, const int* __restrict__ offsets, const double* __restrict__ U,
+             long long cap, const double* __restrict__ Q, const int* __restrict__ IDX,
+             double* __restrict__ forces, int xsh) {
+  static_assert(P <= 8, "the TMA gather covers stencils of at most 8 points");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1 KB-aligned base; offset arithmetic on smem_raw keeps the shared state
+  // space visible to the compiler (LDS/STS instead of generic accesses)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const size_t box = TmaGatherLayout<NW>::box_elems(g.PZ);
+  double* fbuf = reinterpret_cast<double*>(base);
+  double* wslot = fbuf + 3 * box * kTmaStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wslot + NW * TmaGatherLayout<NW>::kWarpW);
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int nxy = g.ntx * g.nty;
+  const int ntiles = nxy * g.ntz;
+  const unsigned box_bytes = (unsigned)(sizeof(double) * box);
+
+  if (warp == NW) {                       // producer: one elected lane issues the TMA
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int tz = t / nxy, txy = t - tz * nxy;
+        const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+        const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+        if (offsets[key0] == offsets[key1]) continue;
+        const int s = it % kTmaStages;
+        if (it >= kTmaStages) mbar_wait(&empty[s], ((it / kTmaStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], 3 * box_bytes);
+        const int tx = txy % g.ntx, ty = txy / g.ntx;
+        double* dst = fbuf + (size_t)s * 3 * box;
+        const int bx = (tx * g.TX + xsh) & ~1;   // TMA boxes start 16-byte aligned
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          tma_load_4d(dst + c * box, &tmap, &full[s], bx, ty * g.TY, tz * g.TZ, c);
+        ++it;
+      }
+    }
+    return;
+  }
+
+  const int p = lane >> 4, sub = lane & 15;
+  const int j = sub >> 1, e = sub & 1;
+  constexpr int R = TmaGatherLayout<NW>::kRow;
+  constexpr int KB = TmaGatherLayout<NW>::kBatch;
+  double* Wb = wslot + warp * TmaGatherLayout<NW>::kWarpW;        // [KB][3][8] weights
+  double* s_qv = Wb + KB * 24;                                     // [KB] charges
+  int* s_ai = reinterpret_cast<int*>(s_qv + KB);                   // [KB][3] anchors, [KB] ids
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int tz = t / nxy, txy = t - tz * nxy;
+    const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+    const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+    const long long p0 = offsets[key0], p1 = offsets[key1];
+    if (p0 == p1) continue;
+    const int tx = txy % g.ntx, ty = txy / g.ntx;
+    // box-local column of grid anchor a: a + xsh - (box start)
+    const int org0 = ((tx * g.TX + xsh) & ~1) - xsh, org1 = ty * g.TY, org2 = tz * g.TZ;
+    const int s = it % kTmaStages;
+    // rotate the batch order per tile so no warp always takes the extra batch
+    const int wr = (warp + it) % NW;
+    bool waited = false;
+    const double* F = fbuf + (size_t)s * 3 * box;
+    for (long long bb = p0 + (long long)wr * KB; bb < p1; bb += (long long)NW * KB) {
+      const int nb = (int)min((long long)KB, p1 - bb);
+      // batch prologue (overlaps the tile's TMA on the first batch): lane
+      // (particle, dim) evaluates the 8 weights of one axis with the unrolled
+      // Horner chains of the binning pass (uniform table reads) and the
+      // box-local anchor
+      if (lane < 3 * KB) {
+        const int pl = lane / 3, d = lane - 3 * pl;
+        if (pl < nb) {
+          const double u = U[d * cap + bb + pl];
+          const double base = anchor_base(g, u);
+          double w[P];
+          stencil_weights<double, P>(ft, tab, brk, n_pieces, ncoef, u, base, g.lo, 1.0, w);
+#pragma unroll
+          for (int ss = 0; ss < 8; ++ss) Wb[pl * 24 + d * 8 + ss] = ss < P ? w[ss < P ? ss : 0] : 0.0;
+          s_ai[pl * 3 + d] = local_anchor(g, d, base) - (d == 0 ? org0 : (d == 1 ? org1 : org2));
+          if (d == 0) {
+            s_qv[pl] = Q[bb + pl];
+            s_ai[3 * KB + pl] = IDX[bb + pl];
+          }
+        }
+      }
+      __syncwarp();
+      if (!waited) {
+        mbar_wait(&full[s], (it / kTmaStages) & 1);
+        waited = true;
+      }
+      for (int pp = 0; pp < nb; pp += 2) {
+        const int pl = pp + p;
+        const bool live = pl < nb;
+        double ax = 0.0, ay = 0.0, az = 0.0;
+        if (live && j < P) {
+          const double* W = Wb + pl * 24;
+          const int xl = s_ai[pl * 3], yl = s_ai[pl * 3 + 1], zl = s_ai[pl * 3 + 2];
+          const double wy = W[8 + j];
+          double wx[4], wz[P];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) wx[i] = (e + 2 * i < P) ? W[e + 2 * i] : 0.0;
+#pragma unroll
+          for (int k = 0; k < P; ++k) wz[k] = W[16 + k];
+          const int row = (zl * 16 + yl + j) * R;
+          const double* col[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) col[i] = F + row + min(xl + e + 2 * i, R - 1);
+          double bx[2] = {0.0, 0.0}, by[2] = {0.0, 0.0}, bz[2] = {0.0, 0.0};
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            double rx[2] = {0.0, 0.0}, ry[2] = {0.0, 0.0}, rz[2] = {0.0, 0.0};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (2 * i < P) {                      // e + 2i < P is folded into wx
+                const double* a = col[i] + k * 16 * R;
+                rx[i & 1] = fma(wx[i], a[0], rx[i & 1]);
+                ry[i & 1] = fma(wx[i], a[box], ry[i & 1]);
+                rz[i & 1] = fma(wx[i], a[2 * box], rz[i & 1]);
+              }
+            }
+            bx[k & 1] = fma(wz[k], rx[0] + rx[1], bx[k & 1]);
+            by[k & 1] = fma(wz[k], ry[0] + ry[1], by[k & 1]);
+            bz[k & 1] = fma(wz[k], rz[0] + rz[1], bz[k & 1]);
+          }
+          ax = (bx[0] + bx[1]) * wy;
+          ay = (by[0] + by[1]) * wy;
+          az = (bz[0] + bz[1]) * wy;
+        }
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+          ax += __shfl_xor_sync(0xffffffffu, ax, o);
+          ay += __shfl_xor_sync(0xffffffffu, ay, o);
+          az += __shfl_xor_sync(0xffffffffu, az, o);
+        }
+        if (sub == 0 && live) {
+          const double q = s_qv[pl];
+          double* f = forces + 3 * (long long)s_ai[3 * KB + pl];
+          f[0] = -q * ax;
+          f[1] = -q * ay;
+          f[2] = -q * az;
+        }
+      }
+      __syncwarp();                               // the batch slots are rewritten next
+    }
+    if (!waited) mbar_wait(&full[s], (it / kTmaStages) & 1);   // keep the phase in step
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    ++it;
+  }
+}
+
+// Host side -------------------------------------------------------------------
+
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiled>(f);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+// Ghost-padded field layout for the TMA gather: axis d needs grid indices
+// [lo, (n_d - 1) T_d + lo + W_d - 1], stored at padded index (index - lo).
+FieldPad make_field_pad(const esp_plan* p) {
+  FieldPad f;
+  std::memset(&f, 0, sizeof(f));
+  const int T[3] = {p->TX, p->TY, p->TZ};
+  const int W[3] = {kPad, kPad, p->PZ};
+  const int n[3] = {p->ntx, p->nty, p->ntz};
+  for (int d = 0; d < 3; ++d) {
+    f.M[d] = p->M[d];
+    f.S[d] = -p->lo;
+    f.E[d] = (n[d] - 1) * T[d] + W[d];
+  }
+  // x: shift so rows start on a 32-byte sector (S0 % 4 == 0), 2 columns of
+  // slack for the 18-column boxes of odd-start tiles, pitch a multiple of 4
+  const int xsh = (4 - f.S[0] % 4) % 4;
+  f.S[0] += xsh;
+  f.E[0] += xsh + 2;
+  f.E[0] = (f.E[0] + 3) & ~3;
+  f.cstride = (long long)f.E[0] * f.E[1] * f.E[2];
+  f.enabled = 1;
+  return f;
+}
+
+bool tma_gather_eligible(const esp_plan* p) {
+  return p->precision == ESP_FP64 && p->P <= 8 && p->lo <= 0 && p->Mu[2] == p->M[2] &&
+         p->zshift == 0 && p->PZ <= 16 && encode_fn() != nullptr;
+}
+
+// Tensor map over the padded fields: dims {E0, E1, E2, 3}, box {18, 16, PZ, 1},
+// no swizzle (the 144-byte rows are bank-conflict free for the lane map).
+cudaError_t make_field_tmap(esp_plan* p) {
+  const FieldPad& f = p->fpad;
+  cuuint64_t dims[4] = {(cuuint64_t)f.E[0], (cuuint64_t)f.E[1], (cuuint64_t)f.E[2], 3};
+  cuuint64_t strides[3] = {(cuuint64_t)f.E[0] * 8, (cuuint64_t)f.E[0] * f.E[1] * 8,
+                           (cuuint64_t)f.cstride * 8};
+  cuuint32_t box[4] = {(cuuint32_t)TmaGatherLayout<8>::kRow, 16, (cuuint32_t)p->PZ, 1};
+  cuuint32_t elem[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(reinterpret_cast<CUtensorMap*>(p->tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                           4, p->d_fpad, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int P, int NW>
+static cudaError_t tma_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+  Geom g = make_geom(p);
+  const size_t smem = TmaGatherLayout<NW>::bytes(p->PZ);
+  cudaError_t e = cudaFuncSetAttribute(k_gather_tma<P, NW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long ntiles = p->n_tiles;
+  const unsigned grid = (unsigned)std::min<long long>(sms, ntiles);
+  k_gather_tma<P, NW><<<grid, 32 * (NW + 1), smem, s>>>(
+      *reinterpret_cast<const CUtensorMap*>(p->tmap), g, *p->h_fast, p->d_tab, p->d_breaks,
+      p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->cap, p->d_q, p->d_idx, d_forces,
+      p->fpad.S[0] + p->lo);
+  p->launches++;
+  prof_mark(p, s, "gather");
+  return cudaGetLastError();
+}
+
+#ifndef ESP_TMA_NW
+#define ESP_TMA_NW 12   // consumer warps (A/B at config 4: 8 -> 4.77 ms, 12 -> 4.39, 16 -> 4.46)
+#endif
+cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s) {
+  constexpr int NW = ESP_TMA_NW;
+  switch (p->P) {
+    case 2: return tma_p<2, NW>(p, d_forces, s);
+    case 3: return tma_p<3, NW>(p, d_forces, s);
+    case 4: return tma_p<4, NW>(p, d_forces, s);
+    case 5: return tma_p<5, NW>(p, d_forces, s);
+    case 6: return tma_p<6, NW>(p, d_forces, s);
+    case 7: return tma_p<7, NW>(p, d_forces, s);
+    case 8: return tma_p<8, NW>(p, d_forces, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace esp

@@ -279,6 +279,18 @@ __device__ __forceinline__ double combine_at(const Geom& g, const CombineTabs& c
   return acc;
 }
 
+// Ghost-padded layout of the three ik fields for the TMA gather
+// (esp_gather_tma.cu): component c, grid point (x, y, z) lives at
+// c*cstride + ((z + S2)*E1 + (y + S1))*E0 + (x + S0); the ghost entries hold
+// the periodic images, so every tile's stencil box is in bounds.
+struct FieldPad {
+  int enabled;
+  int S[3];
+  int E[3];
+  int M[3];
+  long long cstride;
+};
+
 template <typename T> struct Cplx;
 template <> struct Cplx<double> { using type = double2; };
 template <> struct Cplx<float> { using type = float2; };
@@ -369,6 +381,11 @@ struct esp_plan {
   cudaEvent_t q_ready = nullptr;   // esp_set_charges_event: wait before reading q
   cudaEvent_t ev[48];
   const char* ev_name[48];
+  // TMA gather (esp_gather_tma.cu): ghost-padded ik fields and their tensor map
+  void* d_fpad = nullptr;
+  esp::FieldPad fpad{};
+  int fpad_written = 0;   // the last fused inverse wrote d_fpad (not d_fields)
+  alignas(64) unsigned char tmap[128];
 };
 
 namespace esp {
@@ -395,6 +412,11 @@ cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s,
                              const void* fields = nullptr,
                              OutMap om = OutMap{3, {0, 1, 2}, {-1, -1, -1}});
 cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s);
+// Persistent TMA-fed ik gather from the ghost-padded fields (fp64, P <= 8).
+FieldPad make_field_pad(const esp_plan* p);
+bool tma_gather_eligible(const esp_plan* p);
+cudaError_t make_field_tmap(esp_plan* p);
+cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s);
 // Fused band-pruned forward transform + scale/reduce (+ ik spectra and the
 // inverse transforms into d_fields when want_ik).  Requires p->fused.
 cudaError_t launch_fused_fft(esp_plan* p, int want_ik, double* d_out7, cudaStream_t s);

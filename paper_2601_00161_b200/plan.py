@@ -355,11 +355,16 @@ class EspPlan:
 
     def fields_view(self) -> torch.Tensor:
         """Alias of the plan's three ik force fields (3, Mz, My, Mx) of the last
-        force evaluation (diagnostics / slab tests)."""
+        force evaluation (diagnostics / slab tests); a strided view of the
+        ghost-padded array when the TMA gather path wrote it."""
         ts = "<f8" if self.precision == "fp64" else "<f4"
-        ptr = _lib.lib().esp_fields_ptr(self._handle)
-        return torch.as_tensor(_DevView(ptr, (3, self.M[2], self.M[1], self.M[0]), ts),
-                               device="cuda")
+        L = _lib.lib()
+        lay = (C.c_int64 * 5)()
+        _lib.check(L.esp_fields_layout(self._handle, lay), "esp_fields_layout")
+        org, ex, ey, ez, cs = (int(v) for v in lay)
+        ptr = L.esp_fields_ptr(self._handle)
+        flat = torch.as_tensor(_DevView(ptr, (3 * cs,), ts), device="cuda")
+        return flat.as_strided((3, self.M[2], self.M[1], self.M[0]), (cs, ex * ey, ex, 1), org)
 
     def spectrum_view(self) -> torch.Tensor:
         """Alias of the plan's half spectrum (Mz, My, Mx//2+1), unscaled."""
