@@ -737,12 +737,17 @@ def run_reference(args):
 
 
 def run_slab(args):
-    """Strong scaling: one config-4 system decomposed into z-slabs over the
-    ranks (NCCL halo send/recv, transposes stored over peer memory by the
-    band-pruned transform kernels, 7-double all-gather)."""
+    """Strong scaling (the default under torchrun): one config-4 system
+    decomposed into z-slabs over the ranks — spread on a z-slab plan, ghost
+    planes by NCCL send/recv, band-pruned transforms whose transposes are
+    stored into the peer ranks' buffers (symmetric memory over NVLink),
+    7-double all-gather summed in rank order on the device, gather.  The
+    step (SlabKSpaceSolver.evaluate_device) has no host synchronisation and
+    is replayed as one CUDA graph per rank when NCCL capture is available."""
     import torch
 
-    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver, workloads
+    from paper_2601_00161_b200 import workloads
+    from paper_2601_00161_b200.plan import probe_fp64_tflops
     from paper_2601_00161_b200.pswf import build_pswf, solve_bandwidth, tabulate_window
     from paper_2601_00161_b200.slab import SlabKSpaceSolver
 
@@ -759,14 +764,43 @@ def run_slab(args):
     mine = s.owned(pos_np)
     pos = torch.as_tensor(pos_np[mine], device=dev)
     q = torch.as_tensor(q_np[mine], device=dev)
+    n_mine = int(mine.sum())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
-
+    K, W = args.steps, args.warmup
     stats = {}
 
-    def timed(want_forces, K, W):
-        return timed_steps(lambda: s.evaluate(pos, q, want_forces), K, W, flush, stream,
-                           dist, dev, stats, "force_pressure" if want_forces else "pressure_only")
+    # one CUDA graph per rank and path; eager stream-ordered steps otherwise
+    capture = "cuda_graph"
+    try:
+        g_fp, o7, F = s.graphed(pos, q, True)
+        g_po, o7_po, _ = s.graphed(pos, q, False)
+        step_fp, step_po = g_fp.replay, g_po.replay
+    except Exception as exc:   # NCCL capture unavailable: keep the eager step
+        capture = f"eager ({type(exc).__name__})"
+        o7 = torch.empty(7, dtype=torch.float64, device=dev)
+        F = torch.empty((n_mine, 3), dtype=torch.float64, device=dev)
+        step_fp = lambda: s.evaluate_device(pos, q, True, o7, F)         # noqa: E731
+        step_po = lambda: s.evaluate_device(pos, q, False, o7, None)     # noqa: E731
+
+    # public-API end to end: this rank's charges from pinned host buffers,
+    # the step, forces and the 7 sums back to pinned host memory
+    h_pos = torch.empty((n_mine, 3), dtype=torch.float64).pin_memory()
+    h_q = torch.empty(n_mine, dtype=torch.float64).pin_memory()
+    h_F = torch.empty((n_mine, 3), dtype=torch.float64).pin_memory()
+    h_7 = torch.empty(7, dtype=torch.float64).pin_memory()
+    h_pos.copy_(torch.as_tensor(pos_np[mine]))
+    h_q.copy_(torch.as_tensor(q_np[mine]))
+
+    def step_e2e():
+        pos.copy_(h_pos, non_blocking=True)
+        q.copy_(h_q, non_blocking=True)
+        step_fp()
+        h_F.copy_(F, non_blocking=True)
+        h_7.copy_(o7, non_blocking=True)
+
+    def timed(fn, tag, k=K, wu=W):
+        return timed_steps(fn, k, wu, flush, stream, dist, dev, stats, tag)
 
     near = None
     if args.near:
@@ -778,32 +812,76 @@ def run_slab(args):
                                                              Cell(np.asarray(w.h, float))))
         sn.ops.plan.reserve(pos.shape[0] + pos.shape[0] // 2)
 
-    def timed_near(K, W):
-        return timed_steps(lambda: sn.evaluate(pos, q), K, W, flush, stream, dist, dev,
-                           stats, "near_field")
-
+    quiet_host_pools()
     with ClockSampler(local) as clk:
-        ms_fp = timed(True, args.steps, args.warmup)
-        ms_po = timed(False, args.steps, args.warmup)
+        ms_fp = timed(step_fp, "force_pressure")
+        ms_po = timed(step_po, "pressure_only")
+        ms_e2e = timed(step_e2e, "e2e")
         if args.near:
-            ms_near = timed_near(max(3, min(args.steps, 5)), 2)
+            ms_near = timed(lambda: sn.evaluate(pos, q), "near_field", max(3, min(K, 5)), 2)
             near = {"ms_per_step": ms_near, "value": w.n / (ms_near * 1e-3), "unit": UNIT,
                     "what": "slab near field (ghost all-to-all, slab-local pair sums, "
                             "rank-ordered reduction), slab_near.SlabNearField"}
+    clocks = clk.summary()
+    assert np.isfinite(h_F.numpy()).all() and np.isfinite(h_7.numpy()).all()
+
+    # per-kernel profile of this rank's slab plan (bin, spread, combine, gather)
+    plan, spectral = s.ops.plan, s.ops.spectral
+    prof = {}
+    for _ in range(3):
+        flush.zero_()
+        plan.set_profiling(True)           # resets the event list and launch count
+        spectral.set_profiling(True)
+        s.evaluate_device(pos, q, True)
+        for name, t in plan.profile():
+            prof[name] = prof.get(name, 0.0) + t / 3
+        launches = plan.launches_last_step() + spectral.launches_last_step()
+    plan.set_profiling(False)
+    spectral.set_profiling(False)
+    hbm_peak, peak_kind = measured_peaks()
+    real_b = 8 if args.precision == "fp64" else 4
+    alg = algorithmic(w, n_mine, plan.tables.band, real_b)
+    roof = None
+    kern_t = {k: v for k, v in prof.items() if k in ("gather", "spread")}
+    if kern_t:
+        dom = max(kern_t, key=kern_t.get)
+        t = kern_t[dom] * 1e-3
+        ach = alg[dom]["bytes"] / t / 1e9
+        fp64 = probe_fp64_tflops()
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 2), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "traffic": None,
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
+                "avg_launch_ms": round(kern_t[dom], 5),
+                "fp64": {"achieved_tflops": round(alg[dom]["flops"] / t / 1e12, 3),
+                         "peak_tflops": round(fp64, 2)},
+                "scope": f"rank {rank}'s slab plan ({n_mine} charges)"}
+    h2d = int((h_pos.numel() + h_q.numel()) * 8)
+    d2h = int((h_F.numel() + h_7.numel()) * 8)
     line = {"metric": METRIC, "value": w.n / (ms_fp * 1e-3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_fp,
+            "steps": K, "warmup": W, "ms_per_step": ms_fp,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic (seeded config recipe, SURVEY §8(d.1))",
             "config": {"workload": w.name, "n_charges": w.n, "grid": list(w.M), "P": w.P,
+                       "delta": w.delta, "r_c": w.r_c, "cell_type": w.cell_type,
                        "parallelism": f"zslab{world}", "precision": args.precision,
-                       "l2": "flushed between timed steps (256 MB write)"},
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "statistic": "median step time, max over ranks",
+                       "capture": capture},
             "pressure_only": {"value": w.n / (ms_po * 1e-3), "unit": UNIT,
                               "ms_per_step": ms_po},
+            "e2e": {"value": w.n / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "SlabKSpaceSolver step per rank from pinned host buffers "
+                           "(bytes are rank 0's share)"},
+            "gpu_launches": int(launches * K), "gpu_launches_per_step": launches,
             "timing": dict(stats, statistic="median over the K timed steps, max over ranks"),
-            "clocks": clk.summary()}
+            "clocks": clocks, "roofline": roof,
+            "kernel_ms": {k: round(v, 5) for k, v in prof.items()}}
     if near is not None:
         line["near_field"] = near
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_port(cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -773,6 +773,7 @@ int esp_set_profiling(esp_plan* p, int32_t on) {
   }
   p->profiling = on ? 1 : 0;
   p->n_ev = 0;
+  p->launches = 0;   // stage-level callers (slab plans) count launches from here
   return ESP_OK;
 }
 

@@ -264,7 +264,20 @@ class SlabKSpaceSolver:
     # -- the step ------------------------------------------------------------------
     def evaluate(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool = True):
         """pos/q: this rank's charges.  Returns (E, P (3x3 numpy), F (n,3) or
-        None); E and P are global (identical on every rank)."""
+        None); E and P are global (identical on every rank).  One host
+        synchronisation (the 7 reduced doubles); evaluate_device has none."""
+        out7, F = self.evaluate_device(pos, q, want_forces)
+        v = out7.cpu().numpy()
+        pp = v[1:]
+        Pt = np.array([[pp[0], pp[1], pp[2]], [pp[1], pp[3], pp[4]], [pp[2], pp[4], pp[5]]])
+        return float(v[0]), Pt, F
+
+    def evaluate_device(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool = True,
+                        out7: torch.Tensor | None = None, forces: torch.Tensor | None = None):
+        """The whole distributed step, stream-ordered with no host
+        synchronisation (CUDA-graph capturable): returns (out7, F) with out7 =
+        [E, Pxx, Pxy, Pxz, Pyy, Pyz, Pzz] on the device, the 7 per-rank sums
+        added in rank order (bit-stable at a fixed GPU count)."""
         lay, P, M = self.layout, self.P, self.M
         nlo, nup, nz = lay.nlo, lay.nup, self.nz
         slab = self.ops.spread(pos, q)                     # (nz+P-1, My, Mx)
@@ -274,7 +287,7 @@ class SlabKSpaceSolver:
         own[:nup] += from_prev                             # prev's upper ghosts
         own[nz - nlo:] += from_next                        # next's lower ghosts
         if self._fused:
-            return self._evaluate_fused(own, pos, q, want_forces)
+            return self._evaluate_fused(own, pos, q, want_forces, out7, forces)
         # forward transform: (y, x) per plane, transpose, z
         X = torch.fft.rfft2(own, dim=(-2, -1))             # (nz, My, Hx)
         Hx = X.shape[-1]
@@ -295,21 +308,13 @@ class SlabKSpaceSolver:
         part = torch.stack([wa.sum(), (tb * kx * kx + wa).sum(), (tb * kx * ky).sum(),
                             (tb * kx * kz).sum(), (tb * ky * ky + wa).sum(),
                             (tb * ky * kz).sum(), (tb * kz * kz + wa).sum()])
-        if self.R > 1:
-            allp = [torch.empty_like(part) for _ in range(self.R)]
-            dist.all_gather(allp, part, group=self.group)
-            tot = allp[0].clone()
-            for r in range(1, self.R):
-                tot = tot + allp[r]
-        else:
-            tot = part
+        tot = self._rank_ordered_sum(part)
         h3sq = self.h3 * self.h3
-        v = tot.cpu().numpy()
-        E = float(v[0] * h3sq / (2.0 * self.volume))
-        pp = v[1:] * h3sq / (2.0 * self.volume ** 2)
-        Pt = np.array([[pp[0], pp[1], pp[2]], [pp[1], pp[3], pp[4]], [pp[2], pp[4], pp[5]]])
+        scale = torch.tensor([h3sq / (2.0 * self.volume)] + [h3sq / (2.0 * self.volume ** 2)] * 6,
+                             dtype=torch.float64, device=tot.device)
+        out7 = self._out7(out7, tot * scale)
         if not want_forces:
-            return E, Pt, None
+            return out7, None
         # ik spectra (rho_hat = h3 X), inverse z, transpose back, inverse (y, x)
         c = self._A * self.h3
         spec = torch.zeros((3,) + tuple(self._shape), dtype=Y.dtype, device=Y.device)
@@ -336,9 +341,33 @@ class SlabKSpaceSolver:
         dt = torch.float64 if getattr(getattr(self.ops, "plan", None), "precision",
                                       "fp64") == "fp64" else torch.float32
         F = self.ops.gather(ext.to(dt).contiguous(), pos, q)
-        return E, Pt, F
+        if forces is not None:
+            forces.copy_(F)
+            F = forces
+        return out7, F
 
-    def _evaluate_fused(self, own: torch.Tensor, pos, q, want_forces: bool):
+    def _rank_ordered_sum(self, part: torch.Tensor) -> torch.Tensor:
+        """All-gather the 7 per-rank partial sums and add them in rank order
+        on the device (no host round trip; bit-stable at a fixed GPU count)."""
+        if self.R == 1:
+            return part
+        flat = torch.empty(self.R * part.numel(), dtype=part.dtype, device=part.device)
+        dist.all_gather_into_tensor(flat, part.contiguous(), group=self.group)
+        allp = flat.view(self.R, -1)
+        tot = allp[0].clone()
+        for r in range(1, self.R):
+            tot = tot + allp[r]
+        return tot
+
+    @staticmethod
+    def _out7(out7, val):
+        if out7 is None:
+            return val
+        out7.copy_(val)
+        return out7
+
+    def _evaluate_fused(self, own: torch.Tensor, pos, q, want_forces: bool, out7=None,
+                        forces=None):
         """The spectral part on the band-pruned kernels with the transposes
         fused into them (peer stores), NCCL only for the 7-double reduction
         and the ghost planes."""
@@ -347,20 +376,9 @@ class SlabKSpaceSolver:
         spec.slab_forward(self._desc, own.to(spec.real_dtype))
         self._rank_barrier()
         part = spec.slab_reduce(self._desc, self._recv_fwd, want_forces)
-        if self.R > 1:
-            allp = [torch.empty_like(part) for _ in range(self.R)]
-            dist.all_gather(allp, part, group=self.group)
-            tot = allp[0].clone()
-            for r in range(1, self.R):
-                tot = tot + allp[r]
-        else:
-            tot = part
-        v = tot.cpu().numpy()
-        E = float(v[0])
-        pp = v[1:]
-        Pt = np.array([[pp[0], pp[1], pp[2]], [pp[1], pp[3], pp[4]], [pp[2], pp[4], pp[5]]])
+        out7 = self._out7(out7, self._rank_ordered_sum(part))
         if not want_forces:
-            return E, Pt, None
+            return out7, None
         self._rank_barrier()
         fields = torch.empty((3, nz, M[1], M[0]), dtype=spec.real_dtype, device=own.device)
         spec.slab_inverse(self._desc, self._recv_back, fields)
@@ -369,8 +387,35 @@ class SlabKSpaceSolver:
                                              (3, nup) + tuple(fields.shape[2:]))
         ext = torch.cat([from_prev_f, fields, from_next_f], dim=1)
         F = self.ops.gather(ext.contiguous(), pos, q)
-        return E, Pt, F
+        if forces is not None:
+            forces.copy_(F)
+            F = forces
+        return out7, F
 
+    def graphed(self, pos: torch.Tensor, q: torch.Tensor, want_forces: bool = True):
+        """Capture evaluate_device on fixed buffers into one CUDA graph
+        (spread, halo send/recv, fused transforms with peer-store transposes,
+        device barriers, the rank-ordered reduction and the gather).  Returns
+        (graph, out7, forces); ``graph.replay()`` re-runs the step after the
+        caller updates pos / q in place.  Collective capture needs NCCL graph
+        support; on failure the caller keeps the eager step."""
+        dev = pos.device
+        out7 = torch.empty(7, dtype=torch.float64, device=dev)
+        F = torch.empty((pos.shape[0], 3), dtype=torch.float64, device=dev) if want_forces \
+            else None
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.evaluate_device(pos, q, want_forces, out7, F)      # warm-up
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        if self.R > 1:
+            dist.barrier(group=self.group)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.evaluate_device(pos, q, want_forces, out7, F)
+        torch.cuda.synchronize()
+        return g, out7, F
 
 class _SlabPeers:
     """esp_slab_desc of one rank from raw peer base addresses."""

@@ -411,6 +411,37 @@ def test_slab_solver_single_rank_on_gpu():
     assert O.rms_rel_forces(F.cpu().numpy(), r.forces) <= 1e-12
 
 
+@pytest.mark.parametrize("idx", [1, 4])
+def test_slab_step_graph_captured_matches_single_plan(idx):
+    """The multi-GPU step (SlabKSpaceSolver.evaluate_device: spread, halo
+    exchange, fused transforms with the peer-store transposes, device-side
+    rank-ordered reduction, gather) captured in one CUDA graph at R = 1 —
+    the run bench.py --gpus N makes on every rank — equals the single-plan
+    step to 1e-12 (config 1, and config 4 at full size), also after the
+    positions are updated in place."""
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    from paper_2601_00161_b200.plan import out7_to_tensor
+    from paper_2601_00161_b200.slab import SlabKSpaceSolver
+    w, pos, q = workloads.generate(idx)
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M),
+                     capacity=w.n)
+    sl = SlabKSpaceSolver(w.h, w.M, w.P, s.kern.basis, s.spec.window, w.r_c, capacity=w.n)
+    P_, Q_ = _dev(torch, pos), _dev(torch, q)
+    g, o7, F = sl.graphed(P_, Q_, True)
+    for shift in (0.0, 0.37):
+        if shift:
+            P_.copy_(_dev(torch, workloads.wrap_positions(w.h, pos + shift)))
+        g.replay()
+        r7, rF = s.evaluate_device(P_, Q_)
+        torch.cuda.synchronize()
+        E, Pt = out7_to_tensor(o7)
+        Er, Ptr = out7_to_tensor(r7)
+        assert O.rel_scalar(E, Er) <= 1e-12
+        assert O.rel_frobenius(Pt, Ptr) <= 1e-12
+        assert O.rms_rel_forces(F.cpu().numpy(), rF.cpu().numpy()) <= 1e-12
+
+
 @pytest.mark.parametrize("name", ["small_cube_p5", "small_brick_p6", "small_brick_p8",
                                   "small_brick_p7", "small_cube_p4"])
 def test_analytic_forces_and_local_pressure_match_reference(name):
