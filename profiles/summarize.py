@@ -60,7 +60,7 @@ def stalls(rep, kernel_regex):
 
 def main(rep):
     print(f"# ncu summary: `{rep}`\n")
-    print("| kernel | us | DRAM rd MB | DRAM wr MB | warp inst (M) | smem wavefronts (M) "
+    print("| kernel | ms | DRAM rd MB | DRAM wr MB | warp inst (M) | smem wavefronts (M) "
           "| warps active % | issue active % | FP64 pipe % | regs |")
     print("|---|---|---|---|---|---|---|---|---|---|")
     kernels = raw_metrics(rep)
@@ -77,6 +77,9 @@ def main(rep):
             if name.startswith("dram__bytes"):
                 x *= {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
                 return f"{x:.2f}"
+            if name == "gpu__time_duration.sum":      # always milliseconds in the table
+                x *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1.0)
+                return f"{x:.4f}"
             return f"{x * scale:.2f}"
         name = k["Kernel Name"][0].split("(")[0][:48]
         fp = g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
