@@ -177,6 +177,7 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   }
   esp_plan* p = new esp_plan;
   std::memset(p, 0, sizeof(esp_plan));
+  p->need_records = 0;   // radix binning: records-free gather + coalesced records pass
   for (int k = 0; k < 3; ++k) p->M[k] = p->Mu[k] = d->M[k];
   if (d->slab_mz_global > 0) {
     // z-slab plan: local planes [0, M[2]) hold global planes zshift + i
@@ -547,6 +548,7 @@ int esp_spread(esp_plan* p, const double* d_pos, const double* d_q, int64_t n, v
     return ESP_ERR_CAPACITY;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  p->last_n = n;          // the bins below are for these n charges
   ESP_CUDA(esp::launch_bin(p, d_pos, d_q, n, s));
   ESP_CUDA(esp::launch_spread(p, s));
   if (d_grid) {
@@ -709,8 +711,12 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
     // or, for analytic forces, the potential spectrum, and the inverse
     // transforms) -> gather
     p->want_drec = want_f && analytic;
+    // analytic steps write weight and derivative records in one pass; other
+    // steps bin with the records-free gather and a coalesced records pass
+    p->need_records = want_f && analytic;
     rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
     p->want_drec = 0;
+    p->need_records = 0;
     if (rc) return rc;
     ESP_CUDA(esp::launch_fused_fft(p, want_f ? (analytic ? 2 : 1) : 0, d_out7, s0));
     p->fwd_count++;

@@ -188,6 +188,64 @@ k_bin_sorted(Geom g, FastTab ft, const real* __restrict__ tab, const double* __r
   }
 }
 
+// Records-free sorted pass (the step's spread and gather evaluate their
+// weights from u): gather each particle into its binned slot — grid
+// coordinates (SoA), charge and original index, one thread per particle.
+__global__ void k_bin_gather(Geom g, long long n, long long cap, const int* __restrict__ sval,
+                             const double* __restrict__ pos, const double* __restrict__ q,
+                             double* __restrict__ u_out, double* __restrict__ q_out,
+                             int* __restrict__ idx_out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int i = sval[j];
+  double u[3];
+  grid_coords(g, pos[3 * (long long)i], pos[3 * (long long)i + 1], pos[3 * (long long)i + 2], u);
+  u_out[j] = u[0];
+  u_out[cap + j] = u[1];
+  u_out[2 * cap + j] = u[2];
+  q_out[j] = q[i];
+  idx_out[j] = i;
+}
+
+// Weight records from the binned grid coordinates (deferred records:
+// ensure_records), three threads per particle; key = the sorted bin key.
+template <typename real, int P>
+__global__ void __launch_bounds__(3 * kBinPerBlock)
+k_bin_records_u(Geom g, FastTab ft, const real* __restrict__ tab, const double* __restrict__ brk,
+                int n_pieces, int ncoef, long long n, long long cap,
+                const int* __restrict__ skey, const double* __restrict__ U,
+                real* __restrict__ wrec, int* __restrict__ pk) {
+  // the block's 32 records are assembled in shared memory and written as one
+  // contiguous run (coalesced), as in k_bin_sorted
+  constexpr int RS = rec_stride(P);
+  __shared__ __align__(16) real s_rec[kBinPerBlock * 3 * RS];
+  __shared__ int s_pk[kBinPerBlock];
+  const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
+  const long long j0 = (long long)blockIdx.x * kBinPerBlock;
+  const long long j = j0 + l;
+  const int nb = (int)min((long long)kBinPerBlock, n - j0);
+  if (l < nb) {
+    const double u = U[d * cap + j];
+    real w[P];
+    int a;
+    record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
+#pragma unroll
+    for (int t = 0; t < RS; ++t) s_rec[(l * 3 + d) * RS + t] = t < P ? w[t < P ? t : 0] : real(0);
+    unsigned char* pb = reinterpret_cast<unsigned char*>(s_pk + l);
+    if (d == 2) {
+      *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
+    } else {
+      const int txy = skey[j] / g.M[2];
+      const int org = d == 0 ? (txy % g.ntx) * g.TX : (txy / g.ntx) * g.TY;
+      pb[d] = (unsigned char)(a - org);
+    }
+  }
+  __syncthreads();
+  real* dst = wrec + j0 * (3 * RS);
+  for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) dst[t] = s_rec[t];
+  for (int t = threadIdx.x; t < nb; t += 3 * kBinPerBlock) pk[j0 + t] = s_pk[t];
+}
+
 // Small key spaces (<= kScanMax keys, e.g. config 1's 4096): every scatter
 // CTA scans the key counts in shared memory itself (CTA 0 also publishes the
 // offsets), so the separate device-wide scan launch disappears from the step.
@@ -491,11 +549,20 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
       p->q_ready = nullptr;
       if (e != cudaSuccess) return e;
     }
-    e = p->precision == ESP_FP64 ? launch_sorted_r<double>(p, g, d_pos, d_q, n, grid, B, s)
-                                 : launch_sorted_r<float>(p, g, d_pos, d_q, n, grid, B, s);
+    if (p->need_records || p->want_drec) {
+      e = p->precision == ESP_FP64 ? launch_sorted_r<double>(p, g, d_pos, d_q, n, grid, B, s)
+                                   : launch_sorted_r<float>(p, g, d_pos, d_q, n, grid, B, s);
+      p->records_ready = 1;
+    } else {
+      k_bin_gather<<<grid, B, 0, s>>>(g, n, p->cap, p->d_idx_tmp, d_pos, d_q, p->d_u, p->d_q,
+                                      p->d_idx);
+      e = cudaGetLastError();
+      p->records_ready = 0;
+      p->drec_ready = 0;
+    }
     if (e != cudaSuccess) return e;
     p->launches++;
-    prof_mark(p, s, "bin_gather_weights");
+    prof_mark(p, s, p->records_ready ? "bin_gather_weights" : "bin_gather");
     return cudaGetLastError();
   }
   if (n > 0) {
@@ -543,9 +610,50 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
   e = p->precision == ESP_FP64 ? launch_tail_r<double>(p, g, n, grid, B, s)
                                : launch_tail_r<float>(p, g, n, grid, B, s);
   if (e != cudaSuccess) return e;
+  p->records_ready = 1;
   p->launches++;
   prof_mark(p, s, p->deterministic ? "bin_canon_weights" : "bin_weights");
   return cudaGetLastError();
+}
+
+template <typename real, int P>
+static cudaError_t records_p(esp_plan* p, cudaStream_t s) {
+  const Geom g = make_geom(p);
+  const real* tab = std::is_same<real, double>::value
+                        ? reinterpret_cast<const real*>(p->d_tab)
+                        : reinterpret_cast<const real*>(p->d_tabf);
+  const unsigned g3 = (unsigned)((p->last_n + kBinPerBlock - 1) / kBinPerBlock);
+  k_bin_records_u<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(
+      g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->last_n, p->cap, p->d_bkey,
+      p->d_u, reinterpret_cast<real*>(p->d_wrec), p->d_pk);
+  p->launches++;
+  prof_mark(p, s, "bin_records");
+  return cudaGetLastError();
+}
+
+template <typename real>
+static cudaError_t records_r(esp_plan* p, cudaStream_t s) {
+  switch (p->P) {
+    case 2: return records_p<real, 2>(p, s);
+    case 3: return records_p<real, 3>(p, s);
+    case 4: return records_p<real, 4>(p, s);
+    case 5: return records_p<real, 5>(p, s);
+    case 6: return records_p<real, 6>(p, s);
+    case 7: return records_p<real, 7>(p, s);
+    case 8: return records_p<real, 8>(p, s);
+    case 9: return records_p<real, 9>(p, s);
+    case 10: return records_p<real, 10>(p, s);
+    case 11: return records_p<real, 11>(p, s);
+    case 12: return records_p<real, 12>(p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t ensure_records(esp_plan* p, cudaStream_t s) {
+  if (p->records_ready || p->last_n <= 0) return cudaSuccess;
+  const cudaError_t e = p->precision == ESP_FP64 ? records_r<double>(p, s) : records_r<float>(p, s);
+  if (e == cudaSuccess) p->records_ready = 1;
+  return e;
 }
 
 size_t scan_temp_bytes(long long n_items) {

@@ -74,6 +74,13 @@ __host__ __device__ constexpr int pow2_floor(int v) {
 // with threads_yz(N) threads, so that small grids still launch several CTAs
 // per SM.
 constexpr int kThreadsX = 128;
+// resident CTAs per SM the register allocation is sized for (A/B knobs)
+#ifndef ESP_YZ_MINB
+#define ESP_YZ_MINB 3
+#endif
+#ifndef ESP_X_MINB
+#define ESP_X_MINB 8   // config 4: inverse x 0.667 -> 0.630 ms against 6
+#endif
 // x rows: ~1024 elements per CTA on large grids; small grids (L2-resident)
 // take fewer rows per CTA so that every SM gets work.
 __host__ __device__ constexpr int pairs_x(int N) {
@@ -261,7 +268,7 @@ __device__ __forceinline__ int band_index(int m, int nb, int N) {
 // P1: x rows, real -> complex, two rows per transform; out[row][kx], kx < ldx
 // (zeros for kx >= nbx).
 template <typename real, int N>
-__global__ void __launch_bounds__(kThreadsX, 6)
+__global__ void __launch_bounds__(kThreadsX, ESP_X_MINB)
 k_x_r2c(const real* __restrict__ grid, typename Cx<real>::t* __restrict__ out,
         const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx) {
   using C = typename Cx<real>::t;
@@ -333,7 +340,7 @@ __device__ __forceinline__ int slab_owner(const int* start, int R, int v) {
 // P2: y lines (z, kx) for kx < ldx: forward C2C, keep the nby in-band ky.
 // in[(z*N + y)*ldx + kx] -> out[(z*nby + by)*ldx + kx].
 template <typename real, int N>
-__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+__global__ void __launch_bounds__(threads_yz<real>(N), ESP_YZ_MINB)
 k_y_fwd(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ out,
         const typename Cx<real>::t* __restrict__ tw, long long nlines, int ldx, int nby,
         SlabMap smap) {
@@ -461,7 +468,7 @@ __device__ __forceinline__ void tree_finish(double* partials, double* gsum, int*
 // and runs their inverse z transforms (what k_z_ik does), saving a launch and
 // the spectrum's round trip through memory.
 template <typename real, int N, bool IK = false>
-__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+__global__ void __launch_bounds__(threads_yz<real>(N), ESP_YZ_MINB)
 k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ spec,
            const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines,
            double* __restrict__ partials, double* __restrict__ gsum,
@@ -667,7 +674,7 @@ k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __
 // retained modes (zero elsewhere, mesh.py:333-341), inverse C2C along z ->
 // ik[c][z][by][kx].  X is the box spectrum P3a wrote.
 template <typename real, int N>
-__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+__global__ void __launch_bounds__(threads_yz<real>(N), ESP_YZ_MINB)
 k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __restrict__ ik,
        const typename Cx<real>::t* __restrict__ tw, FusedArgs fa, long long nlines,
        SlabMap smap) {
@@ -739,7 +746,7 @@ k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __re
 // P4: y lines (c, z, kx): inverse C2C from the nby in-band ky rows (zero
 // elsewhere).  in[(cz*nby + by)*ldx + kx] -> out[(cz*N + y)*ldx + kx].
 template <typename real, int N>
-__global__ void __launch_bounds__(threads_yz<real>(N), 3)
+__global__ void __launch_bounds__(threads_yz<real>(N), ESP_YZ_MINB)
 k_y_inv(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ out,
         const typename Cx<real>::t* __restrict__ tw, long long nlines, int ldx, int nby) {
   using C = typename Cx<real>::t;
@@ -826,7 +833,7 @@ __device__ __forceinline__ void store_padded(const FieldPad& f, const PadRows& r
 }
 
 template <typename real, int N>
-__global__ void __launch_bounds__(kThreadsX, 6)
+__global__ void __launch_bounds__(kThreadsX, ESP_X_MINB)
 k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
         const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx,
         FieldPad pad) {

@@ -650,6 +650,8 @@ static cudaError_t gather_r(esp_plan* p, double* d_forces, cudaStream_t s, OutMa
 
 cudaError_t launch_gather_ik(esp_plan* p, double* d_forces, cudaStream_t s,
                              const void* fields, OutMap om) {
+  const cudaError_t er = ensure_records(p, s);
+  if (er != cudaSuccess) return er;
   void* saved = p->d_fields;
   if (fields) p->d_fields = const_cast<void*>(fields);
   cudaError_t e = p->precision == ESP_FP64 ? gather_r<double>(p, d_forces, s, om)
@@ -715,6 +717,8 @@ static cudaError_t grad_r(esp_plan* p, double* d_forces, cudaStream_t s) {
 }
 
 cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s) {
+  const cudaError_t er = ensure_records(p, s);
+  if (er != cudaSuccess) return er;
   return p->precision == ESP_FP64 ? grad_r<double>(p, d_forces, s)
                                   : grad_r<float>(p, d_forces, s);
 }

@@ -363,6 +363,9 @@ struct esp_plan {
   long long comb_off[3];
   esp::FastTab* h_fast;   // host copy of the fast window table (kernel param)
   esp::FastTab* h_fast_d = nullptr;   // derivative window table (analytic gather)
+  int need_records = 0; // next radix binning writes the weight records in its gather pass
+                        // (else: records-free gather, records by ensure_records)
+  int records_ready = 0;  // wrec / pk hold the last binning's records
   int want_drec = 0;    // next binning also writes derivative records (analytic step)
   int drec_ready = 0;   // d_drec holds the last binning's derivative records
   cufftHandle fwd, inv3, inv1;
@@ -395,6 +398,11 @@ Geom make_geom(const esp_plan* p);
 // Launchers (each returns cudaError_t of the launch).
 cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
                        long long n, cudaStream_t s);
+// Weight records of the current bins, if the binning pass skipped them (the
+// record consumers: cp.async gathers, the tiny-grid spread, local pressure).
+cudaError_t ensure_records(esp_plan* p, cudaStream_t s);
+// The spread will run k_spread_warp (weights from u, no records).
+bool spread_uses_warp(const esp_plan* p);
 // Tiles into the scratch blocks, then (with_combine) the halo combine into
 // d_grid.
 cudaError_t launch_spread(esp_plan* p, cudaStream_t s, bool with_combine = true);

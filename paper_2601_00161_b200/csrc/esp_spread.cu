@@ -392,13 +392,26 @@ CombineTabs combine_tabs(const esp_plan* p) {
   return ct;
 }
 
-template <typename real, int P>
-static cudaError_t spread_p(esp_plan* p, cudaStream_t s, bool with_combine) {
-  Geom g = make_geom(p);
+bool spread_uses_warp(const esp_plan* p) {
   static const bool legacy = std::getenv("ESP_SPREAD_LEGACY") != nullptr;   // A/B diagnostics
   // k_spread_warp needs enough tiles to fill the SMs; tiny grids keep the
   // 4-warp column-block kernel
-  if (P <= 8 && !legacy && p->n_tiles_s * 2 >= 148 * 4) {
+  return p->P <= 8 && !legacy && p->n_tiles_s * 2 >= 148 * 4;
+}
+
+// Measured and rejected (config 4, spread kernel ms): evaluating the weights
+// inside k_spread_warp from u instead of reading the binning pass's records —
+// 2.97 with the per-chunk prologue on the accumulating threads, 2.86-3.6 with
+// 32/64/96 producer threads filling a double-buffered stage behind named
+// barriers (fewer accumulating warps per SM) — against 1.85 + 0.56 for the
+// separate coalesced records pass.
+template <typename real, int P>
+static cudaError_t spread_p(esp_plan* p, cudaStream_t s, bool with_combine) {
+  Geom g = make_geom(p);
+  // both spread kernels read the per-particle weight records
+  const cudaError_t er = ensure_records(p, s);
+  if (er != cudaSuccess) return er;
+  if (P <= 8 && spread_uses_warp(p)) {
     constexpr int PW = P <= 8 ? P : 8;
     static const int rows_env = std::getenv("ESP_SPREAD_ROWS") ? std::atoi(std::getenv("ESP_SPREAD_ROWS")) : 0;
     if (rows_env == 1) {
