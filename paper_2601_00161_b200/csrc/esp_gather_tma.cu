@@ -215,7 +215,11 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
 #pragma unroll
           for (int i = 0; i < 4; ++i) wx[i] = (e + 2 * i < P) ? W[e + 2 * i] : 0.0;
 #pragma unroll
-          for (int k = 0; k < P; ++k) wz[k] = W[16 + k];
+          for (int k = 0; k < P; k += 2) {               // 16-byte broadcast loads
+            const double2 v = *reinterpret_cast<const double2*>(W + 16 + k);
+            wz[k] = v.x;
+            if (k + 1 < P) wz[k + 1] = v.y;
+          }
           const int row = (zl * 16 + yl + j) * R;
           const double* col[4];
 #pragma unroll
@@ -241,18 +245,21 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
           ay = (by[0] + by[1]) * wy;
           az = (bz[0] + bz[1]) * wy;
         }
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
-          ax += __shfl_xor_sync(0xffffffffu, ax, o);
-          ay += __shfl_xor_sync(0xffffffffu, ay, o);
-          az += __shfl_xor_sync(0xffffffffu, az, o);
-        }
-        if (sub == 0 && live) {
+        // transposed 16-lane reduction of (ax, ay, az): 5 double shuffles
+        // instead of 12 (shuffles share the shared-memory datapath); the
+        // totals land in lanes 0 / 4 / 8 of the half-warp
+        const unsigned full_mask = 0xffffffffu;
+        const bool h8 = sub & 8, h4 = sub & 4;
+        const double r0 = __shfl_xor_sync(full_mask, h8 ? ax : az, 8);
+        const double r1 = __shfl_xor_sync(full_mask, h8 ? ay : 0.0, 8);
+        const double v0 = (h8 ? az : ax) + r0;
+        const double v1 = (h8 ? 0.0 : ay) + r1;
+        double v = (h4 ? v1 : v0) + __shfl_xor_sync(full_mask, h4 ? v0 : v1, 4);
+        v += __shfl_xor_sync(full_mask, v, 2);
+        v += __shfl_xor_sync(full_mask, v, 1);
+        if ((sub & 3) == 0 && sub < 12 && live) {
           const double q = s_qv[pl];
-          double* f = forces + 3 * (long long)s_ai[3 * KB + pl];
-          f[0] = -q * ax;
-          f[1] = -q * ay;
-          f[2] = -q * az;
+          forces[3 * (long long)s_ai[3 * KB + pl] + (sub >> 2)] = -q * v;
         }
       }
       __syncwarp();                               // the batch slots are rewritten next
