@@ -88,9 +88,12 @@ __host__ __device__ constexpr int pairs_x(int N) {
 }
 // y/z lines: one 128-byte segment of consecutive kx per row on large grids;
 // 2 lines on small grids.
+#ifndef ESP_YZ_SEG
+#define ESP_YZ_SEG 128   // bytes of consecutive kx per row and CTA on large grids
+#endif
 template <typename real>
 __host__ __device__ constexpr int lines_yz(int N) {
-  return N > 128 ? 128 / (2 * (int)sizeof(real)) : 2;
+  return N > 128 ? ESP_YZ_SEG / (2 * (int)sizeof(real)) : 2;
 }
 template <typename real>
 __host__ __device__ constexpr int threads_yz(int N) {

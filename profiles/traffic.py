@@ -14,7 +14,9 @@ STAGE = {
     "k_spread_tiles": "spread", "k_spread_warp": "spread", "k_combine": "combine", "k_x_r2c": "fft_x",
     "k_y_fwd": "fft_y", "k_z_reduce": "fft_z_scale_reduce", "k_z_ik": "ifft_z_ik",
     "k_y_inv": "ifft_y", "k_x_c2r": "ifft_x", "k_xy_fwd": "fft_xy", "k_yx_inv": "ifft_yx", "k_gather_warp": "gather",
-    "k_gather_ik": "gather", "k_scale_reduce": "scale_reduce",
+    "k_gather_ik": "gather", "k_gather_tma": "gather", "k_scale_reduce": "scale_reduce",
+    "k_bin_keys": "bin_keys", "k_bin_gather": "bin_gather", "k_bin_records_u": "bin_records",
+    "k_bin_sorted": "bin_gather_weights",
 }
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
