@@ -89,8 +89,7 @@ def configs():
         r = run_reference(w.h, raw, q, w.M, w.P, w.delta, w.r_c,
                           with_grid=(idx == 0))
         F = r.pop("F")
-        stride = 1 if idx == 0 else 97
-        sel = np.arange(0, w.n, stride)
+        sel = np.arange(w.n)          # every atom's force (full parity, not a sample)
         save(f"cfg{idx}", pos_head=pos[:4], pos_sum=pos.sum(axis=0),
              F_idx=sel, F_sel=F[sel], F_rms=np.sqrt(np.mean(np.sum(F * F, axis=1))),
              F_sum=F.sum(axis=0), **r)
