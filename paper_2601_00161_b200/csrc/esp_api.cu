@@ -477,7 +477,8 @@ int esp_plan_set_cell(esp_plan* p, const esp_cell_desc* c, void* stream) {
                               (p->M[0] == 32 || p->M[0] == 48 || p->M[0] == 64);
       if (p->fused && !p->d_fpad && !plane_grid && esp::tma_gather_eligible(p)) {
         p->fpad = esp::make_field_pad(p);
-        const size_t fb = sizeof(double) * 3 * (size_t)p->fpad.cstride;
+        const size_t fb = (p->precision == ESP_FP64 ? sizeof(double) : sizeof(float)) * 3 *
+                          (size_t)p->fpad.cstride;
         ESP_CUDA(cudaMalloc(&p->d_fpad, fb));
         ESP_CUDA(cudaMemset(p->d_fpad, 0, fb));
         if (esp::make_field_tmap(p) != cudaSuccess) {   // no TMA: the cp.async gather

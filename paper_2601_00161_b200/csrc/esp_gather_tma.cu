@@ -84,6 +84,10 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 }  // namespace
 
 constexpr int kTmaStages = 2;
+#ifndef ESP_TMA_UNROLL
+#define ESP_TMA_UNROLL 1
+#endif
+constexpr int kUnroll64 = ESP_TMA_UNROLL;   // particle pairs in flight per warp (fp64)
 
 template <int NW>
 struct TmaGatherLayout {
@@ -203,6 +207,7 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
         mbar_wait(&full[s], (it / kTmaStages) & 1);
         waited = true;
       }
+#pragma unroll kUnroll64
       for (int pp = 0; pp < nb; pp += 2) {
         const int pl = pp + p;
         const bool live = pl < nb;
@@ -271,6 +276,179 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
   }
 }
 
+// fp32 fields (precision="fp32"): one particle per warp instruction.  Boxes
+// are 20 floats wide (16 needed; fp32 TMA boxes start on 4-float
+// boundaries); lane (row j = lane >> 2, e = lane & 3) sums row y = yl + j,
+// columns xl + e + 4i (i < 2) over the 8 planes: row stride 20 floats puts
+// lane (j, e) at bank 20j + e mod 32 — all 32 distinct, one wavefront per
+// load.  Weights from u in fp32 (the fp32 table, fp64 coordinates and
+// anchors, as the rest of the fp32 path); a transposed 32-lane reduction.
+#ifndef ESP_TMA32_UNROLL
+#define ESP_TMA32_UNROLL 4   // particles in flight per warp (config 4 fp32 gather: 1 -> 3.48 ms,
+                             // 2 -> 3.22, 4 -> 3.03 at 12 warps; 8 -> 3.20)
+#endif
+constexpr int kUnroll32 = ESP_TMA32_UNROLL;
+template <int NW>
+struct TmaGather32Layout {
+  static constexpr int kRow = 20;
+  static constexpr int kBatch = 10;
+  static constexpr int kWarpW = kBatch * 24 + kBatch + 4 * kBatch;   // 4-byte slots: weights,
+                                                                      // spare, anchors + ids
+  __host__ __device__ static size_t box_elems(int PZ) { return (size_t)kRow * 16 * PZ; }
+  __host__ __device__ static size_t bytes(int PZ) {
+    size_t b = 1024;
+    b += sizeof(float) * 3 * box_elems(PZ) * kTmaStages;
+    b += sizeof(float) * (size_t)NW * kWarpW;
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(uint64_t) * 2 * kTmaStages;
+    return b;
+  }
+};
+
+template <int P, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+k_gather_tma32(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
+               const float* __restrict__ tab, const double* __restrict__ brk, int n_pieces,
+               int ncoef, const int* __restrict__ offsets, const double* __restrict__ U,
+               long long cap, const double* __restrict__ Q, const int* __restrict__ IDX,
+               double* __restrict__ forces, int xsh) {
+  static_assert(P <= 8, "the TMA gather covers stencils of at most 8 points");
+  using LY = TmaGather32Layout<NW>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const size_t box = LY::box_elems(g.PZ);
+  float* fbuf = reinterpret_cast<float*>(base);
+  float* wslot = fbuf + 3 * box * kTmaStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      base + ((sizeof(float) * (3 * box * kTmaStages + (size_t)NW * LY::kWarpW) + 15) & ~size_t(15)));
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nxy = g.ntx * g.nty;
+  const int ntiles = nxy * g.ntz;
+  const unsigned box_bytes = (unsigned)(sizeof(float) * box);
+  if (warp == NW) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int tz = t / nxy, txy = t - tz * nxy;
+        const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+        const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+        if (offsets[key0] == offsets[key1]) continue;
+        const int s = it % kTmaStages;
+        if (it >= kTmaStages) mbar_wait(&empty[s], ((it / kTmaStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], 3 * box_bytes);
+        const int tx = txy % g.ntx, ty = txy / g.ntx;
+        float* dst = fbuf + (size_t)s * 3 * box;
+        const int bx = (tx * g.TX + xsh) & ~3;   // fp32 boxes start on 4-float boundaries
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          tma_load_4d(dst + c * box, &tmap, &full[s], bx, ty * g.TY, tz * g.TZ, c);
+        ++it;
+      }
+    }
+    return;
+  }
+  const int j = lane >> 2, e = lane & 3;
+  constexpr int R = LY::kRow;
+  constexpr int KB = LY::kBatch;
+  float* Wb = wslot + warp * LY::kWarpW;                           // [KB][3][8] weights
+  int* s_ai = reinterpret_cast<int*>(Wb + KB * 24 + KB);           // [KB][3] anchors, [KB] ids
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int tz = t / nxy, txy = t - tz * nxy;
+    const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+    const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+    const long long p0 = offsets[key0], p1 = offsets[key1];
+    if (p0 == p1) continue;
+    const int tx = txy % g.ntx, ty = txy / g.ntx;
+    const int org0 = ((tx * g.TX + xsh) & ~3) - xsh, org1 = ty * g.TY, org2 = tz * g.TZ;
+    const int s = it % kTmaStages;
+    const int wr = (warp + it) % NW;
+    bool waited = false;
+    const float* F = fbuf + (size_t)s * 3 * box;
+    for (long long bb = p0 + (long long)wr * KB; bb < p1; bb += (long long)NW * KB) {
+      const int nb = (int)min((long long)KB, p1 - bb);
+      if (lane < 3 * KB) {
+        const int pl = lane / 3, d = lane - 3 * pl;
+        if (pl < nb) {
+          const double u = U[d * cap + bb + pl];
+          const double base = anchor_base(g, u);
+          float w[P];
+          stencil_weights<float, P>(ft, tab, brk, n_pieces, ncoef, u, base, g.lo, 1.0f, w);
+#pragma unroll
+          for (int ss = 0; ss < 8; ++ss) Wb[pl * 24 + d * 8 + ss] = ss < P ? w[ss < P ? ss : 0] : 0.0f;
+          s_ai[pl * 3 + d] = local_anchor(g, d, base) - (d == 0 ? org0 : (d == 1 ? org1 : org2));
+          if (d == 0) s_ai[3 * KB + pl] = IDX[bb + pl];
+        }
+      }
+      __syncwarp();
+      if (!waited) {
+        mbar_wait(&full[s], (it / kTmaStages) & 1);
+        waited = true;
+      }
+#pragma unroll kUnroll32
+      for (int pl = 0; pl < nb; ++pl) {
+        float ax = 0.f, ay = 0.f, az = 0.f;
+        if (j < P) {
+          const float* W = Wb + pl * 24;
+          const int xl = s_ai[pl * 3], yl = s_ai[pl * 3 + 1], zl = s_ai[pl * 3 + 2];
+          const float wy = W[8 + j];
+          float wx[2], wz[P];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) wx[i] = (e + 4 * i < P) ? W[e + 4 * i] : 0.f;
+#pragma unroll
+          for (int k = 0; k < P; ++k) wz[k] = W[16 + k];
+          const int row = (zl * 16 + yl + j) * R;
+          const float* c0 = F + row + min(xl + e, R - 1);
+          const float* c1 = F + row + min(xl + e + 4, R - 1);
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            const float* a = c0 + k * 16 * R;
+            const float* b = c1 + k * 16 * R;
+            const float rx = fmaf(wx[1], b[0], wx[0] * a[0]);
+            const float ry = fmaf(wx[1], b[box], wx[0] * a[box]);
+            const float rz = fmaf(wx[1], b[2 * box], wx[0] * a[2 * box]);
+            ax = fmaf(wz[k], rx, ax);
+            ay = fmaf(wz[k], ry, ay);
+            az = fmaf(wz[k], rz, az);
+          }
+          ax *= wy;
+          ay *= wy;
+          az *= wy;
+        }
+        // transposed 32-lane reduction: totals in lanes 0 / 8 / 16
+        const unsigned fm = 0xffffffffu;
+        const bool h16 = lane & 16, h8 = lane & 8;
+        const float r0 = __shfl_xor_sync(fm, h16 ? ax : az, 16);
+        const float r1 = __shfl_xor_sync(fm, h16 ? ay : 0.f, 16);
+        const float v0 = (h16 ? az : ax) + r0;
+        const float v1 = (h16 ? 0.f : ay) + r1;
+        float v = (h8 ? v1 : v0) + __shfl_xor_sync(fm, h8 ? v0 : v1, 8);
+        v += __shfl_xor_sync(fm, v, 4);
+        v += __shfl_xor_sync(fm, v, 2);
+        v += __shfl_xor_sync(fm, v, 1);
+        if ((lane & 7) == 0 && lane < 24) {
+          const double q = Q[bb + pl];
+          forces[3 * (long long)s_ai[3 * KB + pl] + (lane >> 3)] = -q * (double)v;
+        }
+      }
+      __syncwarp();
+    }
+    if (!waited) mbar_wait(&full[s], (it / kTmaStages) & 1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    ++it;
+  }
+}
+
 // Host side -------------------------------------------------------------------
 
 namespace {
@@ -308,19 +486,23 @@ FieldPad make_field_pad(const esp_plan* p) {
     f.S[d] = -p->lo;
     f.E[d] = (n[d] - 1) * T[d] + W[d];
   }
-  // x: shift so rows start on a 32-byte sector (S0 % 4 == 0), 2 columns of
-  // slack for the 18-column boxes of odd-start tiles, pitch a multiple of 4
-  const int xsh = (4 - f.S[0] % 4) % 4;
+  // x: shift so rows start on a 32-byte sector, columns of slack for the
+  // boxes of tiles that start off a 16-byte boundary (fp64: 18-column boxes
+  // from even columns; fp32: 20-column boxes from multiples of 4), pitch a
+  // whole number of sectors
+  const bool dp = p->precision == ESP_FP64;
+  const int sec = dp ? 4 : 8, slack = dp ? 2 : 4;
+  const int xsh = (sec - f.S[0] % sec) % sec;
   f.S[0] += xsh;
-  f.E[0] += xsh + 2;
-  f.E[0] = (f.E[0] + 3) & ~3;
+  f.E[0] += xsh + slack;
+  f.E[0] = (f.E[0] + sec - 1) / sec * sec;
   f.cstride = (long long)f.E[0] * f.E[1] * f.E[2];
   f.enabled = 1;
   return f;
 }
 
 bool tma_gather_eligible(const esp_plan* p) {
-  return p->precision == ESP_FP64 && p->P <= 8 && p->lo <= 0 && p->Mu[2] == p->M[2] &&
+  return p->P <= 8 && p->lo <= 0 && p->Mu[2] == p->M[2] &&
          p->zshift == 0 && p->PZ <= 16 && encode_fn() != nullptr;
 }
 
@@ -328,12 +510,16 @@ bool tma_gather_eligible(const esp_plan* p) {
 // no swizzle (the 144-byte rows are bank-conflict free for the lane map).
 cudaError_t make_field_tmap(esp_plan* p) {
   const FieldPad& f = p->fpad;
+  const bool dp = p->precision == ESP_FP64;
+  const cuuint64_t es = dp ? 8 : 4;
   cuuint64_t dims[4] = {(cuuint64_t)f.E[0], (cuuint64_t)f.E[1], (cuuint64_t)f.E[2], 3};
-  cuuint64_t strides[3] = {(cuuint64_t)f.E[0] * 8, (cuuint64_t)f.E[0] * f.E[1] * 8,
-                           (cuuint64_t)f.cstride * 8};
-  cuuint32_t box[4] = {(cuuint32_t)TmaGatherLayout<8>::kRow, 16, (cuuint32_t)p->PZ, 1};
+  cuuint64_t strides[3] = {(cuuint64_t)f.E[0] * es, (cuuint64_t)f.E[0] * f.E[1] * es,
+                           (cuuint64_t)f.cstride * es};
+  cuuint32_t box[4] = {(cuuint32_t)(dp ? TmaGatherLayout<8>::kRow : TmaGather32Layout<8>::kRow),
+                       16, (cuuint32_t)p->PZ, 1};
   cuuint32_t elem[4] = {1, 1, 1, 1};
-  CUresult r = encode_fn()(reinterpret_cast<CUtensorMap*>(p->tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+  CUresult r = encode_fn()(reinterpret_cast<CUtensorMap*>(p->tmap),
+                           dp ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                            4, p->d_fpad, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -361,11 +547,47 @@ static cudaError_t tma_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int P, int NW>
+static cudaError_t tma32_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+  Geom g = make_geom(p);
+  const size_t smem = TmaGather32Layout<NW>::bytes(p->PZ);
+  cudaError_t e = cudaFuncSetAttribute(k_gather_tma32<P, NW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<long long>(sms, p->n_tiles);
+  k_gather_tma32<P, NW><<<grid, 32 * (NW + 1), smem, s>>>(
+      *reinterpret_cast<const CUtensorMap*>(p->tmap), g, *p->h_fast, p->d_tabf, p->d_breaks,
+      p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->cap, p->d_q, p->d_idx, d_forces,
+      p->fpad.S[0] + p->lo);
+  p->launches++;
+  prof_mark(p, s, "gather");
+  return cudaGetLastError();
+}
+
+#ifndef ESP_TMA32_NW
+#define ESP_TMA32_NW 12   // fp32 consumer warps (8: 3.62 ms, 12: 3.03, 16: 3.15, 20: 3.29)
+#endif
 #ifndef ESP_TMA_NW
 #define ESP_TMA_NW 12   // consumer warps (A/B at config 4: 8 -> 4.77 ms, 12 -> 4.39, 16 -> 4.46)
 #endif
 cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s) {
   constexpr int NW = ESP_TMA_NW;
+  if (p->precision != ESP_FP64) {
+    constexpr int NW32 = ESP_TMA32_NW;
+    switch (p->P) {
+      case 2: return tma32_p<2, NW32>(p, d_forces, s);
+      case 3: return tma32_p<3, NW32>(p, d_forces, s);
+      case 4: return tma32_p<4, NW32>(p, d_forces, s);
+      case 5: return tma32_p<5, NW32>(p, d_forces, s);
+      case 6: return tma32_p<6, NW32>(p, d_forces, s);
+      case 7: return tma32_p<7, NW32>(p, d_forces, s);
+      case 8: return tma32_p<8, NW32>(p, d_forces, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (p->P) {
     case 2: return tma_p<2, NW>(p, d_forces, s);
     case 3: return tma_p<3, NW>(p, d_forces, s);

@@ -10,7 +10,9 @@ L, M, n = 40.0, (96, 96, 96), 3000
 rng = np.random.default_rng(5)
 pos = workloads.wrap_positions(np.diag([L] * 3), rng.uniform(0, L, (n, 3)))
 q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
-s = KSpaceSolver(np.diag([L] * 3), EwaldParameters(r_c=10.0, delta_split=1e-7, P=8, fixed_M=M))
+prec = sys.argv[1] if len(sys.argv) > 1 else "fp64"
+s = KSpaceSolver(np.diag([L] * 3), EwaldParameters(r_c=10.0, delta_split=1e-7, P=8, fixed_M=M,
+                                                  precision=prec))
 r = s.evaluate(pos, q)
 torch.cuda.synchronize()
 print("fields layout padded:", s.plan.fields_view().stride())
