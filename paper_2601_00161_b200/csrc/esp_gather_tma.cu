@@ -84,6 +84,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 }  // namespace
 
 constexpr int kTmaStages = 2;
+#ifndef ESP_TMA_RECORDS
+#define ESP_TMA_RECORDS 1   // the gathers read the weight records of the binning pass
+                            // (config 4 fp64: 4.21 -> 3.54 ms against evaluating them in
+                            // the batch prologue)
+#endif
 #ifndef ESP_TMA_UNROLL
 #define ESP_TMA_UNROLL 1
 #endif
@@ -110,7 +115,8 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
              const double* __restrict__ tab, const double* __restrict__ brk, int n_pieces,
              int ncoef, const int* __restrict__ offsets, const double* __restrict__ U,
              long long cap, const double* __restrict__ Q, const int* __restrict__ IDX,
-             double* __restrict__ forces, int xsh) {
+             double* __restrict__ forces, int xsh, const double* __restrict__ WREC,
+             const int* __restrict__ PK) {
   static_assert(P <= 8, "the TMA gather covers stencils of at most 8 points");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // 1 KB-aligned base; offset arithmetic on smem_raw keeps the shared state
@@ -182,6 +188,31 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
     const double* F = fbuf + (size_t)s * 3 * box;
     for (long long bb = p0 + (long long)wr * KB; bb < p1; bb += (long long)NW * KB) {
       const int nb = (int)min((long long)KB, p1 - bb);
+#if ESP_TMA_RECORDS
+      // batch prologue: the binning pass's weight records (written for the
+      // spread anyway) land with cp.async; lanes < KB decode the packed
+      // tile-local anchors and fetch q and the index
+      {
+        constexpr int kPieces = KB * 24 * 8 / 16;                 // 16 B pieces of KB records
+        const char* src = reinterpret_cast<const char*>(WREC + bb * 24);
+        const int avail = nb * 24 * 8;
+        for (int c = lane; c < kPieces; c += 32)
+          if (c * 16 < avail) {
+            const unsigned dst = smem_u32(reinterpret_cast<char*>(Wb) + c * 16);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + c * 16));
+          }
+        asm volatile("cp.async.commit_group;");
+        if (lane < nb) {
+          const int pk = PK[bb + lane];
+          s_ai[lane * 3 + 0] = (pk & 0xff) + tx * g.TX - org0;
+          s_ai[lane * 3 + 1] = (pk >> 8) & 0xff;
+          s_ai[lane * 3 + 2] = (pk >> 16) - org2;
+          s_qv[lane] = Q[bb + lane];
+          s_ai[3 * KB + lane] = IDX[bb + lane];
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+#else
       // batch prologue (overlaps the tile's TMA on the first batch): lane
       // (particle, dim) evaluates the 8 weights of one axis with the unrolled
       // Horner chains of the binning pass (uniform table reads) and the
@@ -202,6 +233,7 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
           }
         }
       }
+#endif
       __syncwarp();
       if (!waited) {
         mbar_wait(&full[s], (it / kTmaStages) & 1);
@@ -292,8 +324,9 @@ template <int NW>
 struct TmaGather32Layout {
   static constexpr int kRow = 20;
   static constexpr int kBatch = 10;
-  static constexpr int kWarpW = kBatch * 24 + kBatch + 4 * kBatch;   // 4-byte slots: weights,
-                                                                      // spare, anchors + ids
+  // 4-byte slots: weights, spare, anchors + ids; a multiple of 4 so every
+  // warp's slot starts 16-byte aligned (cp.async targets)
+  static constexpr int kWarpW = (kBatch * 24 + kBatch + 4 * kBatch + 3) & ~3;
   __host__ __device__ static size_t box_elems(int PZ) { return (size_t)kRow * 16 * PZ; }
   __host__ __device__ static size_t bytes(int PZ) {
     size_t b = 1024;
@@ -311,7 +344,8 @@ k_gather_tma32(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
                const float* __restrict__ tab, const double* __restrict__ brk, int n_pieces,
                int ncoef, const int* __restrict__ offsets, const double* __restrict__ U,
                long long cap, const double* __restrict__ Q, const int* __restrict__ IDX,
-               double* __restrict__ forces, int xsh) {
+               double* __restrict__ forces, int xsh, const float* __restrict__ WREC,
+               const int* __restrict__ PK) {
   static_assert(P <= 8, "the TMA gather covers stencils of at most 8 points");
   using LY = TmaGather32Layout<NW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -376,7 +410,30 @@ k_gather_tma32(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
     const float* F = fbuf + (size_t)s * 3 * box;
     for (long long bb = p0 + (long long)wr * KB; bb < p1; bb += (long long)NW * KB) {
       const int nb = (int)min((long long)KB, p1 - bb);
+#if ESP_TMA_RECORDS
+      {
+        constexpr int kPieces = KB * 24 * 4 / 16;                 // 16 B pieces of KB records
+        const char* src = reinterpret_cast<const char*>(WREC + bb * 24);
+        const int avail = nb * 24 * 4;
+        for (int c = lane; c < kPieces; c += 32)
+          if (c * 16 < avail) {
+            const unsigned dst = smem_u32(reinterpret_cast<char*>(Wb) + c * 16);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + c * 16));
+          }
+        asm volatile("cp.async.commit_group;");
+        if (lane < nb) {
+          const int pk = PK[bb + lane];
+          s_ai[lane * 3 + 0] = (pk & 0xff) + tx * g.TX - org0;
+          s_ai[lane * 3 + 1] = (pk >> 8) & 0xff;
+          s_ai[lane * 3 + 2] = (pk >> 16) - org2;
+          s_ai[3 * KB + lane] = IDX[bb + lane];
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      if (false) {
+#else
       if (lane < 3 * KB) {
+#endif
         const int pl = lane / 3, d = lane - 3 * pl;
         if (pl < nb) {
           const double u = U[d * cap + bb + pl];
@@ -541,7 +598,7 @@ static cudaError_t tma_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   k_gather_tma<P, NW><<<grid, 32 * (NW + 1), smem, s>>>(
       *reinterpret_cast<const CUtensorMap*>(p->tmap), g, *p->h_fast, p->d_tab, p->d_breaks,
       p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->cap, p->d_q, p->d_idx, d_forces,
-      p->fpad.S[0] + p->lo);
+      p->fpad.S[0] + p->lo, reinterpret_cast<const double*>(p->d_wrec), p->d_pk);
   p->launches++;
   prof_mark(p, s, "gather");
   return cudaGetLastError();
@@ -561,7 +618,7 @@ static cudaError_t tma32_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   k_gather_tma32<P, NW><<<grid, 32 * (NW + 1), smem, s>>>(
       *reinterpret_cast<const CUtensorMap*>(p->tmap), g, *p->h_fast, p->d_tabf, p->d_breaks,
       p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->cap, p->d_q, p->d_idx, d_forces,
-      p->fpad.S[0] + p->lo);
+      p->fpad.S[0] + p->lo, reinterpret_cast<const float*>(p->d_wrec), p->d_pk);
   p->launches++;
   prof_mark(p, s, "gather");
   return cudaGetLastError();
