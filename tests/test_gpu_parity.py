@@ -502,9 +502,17 @@ def test_analytic_forces_through_mesh_api_and_triclinic():
 FUSED_CASES = [
     ("tri_skew_p8", (64, 64, 96)),     # triclinic, P=8
     ("tri_flex_p7", (48, 48, 64)),     # triclinic, odd P
-    ("small_brick_p6", (48, 64, 64)),  # orthorhombic
+    ("small_brick_p6", (48, 64, 64)),  # orthorhombic (x != y: k_x_c2r + TMA gather)
     ("small_brick_p7", (64, 64, 96)),  # orthorhombic, odd P
     ("small_cube_p5", (48, 48, 48)),   # odd P, cubic
+    # grids whose inverse x pass is k_x_c2r (x != y or x > 64): the ghost-padded
+    # fields and the TMA gathers (fp64 and fp32), every P and odd/even anchoring
+    ("small_cube_p4", (48, 64, 48)),
+    ("small_cube_p5", (64, 48, 96)),
+    ("small_brick_p7", (96, 64, 96)),
+    ("small_brick_p8", (32, 48, 32)),
+    ("tri_flex_p7", (64, 48, 64)),     # triclinic, odd P
+    ("small_single", (48, 64, 48)),    # one charge
 ]
 
 
@@ -520,7 +528,10 @@ def test_fused_fft_path_matches_oracle(name, M, precision):
     tol = F64_TOL if precision == "fp64" else F32_TOL
     assert O.rel_scalar(E, oE) <= tol
     assert O.rel_frobenius(Pt, oP) <= tol
-    assert O.rms_rel_forces(F, oF) <= tol
+    if np.sqrt(np.mean(np.sum(oF ** 2, axis=1))) > 1e-12:
+        assert O.rms_rel_forces(F, oF) <= tol
+    else:   # a lone charge feels no self force: both are round-off zero
+        assert np.max(np.abs(F)) <= (1e-12 if precision == "fp64" else 1e-6)
     # pressure-only step: one forward transform, no inverse, same E and P
     plan.reset_counters()
     E2, P2, _ = _run(plan, g["pos"], g["q"], want_forces=False)
