@@ -714,7 +714,7 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
     p->want_drec = want_f && analytic;
     // analytic steps write weight and derivative records in one pass; other
     // steps bin with the records-free gather and a coalesced records pass
-    p->need_records = want_f && analytic;
+    p->need_records = 0;   // records (and derivative records) by the coalesced pass
     rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
     p->want_drec = 0;
     p->need_records = 0;
@@ -726,7 +726,8 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
     if (want_f) {
       p->inv_count += analytic ? 1 : 3;
       if (p->last_n > 0)
-        ESP_CUDA(analytic          ? esp::launch_gather_grad(p, d_forces, s0)
+        ESP_CUDA(analytic ? (p->fpad_written ? esp::launch_gather_grad_tma(p, d_forces, s0)
+                                             : esp::launch_gather_grad(p, d_forces, s0))
                  : p->fpad_written ? esp::launch_gather_tma(p, d_forces, s0)
                                    : esp::launch_gather_ik(p, d_forces, s0));
     }

@@ -209,16 +209,18 @@ __global__ void k_bin_gather(Geom g, long long n, long long cap, const int* __re
 
 // Weight records from the binned grid coordinates (deferred records:
 // ensure_records), three threads per particle; key = the sorted bin key.
-template <typename real, int P>
+template <typename real, int P, bool DREC>
 __global__ void __launch_bounds__(3 * kBinPerBlock)
 k_bin_records_u(Geom g, FastTab ft, const real* __restrict__ tab, const double* __restrict__ brk,
                 int n_pieces, int ncoef, long long n, long long cap,
                 const int* __restrict__ skey, const double* __restrict__ U,
-                real* __restrict__ wrec, int* __restrict__ pk) {
-  // the block's 32 records are assembled in shared memory and written as one
-  // contiguous run (coalesced), as in k_bin_sorted
+                real* __restrict__ wrec, int* __restrict__ pk, FastTab ftd,
+                const real* __restrict__ dtab, real* __restrict__ drec) {
+  // the block's 32 records (and, for analytic steps, derivative records) are
+  // assembled in shared memory and written as contiguous runs (coalesced)
   constexpr int RS = rec_stride(P);
   __shared__ __align__(16) real s_rec[kBinPerBlock * 3 * RS];
+  __shared__ __align__(16) real s_drec[DREC ? kBinPerBlock * 3 * RS : 2];
   __shared__ int s_pk[kBinPerBlock];
   const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
   const long long j0 = (long long)blockIdx.x * kBinPerBlock;
@@ -231,6 +233,14 @@ k_bin_records_u(Geom g, FastTab ft, const real* __restrict__ tab, const double* 
     record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
 #pragma unroll
     for (int t = 0; t < RS; ++t) s_rec[(l * 3 + d) * RS + t] = t < P ? w[t < P ? t : 0] : real(0);
+    if (DREC) {
+      real dw[P];
+      stencil_weights<real, P>(ftd, dtab, brk, n_pieces, ncoef, u, anchor_base(g, u), g.lo,
+                               real(1), dw);
+#pragma unroll
+      for (int t = 0; t < RS; ++t)
+        s_drec[(l * 3 + d) * RS + t] = t < P ? dw[t < P ? t : 0] : real(0);
+    }
     unsigned char* pb = reinterpret_cast<unsigned char*>(s_pk + l);
     if (d == 2) {
       *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
@@ -244,6 +254,10 @@ k_bin_records_u(Geom g, FastTab ft, const real* __restrict__ tab, const double* 
   real* dst = wrec + j0 * (3 * RS);
   for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) dst[t] = s_rec[t];
   for (int t = threadIdx.x; t < nb; t += 3 * kBinPerBlock) pk[j0 + t] = s_pk[t];
+  if (DREC) {
+    real* ddst = drec + j0 * (3 * RS);
+    for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) ddst[t] = s_drec[t];
+  }
 }
 
 // Small key spaces (<= kScanMax keys, e.g. config 1's 4096): every scatter
@@ -549,7 +563,7 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
       p->q_ready = nullptr;
       if (e != cudaSuccess) return e;
     }
-    if (p->need_records || p->want_drec) {
+    if (p->need_records) {
       e = p->precision == ESP_FP64 ? launch_sorted_r<double>(p, g, d_pos, d_q, n, grid, B, s)
                                    : launch_sorted_r<float>(p, g, d_pos, d_q, n, grid, B, s);
       p->records_ready = 1;
@@ -623,9 +637,21 @@ static cudaError_t records_p(esp_plan* p, cudaStream_t s) {
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
   const unsigned g3 = (unsigned)((p->last_n + kBinPerBlock - 1) / kBinPerBlock);
-  k_bin_records_u<real, P><<<g3, 3 * kBinPerBlock, 0, s>>>(
-      g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->last_n, p->cap, p->d_bkey,
-      p->d_u, reinterpret_cast<real*>(p->d_wrec), p->d_pk);
+  const real* dtab = std::is_same<real, double>::value
+                         ? reinterpret_cast<const real*>(p->d_dtab)
+                         : reinterpret_cast<const real*>(p->d_dtabf);
+  // derivative records too when the step's forces are analytic
+  const bool drec = p->want_drec && P <= 8 && p->h_fast_d->enabled;
+  if (drec)
+    k_bin_records_u<real, P, true><<<g3, 3 * kBinPerBlock, 0, s>>>(
+        g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->last_n, p->cap, p->d_bkey,
+        p->d_u, reinterpret_cast<real*>(p->d_wrec), p->d_pk, *p->h_fast_d, dtab,
+        reinterpret_cast<real*>(p->d_drec));
+  else
+    k_bin_records_u<real, P, false><<<g3, 3 * kBinPerBlock, 0, s>>>(
+        g, *p->h_fast, tab, p->d_breaks, p->n_pieces, p->ncoef, p->last_n, p->cap, p->d_bkey,
+        p->d_u, reinterpret_cast<real*>(p->d_wrec), p->d_pk, *p->h_fast_d, dtab, nullptr);
+  p->drec_ready = drec;
   p->launches++;
   prof_mark(p, s, "bin_records");
   return cudaGetLastError();

@@ -1413,7 +1413,11 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   prof_mark(p, s, "ifft_y");
   if ((e = debug_check(s, "ifft_y")) != cudaSuccess) return e;
   // ik fields of a TMA-gather plan go straight into the ghost-padded layout
-  const bool padded = ncomp == 3 && p->d_fpad != nullptr;
+  // (the fp64 potential of an analytic step too, when its binning wrote
+  // derivative records: the TMA gradient gather reads both)
+  const bool padded = p->d_fpad != nullptr &&
+                      (ncomp == 3 || (p->precision == ESP_FP64 && p->drec_ready &&
+                                      p->records_ready));
   p->fpad_written = padded ? 1 : 0;
   void* fdst = padded ? p->d_fpad : p->d_fields;
   const FieldPad pad = padded ? p->fpad : FieldPad{};

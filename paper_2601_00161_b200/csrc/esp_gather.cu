@@ -288,9 +288,6 @@ k_gather_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
 // field, three derivative sums G_d = sum w..w'_d..w f over the stencil (the
 // derivative on axis d), F_a = -q sum_d G_d J[d][a] with J = du/dr.
 // Same lane mapping and conflict-free strides as k_gather_warp's f_z tile.
-struct Jac {
-  double j[9];
-};
 
 template <typename real, int P>
 __global__ void __launch_bounds__(kTileThreads, 2)
@@ -678,11 +675,7 @@ static cudaError_t grad_p(esp_plan* p, double* d_forces, cudaStream_t s) {
       p->launches++;
       prof_mark(p, s, "dweights");
     }
-    Jac J;
-    for (int d = 0; d < 3; ++d)
-      for (int a = 0; a < 3; ++a)
-        J.j[d * 3 + a] = p->ortho ? (d == a ? 1.0 / p->spacing[d] : 0.0)
-                                  : (double)p->Mu[d] * p->hinv[d * 3 + a];
+    const Jac J = plan_jacobian(p);
     constexpr int RS = rec_stride(P);
     const size_t smem = ((sizeof(real) * (size_t)p->PZ * GatherLayout<real, P>::kPlaneZ + 15) &
                          ~size_t(15)) +
@@ -714,6 +707,15 @@ static cudaError_t grad_r(esp_plan* p, double* d_forces, cudaStream_t s) {
     case 8: return grad_p<real, 8>(p, d_forces, s);
     default: return cudaErrorNotSupported;
   }
+}
+
+Jac plan_jacobian(const esp_plan* p) {
+  Jac J;
+  for (int d = 0; d < 3; ++d)
+    for (int a = 0; a < 3; ++a)
+      J.j[d * 3 + a] = p->ortho ? (d == a ? 1.0 / p->spacing[d] : 0.0)
+                                : (double)p->Mu[d] * p->hinv[d * 3 + a];
+  return J;
 }
 
 cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s) {

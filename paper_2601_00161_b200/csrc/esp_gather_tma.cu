@@ -506,6 +506,202 @@ k_gather_tma32(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
   }
 }
 
+// Analytic forces (mesh.py:343-349): window-gradient gather of the ONE
+// ghost-padded potential field.  Same pipeline and lane map as k_gather_tma
+// (fp64); each batch's weight and derivative-weight records (written by the
+// binning pass of an analytic step) land with cp.async.  Per plane a lane
+// forms S_w = sum_i wx_i f and S_d = sum_i wx'_i f over its 4 columns;
+// A = sum_k wz S_d, B = sum_k wz S_w, C = sum_k wz' S_w give G_x = wy A,
+// G_y = wy' B, G_z = wy C; F_a = -q sum_d G_d J[d][a].
+template <int NW>
+struct TmaGradLayout {
+  static constexpr int kRow = 18;
+  static constexpr int kBatch = 8;
+  static constexpr int kWarpW = kBatch * 48 + kBatch + 2 * kBatch;   // w | w', q, anchors+ids
+  __host__ __device__ static size_t box_elems(int PZ) { return (size_t)kRow * 16 * PZ; }
+  __host__ __device__ static size_t bytes(int PZ) {
+    size_t b = 1024;
+    b += sizeof(double) * box_elems(PZ) * kTmaStages;
+    b += sizeof(double) * (size_t)NW * kWarpW;
+    b += sizeof(uint64_t) * 2 * kTmaStages;
+    return b;
+  }
+};
+
+template <int P, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+k_gather_grad_tma(const __grid_constant__ CUtensorMap tmap, Geom g,
+                  const int* __restrict__ offsets, const double* __restrict__ WREC,
+                  const double* __restrict__ DREC, const int* __restrict__ PK,
+                  const double* __restrict__ Q, const int* __restrict__ IDX, Jac J,
+                  double* __restrict__ forces, int xsh) {
+  static_assert(P <= 8, "the TMA gather covers stencils of at most 8 points");
+  using LY = TmaGradLayout<NW>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const size_t box = LY::box_elems(g.PZ);
+  double* fbuf = reinterpret_cast<double*>(base);
+  double* wslot = fbuf + box * kTmaStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wslot + NW * LY::kWarpW);
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nxy = g.ntx * g.nty;
+  const int ntiles = nxy * g.ntz;
+  const unsigned box_bytes = (unsigned)(sizeof(double) * box);
+  if (warp == NW) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int tz = t / nxy, txy = t - tz * nxy;
+        const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+        const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+        if (offsets[key0] == offsets[key1]) continue;
+        const int s = it % kTmaStages;
+        if (it >= kTmaStages) mbar_wait(&empty[s], ((it / kTmaStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], box_bytes);
+        const int tx = txy % g.ntx, ty = txy / g.ntx;
+        tma_load_4d(fbuf + (size_t)s * box, &tmap, &full[s], (tx * g.TX + xsh) & ~1, ty * g.TY,
+                    tz * g.TZ, 0);
+        ++it;
+      }
+    }
+    return;
+  }
+  const int p = lane >> 4, sub = lane & 15;
+  const int j = sub >> 1, e = sub & 1;
+  constexpr int R = LY::kRow;
+  constexpr int KB = LY::kBatch;
+  double* Wb = wslot + warp * LY::kWarpW;        // [KB][3][8] weights, then [KB][3][8] derivatives
+  double* Db = Wb + KB * 24;
+  double* s_qv = Wb + KB * 48;
+  int* s_ai = reinterpret_cast<int*>(s_qv + KB);
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int tz = t / nxy, txy = t - tz * nxy;
+    const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZ;
+    const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZ);
+    const long long p0 = offsets[key0], p1 = offsets[key1];
+    if (p0 == p1) continue;
+    const int tx = txy % g.ntx;
+    const int org0 = ((tx * g.TX + xsh) & ~1) - xsh, org2 = tz * g.TZ;
+    const int s = it % kTmaStages;
+    const int wr = (warp + it) % NW;
+    bool waited = false;
+    const double* F = fbuf + (size_t)s * box;
+    for (long long bb = p0 + (long long)wr * KB; bb < p1; bb += (long long)NW * KB) {
+      const int nb = (int)min((long long)KB, p1 - bb);
+      {
+        constexpr int kPieces = KB * 24 * 8 / 16;
+        const int avail = nb * 24 * 8;
+        const char* sw = reinterpret_cast<const char*>(WREC + bb * 24);
+        const char* sd = reinterpret_cast<const char*>(DREC + bb * 24);
+        for (int c = lane; c < 2 * kPieces; c += 32) {
+          const int which = c >= kPieces, piece = which ? c - kPieces : c;
+          if (piece * 16 < avail) {
+            const unsigned dst =
+                smem_u32(reinterpret_cast<char*>(which ? Db : Wb) + piece * 16);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"((which ? sd : sw) + piece * 16));
+          }
+        }
+        asm volatile("cp.async.commit_group;");
+        if (lane < nb) {
+          const int pk = PK[bb + lane];
+          s_ai[lane * 3 + 0] = (pk & 0xff) + tx * g.TX - org0;
+          s_ai[lane * 3 + 1] = (pk >> 8) & 0xff;
+          s_ai[lane * 3 + 2] = (pk >> 16) - org2;
+          s_qv[lane] = Q[bb + lane];
+          s_ai[3 * KB + lane] = IDX[bb + lane];
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncwarp();
+      if (!waited) {
+        mbar_wait(&full[s], (it / kTmaStages) & 1);
+        waited = true;
+      }
+      for (int pp = 0; pp < nb; pp += 2) {
+        const int pl = pp + p;
+        const bool live = pl < nb;
+        double gx = 0.0, gy = 0.0, gz = 0.0;
+        if (live && j < P) {
+          const double* W = Wb + pl * 24;
+          const double* D = Db + pl * 24;
+          const int xl = s_ai[pl * 3], yl = s_ai[pl * 3 + 1], zl = s_ai[pl * 3 + 2];
+          double wx[4], dx[4], wz[P], dz[P];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            wx[i] = (e + 2 * i < P) ? W[e + 2 * i] : 0.0;
+            dx[i] = (e + 2 * i < P) ? D[e + 2 * i] : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            wz[k] = W[16 + k];
+            dz[k] = D[16 + k];
+          }
+          const int row = (zl * 16 + yl + j) * R;
+          const double* col[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) col[i] = F + row + min(xl + e + 2 * i, R - 1);
+          double A[2] = {0.0, 0.0}, B[2] = {0.0, 0.0}, C2[2] = {0.0, 0.0};
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            double sw = 0.0, sd = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (2 * i < P) {
+                const double v = col[i][k * 16 * R];
+                sw = fma(wx[i], v, sw);
+                sd = fma(dx[i], v, sd);
+              }
+            }
+            A[k & 1] = fma(wz[k], sd, A[k & 1]);
+            B[k & 1] = fma(wz[k], sw, B[k & 1]);
+            C2[k & 1] = fma(dz[k], sw, C2[k & 1]);
+          }
+          gx = W[8 + j] * (A[0] + A[1]);
+          gy = D[8 + j] * (B[0] + B[1]);
+          gz = W[8 + j] * (C2[0] + C2[1]);
+        }
+        const unsigned fm = 0xffffffffu;
+        const bool h8 = sub & 8, h4 = sub & 4;
+        const double r0 = __shfl_xor_sync(fm, h8 ? gx : gz, 8);
+        const double r1 = __shfl_xor_sync(fm, h8 ? gy : 0.0, 8);
+        const double v0 = (h8 ? gz : gx) + r0;
+        const double v1 = (h8 ? 0.0 : gy) + r1;
+        double v = (h4 ? v1 : v0) + __shfl_xor_sync(fm, h4 ? v0 : v1, 4);
+        v += __shfl_xor_sync(fm, v, 2);
+        v += __shfl_xor_sync(fm, v, 1);
+        // lanes 0 / 4 / 8 of the half hold G_x / G_y / G_z
+        const int hb = lane & 16;
+        const double Gx = __shfl_sync(fm, v, hb + 0);
+        const double Gy = __shfl_sync(fm, v, hb + 4);
+        const double Gz = __shfl_sync(fm, v, hb + 8);
+        if (sub < 3 && live) {
+          const double q = s_qv[pl];
+          const double j0 = sub == 0 ? J.j[0] : (sub == 1 ? J.j[1] : J.j[2]);
+          const double j1 = sub == 0 ? J.j[3] : (sub == 1 ? J.j[4] : J.j[5]);
+          const double j2 = sub == 0 ? J.j[6] : (sub == 1 ? J.j[7] : J.j[8]);
+          forces[3 * (long long)s_ai[3 * KB + pl] + sub] = -q * ((Gx * j0 + Gy * j1) + Gz * j2);
+        }
+      }
+      __syncwarp();
+    }
+    if (!waited) mbar_wait(&full[s], (it / kTmaStages) & 1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    ++it;
+  }
+}
+
 // Host side -------------------------------------------------------------------
 
 namespace {
@@ -622,6 +818,42 @@ static cudaError_t tma32_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   p->launches++;
   prof_mark(p, s, "gather");
   return cudaGetLastError();
+}
+
+template <int P, int NW>
+static cudaError_t grad_tma_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+  Geom g = make_geom(p);
+  const size_t smem = TmaGradLayout<NW>::bytes(p->PZ);
+  cudaError_t e = cudaFuncSetAttribute(k_gather_grad_tma<P, NW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<long long>(sms, p->n_tiles);
+  k_gather_grad_tma<P, NW><<<grid, 32 * (NW + 1), smem, s>>>(
+      *reinterpret_cast<const CUtensorMap*>(p->tmap), g, p->d_offsets,
+      reinterpret_cast<const double*>(p->d_wrec), reinterpret_cast<const double*>(p->d_drec),
+      p->d_pk, p->d_q, p->d_idx, plan_jacobian(p), d_forces, p->fpad.S[0] + p->lo);
+  p->launches++;
+  prof_mark(p, s, "gather_grad");
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_grad_tma(esp_plan* p, double* d_forces, cudaStream_t s) {
+  constexpr int NW = 12;
+  if (p->precision != ESP_FP64 || !p->drec_ready || !p->records_ready)
+    return cudaErrorInvalidValue;
+  switch (p->P) {
+    case 2: return grad_tma_p<2, NW>(p, d_forces, s);
+    case 3: return grad_tma_p<3, NW>(p, d_forces, s);
+    case 4: return grad_tma_p<4, NW>(p, d_forces, s);
+    case 5: return grad_tma_p<5, NW>(p, d_forces, s);
+    case 6: return grad_tma_p<6, NW>(p, d_forces, s);
+    case 7: return grad_tma_p<7, NW>(p, d_forces, s);
+    case 8: return grad_tma_p<8, NW>(p, d_forces, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 #ifndef ESP_TMA32_NW

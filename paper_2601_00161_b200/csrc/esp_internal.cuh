@@ -291,6 +291,11 @@ struct FieldPad {
   long long cstride;
 };
 
+// du/dr (grid units per length) of the gradient gathers: F_a = -q sum_d G_d J[d][a].
+struct Jac {
+  double j[9];
+};
+
 template <typename T> struct Cplx;
 template <> struct Cplx<double> { using type = double2; };
 template <> struct Cplx<float> { using type = float2; };
@@ -425,6 +430,10 @@ FieldPad make_field_pad(const esp_plan* p);
 bool tma_gather_eligible(const esp_plan* p);
 cudaError_t make_field_tmap(esp_plan* p);
 cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s);
+// Analytic (window-gradient) forces from the ghost-padded potential field
+// (fp64), reading the binning pass's weight and derivative-weight records.
+cudaError_t launch_gather_grad_tma(esp_plan* p, double* d_forces, cudaStream_t s);
+Jac plan_jacobian(const esp_plan* p);
 // Fused band-pruned forward transform + scale/reduce (+ ik spectra and the
 // inverse transforms into d_fields when want_ik).  Requires p->fused.
 cudaError_t launch_fused_fft(esp_plan* p, int want_ik, double* d_out7, cudaStream_t s);
