@@ -142,6 +142,14 @@ int esp_host_alloc(int64_t bytes, void** out);
  * its first kernel that reads the charges, so a charge copy on another
  * stream overlaps the position binning (host-buffer step).  One-shot.      */
 int esp_set_charges_event(esp_plan* plan, void* event);
+/* Every later force-computing esp_evaluate also copies its forces (N x 3
+ * doubles, original order) to `host_forces` (page-locked).  With nchunks > 1
+ * the fused ik step gathers the charges in nchunks original-index ranges and
+ * copies each range on a side stream while the next is gathered; other paths
+ * copy once after the gather.  The copy is stream-ordered: it has finished
+ * when the esp_evaluate stream is synchronised.  nchunks = 0 turns it off;
+ * at most 8.                                                                */
+int esp_set_host_forces(esp_plan* plan, double* host_forces, int32_t nchunks);
 int esp_host_free(void* p);
 
 /* --- stages (reference-function granularity) ----------------------------- */

@@ -133,6 +133,7 @@ def lib():
     L.esp_host_alloc.argtypes = [C.c_int64, C.POINTER(vp)]
     L.esp_host_free.argtypes = [vp]
     L.esp_set_charges_event.argtypes = [vp, vp]
+    L.esp_set_host_forces.argtypes = [vp, vp, C.c_int32]
     L.esp_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(vp)]
     L.esp_plan_destroy.argtypes = [vp]
     L.esp_plan_set_cell.argtypes = [vp, C.POINTER(CellDesc), vp]
@@ -188,7 +189,7 @@ def lib():
 EXPORTED = [
     "esp_plan_create", "esp_plan_destroy", "esp_plan_set_cell", "esp_last_error",
     "esp_version", "esp_copy_async", "esp_host_alloc", "esp_host_free",
-    "esp_set_charges_event", "esp_spread", "esp_forward", "esp_scale_reduce", "esp_forces_ik",
+    "esp_set_charges_event", "esp_set_host_forces", "esp_spread", "esp_forward", "esp_scale_reduce", "esp_forces_ik",
     "esp_forces_analytic", "esp_local_pressure", "esp_evaluate", "esp_counters",
     "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
     "esp_binning_radix",

@@ -98,6 +98,7 @@ static void free_all(esp_plan* p) {
   if (p->have_side) {
     cudaEventDestroy(p->ev_fork);
     cudaEventDestroy(p->ev_join);
+    for (int i = 0; i < 8; ++i) cudaEventDestroy(p->ev_chunk[i]);
     cudaStreamDestroy(p->side);
   }
   delete p->h_fast;
@@ -118,6 +119,16 @@ int esp_set_charges_event(esp_plan* p, void* event) {
     return ESP_ERR_PARAM;
   }
   p->q_ready = (cudaEvent_t)event;
+  return ESP_OK;
+}
+
+int esp_set_host_forces(esp_plan* p, double* host_forces, int32_t nchunks) {
+  if (!p || nchunks < 0 || nchunks > 8 || (nchunks > 0 && !host_forces)) {
+    set_error("esp_set_host_forces: null plan, or chunks outside [0, 8] without a buffer");
+    return ESP_ERR_PARAM;
+  }
+  p->host_forces = nchunks ? host_forces : nullptr;
+  p->host_chunks = nchunks;
   return ESP_OK;
 }
 
@@ -307,6 +318,8 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  for (int i = 0; i < 8; ++i)
+    TRY(cudaEventCreateWithFlags(&p->ev_chunk[i], cudaEventDisableTiming));
   p->have_side = 1;
   TRY(dalloc(&p->d_err_out7, 8));
   // fast window table (kernel parameter) and deterministic-combine tables
@@ -725,12 +738,34 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
     p->have_ik = 0;
     if (want_f) {
       p->inv_count += analytic ? 1 : 3;
+      const int chunked = p->host_chunks > 1 && !analytic && p->fpad_written && !p->profiling &&
+                          p->have_side && n >= 8 * p->host_chunks;
+      if (chunked) {
+        // host-buffer step: gather the charges in original-index ranges and
+        // copy each range to the pinned host buffer on the side stream while
+        // the next range is gathered
+        for (int c = 0; c < p->host_chunks; ++c) {
+          const int64_t lo = n * c / p->host_chunks, hi = n * (c + 1) / p->host_chunks;
+          ESP_CUDA(esp::launch_gather_tma(p, d_forces, s0, (int)lo, (int)hi));
+          ESP_CUDA(cudaEventRecord(p->ev_chunk[c], s0));
+          ESP_CUDA(cudaStreamWaitEvent(p->side, p->ev_chunk[c], 0));
+          ESP_CUDA(cudaMemcpyAsync(p->host_forces + 3 * lo, d_forces + 3 * lo,
+                                   3 * (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
+                                   p->side));
+        }
+        ESP_CUDA(cudaEventRecord(p->ev_join, p->side));
+        ESP_CUDA(cudaStreamWaitEvent(s0, p->ev_join, 0));
+        return ESP_OK;
+      }
       if (p->last_n > 0)
         ESP_CUDA(analytic ? (p->fpad_written ? esp::launch_gather_grad_tma(p, d_forces, s0)
                                              : esp::launch_gather_grad(p, d_forces, s0))
                  : p->fpad_written ? esp::launch_gather_tma(p, d_forces, s0)
                                    : esp::launch_gather_ik(p, d_forces, s0));
     }
+    if (want_f && p->host_chunks > 0 && n > 0)
+      ESP_CUDA(cudaMemcpyAsync(p->host_forces, d_forces, 3 * n * sizeof(double),
+                               cudaMemcpyDeviceToHost, s0));
     return ESP_OK;
   }
   if (ikmode && !p->profiling) {
@@ -754,6 +789,9 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
   if (rc) return rc;
   if (want_f) rc = analytic ? esp_forces_analytic(p, d_forces, stream)
                             : esp_forces_ik(p, d_forces, stream);
+  if (!rc && want_f && p->host_chunks > 0 && n > 0)
+    ESP_CUDA(cudaMemcpyAsync(p->host_forces, d_forces, 3 * n * sizeof(double),
+                             cudaMemcpyDeviceToHost, s0));
   return rc;
 }
 

@@ -97,7 +97,8 @@ constexpr int kUnroll64 = ESP_TMA_UNROLL;   // particle pairs in flight per warp
 template <int NW>
 struct TmaGatherLayout {
   static constexpr int kBatch = NW > 12 ? 6 : (NW > 8 ? 8 : 10);   // particles per warp batch
-  static constexpr int kWarpW = kBatch * 24 + kBatch + 2 * kBatch;   // weights, q, anchors+ids (8 B slots)
+  // 8-byte slots: weights, q, then ints: anchors [3 KB], ids [KB], kept list [KB]
+  static constexpr int kWarpW = kBatch * 24 + kBatch + 3 * kBatch;
   static constexpr int kRow = 18;         // box columns (16 needed + alignment slack)
   __host__ __device__ static size_t box_elems(int PZ) { return (size_t)kRow * 16 * PZ; }
   __host__ __device__ static size_t bytes(int PZ) {
@@ -116,7 +117,7 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
              int ncoef, const int* __restrict__ offsets, const double* __restrict__ U,
              long long cap, const double* __restrict__ Q, const int* __restrict__ IDX,
              double* __restrict__ forces, int xsh, const double* __restrict__ WREC,
-             const int* __restrict__ PK) {
+             const int* __restrict__ PK, int id_lo, int id_hi) {
   static_assert(P <= 8, "the TMA gather covers stencils of at most 8 points");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // 1 KB-aligned base; offset arithmetic on smem_raw keeps the shared state
@@ -213,6 +214,7 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
 #else
+#error "the chunked (original-index range) gather needs the records prologue"
       // batch prologue (overlaps the tile's TMA on the first batch): lane
       // (particle, dim) evaluates the 8 weights of one axis with the unrolled
       // Horner chains of the binning pass (uniform table reads) and the
@@ -240,9 +242,22 @@ k_gather_tma(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
         waited = true;
       }
 #pragma unroll kUnroll64
-      for (int pp = 0; pp < nb; pp += 2) {
-        const int pl = pp + p;
-        const bool live = pl < nb;
+      // charges of this pass (original index in [id_lo, id_hi): host-buffer
+      // steps gather in index ranges so each range's copy-out overlaps the
+      // rest), compacted in batch order
+      int* s_keep = s_ai + 4 * KB;
+      int nk;
+      {
+        const int id = lane < nb ? IDX[bb + lane] : 0;
+        const bool keep = lane < nb && id >= id_lo && id < id_hi;
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (keep) s_keep[__popc(mk & ((1u << lane) - 1u))] = lane;
+        nk = __popc(mk);
+      }
+      __syncwarp();
+      for (int pp = 0; pp < nk; pp += 2) {
+        const bool live = pp + p < nk;
+        const int pl = live ? s_keep[pp + p] : 0;
         double ax = 0.0, ay = 0.0, az = 0.0;
         if (live && j < P) {
           const double* W = Wb + pl * 24;
@@ -324,9 +339,9 @@ template <int NW>
 struct TmaGather32Layout {
   static constexpr int kRow = 20;
   static constexpr int kBatch = 10;
-  // 4-byte slots: weights, spare, anchors + ids; a multiple of 4 so every
-  // warp's slot starts 16-byte aligned (cp.async targets)
-  static constexpr int kWarpW = (kBatch * 24 + kBatch + 4 * kBatch + 3) & ~3;
+  // 4-byte slots: weights, spare, anchors + ids + kept list; a multiple of 4
+  // so every warp's slot starts 16-byte aligned (cp.async targets)
+  static constexpr int kWarpW = (kBatch * 24 + kBatch + 5 * kBatch + 3) & ~3;
   __host__ __device__ static size_t box_elems(int PZ) { return (size_t)kRow * 16 * PZ; }
   __host__ __device__ static size_t bytes(int PZ) {
     size_t b = 1024;
@@ -345,7 +360,7 @@ k_gather_tma32(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
                int ncoef, const int* __restrict__ offsets, const double* __restrict__ U,
                long long cap, const double* __restrict__ Q, const int* __restrict__ IDX,
                double* __restrict__ forces, int xsh, const float* __restrict__ WREC,
-               const int* __restrict__ PK) {
+               const int* __restrict__ PK, int id_lo, int id_hi) {
   static_assert(P <= 8, "the TMA gather covers stencils of at most 8 points");
   using LY = TmaGather32Layout<NW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -451,8 +466,19 @@ k_gather_tma32(const __grid_constant__ CUtensorMap tmap, Geom g, FastTab ft,
         mbar_wait(&full[s], (it / kTmaStages) & 1);
         waited = true;
       }
+      int* s_keep = s_ai + 4 * KB;
+      int nk;
+      {
+        const int id = lane < nb ? IDX[bb + lane] : 0;
+        const bool keep = lane < nb && id >= id_lo && id < id_hi;
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (keep) s_keep[__popc(mk & ((1u << lane) - 1u))] = lane;
+        nk = __popc(mk);
+      }
+      __syncwarp();
 #pragma unroll kUnroll32
-      for (int pl = 0; pl < nb; ++pl) {
+      for (int kk = 0; kk < nk; ++kk) {
+        const int pl = s_keep[kk];
         float ax = 0.f, ay = 0.f, az = 0.f;
         if (j < P) {
           const float* W = Wb + pl * 24;
@@ -780,7 +806,7 @@ cudaError_t make_field_tmap(esp_plan* p) {
 }
 
 template <int P, int NW>
-static cudaError_t tma_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+static cudaError_t tma_p(esp_plan* p, double* d_forces, cudaStream_t s, int id_lo, int id_hi) {
   Geom g = make_geom(p);
   const size_t smem = TmaGatherLayout<NW>::bytes(p->PZ);
   cudaError_t e = cudaFuncSetAttribute(k_gather_tma<P, NW>,
@@ -794,14 +820,15 @@ static cudaError_t tma_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   k_gather_tma<P, NW><<<grid, 32 * (NW + 1), smem, s>>>(
       *reinterpret_cast<const CUtensorMap*>(p->tmap), g, *p->h_fast, p->d_tab, p->d_breaks,
       p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->cap, p->d_q, p->d_idx, d_forces,
-      p->fpad.S[0] + p->lo, reinterpret_cast<const double*>(p->d_wrec), p->d_pk);
+      p->fpad.S[0] + p->lo, reinterpret_cast<const double*>(p->d_wrec), p->d_pk, id_lo, id_hi);
   p->launches++;
   prof_mark(p, s, "gather");
   return cudaGetLastError();
 }
 
 template <int P, int NW>
-static cudaError_t tma32_p(esp_plan* p, double* d_forces, cudaStream_t s) {
+static cudaError_t tma32_p(esp_plan* p, double* d_forces, cudaStream_t s, int id_lo,
+                           int id_hi) {
   Geom g = make_geom(p);
   const size_t smem = TmaGather32Layout<NW>::bytes(p->PZ);
   cudaError_t e = cudaFuncSetAttribute(k_gather_tma32<P, NW>,
@@ -814,7 +841,7 @@ static cudaError_t tma32_p(esp_plan* p, double* d_forces, cudaStream_t s) {
   k_gather_tma32<P, NW><<<grid, 32 * (NW + 1), smem, s>>>(
       *reinterpret_cast<const CUtensorMap*>(p->tmap), g, *p->h_fast, p->d_tabf, p->d_breaks,
       p->n_pieces, p->ncoef, p->d_offsets, p->d_u, p->cap, p->d_q, p->d_idx, d_forces,
-      p->fpad.S[0] + p->lo, reinterpret_cast<const float*>(p->d_wrec), p->d_pk);
+      p->fpad.S[0] + p->lo, reinterpret_cast<const float*>(p->d_wrec), p->d_pk, id_lo, id_hi);
   p->launches++;
   prof_mark(p, s, "gather");
   return cudaGetLastError();
@@ -862,29 +889,30 @@ cudaError_t launch_gather_grad_tma(esp_plan* p, double* d_forces, cudaStream_t s
 #ifndef ESP_TMA_NW
 #define ESP_TMA_NW 12   // consumer warps (A/B at config 4: 8 -> 4.77 ms, 12 -> 4.39, 16 -> 4.46)
 #endif
-cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s) {
+cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s, int id_lo,
+                              int id_hi) {
   constexpr int NW = ESP_TMA_NW;
   if (p->precision != ESP_FP64) {
     constexpr int NW32 = ESP_TMA32_NW;
     switch (p->P) {
-      case 2: return tma32_p<2, NW32>(p, d_forces, s);
-      case 3: return tma32_p<3, NW32>(p, d_forces, s);
-      case 4: return tma32_p<4, NW32>(p, d_forces, s);
-      case 5: return tma32_p<5, NW32>(p, d_forces, s);
-      case 6: return tma32_p<6, NW32>(p, d_forces, s);
-      case 7: return tma32_p<7, NW32>(p, d_forces, s);
-      case 8: return tma32_p<8, NW32>(p, d_forces, s);
+      case 2: return tma32_p<2, NW32>(p, d_forces, s, id_lo, id_hi);
+      case 3: return tma32_p<3, NW32>(p, d_forces, s, id_lo, id_hi);
+      case 4: return tma32_p<4, NW32>(p, d_forces, s, id_lo, id_hi);
+      case 5: return tma32_p<5, NW32>(p, d_forces, s, id_lo, id_hi);
+      case 6: return tma32_p<6, NW32>(p, d_forces, s, id_lo, id_hi);
+      case 7: return tma32_p<7, NW32>(p, d_forces, s, id_lo, id_hi);
+      case 8: return tma32_p<8, NW32>(p, d_forces, s, id_lo, id_hi);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (p->P) {
-    case 2: return tma_p<2, NW>(p, d_forces, s);
-    case 3: return tma_p<3, NW>(p, d_forces, s);
-    case 4: return tma_p<4, NW>(p, d_forces, s);
-    case 5: return tma_p<5, NW>(p, d_forces, s);
-    case 6: return tma_p<6, NW>(p, d_forces, s);
-    case 7: return tma_p<7, NW>(p, d_forces, s);
-    case 8: return tma_p<8, NW>(p, d_forces, s);
+    case 2: return tma_p<2, NW>(p, d_forces, s, id_lo, id_hi);
+    case 3: return tma_p<3, NW>(p, d_forces, s, id_lo, id_hi);
+    case 4: return tma_p<4, NW>(p, d_forces, s, id_lo, id_hi);
+    case 5: return tma_p<5, NW>(p, d_forces, s, id_lo, id_hi);
+    case 6: return tma_p<6, NW>(p, d_forces, s, id_lo, id_hi);
+    case 7: return tma_p<7, NW>(p, d_forces, s, id_lo, id_hi);
+    case 8: return tma_p<8, NW>(p, d_forces, s, id_lo, id_hi);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -394,6 +394,12 @@ struct esp_plan {
   esp::FieldPad fpad{};
   int fpad_written = 0;   // the last fused inverse wrote d_fpad (not d_fields)
   alignas(64) unsigned char tmap[128];
+  // esp_set_host_forces: the next force step copies its forces to this pinned
+  // host buffer in `host_chunks` index ranges, each as soon as it is gathered
+  double* host_forces = nullptr;
+  int host_chunks = 0;
+  cudaEvent_t ev_chunk[8] = {};
+  int have_ev_chunk = 0;
 };
 
 namespace esp {
@@ -429,7 +435,10 @@ cudaError_t launch_gather_grad(esp_plan* p, double* d_forces, cudaStream_t s);
 FieldPad make_field_pad(const esp_plan* p);
 bool tma_gather_eligible(const esp_plan* p);
 cudaError_t make_field_tmap(esp_plan* p);
-cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s);
+// Charges with original index in [id_lo, id_hi) only (host-buffer steps
+// gather in index ranges to overlap each range's copy-out).
+cudaError_t launch_gather_tma(esp_plan* p, double* d_forces, cudaStream_t s, int id_lo = 0,
+                              int id_hi = 0x7fffffff);
 // Analytic (window-gradient) forces from the ghost-padded potential field
 // (fp64), reading the binning pass's weight and derivative-weight records.
 cudaError_t launch_gather_grad_tma(esp_plan* p, double* d_forces, cudaStream_t s);

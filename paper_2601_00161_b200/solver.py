@@ -17,6 +17,7 @@ import numpy as np
 import torch
 
 import ctypes as C
+import os
 
 from . import _lib
 from .cells import CellType, infer_cell_type
@@ -200,6 +201,12 @@ class KSpaceSolver:
         return r.energy, r.pressure
 
 
+def host_force_chunks() -> int:
+    """Original-index ranges the host-buffer step gathers and copies out in
+    (ESP_HOST_CHUNKS, default 2; 1 = one copy after the gather)."""
+    return max(1, min(8, int(os.environ.get("ESP_HOST_CHUNKS", "2"))))
+
+
 class _HostStepper:
     def __init__(self, solver: "KSpaceSolver", n: int, want_forces: bool):
         f64 = torch.float64
@@ -233,6 +240,11 @@ class _HostStepper:
         qev = torch.cuda.Event()
         self._qside, self._qev = qside, qev
 
+        # the force copy-out is issued by the step itself, range by range as
+        # the gather finishes each original-index range (esp_set_host_forces)
+        handle = solver.plan._handle
+        chunks = host_force_chunks()
+
         def pre():
             main = torch.cuda.current_stream()
             qside.wait_stream(main)
@@ -240,12 +252,15 @@ class _HostStepper:
                 copy(self._d_q, self.charges)
                 qev.record(qside)
             copy(self._d_pos, self.positions)
-            _lib.check(L.esp_set_charges_event(solver.plan._handle, C.c_void_p(qev.cuda_event)),
+            _lib.check(L.esp_set_charges_event(handle, C.c_void_p(qev.cuda_event)),
                        "esp_set_charges_event")
+            if want_forces:
+                _lib.check(L.esp_set_host_forces(handle, C.c_void_p(self.forces.data_ptr()),
+                                                 chunks), "esp_set_host_forces")
 
         def post():
             if want_forces:
-                copy(self.forces, self._d_F)
+                _lib.check(L.esp_set_host_forces(handle, None, 0), "esp_set_host_forces")
             copy(self.out7, self._d_out7)
 
         self.graph = solver.plan.graph(self._d_pos, self._d_q, want_forces, self._d_out7,

@@ -729,3 +729,32 @@ def test_spread_row_layouts_bitwise_identical():
         assert out.returncode == 0, out.stderr[-2000:]
         hashes[rows] = [ln for ln in out.stdout.splitlines() if ln.startswith("HASH")][0]
     assert len(set(hashes.values())) == 1, hashes
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("chunks", [1, 2, 3, 8])
+def test_host_stepper_chunked_force_copy_bitwise(cfg, chunks, monkeypatch):
+    """The host-buffer step copies its forces out in original-index ranges
+    as the gather finishes each one (esp_set_host_forces); every range count
+    gives the device step's forces bit for bit."""
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    monkeypatch.setenv("ESP_HOST_CHUNKS", str(chunks))
+    w, pos, q = workloads.generate(cfg)
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M,
+                                          cell_type=w.cell_type), capacity=w.n)
+    e7, eF = s.evaluate_device(torch.as_tensor(pos, device="cuda"),
+                               torch.as_tensor(q, device="cuda"))
+    e7, eF = e7.cpu(), eF.cpu()
+    hs = s.host_stepper(w.n)
+    hs.positions.copy_(torch.as_tensor(pos))
+    hs.charges.copy_(torch.as_tensor(q))
+    for _ in range(2):
+        hs.forces.fill_(float("nan"))
+        h7, hF = hs.step()
+        assert torch.equal(h7, e7) and torch.equal(hF, eF)
+    # eager steps after the capture do not write the host buffer
+    hs.forces.zero_()
+    s.evaluate_device(torch.as_tensor(pos, device="cuda"), torch.as_tensor(q, device="cuda"))
+    torch.cuda.synchronize()
+    assert not hs.forces.any()
