@@ -227,11 +227,35 @@ struct CombineTabs {
 // Grid value at (x, y, z): the sum of the (at most 8) spread tile blocks
 // covering it, in a fixed (z, y, x) order (bitwise reproducible).  Used by
 // k_combine and, on the fused-transform path, by the x transform's loads.
+// Scratch layout of the spread's padded tile blocks: [tz][pz][ty][py][tx][px]
+// (px fastest, 16 wide).  One padded row of every tile along x is one
+// contiguous run of ntx * 16 values, so the combine's loads for a grid row
+// (own columns and the left neighbour's halo) stream through contiguous
+// memory instead of 72 / 56-byte pieces of blocks 80 KB apart.
+struct ScrLayout {
+  long long row;     // ntx * 16: stride of py
+  long long plane;   // nty * 16 * row: stride of pz
+};
+__host__ __device__ __forceinline__ ScrLayout scr_layout(const Geom& g) {
+  ScrLayout L;
+  L.row = (long long)g.ntx * kPad;
+  L.plane = (long long)g.nty * kPad * L.row;
+  return L;
+}
+// element (pz, py, px) of tile (tx, ty, tz)
+__host__ __device__ __forceinline__ long long scr_index(const Geom& g, const ScrLayout& L,
+                                                       int tx, int ty, int tz, int pz, int py,
+                                                       int px) {
+  return ((long long)tz * g.PZS + pz) * L.plane + ((long long)ty * kPad + py) * L.row +
+         (long long)tx * kPad + px;
+}
+
 template <typename real>
 __device__ __forceinline__ double combine_at(const Geom& g, const CombineTabs& ct,
                                              const real* __restrict__ scratch, int x, int y,
                                              int z) {
   const int nx = ct.cnt[0][x], ny = ct.cnt[1][y], nz = ct.cnt[2][z];
+  const ScrLayout L = scr_layout(g);
   double acc = 0.0;
   if (nx <= 2 && ny <= 2 && nz <= 2) {
     // common case (each axis covered by <= 2 tiles): issue all <= 8 loads
@@ -247,10 +271,9 @@ __device__ __forceinline__ double combine_at(const Geom& g, const CombineTabs& c
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int ex = ct.ent[0][x * kCombW + (c < nx ? c : 0)];
-          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
-                                 (ez & 0xffff);
           const int i = (a * 2 + b) * 2 + c;
-          addr[i] = ((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad + (ex >> 16);
+          addr[i] = scr_index(g, L, ex & 0xffff, ey & 0xffff, ez & 0xffff, ez >> 16, ey >> 16,
+                              ex >> 16);
           use[i] = a < nz && b < ny && c < nx;
         }
       }
@@ -268,10 +291,8 @@ __device__ __forceinline__ double combine_at(const Geom& g, const CombineTabs& c
         const int ey = ct.ent[1][y * kCombW + b];
         for (int c = 0; c < nx; ++c) {
           const int ex = ct.ent[0][x * kCombW + c];
-          const long long tile = (long long)((ey & 0xffff) * g.ntx + (ex & 0xffff)) * g.ntzs +
-                                 (ez & 0xffff);
-          acc += (double)scratch[((tile * g.PZS + (ez >> 16)) * kPad + (ey >> 16)) * kPad +
-                                 (ex >> 16)];
+          acc += (double)scratch[scr_index(g, L, ex & 0xffff, ey & 0xffff, ez & 0xffff,
+                                           ez >> 16, ey >> 16, ex >> 16)];
         }
       }
     }

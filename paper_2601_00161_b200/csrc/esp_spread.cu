@@ -19,10 +19,13 @@
 //    pass (unrolled Horner on the reference's degree-18 piecewise table,
 //    pswf.py:238-293) and are staged in shared memory as zero-padded rows;
 //    q is folded into the x weights.
-//  * The padded blocks go to a scratch buffer; k_combine sums, for every grid
-//    point, the contributions of the (at most 8) covering tiles in a fixed
-//    order read from precomputed per-axis tables.  No atomics: results are
-//    bitwise reproducible.
+//  * The padded blocks go to a scratch buffer laid out [tz][pz][ty][py][tx][px]
+//    (scr_index): one padded row of all tiles along x is contiguous, so the
+//    combine's loads for a grid row stream (config 4 combine 0.82 -> 0.70 ms
+//    against whole blocks stored one after another).  k_combine sums, for
+//    every grid point, the contributions of the (at most 8) covering tiles in
+//    a fixed order read from precomputed per-axis tables.  No atomics:
+//    results are bitwise reproducible.
 #include <cstdlib>
 
 #include "esp_internal.cuh"
@@ -67,9 +70,11 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
   const long long key0 = (long long)txy * g.M[2] + (long long)tz * g.TZS;
   const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZS);
   const long long p0 = offsets[key0], p1 = offsets[key1];
+  const ScrLayout SL = scr_layout(g);
+  real* blk = scratch + scr_index(g, SL, tx, ty, tz, 0, 0, 0);
   if (p0 == p1) {  // empty tile: a zero block keeps k_combine branch-free
-    real* blk = scratch + (size_t)tile * g.PZS * kPad * kPad;
-    for (int i = threadIdx.x; i < g.PZS * kPad * kPad; i += blockDim.x) blk[i] = real(0);
+    for (int i = threadIdx.x; i < g.PZS * kPad * kPad; i += blockDim.x)
+      blk[(i >> 8) * SL.plane + ((i >> 4) & 15) * SL.row + (i & 15)] = real(0);
     return;
   }
 
@@ -87,9 +92,9 @@ k_spread_tiles(Geom g, const int* __restrict__ offsets, const real* __restrict__
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 8;
   const int cx = wx0 + (lane & 7), cy = wy0 + (lane >> 3);
-  real* outA = scratch + (size_t)tile * g.PZS * kPad * kPad + (size_t)cy * kPad + cx;
-  real* outB = outA + 4 * kPad;
-  const size_t plane = (size_t)kPad * kPad;
+  real* outA = blk + cy * SL.row + cx;
+  real* outB = outA + 4 * SL.row;
+  const size_t plane = (size_t)SL.plane;
 
   real winA[P], winB[P];
 #pragma unroll
@@ -269,9 +274,11 @@ k_spread_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
   const long long key1 = (long long)txy * g.M[2] + min(g.M[2], (tz + 1) * g.TZS);
   const long long p0 = offsets[key0], p1 = offsets[key1];
   const int tid = threadIdx.x;
-  real* blk = scratch + (size_t)tile * g.PZS * kPad * kPad;
+  const ScrLayout SL = scr_layout(g);
+  real* blk = scratch + scr_index(g, SL, txy % g.ntx, txy / g.ntx, tz, 0, 0, 0);
   if (p0 == p1) {  // empty tile: a zero block keeps k_combine branch-free
-    for (int i = tid; i < g.PZS * kPad * kPad; i += NT) blk[i] = real(0);
+    for (int i = tid; i < g.PZS * kPad * kPad; i += NT)
+      blk[(i >> 8) * SL.plane + ((i >> 4) & 15) * SL.row + (i & 15)] = real(0);
     return;
   }
   // zero padding of the x/y rows is written once; chunks overwrite only the
@@ -307,8 +314,9 @@ k_spread_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
 
   // warp w covers rows [w * 2 ROWS, (w + 1) * 2 ROWS)
   const int cx = tid & 15, ry0 = (tid >> 4) * ROWS, wy0 = (tid >> 5) * 2 * ROWS;
-  real* out = blk + (size_t)ry0 * kPad + cx;
-  constexpr size_t plane = (size_t)kPad * kPad;
+  real* out = blk + ry0 * SL.row + cx;
+  const size_t plane = (size_t)SL.plane;
+  const long long rowst = SL.row;
   real win[ROWS][P];
 #pragma unroll
   for (int r = 0; r < ROWS; ++r)
@@ -318,7 +326,7 @@ k_spread_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
   auto slide_to = [&](int zl) {   // planes < zl are final for these columns
     while (zc < zl) {
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r) out[(size_t)zc * plane + r * kPad] = win[r][0];
+      for (int r = 0; r < ROWS; ++r) out[(size_t)zc * plane + r * rowst] = win[r][0];
 #pragma unroll
       for (int r = 0; r < ROWS; ++r) {
 #pragma unroll
@@ -453,6 +461,12 @@ static cudaError_t spread_p(esp_plan* p, cudaStream_t s, bool with_combine) {
     const int v = e ? std::atoi(e) : 0;
     return v >= 32 && v <= 1024 && v % 32 == 0 ? v : 128;
   }();
+  // Measured and rejected (config 4, row-contiguous scratch, combine ms):
+  // 2 / 4 points per thread with every load issued before the sums 0.83 /
+  // 0.95 against 0.70; a column-stationary CTA (32 x 8 columns x 16 planes,
+  // per-column table lookups hoisted) 0.93 (block layout); fusing the combine
+  // into the spread's CTAs (the CTA completing a brick's count sums it from
+  // L2) 6.9 ms for spread + combine: latency-bound tails hold the FMA slots.
   k_combine<real><<<(unsigned)((p->G + B - 1) / B), B, 0, s>>>(
       g, ct, reinterpret_cast<const real*>(p->d_scratch), reinterpret_cast<real*>(p->d_grid));
   p->launches++;
