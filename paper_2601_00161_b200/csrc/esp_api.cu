@@ -564,7 +564,7 @@ int esp_spread(esp_plan* p, const double* d_pos, const double* d_q, int64_t n, v
   cudaStream_t s = (cudaStream_t)stream;
   p->last_n = n;          // the bins below are for these n charges
   ESP_CUDA(esp::launch_bin(p, d_pos, d_q, n, s));
-  ESP_CUDA(esp::launch_spread(p, s));
+  ESP_CUDA(esp::launch_spread(p, s, !p->grid_in_scratch));
   if (d_grid) {
     const size_t real_sz = p->precision == ESP_FP64 ? sizeof(double) : sizeof(float);
     ESP_CUDA(cudaMemcpyAsync(d_grid, p->d_grid, real_sz * p->G, cudaMemcpyDeviceToDevice, s));
@@ -728,11 +728,19 @@ int esp_evaluate(esp_plan* p, const double* d_pos, const double* d_q, int64_t n,
     // analytic steps write weight and derivative records in one pass; other
     // steps bin with the records-free gather and a coalesced records pass
     p->need_records = 0;   // records (and derivative records) by the coalesced pass
+    // the forward x pass sums the spread's tile blocks itself where it can
+    // (no k_combine, d_grid not written by this step)
+    p->grid_in_scratch = esp::fused_x_combines(p) ? 1 : 0;
     rc = esp_spread(p, d_pos, d_q, n, nullptr, stream);
     p->want_drec = 0;
     p->need_records = 0;
-    if (rc) return rc;
-    ESP_CUDA(esp::launch_fused_fft(p, want_f ? (analytic ? 2 : 1) : 0, d_out7, s0));
+    if (rc) {
+      p->grid_in_scratch = 0;
+      return rc;
+    }
+    const cudaError_t fe = esp::launch_fused_fft(p, want_f ? (analytic ? 2 : 1) : 0, d_out7, s0);
+    p->grid_in_scratch = 0;
+    ESP_CUDA(fe);
     p->fwd_count++;
     p->have_spec = 1;   // in-band box of d_spec is current
     p->have_ik = 0;

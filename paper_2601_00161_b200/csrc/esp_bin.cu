@@ -203,8 +203,17 @@ __global__ void k_bin_gather(Geom g, long long n, long long cap, const int* __re
   u_out[j] = u[0];
   u_out[cap + j] = u[1];
   u_out[2 * cap + j] = u[2];
-  q_out[j] = q[i];
+  if (q) q_out[j] = q[i];
   idx_out[j] = i;
+}
+
+// Charges into binned order, for steps whose charges arrive late (the
+// host-buffer step copies them on a side stream): run after the records pass,
+// just before the spread, so the copy hides behind sort, gather and records.
+__global__ void k_bin_charges(long long n, const int* __restrict__ idx,
+                              const double* __restrict__ q, double* __restrict__ q_out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j < n) q_out[j] = q[idx[j]];
 }
 
 // Weight records from the binned grid coordinates (deferred records:
@@ -558,7 +567,14 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
     if (e != cudaSuccess) return e;
     p->launches += 3;
     prof_mark(p, s, "bin_sort");
-    if (p->q_ready) {  // charges copied on another stream (host-buffer step)
+    p->q_deferred = nullptr;
+    if (p->q_ready && !p->need_records) {
+      // charges still in flight on another stream (host-buffer step): bin
+      // them after the records pass (ensure_records), not here
+      p->q_deferred = d_q;
+      p->q_deferred_ev = p->q_ready;
+      p->q_ready = nullptr;
+    } else if (p->q_ready) {
       e = cudaStreamWaitEvent(s, p->q_ready, 0);
       p->q_ready = nullptr;
       if (e != cudaSuccess) return e;
@@ -568,8 +584,8 @@ cudaError_t launch_bin(esp_plan* p, const double* d_pos, const double* d_q,
                                    : launch_sorted_r<float>(p, g, d_pos, d_q, n, grid, B, s);
       p->records_ready = 1;
     } else {
-      k_bin_gather<<<grid, B, 0, s>>>(g, n, p->cap, p->d_idx_tmp, d_pos, d_q, p->d_u, p->d_q,
-                                      p->d_idx);
+      k_bin_gather<<<grid, B, 0, s>>>(g, n, p->cap, p->d_idx_tmp, d_pos,
+                                      p->q_deferred ? nullptr : d_q, p->d_u, p->d_q, p->d_idx);
       e = cudaGetLastError();
       p->records_ready = 0;
       p->drec_ready = 0;
@@ -676,9 +692,26 @@ static cudaError_t records_r(esp_plan* p, cudaStream_t s) {
 }
 
 cudaError_t ensure_records(esp_plan* p, cudaStream_t s) {
-  if (p->records_ready || p->last_n <= 0) return cudaSuccess;
-  const cudaError_t e = p->precision == ESP_FP64 ? records_r<double>(p, s) : records_r<float>(p, s);
-  if (e == cudaSuccess) p->records_ready = 1;
+  cudaError_t e = cudaSuccess;
+  if (!p->records_ready && p->last_n > 0) {
+    e = p->precision == ESP_FP64 ? records_r<double>(p, s) : records_r<float>(p, s);
+    if (e == cudaSuccess) p->records_ready = 1;
+  }
+  if (e == cudaSuccess && p->q_deferred) {
+    // late charges (launch_bin): wait for their copy, then bin them
+    const double* q = p->q_deferred;
+    p->q_deferred = nullptr;
+    e = cudaStreamWaitEvent(s, p->q_deferred_ev, 0);
+    if (e != cudaSuccess) return e;
+    if (p->last_n > 0) {
+      const int B = 256;
+      k_bin_charges<<<(unsigned)((p->last_n + B - 1) / B), B, 0, s>>>(p->last_n, p->d_idx, q,
+                                                                      p->d_q);
+      p->launches++;
+      prof_mark(p, s, "bin_charges");
+      e = cudaGetLastError();
+    }
+  }
   return e;
 }
 

@@ -319,6 +319,161 @@ k_x_r2c(const real* __restrict__ grid, typename Cx<real>::t* __restrict__ out,
   }
 }
 
+// P1 with the spread's halo combine folded in (single-GPU esp_evaluate): the
+// CTA's rows are summed straight from the spread scratch ([tz][pz][ty][py][tx][px],
+// scr_index) instead of being read from a combined grid, so the grid is never
+// written or re-read (config 4: k_combine 0.70 ms + k_x_r2c 0.17 ms -> one
+// pass over the scratch).  Per row the <= 4 covering scratch rows (z tile x
+// y tile) are looked up once per CTA into shared memory; per thread the <= 2
+// covering x entries of its (at most 3) columns are looked up once.  Every
+// point adds its <= 8 contributions in k_combine's (z, y, x) order, so the
+// sums are bitwise those of combine_at; coordinates covered by more than two
+// tiles on an axis (the periodic wrap of a partial last tile) call
+// combine_at itself.
+__host__ __device__ constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+
+template <typename real, int N>
+__global__ void __launch_bounds__(kThreadsX, ESP_X_MINB)
+k_x_comb_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
+             typename Cx<real>::t* __restrict__ out,
+             const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx) {
+  using C = typename Cx<real>::t;
+  constexpr int PP = pairs_x(N), LP = pitch(N), NT = kThreadsX, NR = 2 * PP;
+  constexpr int XP = N / gcd_c(N, NT);   // distinct columns per thread
+  static_assert(NR * 6 <= NT, "row-base setup: one thread per (row, z tile, y tile)");
+  __shared__ C buf[PP * LP];
+  // scratch row bases of (z tile a < 2, y tile b < 3): slots a * 2 + b for
+  // b < 2, 4 + a for the third y tile of a wrapped coordinate; -1 unused
+  __shared__ long long s_rb[NR][6];
+  __shared__ int s_yz[NR][2];
+  const long long r0 = 2LL * blockIdx.x * PP;
+  const ScrLayout SL = scr_layout(g);
+  bool slow = false;
+  if (threadIdx.x < NR * 6) {
+    const int rr = threadIdx.x / 6, slot = threadIdx.x - rr * 6;
+    const int a = slot < 4 ? slot >> 1 : slot - 4, b = slot < 4 ? slot & 1 : 2;
+    const long long ra = r0 + rr;
+    long long v = -1;
+    if (ra < nrows) {
+      const int z = (int)(ra / g.M[1]), y = (int)(ra - (long long)z * g.M[1]);
+      const int nz = ct.cnt[2][z], ny = ct.cnt[1][y];
+      slow = nz > 2 || ny > 3;
+      if (!slow && a < nz && b < ny) {
+        const int ez = ct.ent[2][z * kCombW + a], ey = ct.ent[1][y * kCombW + b];
+        v = scr_index(g, SL, 0, ey & 0xffff, ez & 0xffff, ez >> 16, ey >> 16, 0);
+      }
+      if (slot == 0) {
+        s_yz[rr][0] = y;
+        s_yz[rr][1] = z;
+      }
+    } else if (slot == 0) {
+      s_yz[rr][0] = -1;
+    }
+    s_rb[rr][slot] = v;
+  }
+  int xo[XP][3];
+#pragma unroll
+  for (int k = 0; k < XP; ++k) {
+    const int i = (threadIdx.x + k * NT) % N;
+    const int nx = ct.cnt[0][i];
+    slow = slow || nx > 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int ex = ct.ent[0][i * kCombW + (c < nx ? c : 0)];
+      xo[k][c] = c < nx ? (ex & 0xffff) * kPad + (ex >> 16) : -1;
+    }
+  }
+  // CTA-uniform: a coordinate of this CTA covered by more tiles than the
+  // straight-line path handles (tiny grids whose tiles wrap more than once)
+  const bool general = __syncthreads_or(slow) != 0;
+  constexpr int nld = (PP * N + NT - 1) / NT;
+  if (!general) {
+    // the 8 common loads of a point are unconditional (unused slots re-read a
+    // valid address and are not added), so they batch up; third tiles
+    // (periodic wrap) are rare and loaded where they are added.  Measured at
+    // config 4 (x pass ms): this form at 8 CTAs per SM 0.68-0.70; the loads of
+    // both rows of a pair (16) or of 2-3 pairs issued before the first sum at
+    // 8 / 5 / 4 CTAs per SM 0.78 / 1.08 / 1.22 (spills, then fewer warps):
+    // resident warps matter more than loads in flight per thread.
+#pragma unroll
+    for (int it = 0; it < nld; ++it) {
+      const int e = threadIdx.x + it * NT;
+      if ((PP * N) % NT != 0 && e >= PP * N) break;
+      const int l = e / N, i = e - l * N;
+      const int k = it % XP;
+      const int x0 = xo[k][0], x1 = xo[k][1] >= 0 ? xo[k][1] : xo[k][0], x2 = xo[k][2];
+      const bool two = xo[k][1] >= 0;
+      real v2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = 2 * l + h;
+        real v[8];
+        long long bs[4];
+#pragma unroll
+        for (int ab = 0; ab < 4; ++ab) {
+          bs[ab] = s_rb[rr][ab];
+          const real* src = scratch + (bs[ab] >= 0 ? bs[ab] : 0);
+          v[2 * ab] = src[x0];
+          v[2 * ab + 1] = src[x1];
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int ab = a * 2 + b;
+            if (bs[ab] >= 0) {
+              acc += (double)v[2 * ab];
+              if (two) acc += (double)v[2 * ab + 1];
+              if (x2 >= 0) acc += (double)scratch[bs[ab] + x2];
+            }
+          }
+          const long long b3 = s_rb[rr][4 + a];
+          if (b3 >= 0) {
+            acc += (double)scratch[b3 + x0];
+            if (two) acc += (double)scratch[b3 + x1];
+            if (x2 >= 0) acc += (double)scratch[b3 + x2];
+          }
+        }
+        v2[h] = (real)acc;
+      }
+      C z;
+      z.x = v2[0];
+      z.y = v2[1];
+      buf[l * LP + pidx(i)] = z;
+    }
+  } else {
+    for (int e = threadIdx.x; e < PP * N; e += NT) {
+      const int l = e / N, i = e - l * N;
+      C z;
+      z.x = s_yz[2 * l][0] < 0
+                ? real(0)
+                : (real)combine_at(g, ct, scratch, i, s_yz[2 * l][0], s_yz[2 * l][1]);
+      z.y = s_yz[2 * l + 1][0] < 0
+                ? real(0)
+                : (real)combine_at(g, ct, scratch, i, s_yz[2 * l + 1][0], s_yz[2 * l + 1][1]);
+      buf[l * LP + pidx(i)] = z;
+    }
+  }
+  __syncthreads();
+  fft_ip<N, 1, PP, NT, -1>(buf, tw);
+  for (int e = threadIdx.x; e < PP * ldx; e += NT) {
+    const int l = e / ldx, k = e - l * ldx;
+    const long long ra = r0 + 2 * l;
+    C A, B;
+    A.x = A.y = B.x = B.y = real(0);
+    if (k < nbx) {
+      const C zk = buf[l * LP + pidx(k)], zm = buf[l * LP + pidx((N - k) % N)];
+      A.x = real(0.5) * (zk.x + zm.x);   // (Zk + conj Zm) / 2
+      A.y = real(0.5) * (zk.y - zm.y);
+      B.x = real(0.5) * (zk.y + zm.y);   // (Zk - conj Zm) / 2i
+      B.y = real(-0.5) * (zk.x - zm.x);
+    }
+    if (ra < nrows) out[ra * ldx + k] = A;
+    if (ra + 1 < nrows) out[(ra + 1) * ldx + k] = B;
+  }
+}
+
 // Distributed (z-slab) layout of the fused transforms.  R == 0: one GPU.
 // Otherwise the in-band ky rows are split over the R ranks (by_start) and
 // the z planes too (z_start); the forward y pass and the ik pass store
@@ -1051,6 +1206,19 @@ static cudaError_t launch_x_r2c(const esp_plan* p, const void* grid, void* out, 
 }
 
 template <typename real, int N>
+static cudaError_t launch_x_comb_r2c(const esp_plan* p, void* out, const void* tw, int ldx,
+                                     int nz, cudaStream_t s) {
+  using C = typename Cx<real>::t;
+  constexpr int PP = pairs_x(N);
+  const long long nrows = (long long)p->M[1] * nz;
+  const long long nblk = (nrows + 2 * PP - 1) / (2 * PP);
+  k_x_comb_r2c<real, N><<<(unsigned)nblk, kThreadsX, 0, s>>>(
+      make_geom(p), combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
+      reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx);
+  return cudaGetLastError();
+}
+
+template <typename real, int N>
 static cudaError_t launch_y_fwd(const esp_plan* p, const void* in, void* out, const void* tw,
                                 int ldx, int nz, const SlabMap& smap, cudaStream_t s) {
   using C = typename Cx<real>::t;
@@ -1281,6 +1449,18 @@ static cudaError_t debug_check(cudaStream_t s, const char* what) {
   return e;
 }
 
+// small square planes: x and y in one kernel per plane
+static bool fused_plane(const esp_plan* p) {
+  static const bool no_plane = std::getenv("ESP_FFT_NO_PLANE") != nullptr;   // A/B diagnostics
+  return !no_plane && p->M[0] == p->M[1] && (p->M[0] == 32 || p->M[0] == 48 || p->M[0] == 64);
+}
+
+bool fused_x_combines(const esp_plan* p) {
+  // A/B diagnostics and the bitwise test; read per call so a test can switch it
+  const bool off = std::getenv("ESP_NO_XCOMBINE") != nullptr;
+  return p->fused && !off && !fused_plane(p) && p->Mu[2] == p->M[2] && p->zshift == 0;
+}
+
 template <typename real>
 static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_out7,
                              cudaStream_t s) {
@@ -1289,10 +1469,7 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   const int ldx = f->ldx;
   SlabMap one;   // single-GPU layout
   std::memset(&one, 0, sizeof(one));
-  // small square planes: x and y in one kernel per plane
-  static const bool no_plane = std::getenv("ESP_FFT_NO_PLANE") != nullptr;   // A/B diagnostics
-  const bool plane = !no_plane && p->M[0] == p->M[1] &&
-                     (p->M[0] == 32 || p->M[0] == 48 || p->M[0] == 64);
+  const bool plane = fused_plane(p);
   if (plane) {
     switch (p->M[0]) {
       case 32: e = launch_xy_fwd<real, 32>(p, f->bufB, f->tw[0], ldx, s); break;
@@ -1304,11 +1481,21 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
     prof_mark(p, s, "fft_xy");
     if ((e = debug_check(s, "fft_xy")) != cudaSuccess) return e;
   } else {
-    switch (p->M[0]) {
+    if (p->grid_in_scratch) {
+      // the spread left its tile blocks uncombined: sum them in the x pass
+      switch (p->M[0]) {
+#define ESP_CASE(v) \
+  case v: e = launch_x_comb_r2c<real, v>(p, f->bufA, f->tw[0], ldx, p->M[2], s); break;
+        ESP_FFT_SIZES(ESP_CASE)
+#undef ESP_CASE
+      }
+    } else {
+      switch (p->M[0]) {
 #define ESP_CASE(v) \
   case v: e = launch_x_r2c<real, v>(p, p->d_grid, f->bufA, f->tw[0], ldx, p->M[2], s); break;
-      ESP_FFT_SIZES(ESP_CASE)
+        ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
+      }
     }
     if (e != cudaSuccess) return e;
     p->launches++;

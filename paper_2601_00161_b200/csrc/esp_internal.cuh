@@ -408,12 +408,20 @@ struct esp_plan {
   int profiling;
   int n_ev;
   cudaEvent_t q_ready = nullptr;   // esp_set_charges_event: wait before reading q
+  // radix binning with late charges: the caller's q, binned by ensure_records
+  // after the records pass (k_bin_charges) once q_deferred_ev has fired
+  const double* q_deferred = nullptr;
+  cudaEvent_t q_deferred_ev = nullptr;
   cudaEvent_t ev[48];
   const char* ev_name[48];
   // TMA gather (esp_gather_tma.cu): ghost-padded ik fields and their tensor map
   void* d_fpad = nullptr;
   esp::FieldPad fpad{};
   int fpad_written = 0;   // the last fused inverse wrote d_fpad (not d_fields)
+  // esp_evaluate on the band-pruned transforms: the spread leaves its tile
+  // blocks in d_scratch and the forward x pass sums them (k_x_comb_r2c);
+  // d_grid is then not written by that step
+  int grid_in_scratch = 0;
   alignas(64) unsigned char tmap[128];
   // esp_set_host_forces: the next force step copies its forces to this pinned
   // host buffer in `host_chunks` index ranges, each as soon as it is gathered
@@ -439,6 +447,9 @@ bool spread_uses_warp(const esp_plan* p);
 // d_grid.
 cudaError_t launch_spread(esp_plan* p, cudaStream_t s, bool with_combine = true);
 CombineTabs combine_tabs(const esp_plan* p);
+// The fused transforms' forward x pass can sum the spread's tile blocks itself
+// (no k_combine, no grid round trip): separate x and y passes, one GPU.
+bool fused_x_combines(const esp_plan* p);
 cudaError_t launch_scale_reduce(esp_plan* p, double* d_out7, int write_ik,
                                 cudaStream_t s);
 // Output placement of the 3 gathered values of particle id:

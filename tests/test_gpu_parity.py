@@ -561,6 +561,26 @@ def test_fused_and_cufft_paths_agree(monkeypatch):
     assert O.rel_scalar(E3, Ea) <= 1e-14 and O.rel_frobenius(P3, Pa) <= 1e-14
 
 
+@pytest.mark.parametrize("name,M", [("small_brick_p8", (32, 48, 32)), ("small_brick_p7", (96, 64, 96)),
+                                    ("small_cube_p4", (48, 64, 48)), ("tri_flex_p7", (64, 48, 64)),
+                                    ("small_brick_p6", (128, 96, 64))])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_x_pass_combine_bitwise_equals_separate_combine(name, M, precision, monkeypatch):
+    """esp_evaluate sums the spread's tile blocks inside the forward x pass
+    (k_x_comb_r2c); ESP_NO_XCOMBINE keeps k_combine + k_x_r2c.  Same sums in
+    the same order: bitwise-identical energy, pressure and forces, also where
+    the periodic wrap puts more than two tiles on a coordinate."""
+    g = golden(name)
+    plan = _plan_for(g, M=M, precision=precision)
+    assert plan.fft_path == "fused"
+    Ea, Pa, Fa = _run(plan, g["pos"], g["q"])
+    la = plan.launches_last_step()
+    monkeypatch.setenv("ESP_NO_XCOMBINE", "1")
+    Eb, Pb, Fb = _run(plan, g["pos"], g["q"])
+    assert plan.launches_last_step() == la + 1
+    assert Ea == Eb and np.array_equal(Pa, Pb) and np.array_equal(Fa, Fb)
+
+
 def test_unsupported_lengths_fall_back_to_cufft():
     g = golden("tri_skew_p8")                  # M = (64, 64, 80): 80 not a fused length
     plan = _plan_for(g)
@@ -731,15 +751,19 @@ def test_spread_row_layouts_bitwise_identical():
     assert len(set(hashes.values())) == 1, hashes
 
 
-@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("cfg,radix", [(1, False), (2, False), (1, True), (2, True)])
 @pytest.mark.parametrize("chunks", [1, 2, 3, 8])
-def test_host_stepper_chunked_force_copy_bitwise(cfg, chunks, monkeypatch):
+def test_host_stepper_chunked_force_copy_bitwise(cfg, radix, chunks, monkeypatch):
     """The host-buffer step copies its forces out in original-index ranges
     as the gather finishes each one (esp_set_host_forces); every range count
-    gives the device step's forces bit for bit."""
+    gives the device step's forces bit for bit.  ``radix``: the large-N
+    binning path, where the step bins the late charges after the records
+    pass (k_bin_charges) so their copy hides behind the binning."""
     torch = _torch()
     from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
     monkeypatch.setenv("ESP_HOST_CHUNKS", str(chunks))
+    if radix:
+        monkeypatch.setenv("ESP_SORT_THRESHOLD", "0")
     w, pos, q = workloads.generate(cfg)
     s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M,
                                           cell_type=w.cell_type), capacity=w.n)
