@@ -186,7 +186,11 @@ int esp_evaluate(esp_plan* plan, const double* d_pos, const double* d_q,
 int esp_counters(const esp_plan* plan, int64_t* forward, int64_t* inverse);
 int esp_reset_counters(esp_plan* plan);
 /* Device pointers into the plan (valid until destroy / next set_cell).     */
-void* esp_grid_ptr(esp_plan* plan);       /* real grid, [z][y][x]          */
+void* esp_grid_ptr(esp_plan* plan);       /* real grid, [z][y][x]: the grid of the
+                                             last esp_spread (esp_evaluate on the
+                                             fused transforms sums the spread's tile
+                                             blocks inside its x pass and does not
+                                             write this grid)                  */
 void* esp_spectrum_ptr(esp_plan* plan);   /* complex half spectrum          */
 void* esp_fields_ptr(esp_plan* plan);     /* 3 ik force fields (layout below) */
 /* Layout of the fields behind esp_fields_ptr after the last force step:

@@ -1,0 +1,72 @@
+// DFMA issue-rate probe for the spread's operand pattern: 32 accumulators
+// (4 rows x 8 planes) per thread, acc[r][s] += a[r] * wz[s], against the
+// resident warps per SM.  Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a
+//   -o tools/bin/fp64_pattern_probe tools/fp64_pattern_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int MODE>
+__global__ void __launch_bounds__(64) k(double* out, int iters, const double* __restrict__ w) {
+  __shared__ double sw[64 * 16];
+  for (int i = threadIdx.x; i < 64 * 16; i += 64) sw[i] = w[i];
+  __syncthreads();
+  double acc[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) acc[r][s] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+    const double* p = sw + (i & 63) * 16;
+    double wz[8], a[4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) wz[s] = p[s];                 // broadcast loads
+    if (MODE == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = p[8 + r] * p[12 + (threadIdx.x & 3)];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = p[8 + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int s = 0; s < 8; ++s) acc[r][s] = fma(a[r], wz[s], acc[r][s]);
+  }
+  double t = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) t += acc[r][s];
+  if (t == 1234.5) out[0] = t;
+}
+
+int main() {
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  double *d, *w;
+  cudaMalloc(&d, 8);
+  cudaMalloc(&w, 64 * 16 * 8);
+  cudaMemset(w, 0, 64 * 16 * 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000;
+  for (int mode = 0; mode < 2; ++mode)
+    for (int cps : {1, 2, 4, 6, 8, 12, 16}) {   // CTAs (2 warps each) per SM
+      // limit residency with dynamic shared memory
+      const int smem = 220 * 1024 / cps - 9 * 1024;
+      auto kern = mode == 0 ? k<0> : k<1>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      kern<<<nsm * cps, 64, smem>>>(d, 100, w);
+      cudaEventRecord(e0);
+      kern<<<nsm * cps, 64, smem>>>(d, iters, w);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double fl = 2.0 * 32 * iters * (double)nsm * cps * 64;
+      printf("mode %d warps/SM %2d: %.2f TFLOP/s (%.3f ms) %s\n", mode, 2 * cps, fl / ms / 1e9, ms,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
