@@ -185,6 +185,11 @@ int esp_evaluate(esp_plan* plan, const double* d_pos, const double* d_q,
 /* --- introspection -------------------------------------------------------- */
 int esp_counters(const esp_plan* plan, int64_t* forward, int64_t* inverse);
 int esp_reset_counters(esp_plan* plan);
+/* Add to the transform counters: a captured CUDA graph counts its transforms
+ * when it is captured, not when it replays, so the graph owner adds the
+ * captured step's counts at every replay (TransformProvider counters,
+ * mesh.py:33-55).                                                           */
+int esp_add_counters(esp_plan* plan, int64_t forward, int64_t inverse);
 /* Device pointers into the plan (valid until destroy / next set_cell).     */
 void* esp_grid_ptr(esp_plan* plan);       /* real grid, [z][y][x]: the grid of the
                                              last esp_spread (esp_evaluate on the

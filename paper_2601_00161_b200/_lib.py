@@ -147,6 +147,7 @@ def lib():
     L.esp_evaluate.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp]
     L.esp_counters.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.esp_reset_counters.argtypes = [vp]
+    L.esp_add_counters.argtypes = [vp, C.c_int64, C.c_int64]
     L.esp_grid_ptr.argtypes = [vp]
     L.esp_grid_ptr.restype = vp
     L.esp_spectrum_ptr.argtypes = [vp]
@@ -191,7 +192,7 @@ EXPORTED = [
     "esp_version", "esp_copy_async", "esp_host_alloc", "esp_host_free",
     "esp_set_charges_event", "esp_set_host_forces", "esp_spread", "esp_forward", "esp_scale_reduce", "esp_forces_ik",
     "esp_forces_analytic", "esp_local_pressure", "esp_evaluate", "esp_counters",
-    "esp_reset_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
+    "esp_reset_counters", "esp_add_counters", "esp_grid_ptr", "esp_spectrum_ptr", "esp_grid_info",
     "esp_binning_radix",
     "esp_set_spectrum", "esp_set_profiling", "esp_profile_read", "esp_probe_fp64",
     "esp_gather_fields", "esp_fields_ptr", "esp_fields_layout", "esp_fft_path",

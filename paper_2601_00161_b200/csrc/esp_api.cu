@@ -810,6 +810,13 @@ int esp_counters(const esp_plan* p, int64_t* forward, int64_t* inverse) {
   return ESP_OK;
 }
 
+int esp_add_counters(esp_plan* p, int64_t forward, int64_t inverse) {
+  if (!p) return ESP_ERR_PARAM;
+  p->fwd_count += forward;
+  p->inv_count += inverse;
+  return ESP_OK;
+}
+
 int esp_reset_counters(esp_plan* p) {
   if (!p) return ESP_ERR_PARAM;
   p->fwd_count = 0;

@@ -506,10 +506,13 @@ class EspPlan:
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        before = self.counters()
         with torch.cuda.graph(g):
             body()
         torch.cuda.synchronize()
-        return PlanGraph(g, [self])
+        after = self.counters()
+        # the capture counted the step's transforms once; replays add them
+        return PlanGraph(g, [self], counted=(self, after[0] - before[0], after[1] - before[1]))
 
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.lib().esp_set_profiling(self._handle, int(bool(on))), "esp_set_profiling")
@@ -536,9 +539,13 @@ class PlanGraph:
     geometry.  Graphs are tied to a fixed N and cell; re-capture after a
     rebind."""
 
-    def __init__(self, graph, plans):
+    def __init__(self, graph, plans, counted=None):
         self.graph = graph
         self._deps = [(p, p.generation) for p in plans]
+        # (plan, forward, inverse): transforms of one captured step, added to
+        # the plan's counters at every replay (the C entries count at call
+        # time, i.e. during capture only)
+        self._counted = counted
 
     @property
     def valid(self) -> bool:
@@ -549,6 +556,10 @@ class PlanGraph:
             raise ParameterError("CUDA graph captured before a cell rebind or capacity growth "
                                  "of its plan; capture it again")
         self.graph.replay()
+        if self._counted is not None:
+            plan, fwd, inv = self._counted
+            if fwd or inv:
+                _lib.lib().esp_add_counters(plan._handle, fwd, inv)
 
 
 def probe_fp64_tflops(stream=None) -> float:

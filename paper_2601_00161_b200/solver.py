@@ -390,10 +390,14 @@ class CoulombSolver:
         torch.cuda.current_stream().wait_stream(warm)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        kp = self.kspace.plan
+        before = kp.counters()
         with torch.cuda.graph(g):
             body()
         torch.cuda.synchronize()
-        return PlanGraph(g, [self.kspace.plan, self.near]), out
+        after = kp.counters()
+        return PlanGraph(g, [kp, self.near],
+                         counted=(kp, after[0] - before[0], after[1] - before[1])), out
 
     def evaluate(self, sys, want_forces: bool = True, want_pressure: bool = True,
                  neighbors=None) -> EnergyBreakdown:

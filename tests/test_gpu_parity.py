@@ -274,9 +274,14 @@ def test_cuda_graph_replay_matches_eager():
     g, o7, oF = s.graphed(P_, Q_)
     o7.zero_()
     oF.zero_()
+    s.plan.reset_counters()
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(o7, e7) and torch.equal(oF, eF)
+    # replays count their transforms (1 forward + 3 inverse per ik step)
+    assert s.plan.counters() == (1, 3)
+    g.replay()
+    assert s.plan.counters() == (2, 6)
     # new positions in place -> replay recomputes
     P_.add_(0.37)
     g.replay()
