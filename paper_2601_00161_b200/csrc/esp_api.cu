@@ -361,6 +361,8 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
         }
       }
       p->comb_off[a] = off;
+      p->comb_max[a] = 0;
+      for (int c : cnt) p->comb_max[a] = std::max(p->comb_max[a], c);
       off += p->M[a];
       ent_all.insert(ent_all.end(), ent.begin(), ent.end());
       cnt_all.insert(cnt_all.end(), cnt.begin(), cnt.end());

@@ -474,6 +474,156 @@ k_x_comb_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
   }
 }
 
+// The same pass with the scratch rows staged by the copy engine (large grids:
+// N a multiple of 128, >= 256; one row pair per CTA; every coordinate covered
+// by <= 3 x, <= 3 y and <= 2 z tiles).  A grid row's <= 4 covering scratch
+// rows are contiguous runs of ntx * 16 values (scr_index), so one thread
+// issues one cp.async.bulk per run, completing on an mbarrier: no registers
+// hold loads in flight.  The sums then read shared memory, in k_combine's
+// (z, y, x) order (bitwise the same); third y tiles (periodic wrap) come from
+// global memory where they are added.  Config 4: 0.66 ms against 0.68 for the
+// register-staged pass.  A persistent 2-stage ring of this kernel (two CTAs
+// per SM, the next pair's copies issued before the current pair's sums) is
+// slower, 0.85 ms: one 384-point line takes ~5 us through its six barriers,
+// so the pass needs many lines in flight per SM, which the 44 KB of staging
+// per pair caps at four here.
+__device__ __forceinline__ unsigned bulk_smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bulk_mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred done;\n"
+      "WAITX_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+      "@!done bra WAITX_%=;\n"
+      "}\n" ::"r"(bulk_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kThreadsXB = 128;
+template <typename real, int N>
+__global__ void __launch_bounds__(kThreadsXB, 4)
+k_x_bulk_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
+             typename Cx<real>::t* __restrict__ out,
+             const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx) {
+  using C = typename Cx<real>::t;
+  constexpr int LP = pitch(N), NT = kThreadsXB, NR = 2;
+  static_assert(N % NT == 0, "a thread owns N / NT columns");
+  constexpr int XC = N / NT;
+  extern __shared__ __align__(128) unsigned char xb_sm[];
+  const ScrLayout SL = scr_layout(g);
+  const int row_elems = (int)SL.row;                     // ntx * 16
+  real* stage = reinterpret_cast<real*>(xb_sm);          // [2 rows][4 slots][row_elems]
+  C* buf = reinterpret_cast<C*>(xb_sm + (((size_t)8 * row_elems * sizeof(real) + 15) & ~size_t(15)));
+  __shared__ long long s_rb[NR][6];   // slots a * 2 + b (z tile a, y tile b < 2), 4 + a: third y tile
+  __shared__ __align__(8) uint64_t bar;
+  const long long r0 = 2LL * blockIdx.x;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bulk_smem_u32(&bar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < NR * 6) {
+    const int rr = threadIdx.x / 6, slot = threadIdx.x - rr * 6;
+    const int a = slot < 4 ? slot >> 1 : slot - 4, b = slot < 4 ? slot & 1 : 2;
+    const long long ra = r0 + rr;
+    long long v = -1;
+    if (ra < nrows) {
+      const int z = (int)(ra / g.M[1]), y = (int)(ra - (long long)z * g.M[1]);
+      const int nz = ct.cnt[2][z], ny = ct.cnt[1][y];
+      if (a < nz && b < ny) {
+        const int ez = ct.ent[2][z * kCombW + a], ey = ct.ent[1][y * kCombW + b];
+        v = scr_index(g, SL, 0, ey & 0xffff, ez & 0xffff, ez >> 16, ey >> 16, 0);
+      }
+    }
+    s_rb[rr][slot] = v;
+  }
+  int xo[XC][3];
+#pragma unroll
+  for (int k = 0; k < XC; ++k) {
+    const int i = threadIdx.x + k * NT;
+    const int nx = ct.cnt[0][i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int ex = ct.ent[0][i * kCombW + (c < nx ? c : 0)];
+      xo[k][c] = c < nx ? (ex & 0xffff) * kPad + (ex >> 16) : -1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned row_bytes = (unsigned)(row_elems * sizeof(real));
+    unsigned total = 0;
+#pragma unroll
+    for (int s8 = 0; s8 < 8; ++s8)
+      if (s_rb[s8 >> 2][s8 & 3] >= 0) total += row_bytes;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     bulk_smem_u32(&bar)),
+                 "r"(total)
+                 : "memory");
+#pragma unroll
+    for (int s8 = 0; s8 < 8; ++s8) {
+      const long long b = s_rb[s8 >> 2][s8 & 3];
+      if (b >= 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(bulk_smem_u32(stage + (size_t)s8 * row_elems)),
+            "l"(scratch + b), "r"(row_bytes), "r"(bulk_smem_u32(&bar))
+            : "memory");
+    }
+  }
+  bulk_mbar_wait(&bar, 0);
+#pragma unroll
+  for (int k = 0; k < XC; ++k) {
+    const int i = threadIdx.x + k * NT;
+    const int x0 = xo[k][0], x1 = xo[k][1], x2 = xo[k][2];
+    real v2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int ab = a * 2 + b;
+          if (s_rb[h][ab] >= 0) {
+            const real* row = stage + (size_t)(h * 4 + ab) * row_elems;
+            acc += (double)row[x0];
+            if (x1 >= 0) acc += (double)row[x1];
+            if (x2 >= 0) acc += (double)row[x2];
+          }
+        }
+        const long long b3 = s_rb[h][4 + a];
+        if (b3 >= 0) {
+          acc += (double)scratch[b3 + x0];
+          if (x1 >= 0) acc += (double)scratch[b3 + x1];
+          if (x2 >= 0) acc += (double)scratch[b3 + x2];
+        }
+      }
+      v2[h] = (real)acc;
+    }
+    C z;
+    z.x = v2[0];
+    z.y = v2[1];
+    buf[pidx(i)] = z;
+  }
+  __syncthreads();
+  fft_ip<N, 1, 1, NT, -1>(buf, tw);
+  for (int k = threadIdx.x; k < ldx; k += NT) {
+    C A, B;
+    A.x = A.y = B.x = B.y = real(0);
+    if (k < nbx) {
+      const C zk = buf[pidx(k)], zm = buf[pidx((N - k) % N)];
+      A.x = real(0.5) * (zk.x + zm.x);   // (Zk + conj Zm) / 2
+      A.y = real(0.5) * (zk.y - zm.y);
+      B.x = real(0.5) * (zk.y + zm.y);   // (Zk - conj Zm) / 2i
+      B.y = real(-0.5) * (zk.x - zm.x);
+    }
+    if (r0 < nrows) out[r0 * ldx + k] = A;
+    if (r0 + 1 < nrows) out[(r0 + 1) * ldx + k] = B;
+  }
+}
+
 // Distributed (z-slab) layout of the fused transforms.  R == 0: one GPU.
 // Otherwise the in-band ky rows are split over the R ranks (by_start) and
 // the z planes too (z_start); the forward y pass and the ik pass store
@@ -1040,19 +1190,80 @@ k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
   __syncthreads();
   fft_ip<N, 1, PP, NT, +1>(buf, tw);
   constexpr int nld = (PP * N + NT - 1) / NT;
+  if constexpr (N % NT == 0) {
+    // a thread's elements are its N / NT columns of every row pair: the x
+    // ghost image of each column is looked up once, the row bases come from
+    // shared memory, and a row's y / z ghost copies (a few rows per plane)
+    // take the general store (config 4: the store phase was half of this
+    // kernel's instructions)
+    constexpr int XC = N / NT;
+    if (pad.enabled) {
+      int xi[XC];
+#pragma unroll
+      for (int k = 0; k < XC; ++k) {
+        const int x = threadIdx.x + k * NT;
+        xi[k] = x + pad.S[0] + N < pad.E[0] ? N : (x + pad.S[0] - N >= 0 ? -N : 0);
+      }
+#pragma unroll
+      for (int l = 0; l < PP; ++l) {
+        const bool okA = r0 + 2 * l < nrows, okB = r0 + 2 * l + 1 < nrows;
+        const PadRows& rA = s_rows[2 * l];
+        const PadRows& rB = s_rows[2 * l + 1];
+        real* rowA = fld + (okA ? rA.base[0] : 0);
+        real* rowB = fld + (okB ? rB.base[0] : 0);
+        const int nA = okA ? rA.n : 0, nB = okB ? rB.n : 0;
+#pragma unroll
+        for (int k = 0; k < XC; ++k) {
+          const int x = threadIdx.x + k * NT;
+          const C z = buf[l * LP + pidx(x)];
+          if (okA) {
+            __stcs(rowA + x, z.x);
+            if (xi[k]) __stcs(rowA + x + xi[k], z.x);
+          }
+          if (okB) {
+            __stcs(rowB + x, z.y);
+            if (xi[k]) __stcs(rowB + x + xi[k], z.y);
+          }
+          if (nA > 1 || nB > 1) {   // y / z ghost copies of these rows
+            for (int m = 1; m < nA; ++m) {
+              __stcs(fld + rA.base[m] + x, z.x);
+              if (xi[k]) __stcs(fld + rA.base[m] + x + xi[k], z.x);
+            }
+            for (int m = 1; m < nB; ++m) {
+              __stcs(fld + rB.base[m] + x, z.y);
+              if (xi[k]) __stcs(fld + rB.base[m] + x + xi[k], z.y);
+            }
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < PP; ++l) {
+        const long long ra = r0 + 2 * l;
+#pragma unroll
+        for (int k = 0; k < XC; ++k) {
+          const int x = threadIdx.x + k * NT;
+          const C z = buf[l * LP + pidx(x)];
+          if (ra < nrows) __stcs(fld + ra * N + x, z.x);
+          if (ra + 1 < nrows) __stcs(fld + (ra + 1) * N + x, z.y);
+        }
+      }
+    }
+  } else {
 #pragma unroll 4
-  for (int it = 0; it < nld; ++it) {
-    const int e = threadIdx.x + it * NT;
-    if ((PP * N) % NT == 0 || e < PP * N) {
-      const int l = e / N, i = e - l * N;
-      const long long ra = r0 + 2 * l;
-      const C z = buf[l * LP + pidx(i)];
-      if (pad.enabled) {
-        if (ra < nrows) store_padded(pad, s_rows[2 * l], fld, i, z.x);
-        if (ra + 1 < nrows) store_padded(pad, s_rows[2 * l + 1], fld, i, z.y);
-      } else {
-        if (ra < nrows) __stcs(fld + ra * N + i, z.x);
-        if (ra + 1 < nrows) __stcs(fld + (ra + 1) * N + i, z.y);
+    for (int it = 0; it < nld; ++it) {
+      const int e = threadIdx.x + it * NT;
+      if ((PP * N) % NT == 0 || e < PP * N) {
+        const int l = e / N, i = e - l * N;
+        const long long ra = r0 + 2 * l;
+        const C z = buf[l * LP + pidx(i)];
+        if (pad.enabled) {
+          if (ra < nrows) store_padded(pad, s_rows[2 * l], fld, i, z.x);
+          if (ra + 1 < nrows) store_padded(pad, s_rows[2 * l + 1], fld, i, z.y);
+        } else {
+          if (ra < nrows) __stcs(fld + ra * N + i, z.x);
+          if (ra + 1 < nrows) __stcs(fld + (ra + 1) * N + i, z.y);
+        }
       }
     }
   }
@@ -1216,6 +1427,34 @@ static cudaError_t launch_x_comb_r2c(const esp_plan* p, void* out, const void* t
       make_geom(p), combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
       reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx);
   return cudaGetLastError();
+}
+
+// Bulk-staged variant for the long rows (N a multiple of 128, >= 256): eight
+// scratch rows plus the FFT line in dynamic shared memory, four CTAs per SM.
+template <typename real, int N>
+static cudaError_t launch_x_bulk_r2c(const esp_plan* p, void* out, const void* tw, int ldx,
+                                     int nz, cudaStream_t s, bool* taken) {
+  using C = typename Cx<real>::t;
+  *taken = false;
+  if constexpr (N % kThreadsXB == 0 && N >= 256) {
+    static const bool off = std::getenv("ESP_NO_XBULK") != nullptr;   // A/B diagnostics
+    const Geom g = make_geom(p);
+    const size_t stage = ((size_t)8 * g.ntx * kPad * sizeof(real) + 15) & ~size_t(15);
+    const size_t smem = stage + sizeof(C) * pitch(N);
+    if (off || smem > 56 * 1024 || p->comb_max[0] > 3 || p->comb_max[1] > 3 ||
+        p->comb_max[2] > 2)
+      return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_x_bulk_r2c<real, N>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long nrows = (long long)p->M[1] * nz;
+    k_x_bulk_r2c<real, N><<<(unsigned)((nrows + 1) / 2), kThreadsXB, smem, s>>>(
+        g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
+        reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx);
+    *taken = true;
+    return cudaGetLastError();
+  }
+  return cudaSuccess;
 }
 
 template <typename real, int N>
@@ -1483,9 +1722,14 @@ static cudaError_t fused_run(esp_plan* p, FusedFft* f, int want_ik, double* d_ou
   } else {
     if (p->grid_in_scratch) {
       // the spread left its tile blocks uncombined: sum them in the x pass
+      bool taken = false;
       switch (p->M[0]) {
-#define ESP_CASE(v) \
-  case v: e = launch_x_comb_r2c<real, v>(p, f->bufA, f->tw[0], ldx, p->M[2], s); break;
+#define ESP_CASE(v)                                                                      \
+  case v:                                                                                \
+    e = launch_x_bulk_r2c<real, v>(p, f->bufA, f->tw[0], ldx, p->M[2], s, &taken);       \
+    if (e == cudaSuccess && !taken)                                                      \
+      e = launch_x_comb_r2c<real, v>(p, f->bufA, f->tw[0], ldx, p->M[2], s);             \
+    break;
         ESP_FFT_SIZES(ESP_CASE)
 #undef ESP_CASE
       }

@@ -387,6 +387,7 @@ struct esp_plan {
   int* d_comb_ent;        // combine candidate tables (3 axes)
   int* d_comb_cnt;
   long long comb_off[3];
+  int comb_max[3];        // most tiles covering one coordinate, per axis
   esp::FastTab* h_fast;   // host copy of the fast window table (kernel param)
   esp::FastTab* h_fast_d = nullptr;   // derivative window table (analytic gather)
   int need_records = 0; // next radix binning writes the weight records in its gather pass
