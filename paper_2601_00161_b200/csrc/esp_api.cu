@@ -325,7 +325,12 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   // fast window table (kernel parameter) and deterministic-combine tables
   p->h_fast = new esp::FastTab;
   std::memset(p->h_fast, 0, sizeof(esp::FastTab));
-  if (p->n_pieces == p->P && p->ncoef == esp::kFastNC && p->P <= esp::kFastMaxP) {
+  // fast table: P pieces, each exactly one grid spacing wide (stencil_weights
+  // shares the in-piece offset between the P weights of an axis)
+  bool unit_pieces = p->n_pieces == p->P;
+  for (int i = 0; unit_pieces && i < p->n_pieces; ++i)
+    unit_pieces = d->h_window_breaks[i + 1] - d->h_window_breaks[i] == 1.0;
+  if (unit_pieces && p->ncoef == esp::kFastNC && p->P <= esp::kFastMaxP) {
     p->h_fast->enabled = 1;
     for (size_t i = 0; i < nt; ++i) {
       p->h_fast->c[i] = d->h_window_coef[i];

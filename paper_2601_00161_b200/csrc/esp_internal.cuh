@@ -180,36 +180,39 @@ __device__ __noinline__ real window_eval_slow(const real* __restrict__ coef,
 }
 
 // w[s] = qf * W(u - (base + lo + s)), s = 0..P-1.
+// Fast table (P unit-width pieces, checked at plan creation): stencil offset s
+// falls in piece P-1-s, and because the pieces are one grid spacing wide the
+// offset inside the piece, x = u - base - lo - brk[P-1], is the same for all
+// P weights — one subtraction and one range test per axis, then P
+// straight-line Horner chains that share x (coefficients are kernel-parameter
+// constants).  A tie on a piece boundary (rounding) drops to the general
+// search for all P weights.
 template <typename real, int P>
 __device__ __forceinline__ void stencil_weights(const FastTab& ft, const real* s_tab,
                                                 const double* s_brk, int n_pieces,
                                                 int ncoef, double u, double base, int lo,
                                                 real qf, real* w) {
   if (ft.enabled) {
-    const real* C = fast_coef<real>(ft);
+    const double t0 = u - (base + (double)lo);       // s = 0: piece P - 1
+    const double xd = t0 - ft.brk[P - 1];
+    if (xd >= 0.0 && t0 < ft.brk[P]) {
+      const real* C = fast_coef<real>(ft);
+      const real x = (real)xd;
 #pragma unroll
-    for (int s = 0; s < P; ++s) {
-      const double t = u - (base + (double)(lo + s));
-      const int j = P - 1 - s;
-      const bool ok = t >= ft.brk[j] && t < ft.brk[j + 1];
-      real v;
-      if (ok) {
-        const real x = (real)(t - ft.brk[j]);
+      for (int s = 0; s < P; ++s) {
+        const int j = P - 1 - s;
         real acc = C[j * kFastNC];
 #pragma unroll
         for (int m = 1; m < kFastNC; ++m) acc = fma(acc, x, C[j * kFastNC + m]);
-        v = acc;
-      } else {
-        v = window_eval_slow<real>(s_tab, s_brk, n_pieces, ncoef, t);
+        w[s] = acc * qf;
       }
-      w[s] = v * qf;
+      return;
     }
-  } else {
-#pragma unroll
-    for (int s = 0; s < P; ++s) {
-      const double t = u - (base + (double)(lo + s));
-      w[s] = window_eval<real>(s_tab, s_brk, n_pieces, ncoef, t) * qf;
-    }
+  }
+#pragma unroll 1
+  for (int s = 0; s < P; ++s) {
+    const double t = u - (base + (double)(lo + s));
+    w[s] = window_eval_slow<real>(s_tab, s_brk, n_pieces, ncoef, t) * qf;
   }
 }
 
