@@ -136,7 +136,7 @@ int esp_version(void);
 int esp_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 /* Page-locked host buffers for the host-buffer step (cudaHostAlloc).  On the
  * measured B200 box, H2D copies from these run at ~52 GB/s against ~12 GB/s
- * from torch's pinned allocator (tools/tools_copy_probe.py).               */
+ * from torch's pinned allocator (copy probe).          */
 int esp_host_alloc(int64_t bytes, void** out);
 /* The next esp_evaluate / esp_spread waits on `event` (a cudaEvent_t) before
  * its first kernel that reads the charges, so a charge copy on another
