@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 STAGE = {
-    "k_spread_tiles": "spread", "k_spread_warp": "spread", "k_combine": "combine", "k_x_comb_r2c": "fft_x", "k_x_r2c": "fft_x",
+    "k_spread_tiles": "spread", "k_spread_warp": "spread", "k_combine": "combine", "k_x_comb_r2c": "fft_x", "k_x_bulk_r2c": "fft_x", "k_x_r2c": "fft_x",
     "k_y_fwd": "fft_y", "k_z_reduce": "fft_z_scale_reduce", "k_z_ik": "ifft_z_ik",
     "k_y_inv": "ifft_y", "k_x_c2r": "ifft_x", "k_xy_fwd": "fft_xy", "k_yx_inv": "ifft_yx", "k_gather_warp": "gather",
     "k_gather_ik": "gather", "k_gather_tma": "gather", "k_scale_reduce": "scale_reduce",
