@@ -85,7 +85,7 @@ static void free_all(esp_plan* p) {
                   p->d_axis_w,  p->d_box_iy,   p->d_box_iz,  p->d_modeA,   p->d_modeB,
                   p->d_partials, p->d_err,       p->d_comb_ent, p->d_comb_cnt,
                   p->d_wrec,     p->d_pk,       p->d_drec,    p->d_err_out7,
-                  p->d_sort_tmp, p->d_partials_fft, p->d_fpad};
+                  p->d_sort_tmp, p->d_partials_fft, p->d_fpad,   p->d_zlist};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   esp_fused_fft_destroy(p->fused);
@@ -354,6 +354,7 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
     const int E[3] = {esp::kPad, esp::kPad, p->PZS};
     const int NT[3] = {p->ntx, p->nty, p->ntzs};
     long long off = 0;
+    std::vector<int> zlist;
     for (int a = 0; a < 3; ++a) {
       std::vector<int> ent, cnt;
       esp::build_combine_axis(p->M[a], T[a], E[a], NT[a], p->lo, ent, cnt);
@@ -368,12 +369,25 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
       p->comb_off[a] = off;
       p->comb_max[a] = 0;
       for (int c : cnt) p->comb_max[a] = std::max(p->comb_max[a], c);
+      if (a == 2) {
+        // z planes by the number of covering z tiles: one first, then more
+        // (the bulk-staged x pass stages half as many scratch rows for the
+        // first class and runs more CTAs per SM on it)
+        zlist.clear();
+        for (int z = 0; z < p->M[2]; ++z)
+          if (cnt[z] == 1) zlist.push_back(z);
+        p->n_z_single = (int)zlist.size();
+        for (int z = 0; z < p->M[2]; ++z)
+          if (cnt[z] != 1) zlist.push_back(z);
+      }
       off += p->M[a];
       ent_all.insert(ent_all.end(), ent.begin(), ent.end());
       cnt_all.insert(cnt_all.end(), cnt.begin(), cnt.end());
     }
     TRY(dalloc(&p->d_comb_ent, ent_all.size()));
     TRY(dalloc(&p->d_comb_cnt, cnt_all.size()));
+    TRY(dalloc(&p->d_zlist, zlist.size()));
+    TRY(cudaMemcpy(p->d_zlist, zlist.data(), sizeof(int) * zlist.size(), cudaMemcpyHostToDevice));
     TRY(cudaMemcpy(p->d_comb_ent, ent_all.data(), sizeof(int) * ent_all.size(),
                    cudaMemcpyHostToDevice));
     TRY(cudaMemcpy(p->d_comb_cnt, cnt_all.data(), sizeof(int) * cnt_all.size(),

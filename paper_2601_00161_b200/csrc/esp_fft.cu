@@ -503,11 +503,16 @@ __device__ __forceinline__ void bulk_mbar_wait(uint64_t* bar, unsigned parity) {
 }
 
 constexpr int kThreadsXB = 128;
-template <typename real, int N>
-__global__ void __launch_bounds__(kThreadsXB, 4)
+// ZT: z tiles covering the planes of this launch.  Most planes lie under one
+// z tile (25 of 32 at config 4) and need 4 staged rows per pair, not 8: they
+// get their own launch (zlist: the plane list of the class, My even), which
+// fits seven CTAs per SM instead of four.
+template <typename real, int N, int ZT>
+__global__ void __launch_bounds__(kThreadsXB, ZT == 1 ? 7 : 4)
 k_x_bulk_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
              typename Cx<real>::t* __restrict__ out,
-             const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx) {
+             const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx,
+             const int* __restrict__ zlist) {
   using C = typename Cx<real>::t;
   constexpr int LP = pitch(N), NT = kThreadsXB, NR = 2;
   static_assert(N % NT == 0, "a thread owns N / NT columns");
@@ -515,11 +520,17 @@ k_x_bulk_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
   extern __shared__ __align__(128) unsigned char xb_sm[];
   const ScrLayout SL = scr_layout(g);
   const int row_elems = (int)SL.row;                     // ntx * 16
-  real* stage = reinterpret_cast<real*>(xb_sm);          // [2 rows][4 slots][row_elems]
-  C* buf = reinterpret_cast<C*>(xb_sm + (((size_t)8 * row_elems * sizeof(real) + 15) & ~size_t(15)));
+  constexpr int NS = 2 * ZT;                             // staged rows per grid row
+  real* stage = reinterpret_cast<real*>(xb_sm);          // [2 rows][NS slots][row_elems]
+  C* buf = reinterpret_cast<C*>(xb_sm +
+                                (((size_t)2 * NS * row_elems * sizeof(real) + 15) & ~size_t(15)));
   __shared__ long long s_rb[NR][6];   // slots a * 2 + b (z tile a, y tile b < 2), 4 + a: third y tile
   __shared__ __align__(8) uint64_t bar;
-  const long long r0 = 2LL * blockIdx.x;
+  // row pair -> first row: pairs of the listed planes (My even)
+  const int ppp = g.M[1] / 2;                            // pairs per plane
+  const long long r0 = zlist ? (long long)zlist[blockIdx.x / ppp] * g.M[1] +
+                                   2LL * (blockIdx.x % ppp)
+                             : 2LL * blockIdx.x;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bulk_smem_u32(&bar)), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -539,6 +550,30 @@ k_x_bulk_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
     }
     s_rb[rr][slot] = v;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned row_bytes = (unsigned)(row_elems * sizeof(real));
+    unsigned total = 0;
+#pragma unroll
+    for (int s8 = 0; s8 < 2 * NS; ++s8)
+      if (s_rb[s8 / NS][s8 % NS] >= 0) total += row_bytes;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     bulk_smem_u32(&bar)),
+                 "r"(total)
+                 : "memory");
+#pragma unroll
+    for (int s8 = 0; s8 < 2 * NS; ++s8) {
+      const long long b = s_rb[s8 / NS][s8 % NS];
+      if (b >= 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(bulk_smem_u32(stage + (size_t)s8 * row_elems)),
+            "l"(scratch + b), "r"(row_bytes), "r"(bulk_smem_u32(&bar))
+            : "memory");
+    }
+  }
+  // the covering x entries of this thread's columns: looked up while the
+  // copies are in flight
   int xo[XC][3];
 #pragma unroll
   for (int k = 0; k < XC; ++k) {
@@ -548,28 +583,6 @@ k_x_bulk_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
     for (int c = 0; c < 3; ++c) {
       const int ex = ct.ent[0][i * kCombW + (c < nx ? c : 0)];
       xo[k][c] = c < nx ? (ex & 0xffff) * kPad + (ex >> 16) : -1;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned row_bytes = (unsigned)(row_elems * sizeof(real));
-    unsigned total = 0;
-#pragma unroll
-    for (int s8 = 0; s8 < 8; ++s8)
-      if (s_rb[s8 >> 2][s8 & 3] >= 0) total += row_bytes;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                     bulk_smem_u32(&bar)),
-                 "r"(total)
-                 : "memory");
-#pragma unroll
-    for (int s8 = 0; s8 < 8; ++s8) {
-      const long long b = s_rb[s8 >> 2][s8 & 3];
-      if (b >= 0)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-            "[%3];" ::"r"(bulk_smem_u32(stage + (size_t)s8 * row_elems)),
-            "l"(scratch + b), "r"(row_bytes), "r"(bulk_smem_u32(&bar))
-            : "memory");
     }
   }
   bulk_mbar_wait(&bar, 0);
@@ -582,12 +595,12 @@ k_x_bulk_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
     for (int h = 0; h < 2; ++h) {
       double acc = 0.0;
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
+      for (int a = 0; a < ZT; ++a) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const int ab = a * 2 + b;
           if (s_rb[h][ab] >= 0) {
-            const real* row = stage + (size_t)(h * 4 + ab) * row_elems;
+            const real* row = stage + (size_t)(h * NS + ab) * row_elems;
             acc += (double)row[x0];
             if (x1 >= 0) acc += (double)row[x1];
             if (x2 >= 0) acc += (double)row[x2];
@@ -1429,8 +1442,11 @@ static cudaError_t launch_x_comb_r2c(const esp_plan* p, void* out, const void* t
   return cudaGetLastError();
 }
 
-// Bulk-staged variant for the long rows (N a multiple of 128, >= 256): eight
-// scratch rows plus the FFT line in dynamic shared memory, four CTAs per SM.
+// Bulk-staged variant for the long rows (N a multiple of 128, >= 256): the
+// scratch rows plus the FFT line in dynamic shared memory.  With My even the
+// planes under one z tile and the planes under two run as two launches (4 and
+// 8 staged rows per pair: seven and four CTAs per SM); otherwise one launch
+// stages 8 rows for every pair.
 template <typename real, int N>
 static cudaError_t launch_x_bulk_r2c(const esp_plan* p, void* out, const void* tw, int ldx,
                                      int nz, cudaStream_t s, bool* taken) {
@@ -1438,19 +1454,39 @@ static cudaError_t launch_x_bulk_r2c(const esp_plan* p, void* out, const void* t
   *taken = false;
   if constexpr (N % kThreadsXB == 0 && N >= 256) {
     static const bool off = std::getenv("ESP_NO_XBULK") != nullptr;   // A/B diagnostics
+    static const bool one_class = std::getenv("ESP_XBULK_ONE") != nullptr;
     const Geom g = make_geom(p);
-    const size_t stage = ((size_t)8 * g.ntx * kPad * sizeof(real) + 15) & ~size_t(15);
-    const size_t smem = stage + sizeof(C) * pitch(N);
-    if (off || smem > 56 * 1024 || p->comb_max[0] > 3 || p->comb_max[1] > 3 ||
+    const size_t row = (size_t)g.ntx * kPad * sizeof(real);
+    const size_t smem8 = ((8 * row + 15) & ~size_t(15)) + sizeof(C) * pitch(N);
+    const size_t smem4 = ((4 * row + 15) & ~size_t(15)) + sizeof(C) * pitch(N);
+    if (off || smem8 > 56 * 1024 || p->comb_max[0] > 3 || p->comb_max[1] > 3 ||
         p->comb_max[2] > 2)
       return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_x_bulk_r2c<real, N>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_x_bulk_r2c<real, N, 2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_x_bulk_r2c<real, N, 1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
     if (e != cudaSuccess) return e;
     const long long nrows = (long long)p->M[1] * nz;
-    k_x_bulk_r2c<real, N><<<(unsigned)((nrows + 1) / 2), kThreadsXB, smem, s>>>(
-        g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
-        reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx);
+    if (!one_class && p->M[1] % 2 == 0 && nz == p->M[2] && p->d_zlist && p->n_z_single > 0) {
+      const long long ppp = p->M[1] / 2;
+      const long long n1 = p->n_z_single * ppp, n2 = (p->M[2] - p->n_z_single) * ppp;
+      k_x_bulk_r2c<real, N, 1><<<(unsigned)n1, kThreadsXB, smem4, s>>>(
+          g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
+          reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx,
+          p->d_zlist);
+      if (n2 > 0) const_cast<esp_plan*>(p)->launches++;   // the caller counts one
+      if (n2 > 0)
+        k_x_bulk_r2c<real, N, 2><<<(unsigned)n2, kThreadsXB, smem8, s>>>(
+            g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
+            reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx,
+            p->d_zlist + p->n_z_single);
+    } else {
+      k_x_bulk_r2c<real, N, 2><<<(unsigned)((nrows + 1) / 2), kThreadsXB, smem8, s>>>(
+          g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
+          reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx, nullptr);
+    }
     *taken = true;
     return cudaGetLastError();
   }

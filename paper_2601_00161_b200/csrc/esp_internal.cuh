@@ -391,6 +391,8 @@ struct esp_plan {
   int* d_comb_cnt;
   long long comb_off[3];
   int comb_max[3];        // most tiles covering one coordinate, per axis
+  int* d_zlist = nullptr; // z planes covered by one z tile (n_z_single of them), then the rest
+  int n_z_single = 0;
   esp::FastTab* h_fast;   // host copy of the fast window table (kernel param)
   esp::FastTab* h_fast_d = nullptr;   // derivative window table (analytic gather)
   int need_records = 0; // next radix binning writes the weight records in its gather pass
