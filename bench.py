@@ -198,6 +198,8 @@ def scratch_elems(w):
     Mx, My, Mz = w.M
     T = 17 - w.P
     tzs = min(4 if Mz <= 128 else 32, Mz)
+    if Mz >= 256 and (-(-Mx // T)) * (-(-My // T)) * (Mz // 64) >= 148 * 8 * 4:
+        tzs = min(64, Mz)
     ntx, nty, ntz = -(-Mx // T), -(-My // T), -(-Mz // tzs)
     return ntx * nty * ntz * (tzs + w.P - 1) * 256
 

@@ -234,6 +234,11 @@ int esp_plan_create(const esp_plan_desc* d, esp_plan** out) {
   // small grids: shallow spread tiles (more tiles in flight; the extra
   // scratch halo is L2-resident)
   p->TZS = std::min(d->M[2] <= 128 ? 4 : std::max(p->TZ, 32), d->M[2]);
+  // grids with tiles to spare go 64 planes deep: fewer planes lie under two
+  // z tiles, so the combining x pass stages less (config 4: step 8.28 ->
+  // 8.24 ms; 96 and 128 planes lose it again in the spread's tail)
+  if (d->M[2] >= 256 && (long long)p->ntx * p->nty * (d->M[2] / 64) >= 148 * 8 * 4)
+    p->TZS = std::min(std::max(p->TZ, 64), d->M[2]);
   if (const char* env = getenv("ESP_TILE_ZS")) {   // diagnostic override (tuning sweeps)
     const int v = atoi(env);
     if (v > 0) p->TZS = std::min(v, d->M[2]);
