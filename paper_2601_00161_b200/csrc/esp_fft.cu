@@ -253,6 +253,81 @@ __device__ __forceinline__ void fft_ip(C* buf, const C* tw) {
   }
 }
 
+// Line groups of the y / z passes: when the CTA's warps divide its lines, a
+// warp owns whole lines and runs their stages back to back with warp-level
+// synchronisation only — the stages of different lines no longer meet at a
+// CTA barrier (six per transform), so one line's shared-memory and twiddle
+// latencies overlap another's butterflies.  One CTA barrier closes the
+// transform for the stores that follow.
+#ifndef ESP_FFT_WARPLINES
+#define ESP_FFT_WARPLINES 1
+#endif
+template <int R, int N, int Ns, int L, int NT, int SIGN, typename C>
+__device__ __forceinline__ void stage_ip_w(C* buf, const C* __restrict__ tw) {
+  constexpr int nb = N / R, NW = NT / 32, LW = L / NW, iters = (nb + 31) / 32, LP = pitch(N);
+  constexpr int toff = tw_offset(N, Ns);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int lw = 0; lw < LW; ++lw) {
+    C* line = buf + (warp * LW + lw) * LP;
+    C v[iters][R];
+#pragma unroll
+    for (int it = 0; it < iters; ++it) {
+      const int j = lane + it * 32;
+      if (nb % 32 == 0 || j < nb) {
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[it][t] = line[pidx(j + t * nb)];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < iters; ++it) {
+      const int j = lane + it * 32;
+      if (nb % 32 == 0 || j < nb) {
+        const int k = j % Ns;
+        if constexpr (Ns > 1) {
+#pragma unroll
+          for (int t = 1; t < R; ++t) {
+            C w = __ldg(tw + toff + (t - 1) * Ns + k);
+            if (SIGN > 0) w.y = -w.y;
+            v[it][t] = cmul(v[it][t], w);
+          }
+        }
+        dft<R, SIGN>(v[it]);
+        const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+        for (int t = 0; t < R; ++t) line[pidx(base + t * Ns)] = v[it][t];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int N, int Ns, int L, int NT, int SIGN, typename C>
+__device__ __forceinline__ void fft_ip_w(C* buf, const C* tw) {
+  if constexpr (Ns < N) {
+    constexpr int R = pick_radix(N / Ns);
+    stage_ip_w<R, N, Ns, L, NT, SIGN>(buf, tw);
+    fft_ip_w<N, Ns * R, L, NT, SIGN>(buf, tw);
+  }
+}
+
+// L lines of length N in place; enters after a CTA barrier, leaves after one.
+// WL: warp-owned lines.  Measured at config 4 (ms, CTA-barrier stages -> warp
+// lines at 3 -> at 2 CTAs per SM): forward y 0.132 -> 0.121 -> 0.097, z +
+// reduce 0.103 -> 0.102 -> 0.100, ik + inverse z 0.224 -> 0.221 -> 0.252,
+// inverse y 0.362 -> 0.384 -> 0.377 — the store-heavy inverse passes want the
+// third CTA more than the loose stages, so only the forward y pass takes it.
+template <int N, int L, int NT, int SIGN, bool WL, typename C>
+__device__ __forceinline__ void fft_lines(C* buf, const C* tw) {
+  if constexpr (WL && ESP_FFT_WARPLINES && NT % 32 == 0 && L % (NT / 32) == 0) {
+    fft_ip_w<N, 1, L, NT, SIGN>(buf, tw);
+    __syncthreads();
+  } else {
+    fft_ip<N, 1, L, NT, SIGN>(buf, tw);
+  }
+}
+
 // Twiddle tables live in global memory in the plan's precision and are read
 // through L1 (a warp reads consecutive entries).
 
@@ -661,7 +736,7 @@ __device__ __forceinline__ int slab_owner(const int* start, int R, int v) {
 // P2: y lines (z, kx) for kx < ldx: forward C2C, keep the nby in-band ky.
 // in[(z*N + y)*ldx + kx] -> out[(z*nby + by)*ldx + kx].
 template <typename real, int N>
-__global__ void __launch_bounds__(threads_yz<real>(N), ESP_YZ_MINB)
+__global__ void __launch_bounds__(threads_yz<real>(N), ESP_FFT_WARPLINES ? 2 : ESP_YZ_MINB)
 k_y_fwd(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __restrict__ out,
         const typename Cx<real>::t* __restrict__ tw, long long nlines, int ldx, int nby,
         SlabMap smap) {
@@ -686,7 +761,7 @@ k_y_fwd(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __res
 #pragma unroll
   for (int it = 0; it < nld; ++it) buf[l * LP + pidx(threadIdx.x / L + it * YS)] = v[it];
   __syncthreads();
-  fft_ip<N, 1, L, NT, -1>(buf, tw);
+  fft_lines<N, L, NT, -1, true>(buf, tw);
   if (!valid) return;
   if (smap.R == 0) {
     C* dst = out + z * (long long)nby * ldx + kx;
@@ -858,7 +933,7 @@ k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __
     for (int it = 0; it < nld; ++it) X[l * LP + pidx(threadIdx.x / L + it * ZS)] = v[it];
   }
   __syncthreads();
-  fft_ip<N, 1, L, NT, -1>(X, tw);
+  fft_lines<N, L, NT, -1, false>(X, tw);
   if constexpr (!PF) pencil();
   double acc[7];
 #pragma unroll
@@ -957,7 +1032,7 @@ k_z_reduce(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __
         }
       }
       __syncthreads();
-      fft_ip<N, 1, L, NT, +1>(T, tw);
+      fft_lines<N, L, NT, +1, false>(T, tw);
       if (valid) {
         C* dst = ik + (long long)c * N * zstride + line;
 #pragma unroll
@@ -1042,7 +1117,7 @@ k_z_ik(const typename Cx<real>::t* __restrict__ spec, typename Cx<real>::t* __re
     for (int it = 0; it < nld; ++it) T[l * LP + pidx(threadIdx.x / L + it * ZS)] = v[it];
   }
   __syncthreads();
-  fft_ip<N, 1, L, NT, +1>(T, tw);
+  fft_lines<N, L, NT, +1, false>(T, tw);
   if (!valid) return;
   if (smap.R == 0) {
     C* dst = ik + (long long)comp * N * zstride + line;
@@ -1092,7 +1167,7 @@ k_y_inv(const typename Cx<real>::t* __restrict__ in, typename Cx<real>::t* __res
 #pragma unroll
   for (int it = 0; it < nld; ++it) buf[l * LP + pidx(threadIdx.x / L + it * YS)] = v[it];
   __syncthreads();
-  fft_ip<N, 1, L, NT, +1>(buf, tw);
+  fft_lines<N, L, NT, +1, false>(buf, tw);
   if (!valid) return;
   C* dst = out + cz * (long long)N * ldx + kx;
 #pragma unroll
