@@ -28,16 +28,20 @@ def main(rep, workload, precision):
     hdr, units, data = rows[0], rows[1], rows[2:]
     ki = hdr.index("Kernel Name")
     rd, wr = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    # per kernel instantiation: mean over its captured launches; a stage that
+    # runs as several instantiations per step (the bulk-staged x pass: one
+    # launch per z-plane class) is their sum
     acc = {}
     for r in data:
-        base = r[ki].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1].strip()
+        full = r[ki].split("(")[0].replace("void ", "").strip()
+        base = full.split("<")[0].split("::")[-1].strip()
         st = STAGE.get(base)
         if not st:
             continue
         b = (float(r[rd].replace(",", "")) * SCALE[units[rd]] +
              float(r[wr].replace(",", "")) * SCALE[units[wr]])
-        acc.setdefault(st, []).append(b)
-    res = {k: int(sum(v) / len(v)) for k, v in acc.items()}
+        acc.setdefault(st, {}).setdefault(full, []).append(b)
+    res = {k: int(sum(sum(v) / len(v) for v in inst.values())) for k, inst in acc.items()}
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dram_traffic.json")
     d = json.load(open(path)) if os.path.exists(path) else {}
     d[f"{workload}/{precision}"] = res

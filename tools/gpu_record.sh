@@ -8,7 +8,7 @@ ARGS="--config $CFG --precision $PREC"
 timeout 300 python bench.py $ARGS --profile-only --steps 2 --warmup 1 || exit 1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py $ARGS --profile-only --steps 2 --warmup 1 > /dev/null 2>&1
 KREGEX='regex:k_(bin|spread|combine|x_|y_|z_|gather|scale)'
-NK=$(python -c "print(11 if $CFG in (3, 4) else 9)")   # our kernels per step (skip the first step)
+NK=$(python -c "print({3: 11, 4: 12}.get($CFG, 9))")   # our kernels per step (skip the first step; config 4: the x pass is two launches)
 timeout 900 ncu --set full --clock-control none --import-source on -k "$KREGEX" -s $NK -c $NK -o gpurun_out/prof_$TAG python bench.py $ARGS --profile-only --steps 2 --warmup 1 > gpurun_out/ncu_$TAG.log 2>&1; tail -1 gpurun_out/ncu_$TAG.log
 W=$(python -c "from paper_2601_00161_b200 import workloads; print(workloads.CONFIGS[$CFG]['name'])")
 python profiles/traffic.py gpurun_out/prof_$TAG.ncu-rep $W $PREC && cp profiles/dram_traffic.json gpurun_out/dram_traffic.json
