@@ -232,40 +232,59 @@ k_bin_records_u(Geom g, FastTab ft, const real* __restrict__ tab, const double* 
   __shared__ __align__(16) real s_drec[DREC ? kBinPerBlock * 3 * RS : 2];
   __shared__ int s_pk[kBinPerBlock];
   const int d = threadIdx.x / kBinPerBlock, l = threadIdx.x % kBinPerBlock;
-  const long long j0 = (long long)blockIdx.x * kBinPerBlock;
-  const long long j = j0 + l;
-  const int nb = (int)min((long long)kBinPerBlock, n - j0);
-  if (l < nb) {
-    const double u = U[d * cap + j];
-    real w[P];
-    int a;
-    record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
+  // grid-stride over 32-charge groups; the next group's coordinate and key
+  // are loaded before this group's weights are evaluated (each thread has one
+  // load per group: without the prefetch its latency is fully exposed)
+  const long long ngroups = (n + kBinPerBlock - 1) / kBinPerBlock;
+  double u_next = 0.0;
+  int key_next = 0;
+  auto prefetch = [&](long long grp) {
+    const long long jn = grp * kBinPerBlock + l;
+    if (jn < n) {
+      u_next = U[d * cap + jn];
+      if (d < 2) key_next = skey[jn];
+    }
+  };
+  long long grp = blockIdx.x;
+  if (grp < ngroups) prefetch(grp);
+  for (; grp < ngroups; grp += gridDim.x) {
+    const double u = u_next;
+    const int key = key_next;
+    if (grp + gridDim.x < ngroups) prefetch(grp + gridDim.x);
+    const long long j0 = grp * kBinPerBlock;
+    const int nb = (int)min((long long)kBinPerBlock, n - j0);
+    if (l < nb) {
+      real w[P];
+      int a;
+      record_dim_compute<real, P>(g, ft, tab, brk, n_pieces, ncoef, d, u, w, a);
 #pragma unroll
-    for (int t = 0; t < RS; ++t) s_rec[(l * 3 + d) * RS + t] = t < P ? w[t < P ? t : 0] : real(0);
+      for (int t = 0; t < RS; ++t) s_rec[(l * 3 + d) * RS + t] = t < P ? w[t < P ? t : 0] : real(0);
+      if (DREC) {
+        real dw[P];
+        stencil_weights<real, P>(ftd, dtab, brk, n_pieces, ncoef, u, anchor_base(g, u), g.lo,
+                                 real(1), dw);
+#pragma unroll
+        for (int t = 0; t < RS; ++t)
+          s_drec[(l * 3 + d) * RS + t] = t < P ? dw[t < P ? t : 0] : real(0);
+      }
+      unsigned char* pb = reinterpret_cast<unsigned char*>(s_pk + l);
+      if (d == 2) {
+        *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
+      } else {
+        const int txy = key / g.M[2];
+        const int org = d == 0 ? (txy % g.ntx) * g.TX : (txy / g.ntx) * g.TY;
+        pb[d] = (unsigned char)(a - org);
+      }
+    }
+    __syncthreads();
+    real* dst = wrec + j0 * (3 * RS);
+    for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) dst[t] = s_rec[t];
+    for (int t = threadIdx.x; t < nb; t += 3 * kBinPerBlock) pk[j0 + t] = s_pk[t];
     if (DREC) {
-      real dw[P];
-      stencil_weights<real, P>(ftd, dtab, brk, n_pieces, ncoef, u, anchor_base(g, u), g.lo,
-                               real(1), dw);
-#pragma unroll
-      for (int t = 0; t < RS; ++t)
-        s_drec[(l * 3 + d) * RS + t] = t < P ? dw[t < P ? t : 0] : real(0);
+      real* ddst = drec + j0 * (3 * RS);
+      for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) ddst[t] = s_drec[t];
     }
-    unsigned char* pb = reinterpret_cast<unsigned char*>(s_pk + l);
-    if (d == 2) {
-      *reinterpret_cast<unsigned short*>(pb + 2) = (unsigned short)a;   // absolute z
-    } else {
-      const int txy = skey[j] / g.M[2];
-      const int org = d == 0 ? (txy % g.ntx) * g.TX : (txy / g.ntx) * g.TY;
-      pb[d] = (unsigned char)(a - org);
-    }
-  }
-  __syncthreads();
-  real* dst = wrec + j0 * (3 * RS);
-  for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) dst[t] = s_rec[t];
-  for (int t = threadIdx.x; t < nb; t += 3 * kBinPerBlock) pk[j0 + t] = s_pk[t];
-  if (DREC) {
-    real* ddst = drec + j0 * (3 * RS);
-    for (int t = threadIdx.x; t < nb * 3 * RS; t += 3 * kBinPerBlock) ddst[t] = s_drec[t];
+    __syncthreads();   // the staging rows are rewritten by the next group
   }
 }
 
@@ -652,7 +671,12 @@ static cudaError_t records_p(esp_plan* p, cudaStream_t s) {
   const real* tab = std::is_same<real, double>::value
                         ? reinterpret_cast<const real*>(p->d_tab)
                         : reinterpret_cast<const real*>(p->d_tabf);
-  const unsigned g3 = (unsigned)((p->last_n + kBinPerBlock - 1) / kBinPerBlock);
+  // grid-stride groups: a few waves of CTAs, so every thread prefetches
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long long ngroups = (p->last_n + kBinPerBlock - 1) / kBinPerBlock;
+  const unsigned g3 = (unsigned)std::max<long long>(1, std::min<long long>(ngroups, (long long)nsm * 64));
   const real* dtab = std::is_same<real, double>::value
                          ? reinterpret_cast<const real*>(p->d_dtab)
                          : reinterpret_cast<const real*>(p->d_dtabf);
