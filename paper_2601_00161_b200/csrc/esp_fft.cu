@@ -1238,6 +1238,47 @@ k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
   constexpr int half = N / 2, NH = half + 1;
   __shared__ C buf[PP * LP];
   const long long r0 = 2LL * blockIdx.x * PP;
+  // in-band columns: thread k < nbx loads column k of every row of the CTA
+  // (all loads first), places Z_k = A + i B and its mirror Z_{N-k}; the
+  // out-of-band entries nbx .. N - nbx of each line are zero-filled
+  if (nbx <= NT) {
+    C va[PP], vb[PP];
+    const int k = threadIdx.x;
+    if (k < nbx) {
+#pragma unroll
+      for (int l = 0; l < PP; ++l) {
+        const long long ra = r0 + 2 * l;
+        va[l].x = va[l].y = vb[l].x = vb[l].y = real(0);
+        if (ra < nrows) va[l] = __ldcs(in + ra * ldx + k);
+        if (ra + 1 < nrows) vb[l] = __ldcs(in + (ra + 1) * ldx + k);
+      }
+    }
+    for (int e = threadIdx.x; e < PP * (N + 1 - 2 * nbx); e += NT) {
+      const int l = e / (N + 1 - 2 * nbx), i = nbx + (e - l * (N + 1 - 2 * nbx));
+      C z;
+      z.x = z.y = real(0);
+      buf[l * LP + pidx(i)] = z;
+    }
+    if (k < nbx) {
+#pragma unroll
+      for (int l = 0; l < PP; ++l) {
+        C A = va[l], B = vb[l];
+        if (k == 0 || k == half) {
+          A.y = real(0);
+          B.y = real(0);
+        }
+        C z;   // Z_k = A + i B
+        z.x = A.x - B.y;
+        z.y = A.y + B.x;
+        buf[l * LP + pidx(k)] = z;
+        if (k != 0 && k != half) {   // Z_{N-k} = conj A + i conj B
+          z.x = A.x + B.y;
+          z.y = B.x - A.y;
+          buf[l * LP + pidx(N - k)] = z;
+        }
+      }
+    }
+  } else {
   constexpr int nhl = (PP * NH + NT - 1) / NT;
   C va[nhl], vb[nhl];
 #pragma unroll
@@ -1271,6 +1312,7 @@ k_x_c2r(const typename Cx<real>::t* __restrict__ in, real* __restrict__ fld,
         buf[l * LP + pidx(N - k)] = z;
       }
     }
+  }
   }
   __shared__ PadRows s_rows[pad_rows_smem(PP)];
   if (pad.enabled && threadIdx.x < 2 * PP && r0 + threadIdx.x < nrows)
