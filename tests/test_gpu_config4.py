@@ -83,6 +83,37 @@ def test_config4_full_size_against_reference(cfg4, precision, tol):
     del s, F
 
 
+@pytest.mark.slow
+def test_config4_host_buffer_step_equals_device_step(cfg4):
+    """The host-buffer step at full size (positions copied first, charges
+    behind them on the side stream and binned after the records pass, forces
+    copied out in two index ranges) gives the device step's numbers bit for
+    bit, also after the host buffers change."""
+    torch = _torch()
+    from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
+    w, P_, Q_, g = cfg4
+    s = KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P, fixed_M=w.M,
+                                          cell_type=w.cell_type), capacity=w.n)
+    e7, eF = s.evaluate_device(P_, Q_)
+    e7, eF = e7.cpu(), eF.cpu()
+    hs = s.host_stepper(w.n)
+    hs.positions.copy_(P_.cpu())
+    hs.charges.copy_(Q_.cpu())
+    h7, hF = hs.step()
+    assert torch.equal(h7, e7) and torch.equal(hF, eF)
+    # new charges and shifted positions through the host buffers
+    q2 = Q_.cpu() * torch.linspace(0.5, 1.5, w.n, dtype=torch.float64)
+    p2 = P_.cpu() + 0.37
+    hs.charges.copy_(q2)
+    hs.positions.copy_(p2)
+    hs.forces.fill_(float("nan"))
+    h7, hF = hs.step()
+    r7, rF = s.evaluate_device(p2.cuda(), q2.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(h7, r7.cpu()) and torch.equal(hF, rF.cpu())
+    del s, hs
+
+
 def _solver(w, force_mode="ik", precision="fp64"):
     from paper_2601_00161_b200 import EwaldParameters, KSpaceSolver
     return KSpaceSolver(w.h, EwaldParameters(r_c=w.r_c, delta_split=w.delta, P=w.P,
