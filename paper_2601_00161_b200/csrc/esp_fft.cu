@@ -7,7 +7,10 @@
 // reduction (mesh.py:285-312), the ik spectra (mesh.py:333-341) and the
 // first inverse stage:
 //
-//   P1  x rows:  real -> complex (two rows per complex FFT), keep kx <= band
+//   P1  x rows:  real -> complex (two rows per complex FFT), keep kx <= band;
+//                in esp_evaluate the rows are summed straight from the
+//                spread's tile blocks (k_x_bulk_r2c: scratch rows staged by
+//                cp.async.bulk on an mbarrier; k_x_comb_r2c: register-staged)
 //   P2  y lines: C2C, keep |ky| <= band
 //   P3a z lines: C2C; reduce E, P_ab over the retained modes; write the box
 //                spectrum
@@ -22,7 +25,8 @@
 //
 // Line transforms: compile-time length N, mixed-radix (8, 6, 4, 3, 2)
 // Stockham auto-sort stages executed in place in shared memory through
-// registers (load R inputs -> barrier -> twiddle, DFT, store).  Shared rows
+// registers (load R inputs -> barrier -> twiddle, DFT, store; the forward y
+// pass gives each warp whole lines and synchronises per warp, fft_lines).  Shared rows
 // use pitch N + N/8 + 1 and index i + i/8 so that strided butterflies and
 // the line-transposing loads are bank-conflict free; per-stage twiddle
 // tables are laid out [t-1][k] so a warp reads consecutive entries.

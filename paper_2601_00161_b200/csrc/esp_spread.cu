@@ -25,7 +25,9 @@
 //    against whole blocks stored one after another).  k_combine sums, for
 //    every grid point, the contributions of the (at most 8) covering tiles in
 //    a fixed order read from precomputed per-axis tables.  No atomics:
-//    results are bitwise reproducible.
+//    results are bitwise reproducible.  esp_evaluate on the fused transforms
+//    skips k_combine: its forward x pass sums the same blocks in the same
+//    order (esp_fft.cu: k_x_bulk_r2c / k_x_comb_r2c).
 #include <cstdlib>
 
 #include "esp_internal.cuh"
