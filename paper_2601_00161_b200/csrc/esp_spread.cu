@@ -32,6 +32,9 @@
 
 #include "esp_internal.cuh"
 
+#ifndef ESP_SPREAD_U8
+#define ESP_SPREAD_U8 2   // charges unrolled in the 8-rows-per-thread layout (diagnostic: 1.98 ms against 2.19 at 1)
+#endif
 namespace esp {
 
 // Per-particle staging record (reals): x weights and y weights each stored
@@ -264,6 +267,7 @@ k_spread_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
   constexpr int C = 32;                       // charges per staged chunk
   constexpr int RS = rec_stride(P), KREC = 3 * RS;
   constexpr int OFF = WarpRow<P>::OFF, RL = WarpRow<P>::RL;
+  constexpr int kChargeUnroll = ROWS == 8 ? ESP_SPREAD_U8 : 4;
   __shared__ __align__(16) real s_raw[2][C * KREC];
   __shared__ __align__(16) real s_row[C][2 * RL];
   __shared__ int s_pk[2][C];
@@ -357,7 +361,7 @@ k_spread_warp(Geom g, const int* __restrict__ offsets, const real* __restrict__ 
     if (c0 + C < p1) fetch(c0 + C, b ^ 1);   // next chunk lands during this one
     // 4 charges unrolled: their record loads overlap the previous FMAs
     // (config 1 spread 47 -> 42.5 us, config 4 2.06 -> 1.86 ms; 8 is slower)
-#pragma unroll 4
+#pragma unroll kChargeUnroll
     for (int t = 0; t < n; ++t) {
       const int pk = s_pk[b][t];
       const int xl = pk & 0xff, yl = (pk >> 8) & 0xff;
