@@ -554,7 +554,7 @@ k_x_comb_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
 }
 
 // The same pass with the scratch rows staged by the copy engine (large grids:
-// N a multiple of 128, >= 256; one row pair per CTA; every coordinate covered
+// N a multiple of 64, >= 192; one row pair per CTA; every coordinate covered
 // by <= 3 x, <= 3 y and <= 2 z tiles).  A grid row's <= 4 covering scratch
 // rows are contiguous runs of ntx * 16 values (scr_index), so one thread
 // issues one cp.async.bulk per run, completing on an mbarrier: no registers
@@ -581,19 +581,20 @@ __device__ __forceinline__ void bulk_mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-constexpr int kThreadsXB = 128;
+// threads per CTA: 128 on rows that are a multiple of 128, else 64
+__host__ __device__ constexpr int threads_xb(int N) { return N % 128 == 0 ? 128 : 64; }
 // ZT: z tiles covering the planes of this launch.  Most planes lie under one
 // z tile (25 of 32 at config 4) and need 4 staged rows per pair, not 8: they
 // get their own launch (zlist: the plane list of the class, My even), which
 // fits seven CTAs per SM instead of four.
 template <typename real, int N, int ZT>
-__global__ void __launch_bounds__(kThreadsXB, ZT == 1 ? 7 : 4)
+__global__ void __launch_bounds__(threads_xb(N), (ZT == 1 ? 7 : 4) * (128 / threads_xb(N)))
 k_x_bulk_r2c(Geom g, CombineTabs ct, const real* __restrict__ scratch,
              typename Cx<real>::t* __restrict__ out,
              const typename Cx<real>::t* __restrict__ tw, long long nrows, int ldx, int nbx,
              const int* __restrict__ zlist) {
   using C = typename Cx<real>::t;
-  constexpr int LP = pitch(N), NT = kThreadsXB, NR = 2;
+  constexpr int LP = pitch(N), NT = threads_xb(N), NR = 2;
   static_assert(N % NT == 0, "a thread owns N / NT columns");
   constexpr int XC = N / NT;
   extern __shared__ __align__(128) unsigned char xb_sm[];
@@ -1563,7 +1564,7 @@ static cudaError_t launch_x_comb_r2c(const esp_plan* p, void* out, const void* t
   return cudaGetLastError();
 }
 
-// Bulk-staged variant for the long rows (N a multiple of 128, >= 256): the
+// Bulk-staged variant for the long rows (N a multiple of 64, >= 192): the
 // scratch rows plus the FFT line in dynamic shared memory.  With My even the
 // planes under one z tile and the planes under two run as two launches (4 and
 // 8 staged rows per pair: seven and four CTAs per SM); otherwise one launch
@@ -1573,7 +1574,7 @@ static cudaError_t launch_x_bulk_r2c(const esp_plan* p, void* out, const void* t
                                      int nz, cudaStream_t s, bool* taken) {
   using C = typename Cx<real>::t;
   *taken = false;
-  if constexpr (N % kThreadsXB == 0 && N >= 256) {
+  if constexpr (N % 64 == 0 && N >= 192) {
     static const bool off = std::getenv("ESP_NO_XBULK") != nullptr;   // A/B diagnostics
     static const bool one_class = std::getenv("ESP_XBULK_ONE") != nullptr;
     const Geom g = make_geom(p);
@@ -1593,18 +1594,18 @@ static cudaError_t launch_x_bulk_r2c(const esp_plan* p, void* out, const void* t
     if (!one_class && p->M[1] % 2 == 0 && nz == p->M[2] && p->d_zlist && p->n_z_single > 0) {
       const long long ppp = p->M[1] / 2;
       const long long n1 = p->n_z_single * ppp, n2 = (p->M[2] - p->n_z_single) * ppp;
-      k_x_bulk_r2c<real, N, 1><<<(unsigned)n1, kThreadsXB, smem4, s>>>(
+      k_x_bulk_r2c<real, N, 1><<<(unsigned)n1, threads_xb(N), smem4, s>>>(
           g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
           reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx,
           p->d_zlist);
       if (n2 > 0) const_cast<esp_plan*>(p)->launches++;   // the caller counts one
       if (n2 > 0)
-        k_x_bulk_r2c<real, N, 2><<<(unsigned)n2, kThreadsXB, smem8, s>>>(
+        k_x_bulk_r2c<real, N, 2><<<(unsigned)n2, threads_xb(N), smem8, s>>>(
             g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
             reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx,
             p->d_zlist + p->n_z_single);
     } else {
-      k_x_bulk_r2c<real, N, 2><<<(unsigned)((nrows + 1) / 2), kThreadsXB, smem8, s>>>(
+      k_x_bulk_r2c<real, N, 2><<<(unsigned)((nrows + 1) / 2), threads_xb(N), smem8, s>>>(
           g, combine_tabs(p), reinterpret_cast<const real*>(p->d_scratch),
           reinterpret_cast<C*>(out), reinterpret_cast<const C*>(tw), nrows, ldx, p->nbx, nullptr);
     }

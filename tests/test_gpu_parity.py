@@ -523,6 +523,7 @@ FUSED_CASES = [
     ("small_brick_p8", (256, 48, 32)),
     ("small_brick_p7", (384, 32, 48)),
     ("tri_flex_p7", (256, 32, 32)),
+    ("small_brick_p6", (192, 48, 32)),   # 64-thread CTAs
 ]
 
 
@@ -574,7 +575,8 @@ def test_fused_and_cufft_paths_agree(monkeypatch):
 @pytest.mark.parametrize("name,M", [("small_brick_p8", (32, 48, 32)), ("small_brick_p7", (96, 64, 96)),
                                     ("small_cube_p4", (48, 64, 48)), ("tri_flex_p7", (64, 48, 64)),
                                     ("small_brick_p6", (128, 96, 64)),
-                                    ("small_brick_p8", (256, 48, 32)), ("small_cube_p5", (384, 32, 48))])
+                                    ("small_brick_p8", (256, 48, 32)), ("small_cube_p5", (384, 32, 48)),
+                                    ("tri_flex_p7", (192, 32, 48))])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_x_pass_combine_bitwise_equals_separate_combine(name, M, precision, monkeypatch):
     """esp_evaluate sums the spread's tile blocks inside the forward x pass
